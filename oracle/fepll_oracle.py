@@ -1,0 +1,447 @@
+"""CPU oracle for the FEPLL restoration loop — TEST INFRASTRUCTURE ONLY.
+
+A numpy restatement of the reference hot path (`/root/reference/pkg`,
+package ``fepll``), used exclusively as the checker by ``tests/``,
+``__graft_entry__.smoke()`` and the ``cpu_baseline`` / ``--impl reference``
+legs of ``bench.py``.  The product path (``paper_1710_08124_b200``) never
+imports this module.
+
+Parity pin: ``tests/test_oracle_golden.py`` checks this oracle against the
+golden vectors in ``tests/golden/`` which ``oracle/make_golden.py`` produced
+by executing the reference package itself in the build container
+(per-iteration labels, lambda, counters, final images).
+
+Every function cites the reference lines it restates.  Arithmetic is FP64
+with numpy/pocketfft like the reference, so results agree with it to
+rounding (labels exactly).
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import time
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
+
+import numpy as np
+
+CHUNK = 4096  # pkg/src/fepll/solver.py:60
+
+
+# ---------------------------------------------------------------- sampling plan
+def axis_anchors(extent, side, spacing):
+    """pkg/src/fepll/patches.py:79-86"""
+    last = extent - side
+    a = list(range(0, last + 1, spacing))
+    if a[-1] != last:
+        a.append(last)
+    return np.asarray(a, dtype=np.int64)
+
+
+def regular_grid(H, W, P, s):
+    """pkg/src/fepll/patches.py:89-99"""
+    side = math.isqrt(P)
+    r, c = np.meshgrid(axis_anchors(H, side, s), axis_anchors(W, side, s), indexing="ij")
+    return np.stack([r.ravel(), c.ravel()], axis=1)
+
+
+def jittered_grid(H, W, P, s, seed, t):
+    """pkg/src/fepll/patches.py:102-132 (Philox keyed [seed, t])."""
+    side = math.isqrt(P)
+    base = regular_grid(H, W, P, s)
+    half = (side - s) // 2
+    if half == 0:
+        return base
+    rng = np.random.Generator(np.random.Philox(key=[seed & (2 ** 64 - 1), t]))
+    shift = rng.integers(0, s, size=2)
+    eff = shift % (2 * half + 1) - half
+    jit = rng.integers(-half, half + 1, size=base.shape)
+    off = np.clip(eff[None, :] + jit, -half, half)
+    off[(base[:, 0] == 0) | (base[:, 0] == H - side), 0] = 0
+    off[(base[:, 1] == 0) | (base[:, 1] == W - side), 1] = 0
+    pos = base + off
+    pos[:, 0] = np.clip(pos[:, 0], 0, H - side)
+    pos[:, 1] = np.clip(pos[:, 1], 0, W - side)
+    return pos
+
+
+# ---------------------------------------------------------------- extraction
+def pairwise_mean(rows):
+    """pkg/src/fepll/patches.py:153-164: halve the width until one column
+    remains, folding an odd trailing column into the last slot."""
+    acc = rows.copy()
+    while acc.shape[1] > 1:
+        w = acc.shape[1]
+        tail = acc[:, -1].copy() if w % 2 else None
+        h = w // 2
+        acc = acc[:, :h] + acc[:, h:2 * h]
+        if tail is not None:
+            acc[:, -1] += tail
+    return acc[:, 0] / rows.shape[1]
+
+
+def extract(x, pos, side):
+    """pkg/src/fepll/patches.py:167-183 -> (patches, dc)."""
+    win = np.lib.stride_tricks.sliding_window_view(x, (side, side))[pos[:, 0], pos[:, 1]]
+    win = win.reshape(pos.shape[0], side * side)
+    dc = pairwise_mean(win)
+    return win - dc[:, None], dc
+
+
+def flat_index(pos, side, W):
+    """pkg/src/fepll/patches.py:186-188"""
+    o = (np.arange(side)[:, None] * W + np.arange(side)[None, :]).ravel()
+    return (pos[:, 0] * W + pos[:, 1])[:, None] + o[None, :]
+
+
+def reproject(est, dc, pos, side, H, W):
+    """pkg/src/fepll/patches.py:198-222 (bincount average, lo==hi verbatim)."""
+    idx = flat_index(pos, side, W).ravel()
+    vals = (est + dc[:, None]).ravel()
+    cnt = np.bincount(idx, minlength=H * W)
+    if cnt.min() < 1:
+        raise ValueError("reprojection target has uncovered pixels")
+    s = np.bincount(idx, weights=vals, minlength=H * W)
+    lo = np.full(H * W, np.inf)
+    hi = np.full(H * W, -np.inf)
+    np.minimum.at(lo, idx, vals)
+    np.maximum.at(hi, idx, vals)
+    return np.where(lo == hi, lo, s / cnt).reshape(H, W)
+
+
+# ---------------------------------------------------------------- prior arithmetic
+class Ctx:
+    """pkg/src/fepll/gmm.py:275-307 (ScoreContext constants)."""
+
+    def __init__(self, comps, beta):
+        ib = 1.0 / beta
+        self.U = [np.asarray(c.kept_basis, dtype=np.float64) for c in comps]
+        self.rank = [u.shape[1] for u in self.U]
+        self.nu_tail = np.empty(len(comps))
+        self.gamma_tail = np.empty(len(comps))
+        self.const = np.empty(len(comps))
+        self.sqw, self.shrink = [], []
+        for k, c in enumerate(comps):
+            ev = np.asarray(c.kept_eigenvalues, dtype=np.float64)
+            nu = ev + ib
+            nt = c.tail_value + ib
+            self.nu_tail[k] = nt
+            self.gamma_tail[k] = c.tail_value / nt
+            self.sqw.append(1.0 / nu - 1.0 / nt)
+            self.shrink.append(ev / nu - c.tail_value / nt)
+            tail_dim = self.U[k].shape[0] - self.U[k].shape[1]
+            self.const[k] = (-2.0 * math.log(c.weight) + tail_dim * math.log(nt) + np.log(nu).sum())
+
+    def score(self, k, Z, sq):
+        """pkg/src/fepll/gmm.py:323-339"""
+        c = Z @ self.U[k]
+        return self.const[k] + sq / self.nu_tail[k] + np.square(c) @ self.sqw[k]
+
+    def wiener(self, k, Z):
+        """pkg/src/fepll/gmm.py:352-359"""
+        U = self.U[k]
+        return ((Z @ U) * self.shrink[k]) @ U.T + self.gamma_tail[k] * Z
+
+
+def score_cost(r, P):
+    """pkg/src/fepll/gmm.py:254-257"""
+    return r * P + 2 * r + 1
+
+
+def wiener_cost(r, P):
+    """pkg/src/fepll/gmm.py:260-263"""
+    return r * P + r + P
+
+
+def bfs(tree):
+    """pkg/src/fepll/tree.py:253-259 + :399-403 -> (components, children, leaf)."""
+    order = [tree.root]
+    i = 0
+    while i < len(order):
+        order.extend(order[i].children)
+        i += 1
+    pos = {id(n): j for j, n in enumerate(order)}
+    kids = [np.array([pos[id(c)] for c in n.children], dtype=np.int64) for n in order]
+    leaf = np.array([-1 if n.leaf_index is None else n.leaf_index for n in order], dtype=np.int64)
+    return [n.component for n in order], kids, leaf
+
+
+def tree_select(kids, leaf, ctx, Z, P):
+    """pkg/src/fepll/tree.py:387-434: greedy best-child descent, first
+    minimum in child order, with (evals, mults) counters."""
+    n = Z.shape[0]
+    sq = np.einsum("ij,ij->i", Z, Z)
+    cur = np.zeros(n, dtype=np.int64)
+    ev = np.zeros(n, dtype=np.int64)
+    mu = np.full(n, P, dtype=np.int64)
+    act = leaf[cur] < 0
+    while act.any():
+        for u in np.unique(cur[act]):
+            ch = kids[u]
+            sel = np.where(act & (cur == u))[0]
+            sc = np.empty((sel.size, ch.size))
+            cost = 0
+            for j, k in enumerate(ch):
+                sc[:, j] = ctx.score(int(k), Z[sel], sq[sel])
+                cost += score_cost(ctx.rank[int(k)], P)
+            cur[sel] = ch[np.argmin(sc, axis=1)]
+            ev[sel] += ch.size
+            mu[sel] += cost
+        act = leaf[cur] < 0
+    return leaf[cur], ev, mu
+
+
+def select_exhaustive(ctx, Z):
+    """pkg/src/fepll/gmm.py:371-391"""
+    sq = np.einsum("ij,ij->i", Z, Z)
+    sc = np.column_stack([ctx.score(k, Z, sq) for k in range(len(ctx.U))])
+    return np.argmin(sc, axis=1)
+
+
+# ---------------------------------------------------------------- operators
+def kernel_ft(A):
+    """pkg/src/fepll/operators.py:91-100"""
+    H, W = A.input_dims
+    kh, kw = A.kernel.shape
+    pad = np.zeros((H, W))
+    pad[:kh, :kw] = A.kernel
+    return np.fft.fft2(np.roll(pad, (-(kh // 2), -(kw // 2)), axis=(0, 1)))
+
+
+def _conv(x, ft):
+    """pkg/src/fepll/operators.py:196-197"""
+    return np.fft.ifft2(np.fft.fft2(x) * ft).real
+
+
+def ata_diag(A):
+    """pkg/src/fepll/operators.py:102-111"""
+    if A.kind == "identity":
+        return np.ones(A.input_dims)
+    if A.kind == "mask":
+        return np.asarray(A.pixel_map, dtype=np.float64)
+    return np.square(A.pixel_map)
+
+
+class Op:
+    """Forward/adjoint/normal maps of pkg/src/fepll/operators.py:200-235,
+    with the kernel DFT cached."""
+
+    def __init__(self, A):
+        self.A = A
+        self.ft = kernel_ft(A) if A.kind in ("convolution", "decimate") else None
+
+    def apply(self, x):
+        A = self.A
+        if A.kind == "identity":
+            return x.copy()
+        if A.kind == "convolution":
+            return _conv(x, self.ft)
+        if A.kind in ("mask", "gain"):
+            return A.pixel_map * x
+        return _conv(x, self.ft)[::A.factor, ::A.factor].copy()
+
+    def adjoint(self, y):
+        A = self.A
+        if A.kind == "identity":
+            return y.copy()
+        if A.kind == "convolution":
+            return _conv(y, np.conj(self.ft))
+        if A.kind in ("mask", "gain"):
+            return A.pixel_map * y
+        up = np.zeros(A.input_dims)
+        up[::A.factor, ::A.factor] = y
+        return _conv(up, np.conj(self.ft))
+
+    def normal(self, x):
+        return self.adjoint(self.apply(x))
+
+
+def cg(op, rhs, x0, tol, maxit):
+    """pkg/src/fepll/operators.py:242-266 -> (x, converged, iterations, residual)."""
+    rn = float(np.linalg.norm(rhs))
+    if rn == 0.0:
+        return np.zeros_like(rhs), True, 0, 0.0
+    x = x0.copy()
+    r = rhs - op(x)
+    p = r.copy()
+    rs = float(np.vdot(r, r))
+    it = 0
+    for it in range(1, maxit + 1):
+        if math.sqrt(rs) / rn <= tol:
+            it -= 1
+            break
+        Ap = op(p)
+        a = rs / float(np.vdot(p, Ap))
+        x += a * p
+        r -= a * Ap
+        rs2 = float(np.vdot(r, r))
+        p = r + (rs2 / rs) * p
+        rs = rs2
+    res = float(np.linalg.norm(rhs - op(x))) / rn
+    return x, res <= tol, it, res
+
+
+def solve_image(op, y, xt, bs2, tol=1e-6, maxit=200, aty=None):
+    """pkg/src/fepll/operators.py:273-295 -> (x, converged, residual)."""
+    A = op.A
+    aty = op.adjoint(y) if aty is None else aty
+    rhs = aty + bs2 * xt
+    if A.kind in ("identity", "mask", "gain"):
+        return rhs / (ata_diag(A) + bs2), True, 0.0
+    if A.kind == "convolution":
+        den = np.abs(op.ft) ** 2 + bs2
+        return np.fft.ifft2(np.fft.fft2(rhs) / den).real, True, 0.0
+    x, conv, _, res = cg(lambda v: op.normal(v) + bs2 * v, rhs, xt.copy(), tol, maxit)
+    return x, conv, res
+
+
+def power_l2sq(op, iterations=800, tol=1e-9):
+    """pkg/src/fepll/operators.py:298-319"""
+    v = np.random.default_rng(0).standard_normal(op.A.input_dims)
+    v /= np.linalg.norm(v)
+    prev = lam = 0.0
+    for _ in range(iterations):
+        w = op.normal(v)
+        lam = float(np.vdot(v, w))
+        nrm = float(np.linalg.norm(w))
+        if nrm == 0.0:
+            return 0.0
+        v = w / nrm
+        if prev > 0 and abs(lam - prev) <= tol * abs(lam):
+            break
+        prev = lam
+    return lam
+
+
+def frob_ata(op):
+    """pkg/src/fepll/operators.py:322-339"""
+    A = op.A
+    H, W = A.input_dims
+    if A.kind == "identity":
+        return float(H * W)
+    if A.kind in ("mask", "gain"):
+        return float(np.sum(ata_diag(A) ** 2))
+    if A.kind == "convolution":
+        return float(np.sum(np.abs(op.ft) ** 4))
+    d = A.factor
+    auto = np.fft.ifft2(np.abs(op.ft) ** 2).real
+    return float((H * W) / d ** 2 * np.sum(auto[::d, ::d] ** 2))
+
+
+def lambda_param(op, sigma):
+    """pkg/src/fepll/operators.py:342-355"""
+    H, W = op.A.input_dims
+    return min(frob_ata(op) / (H * W * power_l2sq(op)), 250.0 * sigma * sigma)
+
+
+def laplacian_symbol(dims):
+    """pkg/src/fepll/operators.py:358-365"""
+    H, W = dims
+    return (4.0 - 2.0 * np.cos(2 * np.pi * np.fft.fftfreq(H))[:, None]
+            - 2.0 * np.cos(2 * np.pi * np.fft.fftfreq(W))[None, :])
+
+
+def laplacian(x):
+    """pkg/src/fepll/operators.py:368-371"""
+    return (4.0 * x - np.roll(x, 1, 0) - np.roll(x, -1, 0) - np.roll(x, 1, 1) - np.roll(x, -1, 1))
+
+
+def init_estimate(op, y, sigma, lam, tol=1e-6, maxit=200):
+    """pkg/src/fepll/operators.py:374-394"""
+    A = op.A
+    c = 0.2 * sigma * sigma / lam
+    if A.kind in ("identity", "convolution"):
+        ft = op.ft if A.kind == "convolution" else np.ones(A.input_dims)
+        den = np.abs(ft) ** 2 + c * laplacian_symbol(A.input_dims)
+        if den.flat[0] == 0.0:
+            den.flat[0] = 1.0
+        return np.fft.ifft2(np.conj(ft) * np.fft.fft2(y) / den).real
+    aty = op.adjoint(y)
+    x, _, _, _ = cg(lambda v: op.normal(v) + c * laplacian(v), aty, aty.copy(), tol, maxit)
+    return x
+
+
+# ---------------------------------------------------------------- the loop
+@dataclass
+class OracleStats:
+    lam: float = 0.0
+    betas: list = field(default_factory=list)
+    patches: list = field(default_factory=list)
+    evals: list = field(default_factory=list)
+    sel_mults: list = field(default_factory=list)
+    est_mults: list = field(default_factory=list)
+    converged: list = field(default_factory=list)
+    residual: list = field(default_factory=list)
+    trace: list = field(default_factory=list)
+    seconds: float = 0.0
+
+
+def restore(y, A, model, tree=None, sigma=20.0, iterations=5, mults=(1.0, 4.0, 8.0, 16.0, 32.0),
+            spacing=6, sampling="jittered", use_tree=True, seed=0, tol=1e-6, maxit=200,
+            lam=None, trace=False, workers=1):
+    """pkg/src/fepll/solver.py:161-274 (HQS loop).  ``lam`` may be supplied
+    to skip the power iteration (the benchmark's setup exclusion,
+    BASELINE.md section 3)."""
+    t0 = time.perf_counter()
+    y = np.asarray(y, dtype=np.float64)
+    P = model.patch_dim
+    side = math.isqrt(P)
+    H, W = A.input_dims
+    op = Op(A)
+    sig = max(sigma, 0.5) / 255.0
+    if lam is None:
+        lam = lambda_param(op, sig)
+    betas = np.asarray(mults[:iterations], dtype=np.float64) * lam / (sig * sig)
+    st = OracleStats(lam=lam, betas=[float(b) for b in betas])
+    x = y.copy() if A.kind == "identity" else init_estimate(op, y, sig, lam, tol, maxit)
+    aty = op.adjoint(y)
+    if use_tree:
+        tcomps, kids, leaf = bfs(tree)
+    pool = ThreadPoolExecutor(workers) if workers > 1 else None
+    try:
+        for t, beta in enumerate(betas):
+            pos = (jittered_grid(H, W, P, spacing, seed, t) if sampling == "jittered"
+                   else regular_grid(H, W, P, spacing))
+            Z, dc = extract(x, pos, side)
+            mctx = Ctx(model.components, beta)
+            if use_tree:
+                tctx = Ctx(tcomps, beta)
+                work = lambda sl: tree_select(kids, leaf, tctx, Z[sl], P)
+            else:
+                def work(sl):
+                    ks = select_exhaustive(mctx, Z[sl])
+                    per = sum(score_cost(r, P) for r in mctx.rank) + P
+                    m = Z[sl].shape[0]
+                    return ks, np.full(m, len(mctx.U)), np.full(m, per)
+            slices = [slice(i, min(i + CHUNK, Z.shape[0])) for i in range(0, Z.shape[0], CHUNK)]
+            res = list(pool.map(work, slices)) if pool else [work(s) for s in slices]
+            ks = np.concatenate([r[0] for r in res])
+            est = np.empty_like(Z)
+            em = 0
+            for k in np.unique(ks):
+                m = ks == k
+                est[m] = mctx.wiener(int(k), Z[m])
+                em += int(m.sum()) * wiener_cost(mctx.rank[int(k)], P)
+            xt = reproject(est, dc, pos, side, H, W)
+            x, conv, resid = solve_image(op, y, xt, float(beta) * sig * sig, tol, maxit, aty)
+            if not np.isfinite(x).all():
+                raise FloatingPointError(f"non-finite image estimate at iteration {t}")
+            st.patches.append(int(Z.shape[0]))
+            st.evals.append(int(sum(int(r[1].sum()) for r in res)))
+            st.sel_mults.append(int(sum(int(r[2].sum()) for r in res)))
+            st.est_mults.append(em)
+            st.converged.append(bool(conv))
+            st.residual.append(float(resid))
+            if trace:
+                st.trace.append({"beta": float(beta), "positions": pos, "patches": Z, "dc": dc,
+                                 "selected": ks, "estimates": est, "x_tilde": xt, "x": x.copy()})
+    finally:
+        if pool:
+            pool.shutdown()
+    st.seconds = time.perf_counter() - t0
+    return x, st
+
+
+def host_threads():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
