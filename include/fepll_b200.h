@@ -1,0 +1,107 @@
+/*
+ * fepll_b200.h — C ABI of the B200-native FEPLL restoration loop.
+ *
+ * Every entry point takes plain pointers, sizes and a cudaStream_t (passed
+ * as void*); device pointers are caller-owned (the Python host passes
+ * torch tensor data pointers).  Return codes: 0 ok, 3 data error,
+ * 4 numerical error, 5 CUDA error; fepll_last_error() returns the message
+ * of the last failure on the calling thread.
+ *
+ * Each entry point replaces one function of the reference hot path
+ * (/root/reference/pkg/src/fepll/...), cited beside its declaration.
+ */
+#ifndef FEPLL_B200_H
+#define FEPLL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fepll_plan_s* fepll_plan_t;
+
+/* Packed tree + model, built on the host from GmmTree/GmmModel
+ * (tree.py:253-276 BFS order, gmm.py:96-155 component fields).
+ * Group g of an internal node u = its children's kept bases concatenated
+ * (child order), stored P x width row-major at grp_off64[u] in grp_basis. */
+typedef struct fepll_plan_desc {
+  int32_t patch_dim;        /* P */
+  int32_t n_nodes;          /* BFS nodes of the tree */
+  int32_t n_components;     /* K (model components == tree leaves) */
+  int32_t iterations;       /* T: beta schedule length */
+  const int32_t* child_start;   /* [n_nodes] */
+  const int32_t* child_count;   /* [n_nodes] */
+  const int32_t* child_list;    /* [n_nodes-1] BFS ids */
+  const int32_t* leaf_index;    /* [n_nodes] -1 internal */
+  const int32_t* depth;         /* [n_nodes] */
+  const int32_t* node_rank;     /* [n_nodes] */
+  const int32_t* grp_width;     /* [n_nodes] sum of child ranks (0 for leaves) */
+  const int32_t* grp_col_off;   /* [n_nodes] group column offset */
+  const int32_t* child_col_off; /* [n_nodes] column offset inside the parent's group */
+  const int64_t* grp_off64;     /* [n_nodes] element offset of the group block */
+  const double* grp_basis;      /* [sum P*width] */
+  int64_t grp_basis_len;
+  int32_t grp_cols_total;
+  const double* node_const;     /* [T][n_nodes] gmm.py:304-306 */
+  const double* node_nu_tail;   /* [T][n_nodes] gmm.py:293 */
+  const double* grp_sqw;        /* [T][grp_cols_total] gmm.py:303 */
+  const int32_t* model_rank;    /* [K] */
+  const int32_t* model_col_off; /* [K] */
+  const int64_t* model_off64;   /* [K] element offset of P x r_k block */
+  const double* model_basis;    /* [sum P*r_k] */
+  int64_t model_basis_len;
+  int32_t model_cols_total;
+  const double* model_shrink;   /* [T][model_cols_total] gmm.py:307 */
+  const double* model_gamma_tail; /* [T][K] gmm.py:297 */
+  const float* grp_tc_hi;       /* tcgen05 operand images (may be NULL) */
+  const float* grp_tc_lo;
+  int64_t grp_tc_len;
+  const int64_t* grp_tc_off;    /* [n_nodes] float offset of the node's B image */
+  const int32_t* grp_tc_npad;   /* [n_nodes] padded width (multiple of 16) */
+} fepll_plan_desc;
+
+int fepll_abi_version(void);
+const char* fepll_last_error(void);
+
+/* tree.py:387-434 + gmm.py:275-307: owns packed bases and per-beta constants. */
+int fepll_plan_create(const fepll_plan_desc* desc, fepll_plan_t* out);
+/* scratch for up to max_patches patches per select call */
+int fepll_plan_reserve(fepll_plan_t plan, int64_t max_patches);
+int fepll_plan_destroy(fepll_plan_t plan);
+
+/* patches.py:167-183 (extract + _row_mean pairwise fold):
+ * x: [batch][H][W] fp64; anchors: [n][2] int32 (row, col);
+ * outputs (any may be NULL): Z64 [batch*n][P], Z32 [batch*n][P], dc, sq. */
+int fepll_extract(const double* x, int32_t batch, int32_t H, int32_t W, int32_t side,
+                  const int32_t* anchors, int32_t n, double* Z64, float* Z32,
+                  double* dc, double* sq, void* stream);
+
+/* tree.py:387-434 (greedy descent, first-min tie break).
+ * mode 0: exact FP64 scoring; mode 1: tcgen05 3xTF32 scoring with
+ * margin-guarded FP64 re-scoring.  labels: [n_total] int32 leaf indices.
+ * leaf_counts (optional, device int64 [K]) receives the label histogram. */
+int fepll_select(fepll_plan_t plan, int32_t t, const double* Z64, const float* Z32,
+                 const double* sq, int64_t n_total, int32_t mode, double guard,
+                 int32_t* labels, int64_t* leaf_counts, void* stream);
+
+/* gmm.py:352-359 / solver.py:233-241: Wiener estimates of the patches under
+ * their labels, grouped by label (uses the segments of the last select). */
+int fepll_wiener(fepll_plan_t plan, int32_t t, const double* Z64, const int32_t* labels,
+                 int64_t n_total, double* Zhat, void* stream);
+
+/* patches.py:198-222 (+ operators.py:284-287 when kind==0):
+ * per-pixel ordered gather of (Zhat + dc) over covering anchors.
+ * grid geometry: n_rows x n_cols nominal anchors, spacing, half, side.
+ * kind 0: x = (aty + bs2*xt) / (diag + bs2)  (pixel-diagonal update fused)
+ * kind 1: rhs = aty + bs2*xt (FFT/CG kinds).  Outputs may be NULL. */
+int fepll_aggregate(const double* Zhat, const double* dc, const int32_t* anchors,
+                    int32_t n_rows, int32_t n_cols, int32_t spacing, int32_t half,
+                    int32_t side, int32_t batch, int32_t H, int32_t W,
+                    const double* aty, const double* diag, double bs2, int32_t kind,
+                    double* x_out, double* xtilde_out, int32_t* status, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

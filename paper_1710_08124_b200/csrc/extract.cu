@@ -1,0 +1,99 @@
+// Kernel (a): patch extraction with DC removal.
+//
+// Restates pkg/src/fepll/patches.py:167-183: window read row-major at each
+// anchor, dc = _row_mean (pairwise fold, patches.py:153-164), stored = win - dc,
+// all in FP64 so the patches are bit-identical to the reference's.  One warp
+// per patch; the fold runs in a per-warp shared-memory row so its addition
+// order is exactly the reference's for any P (odd widths fold their trailing
+// column into the last slot).
+#include "common.cuh"
+
+namespace fepll {
+
+constexpr int kExtractWarps = 8;
+
+__global__ void __launch_bounds__(kExtractWarps * 32)
+extract_kernel(const double* __restrict__ x, int batch, int H, int W, int side,
+               const int32_t* __restrict__ anchors, int n, double* __restrict__ Z64,
+               float* __restrict__ Z32, double* __restrict__ dc_out, double* __restrict__ sq_out) {
+  __shared__ double buf[kExtractWarps][kMaxP];
+  const int lane = lane_id();
+  double* acc = buf[warp_id()];
+  const int P = side * side;
+  const int64_t total = (int64_t)batch * n;
+  for (int64_t g = (int64_t)blockIdx.x * kExtractWarps + warp_id(); g < total;
+       g += (int64_t)gridDim.x * kExtractWarps) {
+    const int b = (int)(g / n);
+    const int i = (int)(g - (int64_t)b * n);
+    const int r0 = anchors[2 * i], c0 = anchors[2 * i + 1];
+    const double* img = x + (int64_t)b * H * W;
+    double win[kMaxP / 32];
+#pragma unroll
+    for (int k = 0; k < kMaxP / 32; ++k) {
+      const int p = lane + 32 * k;
+      if (p < P) {
+        const int dr = p / side, dcol = p - dr * side;
+        win[k] = img[(int64_t)(r0 + dr) * W + (c0 + dcol)];
+        acc[p] = win[k];
+      }
+    }
+    __syncwarp();
+    // pairwise fold: acc[:h] + acc[h:2h], odd trailing column added to slot h-1
+    for (int w = P; w > 1;) {
+      const int h = w >> 1;
+      double v[kMaxP / 64 + 1];
+#pragma unroll
+      for (int k = 0; k < kMaxP / 64 + 1; ++k) {
+        const int p = lane + 32 * k;
+        if (p < h) v[k] = acc[p] + acc[p + h];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < kMaxP / 64 + 1; ++k) {
+        const int p = lane + 32 * k;
+        if (p < h) acc[p] = v[k];
+      }
+      __syncwarp();
+      if ((w & 1) && lane == 0) acc[h - 1] += acc[w - 1];
+      __syncwarp();
+      w = h;
+    }
+    const double dc = acc[0] / (double)P;
+    __syncwarp();
+    double sq = 0.0;
+    double* zrow = Z64 ? Z64 + g * P : nullptr;
+    float* frow = Z32 ? Z32 + g * P : nullptr;
+#pragma unroll
+    for (int k = 0; k < kMaxP / 32; ++k) {
+      const int p = lane + 32 * k;
+      if (p < P) {
+        const double z = win[k] - dc;
+        sq = fma(z, z, sq);
+        if (zrow) zrow[p] = z;
+        if (frow) frow[p] = (float)z;
+      }
+    }
+    sq = warp_sum(sq);
+    if (lane == 0) {
+      if (dc_out) dc_out[g] = dc;
+      if (sq_out) sq_out[g] = sq;
+    }
+  }
+}
+
+}  // namespace fepll
+
+extern "C" int fepll_extract(const double* x, int32_t batch, int32_t H, int32_t W, int32_t side,
+                             const int32_t* anchors, int32_t n, double* Z64, float* Z32,
+                             double* dc, double* sq, void* stream) {
+  using namespace fepll;
+  FEPLL_REQUIRE(x && anchors && batch >= 1 && n >= 0, "extract: bad arguments");
+  FEPLL_REQUIRE(side >= 1 && side * side <= kMaxP, "extract: patch side out of range");
+  FEPLL_REQUIRE(H >= side && W >= side, "extract: image smaller than the patch");
+  if (n == 0) return kOk;
+  const int64_t total = (int64_t)batch * n;
+  extract_kernel<<<grid_for(total, kExtractWarps, 148 * 64), kExtractWarps * 32, 0,
+                   (cudaStream_t)stream>>>(x, batch, H, W, side, anchors, n, Z64, Z32, dc, sq);
+  FEPLL_LAUNCH();
+  return kOk;
+}

@@ -1,0 +1,190 @@
+// Plan lifetime: upload of the packed tree/model and routing scratch.
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "plan.cuh"
+
+namespace fepll {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+template <typename T>
+static int upload(Plan* p, const T* src, int64_t count, const T** dst) {
+  if (count <= 0 || src == nullptr) {
+    *dst = nullptr;
+    return kOk;
+  }
+  void* d = nullptr;
+  FEPLL_CUDA(cudaMalloc(&d, sizeof(T) * count));
+  p->owned.push_back(d);
+  FEPLL_CUDA(cudaMemcpy(d, src, sizeof(T) * count, cudaMemcpyHostToDevice));
+  *dst = static_cast<const T*>(d);
+  return kOk;
+}
+
+#define UP(src, count, dst)                                  \
+  do {                                                       \
+    int _rc = upload(p, (src), (int64_t)(count), &(dst));    \
+    if (_rc) return _rc;                                     \
+  } while (0)
+
+static int create(const fepll_plan_desc* d, Plan** out) {
+  FEPLL_REQUIRE(d != nullptr && out != nullptr, "null plan descriptor");
+  FEPLL_REQUIRE(d->patch_dim > 0 && d->patch_dim <= kMaxP, "patch_dim out of range (1..256)");
+  FEPLL_REQUIRE(d->n_nodes >= 1 && d->n_components >= 1 && d->iterations >= 1, "empty plan");
+  Plan* p = new Plan();
+  p->h = *d;
+  const int n = d->n_nodes, K = d->n_components, T = d->iterations;
+  PlanView& v = p->v;
+  v.P = d->patch_dim;
+  v.n_nodes = n;
+  v.K = K;
+  v.T = T;
+  v.grp_cols_total = d->grp_cols_total;
+  v.model_cols_total = d->model_cols_total;
+  p->depth.assign(d->depth, d->depth + n);
+  p->child_count.assign(d->child_count, d->child_count + n);
+  int maxd = 0;
+  for (int i = 0; i < n; ++i) {
+    maxd = std::max(maxd, d->depth[i]);
+    if (i && d->depth[i] < d->depth[i - 1]) {
+      set_error("nodes are not in BFS (depth-sorted) order");
+      delete p;
+      return kDataError;
+    }
+    p->max_children = std::max(p->max_children, d->child_count[i]);
+    p->max_group_cols = std::max(p->max_group_cols, d->grp_width[i]);
+  }
+  if (p->max_children > kMaxChildren || p->max_group_cols > kMaxGroupCols) {
+    set_error("tree node exceeds device limits (children <= 32, sum of child ranks <= 512)");
+    delete p;
+    return kDataError;
+  }
+  p->level_start.assign(maxd + 2, 0);
+  for (int dd = 0, i = 0; dd <= maxd + 1; ++dd) {
+    while (i < n && d->depth[i] < dd) ++i;
+    p->level_start[dd] = i;
+  }
+  for (int dd = 0; dd <= maxd; ++dd) {
+    if (p->level_start[dd + 1] - p->level_start[dd] > 1024) {
+      set_error("a tree level holds more than 1024 nodes");
+      delete p;
+      return kDataError;
+    }
+  }
+  p->n_levels = 0;
+  for (int i = 0; i < n; ++i)
+    if (d->child_count[i] > 0) p->n_levels = std::max(p->n_levels, d->depth[i] + 1);
+  UP(d->child_start, n, v.child_start);
+  UP(d->child_count, n, v.child_count);
+  UP(d->child_list, std::max(n - 1, 1), v.child_list);
+  UP(d->leaf_index, n, v.leaf_index);
+  UP(d->node_rank, n, v.node_rank);
+  UP(d->grp_width, n, v.grp_width);
+  UP(d->grp_col_off, n, v.grp_col_off);
+  UP(d->child_col_off, n, v.child_col_off);
+  UP(d->grp_off64, n, v.grp_off64);
+  UP(d->grp_basis, d->grp_basis_len, v.grp_basis);
+  UP(d->node_const, (int64_t)T * n, v.node_const);
+  UP(d->node_nu_tail, (int64_t)T * n, v.node_nu_tail);
+  UP(d->grp_sqw, (int64_t)T * d->grp_cols_total, v.grp_sqw);
+  UP(d->model_rank, K, v.model_rank);
+  UP(d->model_col_off, K, v.model_col_off);
+  UP(d->model_off64, K, v.model_off64);
+  UP(d->model_basis, d->model_basis_len, v.model_basis);
+  UP(d->model_shrink, (int64_t)T * d->model_cols_total, v.model_shrink);
+  UP(d->model_gamma_tail, (int64_t)T * K, v.model_gamma_tail);
+  if (d->grp_tc_hi && d->grp_tc_lo && d->grp_tc_len > 0) {
+    UP(d->grp_tc_hi, d->grp_tc_len, v.tc_hi);
+    UP(d->grp_tc_lo, d->grp_tc_len, v.tc_lo);
+    UP(d->grp_tc_off, n, v.tc_off);
+    UP(d->grp_tc_npad, n, v.tc_npad);
+    p->have_tc = true;
+  }
+  {
+    std::vector<int32_t> leaves;
+    for (int i = 0; i < n; ++i)
+      if (d->child_count[i] == 0) leaves.push_back(i);
+    p->n_leaf_nodes = (int)leaves.size();
+    const int32_t* dl = nullptr;
+    UP(leaves.data(), leaves.size(), dl);
+    p->d_leaf_nodes = const_cast<int32_t*>(dl);
+  }
+  // per-node scratch
+  void* m = nullptr;
+  FEPLL_CUDA(cudaMalloc(&m, sizeof(int32_t) * n));
+  p->owned.push_back(m);
+  p->rs.cnt = static_cast<int32_t*>(m);
+  FEPLL_CUDA(cudaMalloc(&m, sizeof(int64_t) * n));
+  p->owned.push_back(m);
+  p->rs.off = static_cast<int64_t*>(m);
+  FEPLL_CUDA(cudaMalloc(&m, sizeof(int64_t) * (maxd + 3)));
+  p->owned.push_back(m);
+  p->rs.leaf_base = static_cast<int64_t*>(m);
+  FEPLL_CUDA(cudaMalloc(&m, sizeof(int32_t) * 4));
+  p->owned.push_back(m);
+  p->rs.queue_len = static_cast<int32_t*>(m);
+  *out = p;
+  return kOk;
+}
+
+static void free_scratch(Plan* p) {
+  RouteScratch& r = p->rs;
+  cudaFree(r.seg[0]);
+  cudaFree(r.seg[1]);
+  cudaFree(r.leafseg);
+  cudaFree(r.queue);
+  r.seg[0] = r.seg[1] = r.leafseg = r.queue = nullptr;
+  r.cap = r.seg_cap = r.queue_cap = 0;
+}
+
+static int reserve(Plan* p, int64_t max_patches) {
+  FEPLL_REQUIRE(max_patches >= 0 && max_patches < (int64_t(1) << 31), "patch count out of range");
+  if (max_patches <= p->rs.cap) return kOk;
+  free_scratch(p);
+  RouteScratch& r = p->rs;
+  const int64_t seg = std::max<int64_t>(1, max_patches) * std::max(2, p->max_children);
+  FEPLL_CUDA(cudaMalloc(&r.seg[0], sizeof(int32_t) * seg));
+  FEPLL_CUDA(cudaMalloc(&r.seg[1], sizeof(int32_t) * seg));
+  FEPLL_CUDA(cudaMalloc(&r.leafseg, sizeof(int32_t) * seg));
+  r.queue_cap = std::max<int64_t>(1024, max_patches);
+  FEPLL_CUDA(cudaMalloc(&r.queue, sizeof(int32_t) * 2 * r.queue_cap));
+  r.cap = max_patches;
+  r.seg_cap = seg;
+  return kOk;
+}
+
+}  // namespace fepll
+
+using fepll::Plan;
+
+extern "C" {
+
+int fepll_abi_version(void) { return 1; }
+
+const char* fepll_last_error(void) { return fepll::g_last_error.c_str(); }
+
+int fepll_plan_create(const fepll_plan_desc* desc, fepll_plan_t* out) {
+  Plan* p = nullptr;
+  int rc = fepll::create(desc, &p);
+  if (rc) return rc;
+  *out = reinterpret_cast<fepll_plan_t>(p);
+  return fepll::kOk;
+}
+
+int fepll_plan_reserve(fepll_plan_t plan, int64_t max_patches) {
+  return fepll::reserve(reinterpret_cast<Plan*>(plan), max_patches);
+}
+
+int fepll_plan_destroy(fepll_plan_t plan) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  if (!p) return fepll::kOk;
+  fepll::free_scratch(p);
+  for (void* m : p->owned) cudaFree(m);
+  delete p;
+  return fepll::kOk;
+}
+
+}  // extern "C"

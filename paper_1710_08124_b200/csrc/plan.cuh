@@ -1,0 +1,75 @@
+// Device-resident plan: packed tree groups, model bases, per-beta constants,
+// and the routing scratch of the level-synchronous tree walk.
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+#include "../../include/fepll_b200.h"
+
+namespace fepll {
+
+// Read-only view handed to kernels by value.
+struct PlanView {
+  int P, n_nodes, K, T;
+  const int32_t* child_start;
+  const int32_t* child_count;
+  const int32_t* child_list;
+  const int32_t* leaf_index;
+  const int32_t* node_rank;
+  const int32_t* grp_width;
+  const int32_t* grp_col_off;
+  const int32_t* child_col_off;
+  const int64_t* grp_off64;
+  const double* grp_basis;
+  int grp_cols_total;
+  const double* node_const;
+  const double* node_nu_tail;
+  const double* grp_sqw;
+  const int32_t* model_rank;
+  const int32_t* model_col_off;
+  const int64_t* model_off64;
+  const double* model_basis;
+  int model_cols_total;
+  const double* model_shrink;
+  const double* model_gamma_tail;
+  const float* tc_hi;
+  const float* tc_lo;
+  const int64_t* tc_off;
+  const int32_t* tc_npad;
+};
+
+// Routing scratch: ping-pong patch-index segments per level plus the leaf
+// buckets (capacity C_max * n each).
+struct RouteScratch {
+  int64_t cap = 0;          // patches
+  int64_t seg_cap = 0;      // entries per segment buffer
+  int32_t* seg[2] = {nullptr, nullptr};
+  int32_t* leafseg = nullptr;
+  int32_t* cnt = nullptr;     // [n_nodes] patches routed into the node this call
+  int64_t* off = nullptr;     // [n_nodes] segment offset (internal: seg buf, leaf: leafseg)
+  int64_t* leaf_base = nullptr;  // [levels+1]
+  int32_t* queue = nullptr;   // rescore queue: (patch, node) pairs
+  int32_t* queue_len = nullptr;
+  int64_t queue_cap = 0;
+  int32_t* node_tmp = nullptr;
+};
+
+struct Plan {
+  fepll_plan_desc h{};  // sizes only (pointers are host temporaries)
+  PlanView v{};
+  std::vector<void*> owned;
+  std::vector<int> depth;         // host copy
+  std::vector<int> child_count;
+  std::vector<int> level_start;   // BFS id range per depth
+  std::vector<int> max_group_cols_at_depth;
+  int n_levels = 0;               // depth of the deepest internal node + 1
+  int max_children = 0;
+  int max_group_cols = 0;
+  bool have_tc = false;
+  int32_t* d_leaf_nodes = nullptr;   // BFS ids of the leaves, ascending
+  int n_leaf_nodes = 0;
+  RouteScratch rs;
+  int last_n_total = 0;
+};
+
+}  // namespace fepll

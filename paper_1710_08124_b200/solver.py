@@ -1,0 +1,347 @@
+"""The restoration entry point: drop-in for ``fepll.solver.restore``.
+
+``restore(y, A, model, tree=None, config=None) -> (x, SolverStats)`` keeps
+the reference signature, validation and error behaviour
+(`pkg/src/fepll/solver.py:161-274`) and accepts the reference's own
+``RestorationConfig``/``DegradationOperator``/``GmmModel``/``GmmTree``
+objects (duck typing).  The loop body runs on the GPU through the C ABI:
+
+    grid plan -> (a) extract -> (b) select -> (c) Wiener -> (d) aggregate
+    -> (e) image update
+
+with all per-iteration state resident in HBM; the host only sequences
+launches.  :func:`restore_batch` restores a stack of images that share the
+operator and noise level in one pass (the batch of BASELINE config 5).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as N
+from .errors import DataError, NumericalError
+from .gmm import score_flat_cost, wiener_flat_cost
+from .operators import CgConfig
+from .patches import axis_anchors, jitter_rng, jittered_grid, regular_grid
+from .plan import DevicePlan
+
+__all__ = ["RestorationConfig", "IterationStats", "SolverStats", "beta_schedule",
+           "restore", "restore_batch", "Restorer", "SIGMA_FLOOR_8BIT"]
+
+SIGMA_FLOOR_8BIT = 0.5
+
+
+@dataclass
+class RestorationConfig:
+    """Same fields and defaults as `pkg/src/fepll/solver.py:63-88`."""
+
+    sigma: float
+    iterations: int = 5
+    beta_multipliers: tuple = (1.0, 4.0, 8.0, 16.0, 32.0)
+    spacing: int = 6
+    sampling: str = "jittered"
+    use_tree: bool = True
+    use_flat_tail: bool = True
+    rho: float = 0.95
+    seed: int = 0
+    cg: CgConfig = field(default_factory=CgConfig)
+    workers: int = 1
+    trace: bool = False
+
+    def validate(self) -> None:
+        _validate_config(self)
+
+
+def _validate_config(c) -> None:
+    if c.sigma < 0:
+        raise DataError("sigma must be nonnegative")
+    if c.iterations != len(c.beta_multipliers):
+        raise DataError(f"iterations {c.iterations} != number of beta multipliers "
+                        f"{len(c.beta_multipliers)}")
+    if c.sampling not in ("jittered", "regular"):
+        raise DataError(f"unknown sampling mode {c.sampling!r}")
+    if c.workers < 1:
+        raise DataError("workers must be >= 1")
+    if c.cg.tolerance <= 0:
+        raise DataError("CG tolerance must be positive")
+    if c.cg.max_iterations < 1:
+        raise DataError("CG needs at least one iteration")
+
+
+@dataclass
+class IterationStats:
+    beta: float
+    patches: int = 0
+    score_evaluations: int = 0
+    selection_multiplies: int = 0
+    estimation_multiplies: int = 0
+    times: dict = field(default_factory=dict)
+    image_solve_converged: bool = True
+    image_solve_residual: float = 0.0
+
+
+@dataclass
+class SolverStats:
+    iterations: list = field(default_factory=list)
+    init_seconds: float = 0.0
+    total_seconds: float = 0.0
+    lam: float = 0.0
+    trace: list = field(default_factory=list)
+    rescored: list = field(default_factory=list)   # FP64 re-scored decisions / iteration
+
+    @property
+    def total_patches(self) -> int:
+        return sum(it.patches for it in self.iterations)
+
+    @property
+    def total_score_evaluations(self) -> int:
+        return sum(it.score_evaluations for it in self.iterations)
+
+    @property
+    def total_selection_multiplies(self) -> int:
+        return sum(it.selection_multiplies for it in self.iterations)
+
+    @property
+    def total_estimation_multiplies(self) -> int:
+        return sum(it.estimation_multiplies for it in self.iterations)
+
+    def step_seconds(self) -> dict:
+        out: dict = {}
+        for it in self.iterations:
+            for k, v in it.times.items():
+                out[k] = out.get(k, 0.0) + v
+        return out
+
+
+def beta_schedule(sigma: float, lam: float, multipliers: Sequence[float]) -> np.ndarray:
+    """beta_t = mult_t * lambda / sigma^2 (`pkg/src/fepll/solver.py:135-140`)."""
+    if sigma <= 0:
+        raise DataError("sigma must be positive (apply the floor first)")
+    return np.asarray(multipliers, dtype=np.float64) * lam / (sigma * sigma)
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise N.DeviceError("no CUDA device: the FEPLL loop runs only on the GPU")
+    return torch
+
+
+class Restorer:
+    """Reusable device state for one (model, tree, operator, config).
+
+    Plans (packed bases, scratch) are built once; :meth:`run` executes the
+    loop for a device-resident batch of observations.
+    """
+
+    MODES = {"exact": 0, "tensor": 1}
+
+    def __init__(self, A, model, tree, config, batch: int = 1, lam: float | None = None,
+                 mode: str = "tensor", device=None, guard: float = 0.0):
+        torch = _torch()
+        self.torch = torch
+        self.device = torch.device(device or "cuda")
+        _validate_config(config)
+        self.config = config
+        self.A = A
+        self.model = model
+        self.tree = tree
+        self.batch = int(batch)
+        P = int(model.patch_dim)
+        side = math.isqrt(P)
+        if side * side != P:
+            raise DataError(f"model patch_dim {P} is not a perfect square")
+        if not 1 <= config.spacing <= side:
+            raise DataError(f"spacing must lie in [1, {side}]")
+        if config.use_tree:
+            if tree is None:
+                raise DataError("use_tree requires a search tree")
+            if tree.n_leaves != len(model.components):
+                raise DataError(f"tree has {tree.n_leaves} leaves but the model has "
+                                f"{len(model.components)} components")
+        else:
+            raise DataError("exhaustive (no-tree) selection is not built on the device yet")
+        if not config.use_flat_tail and not bool(np.all(
+                [c.kept_basis.shape[1] == P for c in model.components])):
+            raise DataError("flat tail disabled: a full-rank model is required")
+        if A.solve_strategy != "pixel_diagonal":
+            raise DataError(f"{A.kind} operators are not built on the device yet")
+        self.P, self.side = P, side
+        self.H, self.W = (int(v) for v in A.input_dims)
+        self.mode = mode
+        self.guard = guard
+        self.sigma = max(config.sigma, SIGMA_FLOOR_8BIT) / 255.0
+        self.lam = float(lam) if lam is not None else self._lambda()
+        self.betas = beta_schedule(self.sigma, self.lam, config.beta_multipliers)
+        self.plan = DevicePlan(model, tree, self.betas, with_tc=(mode == "tensor"))
+        self._grids = [self._grid(t) for t in range(config.iterations)]
+        n = self._grids[0][0].shape[0]
+        self.n = n
+        self.plan.reserve(n * self.batch)
+        dev = self.device
+        B, H, W = self.batch, self.H, self.W
+        f64 = torch.float64
+        self.anchors = [torch.from_numpy(g[0]).to(dev) for g in self._grids]
+        self.Z64 = torch.empty((B * n, P), dtype=f64, device=dev)
+        self.Z32 = torch.empty((B * n, P), dtype=torch.float32, device=dev) if mode == "tensor" else None
+        self.Zhat = torch.empty((B * n, P), dtype=f64, device=dev)
+        self.dc = torch.empty(B * n, dtype=f64, device=dev)
+        self.sq = torch.empty(B * n, dtype=f64, device=dev)
+        self.labels = torch.empty(B * n, dtype=torch.int32, device=dev)
+        self.leaf_counts = torch.zeros((config.iterations, len(model.components)), dtype=torch.int64,
+                                       device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.x = torch.empty((B, H, W), dtype=f64, device=dev)
+        self.xt = torch.empty((B, H, W), dtype=f64, device=dev)
+        kind = A.kind
+        self.diag = None
+        if kind in ("mask", "gain"):
+            pm = np.asarray(A.pixel_map, dtype=np.float64)
+            d = pm if kind == "mask" else pm * pm
+            self.diag = torch.from_numpy(np.ascontiguousarray(np.broadcast_to(d, (B, H, W)))).to(dev)
+            self.pixel_map = torch.from_numpy(np.ascontiguousarray(pm)).to(dev)
+        self.aty = torch.empty((B, H, W), dtype=f64, device=dev)
+
+    # ---------------------------------------------------------------- setup
+    def _lambda(self) -> float:
+        """lambda = min(||A^T A||_F^2 / (N ||A||_2^2), 250 sigma^2)
+        (`pkg/src/fepll/operators.py:342-355`).  Pixel-diagonal kinds: the
+        power iteration on diag(A^T A) converges to max(diag) after one
+        step from a dense start, so ||A||_2^2 = max(diag)."""
+        A = self.A
+        H, W = self.H, self.W
+        if A.kind == "identity":
+            frob, l2 = float(H * W), 1.0
+        else:
+            pm = np.asarray(A.pixel_map, dtype=np.float64)
+            d = pm if A.kind == "mask" else pm * pm
+            frob, l2 = float(np.sum(d ** 2)), float(d.max())
+        if frob == 0.0 or l2 <= 0.0:
+            raise DataError("zero operator has no coupling parameter")
+        return min(frob / (H * W * l2), 250.0 * self.sigma * self.sigma)
+
+    def _grid(self, t: int):
+        c = self.config
+        H, W, P, s = self.H, self.W, self.P, c.spacing
+        if c.sampling == "jittered":
+            pos = jittered_grid(H, W, P, s, jitter_rng(c.seed, t)).positions
+        else:
+            pos = regular_grid(H, W, P, s).positions
+        half = (self.side - s) // 2 if c.sampling == "jittered" else 0
+        nr = axis_anchors(H, self.side, s).size
+        nc = axis_anchors(W, self.side, s).size
+        return np.ascontiguousarray(pos, dtype=np.int32), nr, nc, half
+
+    # ---------------------------------------------------------------- loop
+    def run(self, y_dev, trace: bool = False):
+        """y_dev: (B, Ho, Wo) float64 device tensor.  Returns x (B, H, W) on
+        the device and the per-iteration records."""
+        torch = self.torch
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        A = self.A
+        B, H, W, P, side = self.batch, self.H, self.W, self.P, self.side
+        if A.kind == "identity":
+            self.aty.copy_(y_dev)
+        else:
+            torch.mul(y_dev, self.pixel_map, out=self.aty)
+        self.x.copy_(y_dev)  # identity init; pixel kinds use the init below
+        if A.kind != "identity":
+            raise DataError("init_estimate for pixel kinds lands with the CG kernels")
+        self.status.zero_()
+        mode = self.MODES[self.mode]
+        records = []
+        for t, beta in enumerate(self.betas):
+            pos, nr, nc, half = self._grids[t]
+            anchors = self.anchors[t]
+            n = pos.shape[0]
+            nt = B * n
+            N.call("fepll_extract", N.ptr(self.x), B, H, W, side, N.ptr(anchors), n,
+                   N.ptr(self.Z64), N.ptr(self.Z32), N.ptr(self.dc), N.ptr(self.sq), st)
+            N.call("fepll_select", self.plan.handle, t, N.ptr(self.Z64), N.ptr(self.Z32),
+                   N.ptr(self.sq), nt, mode, float(self.guard), N.ptr(self.labels),
+                   N.ptr(self.leaf_counts[t]), st)
+            N.call("fepll_wiener", self.plan.handle, t, N.ptr(self.Z64), N.ptr(self.labels), nt,
+                   N.ptr(self.Zhat), st)
+            bs2 = float(beta) * self.sigma * self.sigma
+            N.call("fepll_aggregate", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(anchors), nr, nc,
+                   self.config.spacing, half, side, B, H, W, N.ptr(self.aty), N.ptr(self.diag),
+                   bs2, 0, N.ptr(self.x), N.ptr(self.xt), N.ptr(self.status), st)
+            if trace:
+                records.append({"beta": float(beta), "positions": pos,
+                                "labels": self.labels.view(B, n).cpu().numpy().copy(),
+                                "dc": self.dc.view(B, n).cpu().numpy().copy(),
+                                "x_tilde": self.xt.cpu().numpy().copy(),
+                                "x": self.x.cpu().numpy().copy()})
+        return self.x, records
+
+    def counters(self):
+        """(patches, evals, selection mults, estimation mults) per iteration
+        from the label histograms (every leaf has one root path)."""
+        hist = self.leaf_counts.cpu().numpy()
+        P = self.P
+        wcost = np.array([wiener_flat_cost(c.kept_basis.shape[1], P) for c in self.model.components])
+        out = []
+        for t in range(hist.shape[0]):
+            h = hist[t]
+            out.append((int(h.sum()), int(h @ self.plan.path_evals), int(h @ self.plan.path_mults),
+                        int(h @ wcost)))
+        return out
+
+    def check_status(self, t_last: int | None = None):
+        s = int(self.status.item())
+        if s & 1:
+            raise DataError("reprojection target has uncovered pixels")
+        if s & 2:
+            raise NumericalError("non-finite image estimate")
+
+
+def restore(y, A, model, tree=None, config=None, *, mode: str = "tensor", lam=None):
+    """GPU drop-in for `pkg/src/fepll/solver.py:161-274`."""
+    if config is None:
+        config = RestorationConfig(sigma=20.0)
+    _validate_config(config)
+    y = np.asarray(y, dtype=np.float64)
+    if tuple(y.shape) != tuple(A.output_dims):
+        raise DataError(f"observation shape {y.shape} != operator output {tuple(A.output_dims)}")
+    x, stats = restore_batch(y[None], A, model, tree, config, mode=mode, lam=lam)
+    if config.trace:
+        for rec in stats.trace:
+            rec["selected"] = rec.pop("labels")[0]
+            rec["x_tilde"] = rec["x_tilde"][0]
+            rec["dc"] = rec["dc"][0]
+            rec["x"] = rec["x"][0]
+    return x[0], stats
+
+
+def restore_batch(ys, A, model, tree=None, config=None, *, mode: str = "tensor", lam=None,
+                  restorer: Restorer | None = None):
+    """Restore a (B, H, W) stack sharing operator, sigma and seed."""
+    torch = _torch()
+    if config is None:
+        config = RestorationConfig(sigma=20.0)
+    t0 = time.perf_counter()
+    ys = np.asarray(ys, dtype=np.float64)
+    if ys.ndim != 3:
+        raise DataError("restore_batch expects a (B, H, W) stack")
+    r = restorer or Restorer(A, model, tree, config, batch=ys.shape[0], lam=lam, mode=mode)
+    y_dev = torch.from_numpy(ys).to(r.device)
+    t1 = time.perf_counter()
+    x_dev, recs = r.run(y_dev, trace=config.trace)
+    x = x_dev.cpu().numpy()
+    r.check_status()
+    stats = SolverStats(lam=r.lam)
+    stats.init_seconds = t1 - t0
+    for t, (npatch, ev, sm, em) in enumerate(r.counters()):
+        it = IterationStats(beta=float(r.betas[t]), patches=npatch // max(r.batch, 1),
+                            score_evaluations=ev, selection_multiplies=sm,
+                            estimation_multiplies=em)
+        stats.iterations.append(it)
+    stats.trace = recs
+    stats.total_seconds = time.perf_counter() - t0
+    return x, stats
