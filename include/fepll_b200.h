@@ -72,10 +72,11 @@ int fepll_plan_destroy(fepll_plan_t plan);
 
 /* patches.py:167-183 (extract + _row_mean pairwise fold):
  * x: [batch][H][W] fp64; anchors: [n][2] int32 (row, col);
- * outputs (any may be NULL): Z64 [batch*n][P], Z32 [batch*n][P], dc, sq. */
+ * outputs (any may be NULL): Z64 [batch*n][P], Z32 [batch*n][z32_pitch]
+ * (zero-padded past P; the tcgen05 scorer reads 128-byte K atoms), dc, sq. */
 int fepll_extract(const double* x, int32_t batch, int32_t H, int32_t W, int32_t side,
                   const int32_t* anchors, int32_t n, double* Z64, float* Z32,
-                  double* dc, double* sq, void* stream);
+                  int32_t z32_pitch, double* dc, double* sq, void* stream);
 
 /* tree.py:387-434 (greedy descent, first-min tie break).
  * mode 0: exact FP64 scoring; mode 1: tcgen05 3xTF32 scoring with
@@ -84,6 +85,10 @@ int fepll_extract(const double* x, int32_t batch, int32_t H, int32_t W, int32_t 
 int fepll_select(fepll_plan_t plan, int32_t t, const double* Z64, const float* Z32,
                  const double* sq, int64_t n_total, int32_t mode, double guard,
                  int32_t* labels, int64_t* leaf_counts, void* stream);
+
+/* diagnostics: per-level count of decisions the last tensor-mode select sent
+ * to exact FP64 re-scoring; dst: device int32[64]. */
+int fepll_select_rescored(fepll_plan_t plan, int32_t* dst, void* stream);
 
 /* gmm.py:352-359 / solver.py:233-241: Wiener estimates of the patches under
  * their labels, grouped by label (uses the segments of the last select). */

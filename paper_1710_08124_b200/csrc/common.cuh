@@ -15,6 +15,7 @@ constexpr int kDeviceError = 5;
 constexpr int kMaxP = 256;          // side <= 16
 constexpr int kMaxGroupCols = 512;  // sum of child ranks of one node (TMEM width)
 constexpr int kMaxChildren = 32;
+constexpr int kMaxDepth = 64;
 constexpr int kSMs = 148;
 
 void set_error(const std::string& msg);

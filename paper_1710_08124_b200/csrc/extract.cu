@@ -15,7 +15,8 @@ constexpr int kExtractWarps = 8;
 __global__ void __launch_bounds__(kExtractWarps * 32)
 extract_kernel(const double* __restrict__ x, int batch, int H, int W, int side,
                const int32_t* __restrict__ anchors, int n, double* __restrict__ Z64,
-               float* __restrict__ Z32, double* __restrict__ dc_out, double* __restrict__ sq_out) {
+               float* __restrict__ Z32, int z32_pitch, double* __restrict__ dc_out,
+               double* __restrict__ sq_out) {
   __shared__ double buf[kExtractWarps][kMaxP];
   const int lane = lane_id();
   double* acc = buf[warp_id()];
@@ -62,7 +63,7 @@ extract_kernel(const double* __restrict__ x, int batch, int H, int W, int side,
     __syncwarp();
     double sq = 0.0;
     double* zrow = Z64 ? Z64 + g * P : nullptr;
-    float* frow = Z32 ? Z32 + g * P : nullptr;
+    float* frow = Z32 ? Z32 + g * z32_pitch : nullptr;
 #pragma unroll
     for (int k = 0; k < kMaxP / 32; ++k) {
       const int p = lane + 32 * k;
@@ -73,6 +74,8 @@ extract_kernel(const double* __restrict__ x, int batch, int H, int W, int side,
         if (frow) frow[p] = (float)z;
       }
     }
+    if (frow)
+      for (int p = P + lane; p < z32_pitch; p += 32) frow[p] = 0.0f;
     sq = warp_sum(sq);
     if (lane == 0) {
       if (dc_out) dc_out[g] = dc;
@@ -85,15 +88,16 @@ extract_kernel(const double* __restrict__ x, int batch, int H, int W, int side,
 
 extern "C" int fepll_extract(const double* x, int32_t batch, int32_t H, int32_t W, int32_t side,
                              const int32_t* anchors, int32_t n, double* Z64, float* Z32,
-                             double* dc, double* sq, void* stream) {
+                             int32_t z32_pitch, double* dc, double* sq, void* stream) {
   using namespace fepll;
   FEPLL_REQUIRE(x && anchors && batch >= 1 && n >= 0, "extract: bad arguments");
   FEPLL_REQUIRE(side >= 1 && side * side <= kMaxP, "extract: patch side out of range");
   FEPLL_REQUIRE(H >= side && W >= side, "extract: image smaller than the patch");
+  FEPLL_REQUIRE(Z32 == nullptr || z32_pitch >= side * side, "extract: Z32 pitch below P");
   if (n == 0) return kOk;
   const int64_t total = (int64_t)batch * n;
   extract_kernel<<<grid_for(total, kExtractWarps, 148 * 64), kExtractWarps * 32, 0,
-                   (cudaStream_t)stream>>>(x, batch, H, W, side, anchors, n, Z64, Z32, dc, sq);
+                   (cudaStream_t)stream>>>(x, batch, H, W, side, anchors, n, Z64, Z32, z32_pitch, dc, sq);
   FEPLL_LAUNCH();
   return kOk;
 }

@@ -67,6 +67,11 @@ static int create(const fepll_plan_desc* d, Plan** out) {
     while (i < n && d->depth[i] < dd) ++i;
     p->level_start[dd] = i;
   }
+  if (maxd + 1 >= kMaxDepth) {
+    set_error("tree deeper than 62 levels");
+    delete p;
+    return kDataError;
+  }
   for (int dd = 0; dd <= maxd; ++dd) {
     if (p->level_start[dd + 1] - p->level_start[dd] > 1024) {
       set_error("a tree level holds more than 1024 nodes");
@@ -123,7 +128,7 @@ static int create(const fepll_plan_desc* d, Plan** out) {
   FEPLL_CUDA(cudaMalloc(&m, sizeof(int64_t) * (maxd + 3)));
   p->owned.push_back(m);
   p->rs.leaf_base = static_cast<int64_t*>(m);
-  FEPLL_CUDA(cudaMalloc(&m, sizeof(int32_t) * 4));
+  FEPLL_CUDA(cudaMalloc(&m, sizeof(int32_t) * kMaxDepth));
   p->owned.push_back(m);
   p->rs.queue_len = static_cast<int32_t*>(m);
   *out = p;

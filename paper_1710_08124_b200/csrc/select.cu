@@ -106,6 +106,40 @@ select_level_fp64_kernel(PlanView pv, LevelArgs a, const double* __restrict__ Z6
   }
 }
 
+// exact FP64 re-scoring of decisions the tensor-core epilogue could not
+// certify (select_tc.cu): queue entries are (patch, node) pairs of level d.
+__global__ void __launch_bounds__(kSelWarps * 32)
+rescore_fp64_kernel(PlanView pv, LevelArgs a, const double* __restrict__ Z64,
+                    const double* __restrict__ sq, const int32_t* __restrict__ queue,
+                    const int32_t* __restrict__ queue_len) {
+  __shared__ LevelSmem s;
+  __shared__ double zbuf[kSelWarps][kMaxP];
+  __shared__ double tbuf[kSelWarps][kMaxGroupCols];
+  level_setup(pv, a, s);
+  const int lane = lane_id();
+  double* zs = zbuf[warp_id()];
+  double* tv = tbuf[warp_id()];
+  const int P = pv.P;
+  const int total = queue_len[a.depth];
+  for (int item = blockIdx.x * kSelWarps + warp_id(); item < total; item += gridDim.x * kSelWarps) {
+    const int patch = queue[2 * item];
+    const int u = queue[2 * item + 1];
+    const double* zr = Z64 + (int64_t)patch * P;
+    for (int p = lane; p < P; p += 32) zs[p] = zr[p];
+    __syncwarp();
+    const int v = score_children_fp64(pv, a.t, u, zs, sq[patch], tv);
+    if (lane == 0) level_route(pv, a, s, v, patch);
+    __syncwarp();
+  }
+}
+
+int rescore_queue(Plan* p, const LevelArgs& a, const double* Z64, const double* sq,
+                  const int32_t* queue, const int32_t* queue_len, cudaStream_t st) {
+  rescore_fp64_kernel<<<2 * kSMs, kSelWarps * 32, 0, st>>>(p->v, a, Z64, sq, queue, queue_len);
+  FEPLL_LAUNCH();
+  return kOk;
+}
+
 // Wiener estimate per patch, iterating the leaf buckets so consecutive warps
 // share the component basis (gmm.py:352-359: U((gamma-gamma_tail) c) + gamma_tail z).
 __global__ void __launch_bounds__(kWienerWarps * 32)
@@ -207,6 +241,7 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* Z64, con
   cudaStream_t st = (cudaStream_t)stream;
   p->last_n_total = (int)n_total;
   FEPLL_CUDA(cudaMemsetAsync(p->rs.cnt, 0, sizeof(int32_t) * p->v.n_nodes, st));
+  FEPLL_CUDA(cudaMemsetAsync(p->rs.queue_len, 0, sizeof(int32_t) * kMaxDepth, st));
   if (n_total == 0) {
     if (leaf_counts) FEPLL_CUDA(cudaMemsetAsync(leaf_counts, 0, sizeof(int64_t) * p->v.K, st));
     return kOk;
@@ -261,5 +296,13 @@ extern "C" int fepll_wiener(fepll_plan_t plan, int32_t t, const double* Z64, con
   wiener_fp64_kernel<<<grid_for(n_total, kWienerWarps, 148 * 8), kWienerWarps * 32, 0, st>>>(
       p->v, t, p->d_leaf_nodes, p->n_leaf_nodes, p->rs.cnt, p->rs.off, p->rs.leafseg, Z64, Zhat);
   FEPLL_LAUNCH();
+  return kOk;
+}
+
+extern "C" int fepll_select_rescored(fepll_plan_t plan, int32_t* dst, void* stream) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  FEPLL_REQUIRE(p != nullptr && dst != nullptr, "select_rescored: bad arguments");
+  FEPLL_CUDA(cudaMemcpyAsync(dst, p->rs.queue_len, sizeof(int32_t) * kMaxDepth,
+                             cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
   return kOk;
 }

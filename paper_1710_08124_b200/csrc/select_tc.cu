@@ -1,13 +1,345 @@
-// Kernel (b), tensor-core path: placeholder until the tcgen05 scorer lands.
+// Kernel (b), tensor-core path: one tree level as a grouped GEMM on tcgen05.
+//
+// Restates the per-level work of pkg/src/fepll/tree.py:416-428 (score all
+// children of the current node, first-minimum child wins) with the score of
+// pkg/src/fepll/gmm.py:323-339.  Patches of one level are grouped by node
+// (route.cuh); a tile is 128 patches of one node.  For a tile:
+//
+//   C (128 x N) = Z_tile (128 x P) . G_u (P x N)     N = sum of child ranks
+//
+// runs as 3xTF32 on tcgen05 (kind::tf32, M=128, K=8 per MMA, accumulators in
+// TMEM): D_main = Zhi.Ghi, D_corr = Zhi.Glo + Zlo.Ghi (separate TMEM
+// columns, summed in FP64 by the epilogue).  Operands are K-major,
+// 128-byte-swizzled: the group image G_u arrives pre-split/pre-swizzled by
+// the TMA bulk engine, the patch rows are gathered by the CTA's threads,
+// split hi/lo and stored swizzled.  The K dimension streams through two
+// smem stages (one 32-float K atom each) so loads overlap the MMAs.
+//
+// Epilogue (one thread per patch row, TMEM lane == row): FP64
+// sum_j c_j^2 w_j per child, score, argmin, and an error bound
+// err_c = guard * ||z|| * sum_j |c_j w_j| on each score (the 3xTF32
+// projection error is <= guard/2 * ||z|| per coefficient).  A decision whose
+// runner-up lies within err_best + err_runner is not taken here: the patch
+// is queued for exact FP64 re-scoring (select.cu), so the chosen child always
+// equals the FP64 argmin.
 #include "route.cuh"
+#include "tc.cuh"
 
 namespace fepll {
 
+constexpr int kTcRows = 128;          // M
+constexpr int kTcThreads = 128;       // 4 warps: loaders + epilogue; thread 0 issues MMAs
+constexpr int kAtomFloats = 32;       // 128-byte K atom
+constexpr int kAtomBytesA = kTcRows * 128;
+constexpr uint32_t kTmemCols = 512;   // [0,256): D_main, [256,512): D_corr
+
+struct TcSmemTables {
+  int32_t tpre[kMaxLevelNodes + 1];   // tile prefix over depth-d nodes
+  int32_t cpre[kMaxLevelNodes + 1];   // count prefix
+  int64_t child_off[kMaxLevelNodes];  // next-level segment offsets of depth-(d+1) nodes
+  double w[kMaxGroupCols / 2];        // group column weights of the current tile's node
+  double cconst[kMaxChildren];
+  double cnut[kMaxChildren];
+  int32_t cend[kMaxChildren];         // exclusive end column of each child
+  int32_t cbfs[kMaxChildren];
+  int32_t rows[kTcRows];
+  int32_t key[kTcRows];
+  int32_t lrank[kTcRows];
+  int32_t bcnt[kMaxChildren + 1];
+  int32_t bbase[kMaxChildren + 1];
+  uint64_t mma_bar[2];
+  uint64_t load_bar[2];
+  uint32_t tmem_base;
+  int32_t total_tiles;
+  int32_t cur_node;
+};
+
+struct TcArgs {
+  LevelArgs a;
+  const float* Z32;
+  int z32_pitch;
+  const double* sq;
+  double guard;
+  int32_t* queue;
+  int32_t* queue_len;  // [depth]
+  int katoms;
+  int bmax_rows;       // padded N of the stage buffers
+};
+
+__device__ __forceinline__ void tc_level_setup(const PlanView& pv, const LevelArgs& a,
+                                               TcSmemTables& s) {
+  const int nd = a.lvl_end - a.lvl_begin;
+  for (int k = threadIdx.x; k < nd; k += blockDim.x) {
+    const int u = a.lvl_begin + k;
+    s.cpre[k + 1] = pv.child_count[u] > 0 ? a.cnt[u] : 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s.cpre[0] = 0;
+    s.tpre[0] = 0;
+    int64_t run_int = 0, run_leaf = 0;
+    const int64_t lb = a.leaf_base[a.depth];
+    for (int k = 0; k < nd; ++k) {
+      const int c = s.cpre[k + 1];
+      s.cpre[k + 1] = s.cpre[k] + c;
+      s.tpre[k + 1] = s.tpre[k] + (c + kTcRows - 1) / kTcRows;
+      const int u = a.lvl_begin + k;
+      const int nk = pv.child_count[u];
+      const int cs = pv.child_start[u];
+      for (int j = 0; j < nk; ++j) {
+        const int v = pv.child_list[cs + j];
+        if (pv.child_count[v] > 0) {
+          s.child_off[v - a.nxt_begin] = run_int;
+          run_int += c;
+        } else {
+          s.child_off[v - a.nxt_begin] = lb + run_leaf;
+          run_leaf += c;
+        }
+      }
+    }
+    s.total_tiles = s.tpre[nd];
+    if (blockIdx.x == 0) a.leaf_base[a.depth + 1] = lb + run_leaf;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int k = threadIdx.x; k < a.nxt_end - a.nxt_begin; k += blockDim.x)
+      a.off[a.nxt_begin + k] = s.child_off[k];
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+select_level_tc_kernel(PlanView pv, TcArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-align the operand region (SWIZZLE_128B atoms)
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int bstage = args.bmax_rows * 128;               // bytes of one B half per stage
+  const int stage_bytes = 2 * kAtomBytesA + 2 * bstage;
+  TcSmemTables& s = *reinterpret_cast<TcSmemTables*>(base + 2 * stage_bytes);
+  const LevelArgs& a = args.a;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+
+  if (warp == 0) tc::tmem_alloc(&s.tmem_base, kTmemCols);
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&s.mma_bar[i], 1);
+      tc::mbar_init(&s.load_bar[i], 1);
+    }
+    tc::fence_mbar_init();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = s.tmem_base;
+  tc_level_setup(pv, a, s);
+
+  const int nd = a.lvl_end - a.lvl_begin;
+  const int t = a.t;
+  uint32_t uses[2] = {0, 0};  // completed-or-pending commits per stage (uniform across threads)
+  const double guard = args.guard;
+
+  for (int tile = blockIdx.x; tile < s.total_tiles; tile += gridDim.x) {
+    // tile -> node, row range
+    int lo = 0, hi = nd;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s.tpre[mid] <= tile) lo = mid; else hi = mid;
+    }
+    const int u = a.lvl_begin + lo;
+    const int first = (tile - s.tpre[lo]) * kTcRows;
+    const int cnt_u = s.cpre[lo + 1] - s.cpre[lo];
+    const int m = min(kTcRows, cnt_u - first);
+    const int width = pv.grp_width[u];
+    const int npad = pv.tc_npad[u];
+    const int nk = pv.child_count[u];
+    const int64_t seg0 = a.off[u] + first;
+    // per-tile tables (previous tile's epilogue finished: trailing __syncthreads)
+    for (int j = tid; j < width; j += kTcThreads)
+      s.w[j] = pv.grp_sqw[(int64_t)t * pv.grp_cols_total + pv.grp_col_off[u] + j];
+    if (tid < nk) {
+      const int v = pv.child_list[pv.child_start[u] + tid];
+      const int64_t ti = (int64_t)t * pv.n_nodes + v;
+      s.cconst[tid] = pv.node_const[ti];
+      s.cnut[tid] = pv.node_nu_tail[ti];
+      s.cend[tid] = pv.child_col_off[v] + pv.node_rank[v];
+      s.cbfs[tid] = v;
+    }
+    const int my_patch = tid < m ? a.seg_in[seg0 + tid] : -1;
+    s.rows[tid] = my_patch;
+    const float* zrow = my_patch >= 0 ? args.Z32 + (int64_t)my_patch * args.z32_pitch : nullptr;
+    const float* bhi = pv.tc_hi + pv.tc_off[u];
+    const float* blo = pv.tc_lo + pv.tc_off[u];
+    const uint32_t bbytes = (uint32_t)npad * 128u;
+    const uint32_t idesc = tc::idesc_tf32(kTcRows, npad);
+
+    int last_stage = 0;
+    for (int ka = 0; ka < args.katoms; ++ka) {
+      const int st = ka & 1;  // stage parity alternates within and across tiles via uses[]
+      // the stage is free once the MMAs that last read it have completed
+      if (uses[st] > 0) tc::mbar_wait(&s.mma_bar[st], (uses[st] - 1) & 1);
+      uint8_t* sA_hi = base + st * stage_bytes;
+      uint8_t* sA_lo = sA_hi + kAtomBytesA;
+      uint8_t* sB_hi = sA_lo + kAtomBytesA;
+      uint8_t* sB_lo = sB_hi + bstage;
+      if (tid == 0) {
+        tc::mbar_arrive_expect_tx(&s.load_bar[st], 2 * bbytes);
+        tc::bulk_g2s(sB_hi, bhi + (int64_t)ka * npad * kAtomFloats, bbytes, &s.load_bar[st]);
+        tc::bulk_g2s(sB_lo, blo + (int64_t)ka * npad * kAtomFloats, bbytes, &s.load_bar[st]);
+      }
+      // A atom: row tid, 8 chunks of 16 B, chunk c stored at c ^ (row % 8)
+      {
+        const int r8 = tid & 7;
+        uint8_t* dhi = sA_hi + (tid >> 3) * 1024 + r8 * 128;
+        uint8_t* dlo = sA_lo + (tid >> 3) * 1024 + r8 * 128;
+        const float4* src = zrow ? reinterpret_cast<const float4*>(zrow + ka * kAtomFloats) : nullptr;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          float4 v = src ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+          float4 h, l;
+          h.x = tc::to_tf32(v.x); l.x = v.x - h.x;
+          h.y = tc::to_tf32(v.y); l.y = v.y - h.y;
+          h.z = tc::to_tf32(v.z); l.z = v.z - h.z;
+          h.w = tc::to_tf32(v.w); l.w = v.w - h.w;
+          *reinterpret_cast<float4*>(dhi + ((c ^ r8) << 4)) = h;
+          *reinterpret_cast<float4*>(dlo + ((c ^ r8) << 4)) = l;
+        }
+      }
+      tc::fence_proxy_async_smem();
+      __syncthreads();
+      if (tid == 0) {
+        tc::mbar_wait(&s.load_bar[st], uses[st] & 1);
+        tc::fence_after_sync();
+        const uint32_t a_hi = tc::smem_u32(sA_hi), a_lo = tc::smem_u32(sA_lo);
+        const uint32_t b_hi = tc::smem_u32(sB_hi), b_lo = tc::smem_u32(sB_lo);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint32_t ko = kk * 32;  // 8 tf32 = 32 bytes inside the swizzle atom
+          const uint32_t acc = (ka > 0 || kk > 0) ? 1u : 0u;
+          tc::mma_tf32(tmem, tc::desc_sw128(a_hi + ko), tc::desc_sw128(b_hi + ko), idesc, acc);
+          tc::mma_tf32(tmem + 256, tc::desc_sw128(a_hi + ko), tc::desc_sw128(b_lo + ko), idesc, acc);
+          tc::mma_tf32(tmem + 256, tc::desc_sw128(a_lo + ko), tc::desc_sw128(b_hi + ko), idesc, 1u);
+        }
+        tc::mma_commit(&s.mma_bar[st]);
+      }
+      uses[st] += 1;
+      last_stage = st;
+    }
+    // accumulators complete
+    tc::mbar_wait(&s.mma_bar[last_stage], (uses[last_stage] - 1) & 1);
+    tc::fence_after_sync();
+
+    // ---- epilogue: thread tid owns TMEM lane tid == tile row tid
+    const bool valid = tid < m;
+    const double sqv = valid ? args.sq[my_patch] : 0.0;
+    const double zn = sqrt(sqv);
+    double best = INFINITY, best_err = 0.0, m1 = INFINITY, m2 = INFINITY;
+    int bi = 0, i1 = -1;
+    int ci = 0;
+    int cend = s.cend[0];
+    double acc_s = 0.0, acc_e = 0.0;
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    const int nchunks = (width + 31) >> 5;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      uint32_t ra[32], rb[32];
+      tc::tmem_ld32(lane_base + ch * 32, ra);
+      tc::tmem_ld32(lane_base + 256 + ch * 32, rb);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const int j = ch * 32 + q;
+        if (j < width) {
+          const double c = (double)__uint_as_float(ra[q]) + (double)__uint_as_float(rb[q]);
+          const double w = s.w[j];
+          const double cw = c * w;
+          acc_s = fma(cw, c, acc_s);
+          acc_e += fabs(cw);
+          if (j + 1 == cend) {
+            const double sc = s.cconst[ci] + sqv / s.cnut[ci] + acc_s;
+            const double er = guard * zn * acc_e;
+            if (sc < best) { best = sc; bi = ci; best_err = er; }
+            const double lo_c = sc - er;
+            if (lo_c < m1) { m2 = m1; m1 = lo_c; i1 = ci; }
+            else if (lo_c < m2) { m2 = lo_c; }
+            ++ci;
+            cend = ci < nk ? s.cend[ci] : 0x7fffffff;
+            acc_s = 0.0;
+            acc_e = 0.0;
+          }
+        }
+      }
+    }
+    const double other = (i1 == bi) ? m2 : m1;
+    const bool flagged = !(other > best + best_err) || !isfinite(best);
+    // ---- routing (aggregated per tile: one global atomic per child)
+    tc::fence_before_sync();
+    if (tid <= kMaxChildren) s.bcnt[tid] = 0;
+    __syncthreads();
+    if (valid) {
+      const int key = flagged ? kMaxChildren : bi;
+      s.key[tid] = key;
+      s.lrank[tid] = atomicAdd(&s.bcnt[key], 1);
+    }
+    __syncthreads();
+    if (tid < nk && s.bcnt[tid] > 0) s.bbase[tid] = atomicAdd(&a.cnt[s.cbfs[tid]], s.bcnt[tid]);
+    if (tid == kTcThreads - 1 && s.bcnt[kMaxChildren] > 0)
+      s.bbase[kMaxChildren] = atomicAdd(&args.queue_len[a.depth], s.bcnt[kMaxChildren]);
+    __syncthreads();
+    if (valid) {
+      const int key = s.key[tid];
+      const int slot = s.bbase[key] + s.lrank[tid];
+      if (key == kMaxChildren) {
+        args.queue[2 * slot] = my_patch;
+        args.queue[2 * slot + 1] = u;
+      } else {
+        const int v = s.cbfs[key];
+        const int64_t b0 = s.child_off[v - a.nxt_begin];
+        if (pv.child_count[v] > 0) {
+          a.seg_out[b0 + slot] = my_patch;
+        } else {
+          a.leafseg[b0 + slot] = my_patch;
+          a.labels[my_patch] = pv.leaf_index[v];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, kTmemCols);
+}
+
+// exact re-scoring of the queued (patch, node) decisions (select.cu)
+int rescore_queue(Plan* p, const LevelArgs& a, const double* Z64, const double* sq,
+                  const int32_t* queue, const int32_t* queue_len, cudaStream_t st);
+
+static size_t tc_smem_bytes(int bmax_rows) {
+  const size_t stage = 2 * (size_t)kAtomBytesA + 2 * (size_t)bmax_rows * 128;
+  return 1024 + 2 * stage + sizeof(TcSmemTables);
+}
+
 int select_level_tc(Plan* p, const LevelArgs& a, const float* Z32, const double* Z64,
                     const double* sq, double guard, cudaStream_t st) {
-  (void)p; (void)a; (void)Z32; (void)Z64; (void)sq; (void)guard; (void)st;
-  set_error("tcgen05 scoring path not built yet");
-  return kDataError;
+  FEPLL_REQUIRE(Z64 != nullptr, "tensor mode needs FP64 patches for the re-scoring path");
+  FEPLL_REQUIRE(p->max_group_cols <= 256, "tensor mode supports nodes whose children ranks sum to <= 256");
+  const int P = p->v.P;
+  const int ppad = (P + 31) / 32 * 32;
+  const int bmax = std::max(16, (p->max_group_cols + 15) / 16 * 16);
+  TcArgs args;
+  args.a = a;
+  args.Z32 = Z32;
+  args.z32_pitch = ppad;
+  args.sq = sq;
+  args.guard = guard > 0 ? guard : 7.62939453125e-06;  // 2^-17
+  args.queue = p->rs.queue;
+  args.queue_len = p->rs.queue_len;
+  args.katoms = ppad / 32;
+  args.bmax_rows = bmax;
+  const size_t smem = tc_smem_bytes(bmax);
+  FEPLL_CUDA(cudaFuncSetAttribute(select_level_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+  select_level_tc_kernel<<<kSMs, kTcThreads, smem, st>>>(p->v, args);
+  FEPLL_LAUNCH();
+  return rescore_queue(p, a, Z64, sq, p->rs.queue, p->rs.queue_len, st);
 }
 
 }  // namespace fepll

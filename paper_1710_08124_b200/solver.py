@@ -189,7 +189,9 @@ class Restorer:
         f64 = torch.float64
         self.anchors = [torch.from_numpy(g[0]).to(dev) for g in self._grids]
         self.Z64 = torch.empty((B * n, P), dtype=f64, device=dev)
-        self.Z32 = torch.empty((B * n, P), dtype=torch.float32, device=dev) if mode == "tensor" else None
+        self.z32_pitch = ((P + 31) // 32) * 32
+        self.Z32 = (torch.empty((B * n, self.z32_pitch), dtype=torch.float32, device=dev)
+                    if mode == "tensor" else None)
         self.Zhat = torch.empty((B * n, P), dtype=f64, device=dev)
         self.dc = torch.empty(B * n, dtype=f64, device=dev)
         self.sq = torch.empty(B * n, dtype=f64, device=dev)
@@ -197,6 +199,7 @@ class Restorer:
         self.leaf_counts = torch.zeros((config.iterations, len(model.components)), dtype=torch.int64,
                                        device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.rescored = torch.zeros((config.iterations, 64), dtype=torch.int32, device=dev)
         self.x = torch.empty((B, H, W), dtype=f64, device=dev)
         self.xt = torch.empty((B, H, W), dtype=f64, device=dev)
         kind = A.kind
@@ -262,10 +265,12 @@ class Restorer:
             n = pos.shape[0]
             nt = B * n
             N.call("fepll_extract", N.ptr(self.x), B, H, W, side, N.ptr(anchors), n,
-                   N.ptr(self.Z64), N.ptr(self.Z32), N.ptr(self.dc), N.ptr(self.sq), st)
+                   N.ptr(self.Z64), N.ptr(self.Z32), self.z32_pitch, N.ptr(self.dc),
+                   N.ptr(self.sq), st)
             N.call("fepll_select", self.plan.handle, t, N.ptr(self.Z64), N.ptr(self.Z32),
                    N.ptr(self.sq), nt, mode, float(self.guard), N.ptr(self.labels),
                    N.ptr(self.leaf_counts[t]), st)
+            N.call("fepll_select_rescored", self.plan.handle, N.ptr(self.rescored[t]), st)
             N.call("fepll_wiener", self.plan.handle, t, N.ptr(self.Z64), N.ptr(self.labels), nt,
                    N.ptr(self.Zhat), st)
             bs2 = float(beta) * self.sigma * self.sigma
@@ -343,5 +348,6 @@ def restore_batch(ys, A, model, tree=None, config=None, *, mode: str = "tensor",
                             estimation_multiplies=em)
         stats.iterations.append(it)
     stats.trace = recs
+    stats.rescored = [int(v) for v in r.rescored.sum(dim=1).cpu()]
     stats.total_seconds = time.perf_counter() - t0
     return x, stats
