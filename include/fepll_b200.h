@@ -62,6 +62,8 @@ typedef struct fepll_plan_desc {
 } fepll_plan_desc;
 
 int fepll_abi_version(void);
+/* number of kernels this library has launched in the process (bench evidence) */
+int64_t fepll_launch_count(void);
 const char* fepll_last_error(void);
 
 /* tree.py:387-434 + gmm.py:275-307: owns packed bases and per-beta constants. */

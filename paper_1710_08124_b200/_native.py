@@ -39,6 +39,7 @@ class PlanDesc(C.Structure):
 # name -> (restype, argtypes)
 _SIGS = {
     "fepll_abi_version": (i32, []),
+    "fepll_launch_count": (i64, []),
     "fepll_last_error": (C.c_char_p, []),
     "fepll_plan_create": (i32, [C.POINTER(PlanDesc), C.POINTER(vp)]),
     "fepll_plan_reserve": (i32, [vp, i64]),

@@ -19,6 +19,7 @@ constexpr int kMaxDepth = 64;
 constexpr int kSMs = 148;
 
 void set_error(const std::string& msg);
+void count_launch();
 
 #define FEPLL_CUDA(expr)                                                        \
   do {                                                                          \
@@ -31,6 +32,7 @@ void set_error(const std::string& msg);
 
 #define FEPLL_LAUNCH()                                                          \
   do {                                                                          \
+    ::fepll::count_launch();                                                    \
     cudaError_t _e = cudaGetLastError();                                        \
     if (_e != cudaSuccess) {                                                    \
       ::fepll::set_error(std::string("launch: ") + cudaGetErrorString(_e));     \

@@ -1,5 +1,6 @@
 // Plan lifetime: upload of the packed tree/model and routing scratch.
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <string>
 
@@ -8,7 +9,9 @@
 namespace fepll {
 
 static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
 void set_error(const std::string& msg) { g_last_error = msg; }
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 template <typename T>
 static int upload(Plan* p, const T* src, int64_t count, const T** dst) {
@@ -168,6 +171,8 @@ using fepll::Plan;
 extern "C" {
 
 int fepll_abi_version(void) { return 1; }
+
+int64_t fepll_launch_count(void) { return fepll::g_launches.load(); }
 
 const char* fepll_last_error(void) { return fepll::g_last_error.c_str(); }
 

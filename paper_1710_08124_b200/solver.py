@@ -242,48 +242,75 @@ class Restorer:
         return np.ascontiguousarray(pos, dtype=np.int32), nr, nc, half
 
     # ---------------------------------------------------------------- loop
-    def run(self, y_dev, trace: bool = False):
+    def run(self, y_dev, trace: bool = False, timer: dict | None = None):
         """y_dev: (B, Ho, Wo) float64 device tensor.  Returns x (B, H, W) on
-        the device and the per-iteration records."""
+        the device and the per-iteration records.  ``timer`` (optional dict)
+        collects CUDA-event pairs per phase for profiling."""
         torch = self.torch
         st = torch.cuda.current_stream(self.device).cuda_stream
         A = self.A
-        B, H, W, P, side = self.batch, self.H, self.W, self.P, self.side
         if A.kind == "identity":
             self.aty.copy_(y_dev)
+            self.x.copy_(y_dev)
         else:
             torch.mul(y_dev, self.pixel_map, out=self.aty)
-        self.x.copy_(y_dev)  # identity init; pixel kinds use the init below
-        if A.kind != "identity":
             raise DataError("init_estimate for pixel kinds lands with the CG kernels")
         self.status.zero_()
-        mode = self.MODES[self.mode]
         records = []
-        for t, beta in enumerate(self.betas):
-            pos, nr, nc, half = self._grids[t]
-            anchors = self.anchors[t]
-            n = pos.shape[0]
-            nt = B * n
-            N.call("fepll_extract", N.ptr(self.x), B, H, W, side, N.ptr(anchors), n,
-                   N.ptr(self.Z64), N.ptr(self.Z32), self.z32_pitch, N.ptr(self.dc),
-                   N.ptr(self.sq), st)
-            N.call("fepll_select", self.plan.handle, t, N.ptr(self.Z64), N.ptr(self.Z32),
-                   N.ptr(self.sq), nt, mode, float(self.guard), N.ptr(self.labels),
-                   N.ptr(self.leaf_counts[t]), st)
-            N.call("fepll_select_rescored", self.plan.handle, N.ptr(self.rescored[t]), st)
-            N.call("fepll_wiener", self.plan.handle, t, N.ptr(self.Z64), N.ptr(self.labels), nt,
-                   N.ptr(self.Zhat), st)
-            bs2 = float(beta) * self.sigma * self.sigma
-            N.call("fepll_aggregate", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(anchors), nr, nc,
-                   self.config.spacing, half, side, B, H, W, N.ptr(self.aty), N.ptr(self.diag),
-                   bs2, 0, N.ptr(self.x), N.ptr(self.xt), N.ptr(self.status), st)
+        for t in range(len(self.betas)):
+            self._iteration(t, st, timer)
             if trace:
-                records.append({"beta": float(beta), "positions": pos,
+                B, n = self.batch, self.n
+                records.append({"beta": float(self.betas[t]), "positions": self._grids[t][0],
                                 "labels": self.labels.view(B, n).cpu().numpy().copy(),
                                 "dc": self.dc.view(B, n).cpu().numpy().copy(),
                                 "x_tilde": self.xt.cpu().numpy().copy(),
                                 "x": self.x.cpu().numpy().copy()})
         return self.x, records
+
+    def _mark(self, timer, name):
+        if timer is None:
+            return
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record()
+        timer.setdefault("_marks", []).append((name, ev))
+
+    def _iteration(self, t: int, st, timer=None) -> None:
+        B, H, W, P, side = self.batch, self.H, self.W, self.P, self.side
+        pos, nr, nc, half = self._grids[t]
+        anchors = self.anchors[t]
+        n = pos.shape[0]
+        nt = B * n
+        mode = self.MODES[self.mode]
+        self._mark(timer, "start")
+        N.call("fepll_extract", N.ptr(self.x), B, H, W, side, N.ptr(anchors), n,
+               N.ptr(self.Z64), N.ptr(self.Z32), self.z32_pitch, N.ptr(self.dc),
+               N.ptr(self.sq), st)
+        self._mark(timer, "extract")
+        N.call("fepll_select", self.plan.handle, t, N.ptr(self.Z64), N.ptr(self.Z32),
+               N.ptr(self.sq), nt, mode, float(self.guard), N.ptr(self.labels),
+               N.ptr(self.leaf_counts[t]), st)
+        N.call("fepll_select_rescored", self.plan.handle, N.ptr(self.rescored[t]), st)
+        self._mark(timer, "select")
+        N.call("fepll_wiener", self.plan.handle, t, N.ptr(self.Z64), N.ptr(self.labels), nt,
+               N.ptr(self.Zhat), st)
+        self._mark(timer, "wiener")
+        bs2 = float(self.betas[t]) * self.sigma * self.sigma
+        N.call("fepll_aggregate", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(anchors), nr, nc,
+               self.config.spacing, half, side, B, H, W, N.ptr(self.aty), N.ptr(self.diag),
+               bs2, 0, N.ptr(self.x), N.ptr(self.xt), N.ptr(self.status), st)
+        self._mark(timer, "aggregate")
+
+    @staticmethod
+    def phase_times(timer: dict) -> dict:
+        """Sum of milliseconds per phase from the marks recorded by run()."""
+        out: dict = {}
+        marks = timer.get("_marks", [])
+        for (n0, e0), (n1, e1) in zip(marks, marks[1:]):
+            if n1 == "start":
+                continue
+            out[n1] = out.get(n1, 0.0) + e0.elapsed_time(e1)
+        return out
 
     def counters(self):
         """(patches, evals, selection mults, estimation mults) per iteration
