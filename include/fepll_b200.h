@@ -59,6 +59,10 @@ typedef struct fepll_plan_desc {
   int64_t grp_tc_len;
   const int64_t* grp_tc_off;    /* [n_nodes] float offset of the node's B image */
   const int32_t* grp_tc_npad;   /* [n_nodes] padded width (multiple of 16) */
+  const int32_t* grp_tc_child_col; /* [n_nodes] 16-aligned column of a child in its parent's image */
+  const float* grp_tc_w;        /* [T][grp_tc_w_cols] FP32 column weights (0 on padding) */
+  const int32_t* grp_tc_w_off;  /* [n_nodes] first weight column of a node's image */
+  int32_t grp_tc_w_cols;
 } fepll_plan_desc;
 
 int fepll_abi_version(void);
@@ -80,12 +84,17 @@ int fepll_extract(const double* x, int32_t batch, int32_t H, int32_t W, int32_t 
                   const int32_t* anchors, int32_t n, double* Z64, float* Z32,
                   int32_t z32_pitch, double* dc, double* sq, void* stream);
 
-/* tree.py:387-434 (greedy descent, first-min tie break).
+/* tree.py:387-434 (greedy descent, first-min tie break) over n_total =
+ * batch * n_img patches whose values are re-extracted from the FP64 images x
+ * ([batch][H][W]) at anchors ([n_img][2]) minus dc (patches.py:178).
  * mode 0: exact FP64 scoring; mode 1: tcgen05 3xTF32 scoring with
- * margin-guarded FP64 re-scoring.  labels: [n_total] int32 leaf indices.
- * leaf_counts (optional, device int64 [K]) receives the label histogram. */
-int fepll_select(fepll_plan_t plan, int32_t t, const double* Z64, const float* Z32,
-                 const double* sq, int64_t n_total, int32_t mode, double guard,
+ * margin-guarded FP64 re-scoring (needs Z32, the FP32 patch rows written by
+ * fepll_extract).  guard <= 0 selects the default bound 2^-16 (tc_epi.cuh).
+ * labels: [n_total] int32 leaf indices.  leaf_counts (optional, device
+ * int64 [K]) receives the label histogram. */
+int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32_t W,
+                 const int32_t* anchors, int32_t n_img, const double* dc, const double* sq,
+                 const float* Z32, int64_t n_total, int32_t mode, double guard,
                  int32_t* labels, int64_t* leaf_counts, void* stream);
 
 /* diagnostics: per-level count of decisions the last tensor-mode select sent
@@ -94,8 +103,9 @@ int fepll_select_rescored(fepll_plan_t plan, int32_t* dst, void* stream);
 
 /* gmm.py:352-359 / solver.py:233-241: Wiener estimates of the patches under
  * their labels, grouped by label (uses the segments of the last select). */
-int fepll_wiener(fepll_plan_t plan, int32_t t, const double* Z64, const int32_t* labels,
-                 int64_t n_total, double* Zhat, void* stream);
+int fepll_wiener(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32_t W,
+                 const int32_t* anchors, int32_t n_img, const double* dc, int64_t n_total,
+                 double* Zhat, void* stream);
 
 /* patches.py:198-222 (+ operators.py:284-287 when kind==0):
  * per-pixel ordered gather of (Zhat + dc) over covering anchors.

@@ -33,6 +33,8 @@ class PlanDesc(C.Structure):
         ("model_shrink", P_f64), ("model_gamma_tail", P_f64),
         ("grp_tc_hi", P_f32), ("grp_tc_lo", P_f32), ("grp_tc_len", i64),
         ("grp_tc_off", P_i64), ("grp_tc_npad", P_i32),
+        ("grp_tc_child_col", P_i32), ("grp_tc_w", P_f32), ("grp_tc_w_off", P_i32),
+        ("grp_tc_w_cols", i32),
     ]
 
 
@@ -45,8 +47,8 @@ _SIGS = {
     "fepll_plan_reserve": (i32, [vp, i64]),
     "fepll_plan_destroy": (i32, [vp]),
     "fepll_extract": (i32, [vp, i32, i32, i32, i32, vp, i32, vp, vp, i32, vp, vp, vp]),
-    "fepll_select": (i32, [vp, i32, vp, vp, vp, i64, i32, f64, vp, vp, vp]),
-    "fepll_wiener": (i32, [vp, i32, vp, vp, i64, vp, vp]),
+    "fepll_select": (i32, [vp, i32, vp, i32, i32, vp, i32, vp, vp, vp, i64, i32, f64, vp, vp, vp]),
+    "fepll_wiener": (i32, [vp, i32, vp, i32, i32, vp, i32, vp, i64, vp, vp]),
     "fepll_select_rescored": (i32, [vp, vp, vp]),
     "fepll_aggregate": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, vp, vp, f64,
                               i32, vp, vp, vp, vp]),

@@ -60,6 +60,7 @@ static int create(const fepll_plan_desc* d, Plan** out) {
     p->max_children = std::max(p->max_children, d->child_count[i]);
     p->max_group_cols = std::max(p->max_group_cols, d->grp_width[i]);
   }
+  for (int k = 0; k < K; ++k) p->max_model_rank = std::max(p->max_model_rank, d->model_rank[k]);
   if (p->max_children > kMaxChildren || p->max_group_cols > kMaxGroupCols) {
     set_error("tree node exceeds device limits (children <= 32, sum of child ranks <= 512)");
     delete p;
@@ -89,6 +90,12 @@ static int create(const fepll_plan_desc* d, Plan** out) {
   UP(d->child_count, n, v.child_count);
   UP(d->child_list, std::max(n - 1, 1), v.child_list);
   UP(d->leaf_index, n, v.leaf_index);
+  {
+    std::vector<int32_t> parent(n, 0);
+    for (int u = 0; u < n; ++u)
+      for (int j = 0; j < d->child_count[u]; ++j) parent[d->child_list[d->child_start[u] + j]] = u;
+    UP(parent.data(), n, v.parent);
+  }
   UP(d->node_rank, n, v.node_rank);
   UP(d->grp_width, n, v.grp_width);
   UP(d->grp_col_off, n, v.grp_col_off);
@@ -109,7 +116,12 @@ static int create(const fepll_plan_desc* d, Plan** out) {
     UP(d->grp_tc_lo, d->grp_tc_len, v.tc_lo);
     UP(d->grp_tc_off, n, v.tc_off);
     UP(d->grp_tc_npad, n, v.tc_npad);
+    UP(d->grp_tc_child_col, n, v.tc_child_col);
+    UP(d->grp_tc_w, (int64_t)T * d->grp_tc_w_cols, v.tc_w);
+    UP(d->grp_tc_w_off, n, v.tc_w_off);
+    v.tc_w_cols = d->grp_tc_w_cols;
     p->have_tc = true;
+    for (int i = 0; i < n; ++i) p->max_tc_npad = std::max(p->max_tc_npad, d->grp_tc_npad[i]);
   }
   {
     std::vector<int32_t> leaves;

@@ -14,6 +14,7 @@ struct PlanView {
   const int32_t* child_start;
   const int32_t* child_count;
   const int32_t* child_list;
+  const int32_t* parent;
   const int32_t* leaf_index;
   const int32_t* node_rank;
   const int32_t* grp_width;
@@ -36,6 +37,10 @@ struct PlanView {
   const float* tc_lo;
   const int64_t* tc_off;
   const int32_t* tc_npad;
+  const int32_t* tc_child_col;
+  const float* tc_w;
+  const int32_t* tc_w_off;
+  int tc_w_cols;
 };
 
 // Routing scratch: ping-pong patch-index segments per level plus the leaf
@@ -65,6 +70,8 @@ struct Plan {
   int n_levels = 0;               // depth of the deepest internal node + 1
   int max_children = 0;
   int max_group_cols = 0;
+  int max_model_rank = 0;
+  int max_tc_npad = 0;
   bool have_tc = false;
   int32_t* d_leaf_nodes = nullptr;   // BFS ids of the leaves, ascending
   int n_leaf_nodes = 0;

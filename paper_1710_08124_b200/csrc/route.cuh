@@ -6,9 +6,9 @@
 // child v is appended (atomic slot) to v's segment of the next level.
 // Segment capacity of a child = its parent's count, so the next level's
 // offsets are a prefix sum over the (at most a few hundred) nodes of the
-// level, recomputed redundantly by every CTA from the final counts — no
-// global scan pass.  Leaves get buckets in a separate buffer; their counts
-// are the label histogram used for Wiener grouping and the cost counters.
+// level, recomputed by every CTA from the final counts with a block scan —
+// no global scan pass.  Leaves get buckets in a separate buffer; their
+// counts are the label histogram used for Wiener grouping and the counters.
 #pragma once
 #include "plan.cuh"
 
@@ -30,66 +30,112 @@ struct LevelArgs {
   int t;
 };
 
-struct LevelSmem {
-  int64_t pre[kMaxLevelNodes + 1];   // prefix of counts over depth-d nodes
-  int64_t child_off[kMaxLevelNodes]; // offsets of depth-(d+1) nodes
-  int64_t total;
+struct LevelTables {
+  int32_t cpre[kMaxLevelNodes + 1];   // prefix of counts over depth-d internal nodes
+  int32_t tpre[kMaxLevelNodes + 1];   // prefix of tiles (rows_per_tile) over the same
+  int64_t child_off[kMaxLevelNodes];  // next-level segment offsets of depth-(d+1) nodes
+  uint64_t scan_tmp[256];
+  int32_t total_items;
+  int32_t total_tiles;
 };
 
-// Every CTA: prefix over depth-d counts and the next level's segment offsets.
-__device__ inline void level_setup(const PlanView& pv, const LevelArgs& a, LevelSmem& s) {
-  const int nd = a.lvl_end - a.lvl_begin;
-  for (int k = threadIdx.x; k < nd; k += blockDim.x) {
-    const int u = a.lvl_begin + k;
-    s.pre[k + 1] = pv.child_count[u] > 0 ? (int64_t)a.cnt[u] : 0;
-  }
+// in-place exclusive scan of data[0..n) (smem) by the first <=255 threads;
+// every thread of the block must call it.  Returns the total.
+template <typename T>
+__device__ __forceinline__ T block_exscan(T* data, int n, uint64_t* tmp) {
+  const int nt = min((int)blockDim.x, 255);
+  const bool act = (int)threadIdx.x < nt;
+  const int per = (n + nt - 1) / nt;
+  const int b = threadIdx.x * per, e = act ? min(n, b + per) : b;
+  T s = 0;
+  for (int i = b; i < e; ++i) s += data[i];
+  if (act) tmp[threadIdx.x] = (uint64_t)s;
   __syncthreads();
   if (threadIdx.x == 0) {
-    s.pre[0] = 0;
-    int64_t run_int = 0, run_leaf = 0;
-    const int64_t lb = a.leaf_base[a.depth];
-    for (int k = 0; k < nd; ++k) {
-      const int64_t c = s.pre[k + 1];
-      s.pre[k + 1] = s.pre[k] + c;
-      const int u = a.lvl_begin + k;
-      const int nk = pv.child_count[u];
-      const int cs = pv.child_start[u];
-      for (int j = 0; j < nk; ++j) {
-        const int v = pv.child_list[cs + j];
-        if (pv.child_count[v] > 0) {
-          s.child_off[v - a.nxt_begin] = run_int;
-          run_int += c;
-        } else {
-          s.child_off[v - a.nxt_begin] = lb + run_leaf;
-          run_leaf += c;
-        }
-      }
+    uint64_t run = 0;
+    for (int i = 0; i < nt; ++i) {
+      const uint64_t v = tmp[i];
+      tmp[i] = run;
+      run += v;
     }
-    s.total = s.pre[nd];
-    if (blockIdx.x == 0) a.leaf_base[a.depth + 1] = lb + run_leaf;
+    tmp[nt] = run;
   }
   __syncthreads();
-  if (blockIdx.x == 0) {
-    for (int k = threadIdx.x; k < a.nxt_end - a.nxt_begin; k += blockDim.x)
-      a.off[a.nxt_begin + k] = s.child_off[k];
+  if (act) {
+    T pre = (T)tmp[threadIdx.x];
+    for (int i = b; i < e; ++i) {
+      const T v = data[i];
+      data[i] = pre;
+      pre += v;
+    }
   }
+  const T total = (T)tmp[nt];
+  __syncthreads();
+  return total;
+}
+
+// Every CTA: count/tile prefixes of level d and the offsets of level d+1.
+__device__ inline void level_tables(const PlanView& pv, const LevelArgs& a, LevelTables& s,
+                                    int rows_per_tile) {
+  const int nd = a.lvl_end - a.lvl_begin;
+  const int nn = a.nxt_end - a.nxt_begin;
+  for (int k = threadIdx.x; k < nd; k += blockDim.x) {
+    const int u = a.lvl_begin + k;
+    const int c = pv.child_count[u] > 0 ? a.cnt[u] : 0;
+    s.cpre[k] = c;
+    s.tpre[k] = (c + rows_per_tile - 1) / rows_per_tile;
+  }
+  // packed (leaf capacity << 32 | internal capacity) per next-level node
+  uint64_t* cap = reinterpret_cast<uint64_t*>(s.child_off);
+  for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+    const int v = a.nxt_begin + k;
+    const uint64_t c = (uint64_t)(uint32_t)a.cnt[pv.parent[v]];
+    cap[k] = pv.child_count[v] > 0 ? c : (c << 32);
+  }
+  __syncthreads();
+  const int32_t items = block_exscan(s.cpre, nd, s.scan_tmp);
+  const int32_t tiles = block_exscan(s.tpre, nd, s.scan_tmp);
+  const uint64_t tot = block_exscan(cap, nn, s.scan_tmp);
+  const int64_t lb = a.leaf_base[a.depth];
+  for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+    const int v = a.nxt_begin + k;
+    const uint64_t pre = cap[k];
+    s.child_off[k] = pv.child_count[v] > 0 ? (int64_t)(pre & 0xffffffffull)
+                                           : lb + (int64_t)(pre >> 32);
+  }
+  if (threadIdx.x == 0) {
+    s.cpre[nd] = items;
+    s.tpre[nd] = tiles;
+    s.total_items = items;
+    s.total_tiles = tiles;
+    if (blockIdx.x == 0) a.leaf_base[a.depth + 1] = lb + (int64_t)(tot >> 32);
+  }
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int k = threadIdx.x; k < nn; k += blockDim.x) a.off[a.nxt_begin + k] = s.child_off[k];
+}
+
+// smallest k with pre[k+1] > x  (pre[0] = 0, pre[n] = total)
+__device__ __forceinline__ int prefix_find(const int32_t* pre, int n, int x) {
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (pre[mid] <= x) lo = mid; else hi = mid;
+  }
+  return lo;
 }
 
 // item -> (node, patch)
-__device__ inline void level_item(const LevelArgs& a, const LevelSmem& s, int64_t item,
-                                  int& u, int& patch) {
-  int lo = 0, hi = a.lvl_end - a.lvl_begin;  // pre[lo] <= item < pre[hi]
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (s.pre[mid] <= item) lo = mid; else hi = mid;
-  }
-  u = a.lvl_begin + lo;
-  patch = a.seg_in[a.off[u] + (item - s.pre[lo])];
+__device__ __forceinline__ void level_item(const LevelArgs& a, const LevelTables& s, int item,
+                                           int& u, int& patch) {
+  const int k = prefix_find(s.cpre, a.lvl_end - a.lvl_begin, item);
+  u = a.lvl_begin + k;
+  patch = a.seg_in[a.off[u] + (item - s.cpre[k])];
 }
 
 // append patch to child v's segment of the next level
-__device__ inline void level_route(const PlanView& pv, const LevelArgs& a, const LevelSmem& s,
-                                   int v, int patch) {
+__device__ __forceinline__ void level_route(const PlanView& pv, const LevelArgs& a,
+                                            const LevelTables& s, int v, int patch) {
   const int slot = atomicAdd(&a.cnt[v], 1);
   const int64_t base = s.child_off[v - a.nxt_begin];
   if (pv.child_count[v] > 0) {

@@ -1,5 +1,4 @@
-// Kernel (b) exact path + kernel (c): tree descent with FP64 scoring, and
-// the Wiener estimates grouped by leaf.
+// Kernel (b) exact path, the re-scoring kernel, and kernel (c) Wiener.
 //
 // Scoring restates pkg/src/fepll/gmm.py:323-339 for the children of the
 // patch's current node (pkg/src/fepll/tree.py:417-425):
@@ -7,18 +6,45 @@
 // with np.argmin's first-minimum tie-break over the stored child order.
 // The children of a node are packed as one "group" (P x sum of ranks), so
 // one warp computes every child's projection in a single pass over z.
+//
+// Patches are never materialized in FP64: every kernel re-extracts z from the
+// resident FP64 image as x[window] - dc — the exact operation of
+// pkg/src/fepll/patches.py:178 — so the FP64 paths see the reference's
+// patch values bit for bit.
+#include <algorithm>
+
 #include "route.cuh"
 
 namespace fepll {
 
-constexpr int kSelWarps = 4;   // level kernel (smem: level table + per-warp rows)
+constexpr int kSelWarps = 4;   // level/rescore kernels (smem: level table + per-warp rows)
 constexpr int kWienerWarps = 8;
 constexpr int kColsPerLane = kMaxGroupCols / 32;
 
+struct PatchSrc {
+  const double* x;        // [B][H][W]
+  const int32_t* anchors; // [n_img][2]
+  const double* dc;       // [B*n_img]
+  int n_img, H, W, side;
+};
+
+// warp: zs[0..P) = window(g) - dc[g]
+__device__ __forceinline__ void load_patch(const PatchSrc& ps, int g, int P, double* zs) {
+  const int b = g / ps.n_img;
+  const int ia = g - b * ps.n_img;
+  const int pr = ps.anchors[2 * ia], pc = ps.anchors[2 * ia + 1];
+  const double* src = ps.x + ((int64_t)b * ps.H + pr) * ps.W + pc;
+  const double d = ps.dc[g];
+  for (int p = lane_id(); p < P; p += 32) {
+    const int dr = p / ps.side;
+    zs[p] = src[(int64_t)dr * ps.W + (p - dr * ps.side)] - d;
+  }
+  __syncwarp();
+}
+
 // one warp: best child of node u for the patch in zs (smem); returns BFS id.
 __device__ __forceinline__ int score_children_fp64(const PlanView& pv, int t, int u,
-                                                   const double* zs, double sqv,
-                                                   double* tv) {
+                                                   const double* zs, double sqv, double* tv) {
   const int lane = lane_id();
   const int P = pv.P;
   const int width = pv.grp_width[u];
@@ -83,23 +109,19 @@ __global__ void route_init_kernel(int64_t n_total, int32_t* seg0, int32_t* cnt, 
 }
 
 __global__ void __launch_bounds__(kSelWarps * 32)
-select_level_fp64_kernel(PlanView pv, LevelArgs a, const double* __restrict__ Z64,
-                         const double* __restrict__ sq) {
-  __shared__ LevelSmem s;
+select_level_fp64_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restrict__ sq) {
+  __shared__ LevelTables s;
   __shared__ double zbuf[kSelWarps][kMaxP];
   __shared__ double tbuf[kSelWarps][kMaxGroupCols];
-  level_setup(pv, a, s);
+  level_tables(pv, a, s, 1);
   const int lane = lane_id();
   double* zs = zbuf[warp_id()];
   double* tv = tbuf[warp_id()];
-  const int P = pv.P;
-  for (int64_t item = (int64_t)blockIdx.x * kSelWarps + warp_id(); item < s.total;
-       item += (int64_t)gridDim.x * kSelWarps) {
+  for (int item = blockIdx.x * kSelWarps + warp_id(); item < s.total_items;
+       item += gridDim.x * kSelWarps) {
     int u, patch;
     level_item(a, s, item, u, patch);
-    const double* zr = Z64 + (int64_t)patch * P;
-    for (int p = lane; p < P; p += 32) zs[p] = zr[p];
-    __syncwarp();
+    load_patch(ps, patch, pv.P, zs);
     const int v = score_children_fp64(pv, a.t, u, zs, sq[patch], tv);
     if (lane == 0) level_route(pv, a, s, v, patch);
     __syncwarp();
@@ -107,46 +129,34 @@ select_level_fp64_kernel(PlanView pv, LevelArgs a, const double* __restrict__ Z6
 }
 
 // exact FP64 re-scoring of decisions the tensor-core epilogue could not
-// certify (select_tc.cu): queue entries are (patch, node) pairs of level d.
+// certify: queue entries are (patch, node) pairs of level d.
 __global__ void __launch_bounds__(kSelWarps * 32)
-rescore_fp64_kernel(PlanView pv, LevelArgs a, const double* __restrict__ Z64,
-                    const double* __restrict__ sq, const int32_t* __restrict__ queue,
-                    const int32_t* __restrict__ queue_len) {
-  __shared__ LevelSmem s;
+rescore_fp64_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restrict__ sq,
+                    const int32_t* __restrict__ queue, const int32_t* __restrict__ queue_len) {
+  __shared__ LevelTables s;
   __shared__ double zbuf[kSelWarps][kMaxP];
   __shared__ double tbuf[kSelWarps][kMaxGroupCols];
-  level_setup(pv, a, s);
+  level_tables(pv, a, s, 1);
   const int lane = lane_id();
   double* zs = zbuf[warp_id()];
   double* tv = tbuf[warp_id()];
-  const int P = pv.P;
   const int total = queue_len[a.depth];
   for (int item = blockIdx.x * kSelWarps + warp_id(); item < total; item += gridDim.x * kSelWarps) {
     const int patch = queue[2 * item];
     const int u = queue[2 * item + 1];
-    const double* zr = Z64 + (int64_t)patch * P;
-    for (int p = lane; p < P; p += 32) zs[p] = zr[p];
-    __syncwarp();
+    load_patch(ps, patch, pv.P, zs);
     const int v = score_children_fp64(pv, a.t, u, zs, sq[patch], tv);
     if (lane == 0) level_route(pv, a, s, v, patch);
     __syncwarp();
   }
 }
 
-int rescore_queue(Plan* p, const LevelArgs& a, const double* Z64, const double* sq,
-                  const int32_t* queue, const int32_t* queue_len, cudaStream_t st) {
-  rescore_fp64_kernel<<<2 * kSMs, kSelWarps * 32, 0, st>>>(p->v, a, Z64, sq, queue, queue_len);
-  FEPLL_LAUNCH();
-  return kOk;
-}
-
-// Wiener estimate per patch, iterating the leaf buckets so consecutive warps
-// share the component basis (gmm.py:352-359: U((gamma-gamma_tail) c) + gamma_tail z).
+// Wiener estimate per patch (fallback for large P / rank), iterating the leaf
+// buckets (gmm.py:352-359: U((gamma-gamma_tail) c) + gamma_tail z).
 __global__ void __launch_bounds__(kWienerWarps * 32)
 wiener_fp64_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, int n_leaf_nodes,
                    const int32_t* __restrict__ cnt, const int64_t* __restrict__ off,
-                   const int32_t* __restrict__ leafseg, const double* __restrict__ Z64,
-                   double* __restrict__ Zhat) {
+                   const int32_t* __restrict__ leafseg, PatchSrc ps, double* __restrict__ Zhat) {
   __shared__ int64_t pre[kMaxLevelNodes + 1];
   __shared__ double zbuf[kWienerWarps][kMaxP];
   __shared__ double cbuf[kWienerWarps][kMaxP];
@@ -176,9 +186,7 @@ wiener_fp64_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
     const double* U = pv.model_basis + pv.model_off64[k];
     const double* shrink = pv.model_shrink + (int64_t)t * pv.model_cols_total + pv.model_col_off[k];
     const double gt = pv.model_gamma_tail[(int64_t)t * pv.K + k];
-    const double* zr = Z64 + (int64_t)patch * P;
-    for (int p = lane; p < P; p += 32) zs[p] = zr[p];
-    __syncwarp();
+    load_patch(ps, patch, P, zs);
     for (int j = lane; j < r; j += 32) {
       double c = 0.0;
       for (int p = 0; p < P; ++p) c = fma(zs[p], __ldg(U + (int64_t)p * r + j), c);
@@ -196,15 +204,172 @@ wiener_fp64_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
   }
 }
 
+// Tiled FP64 Wiener (gmm.py:352-359): a tile is up to 64 patches of one leaf
+// component k (the leaf buckets of the last select).  The CTA stages Z
+// (64 x P), U_k (P x r) and U_k^T in shared memory, then
+//   C = (Z U_k) * shrink          (64 x r)
+//   Zhat = C U_k^T + gamma_tail Z (64 x P)
+// with 4x4 register blocks per thread.  FP64 throughout: the estimates feed
+// the next iteration's tree decisions, which must stay those of the FP64
+// reference.
+constexpr int kWRows = 64;
+constexpr int kWThreads = 256;
+
+struct WienerSmemHead {
+  int32_t tpre[kMaxLevelNodes + 1];
+  uint64_t scan_tmp[256];
+  int32_t rows[kWRows];
+};
+
+__global__ void __launch_bounds__(kWThreads)
+wiener_tile_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, int n_leaf_nodes,
+                   const int32_t* __restrict__ cnt, const int64_t* __restrict__ off,
+                   const int32_t* __restrict__ leafseg, PatchSrc ps, double* __restrict__ Zhat,
+                   int rmax) {
+  extern __shared__ __align__(16) uint8_t wsm[];
+  WienerSmemHead& h = *reinterpret_cast<WienerSmemHead*>(wsm);
+  const int P = pv.P;
+  const int zs_ld = P + 1;
+  double* Zs = reinterpret_cast<double*>(wsm + ((sizeof(WienerSmemHead) + 15) & ~size_t(15)));
+  double* Us = Zs + kWRows * zs_ld;        // [P][rmax]
+  double* UT = Us + P * rmax;              // [rmax][P]
+  double* Cs = UT + rmax * P;              // [64][rmax+1]
+  double* sh = Cs + kWRows * (rmax + 1);   // [rmax]
+  const int cs_ld = rmax + 1;
+  const int tid = threadIdx.x;
+  for (int k = tid; k < n_leaf_nodes; k += kWThreads)
+    h.tpre[k] = (cnt[leaf_nodes[k]] + kWRows - 1) / kWRows;
+  __syncthreads();
+  const int tiles = block_exscan(h.tpre, n_leaf_nodes, h.scan_tmp);
+  if (tid == 0) h.tpre[n_leaf_nodes] = tiles;
+  __syncthreads();
+  const int ig = tid >> 4;   // rows 4*ig .. 4*ig+3
+  const int jg = tid & 15;   // columns jg + 16*c
+  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int li = prefix_find(h.tpre, n_leaf_nodes, tile);
+    const int v = leaf_nodes[li];
+    const int comp = pv.leaf_index[v];
+    const int r = pv.model_rank[comp];
+    const int first = (tile - h.tpre[li]) * kWRows;
+    const int m = min(kWRows, cnt[v] - first);
+    if (tid < kWRows) h.rows[tid] = tid < m ? leafseg[off[v] + first + tid] : -1;
+    const double* U = pv.model_basis + pv.model_off64[comp];
+    for (int e = tid; e < P * r; e += kWThreads) {
+      const int p = e / r, j = e - p * r;
+      const double u = U[e];
+      Us[p * rmax + j] = u;
+      UT[j * P + p] = u;
+    }
+    const double* shrink = pv.model_shrink + (int64_t)t * pv.model_cols_total + pv.model_col_off[comp];
+    for (int j = tid; j < r; j += kWThreads) sh[j] = shrink[j];
+    __syncthreads();
+    for (int e = tid; e < kWRows * P; e += kWThreads) {
+      const int i = e / P, p = e - i * P;
+      const int g = h.rows[i];
+      double z = 0.0;
+      if (g >= 0) {
+        const int b = g / ps.n_img;
+        const int ia = g - b * ps.n_img;
+        const int dr = p / ps.side;
+        z = ps.x[((int64_t)b * ps.H + ps.anchors[2 * ia] + dr) * ps.W + ps.anchors[2 * ia + 1] +
+                 (p - dr * ps.side)] - ps.dc[g];
+      }
+      Zs[i * zs_ld + p] = z;
+    }
+    __syncthreads();
+    // C = (Z U) * shrink
+    {
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+      for (int p = 0; p < P; ++p) {
+        double z[4], u[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) z[a] = Zs[(4 * ig + a) * zs_ld + p];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) u[c] = (jg + 16 * c < r) ? Us[p * rmax + jg + 16 * c] : 0.0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[a][c] = fma(z[a], u[c], acc[a][c]);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int j = jg + 16 * c;
+        if (j < r)
+#pragma unroll
+          for (int a = 0; a < 4; ++a) Cs[(4 * ig + a) * cs_ld + j] = acc[a][c] * sh[j];
+      }
+    }
+    __syncthreads();
+    // Zhat = C U^T + gamma_tail Z
+    const double gt = pv.model_gamma_tail[(int64_t)t * pv.K + comp];
+    for (int pc0 = 0; pc0 < P; pc0 += 64) {
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+      for (int j = 0; j < r; ++j) {
+        double cc[4], u[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) cc[a] = Cs[(4 * ig + a) * cs_ld + j];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int p = pc0 + jg + 16 * c;
+          u[c] = p < P ? UT[j * P + p] : 0.0;
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[a][c] = fma(cc[a], u[c], acc[a][c]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int i = 4 * ig + a;
+        const int row = h.rows[i];
+        if (row < 0) continue;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int p = pc0 + jg + 16 * c;
+          if (p < P) Zhat[(int64_t)row * P + p] = acc[a][c] + gt * Zs[i * zs_ld + p];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void leaf_counts_kernel(const int32_t* leaf_nodes, int n_leaf_nodes,
                                    const int32_t* leaf_index, const int32_t* cnt, int64_t* out) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n_leaf_nodes) out[leaf_index[leaf_nodes[k]]] = cnt[leaf_nodes[k]];
 }
 
-// the tcgen05 level kernel lives in select_tc.cu
-int select_level_tc(Plan* p, const LevelArgs& a, const float* Z32, const double* Z64,
-                    const double* sq, double guard, cudaStream_t st);
+// tensor-core level kernels (select_tc.cu: K atoms streamed per tile, any
+// P <= 128; select_ws.cu: warp-specialized pipeline, P <= 64)
+int select_level_tc(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
+                    cudaStream_t st);
+bool select_ws_supported(const Plan* p);
+int select_level_ws(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
+                    cudaStream_t st);
+
+static int side_of(int P) {
+  int s = 1;
+  while (s * s < P) ++s;
+  return s;
+}
+
+int rescore_queue_x(Plan* p, const LevelArgs& a, const double* x, const int32_t* anchors, int n_img,
+                    int H, int W, const double* dc, const double* sq, cudaStream_t st) {
+  PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P)};
+  rescore_fp64_kernel<<<2 * kSMs, kSelWarps * 32, 0, st>>>(p->v, a, ps, sq, p->rs.queue,
+                                                           p->rs.queue_len);
+  FEPLL_LAUNCH();
+  return kOk;
+}
 
 LevelArgs make_level(Plan* p, int d, int t, int32_t* labels) {
   LevelArgs a;
@@ -228,16 +393,23 @@ LevelArgs make_level(Plan* p, int d, int t, int32_t* labels) {
 
 using namespace fepll;
 
-extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* Z64, const float* Z32,
-                            const double* sq, int64_t n_total, int32_t mode, double guard,
-                            int32_t* labels, int64_t* leaf_counts, void* stream) {
+extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32_t W,
+                            const int32_t* anchors, int32_t n_img, const double* dc,
+                            const double* sq, const float* Z32, int64_t n_total, int32_t mode,
+                            double guard, int32_t* labels, int64_t* leaf_counts, void* stream) {
   Plan* p = reinterpret_cast<Plan*>(plan);
-  FEPLL_REQUIRE(p != nullptr && labels != nullptr && sq != nullptr, "select: bad arguments");
+  FEPLL_REQUIRE(p != nullptr && labels != nullptr && sq != nullptr && x != nullptr &&
+                    anchors != nullptr && dc != nullptr,
+                "select: bad arguments");
   FEPLL_REQUIRE(t >= 0 && t < p->v.T, "select: iteration index outside the beta schedule");
   FEPLL_REQUIRE(n_total >= 0 && n_total <= p->rs.cap, "select: patch count exceeds the reserved scratch");
+  FEPLL_REQUIRE(n_img >= 1 && n_total % n_img == 0, "select: n_total must be a multiple of n_img");
+  FEPLL_REQUIRE(n_total * std::max(2, p->max_children) < (int64_t(1) << 32),
+                "select: too many patches for 32-bit segment offsets");
   FEPLL_REQUIRE(mode == 0 || mode == 1, "select: unknown mode");
-  FEPLL_REQUIRE(mode == 1 || Z64 != nullptr, "select: exact mode needs FP64 patches");
-  FEPLL_REQUIRE(mode == 0 || (Z32 != nullptr && p->have_tc), "select: tensor mode needs FP32 patches and a tcgen05 plan");
+  const bool use_ws = mode == 1 && select_ws_supported(p);
+  FEPLL_REQUIRE(mode == 0 || (Z32 != nullptr && p->have_tc),
+                "select: tensor mode needs a tcgen05 plan and the FP32 patch rows");
   cudaStream_t st = (cudaStream_t)stream;
   p->last_n_total = (int)n_total;
   FEPLL_CUDA(cudaMemsetAsync(p->rs.cnt, 0, sizeof(int32_t) * p->v.n_nodes, st));
@@ -250,22 +422,21 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* Z64, con
   route_init_kernel<<<(unsigned)((n_total + 255) / 256), 256, 0, st>>>(
       n_total, p->rs.seg[0], p->rs.cnt, p->rs.off, p->rs.leaf_base, labels, root_leaf);
   FEPLL_LAUNCH();
-  if (root_leaf >= 0) {
-    // single-component model: every patch is at the only leaf
-    leaf_counts_kernel<<<1, 32, 0, st>>>(p->d_leaf_nodes, p->n_leaf_nodes, p->v.leaf_index,
-                                          p->rs.cnt, leaf_counts ? leaf_counts : (int64_t*)nullptr);
-    FEPLL_LAUNCH();
-    return kOk;
-  }
-  for (int d = 0; d < p->n_levels; ++d) {
-    LevelArgs a = make_level(p, d, t, labels);
-    if (mode == 1) {
-      int rc = select_level_tc(p, a, Z32, Z64, sq, guard, st);
+  if (root_leaf < 0) {
+    PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P)};
+    for (int d = 0; d < p->n_levels; ++d) {
+      LevelArgs a = make_level(p, d, t, labels);
+      int rc = kOk;
+      if (mode == 1) {
+        rc = use_ws ? select_level_ws(p, a, Z32, sq, guard, st)
+                    : select_level_tc(p, a, Z32, sq, guard, st);
+        if (!rc) rc = rescore_queue_x(p, a, x, anchors, n_img, H, W, dc, sq, st);
+      } else {
+        select_level_fp64_kernel<<<grid_for(n_total, kSelWarps, 148 * 8), kSelWarps * 32, 0, st>>>(
+            p->v, a, ps, sq);
+        FEPLL_LAUNCH();
+      }
       if (rc) return rc;
-    } else {
-      select_level_fp64_kernel<<<grid_for(n_total, kSelWarps, 148 * 8), kSelWarps * 32, 0, st>>>(
-          p->v, a, Z64, sq);
-      FEPLL_LAUNCH();
     }
   }
   if (leaf_counts) {
@@ -276,33 +447,48 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* Z64, con
   return kOk;
 }
 
-extern "C" int fepll_wiener(fepll_plan_t plan, int32_t t, const double* Z64, const int32_t* labels,
-                            int64_t n_total, double* Zhat, void* stream) {
-  Plan* p = reinterpret_cast<Plan*>(plan);
-  FEPLL_REQUIRE(p != nullptr && Z64 != nullptr && Zhat != nullptr, "wiener: bad arguments");
-  FEPLL_REQUIRE(t >= 0 && t < p->v.T, "wiener: iteration index outside the beta schedule");
-  FEPLL_REQUIRE(n_total == p->last_n_total, "wiener: must follow fepll_select on the same patches");
-  FEPLL_REQUIRE(p->n_leaf_nodes <= kMaxLevelNodes, "wiener: too many leaves");
-  (void)labels;
-  if (n_total == 0) return kOk;
-  cudaStream_t st = (cudaStream_t)stream;
-  if (p->child_count[0] == 0) {
-    // root is the only leaf: its bucket is the identity order
-    FEPLL_CUDA(cudaMemsetAsync(p->rs.off, 0, sizeof(int64_t), st));
-    route_init_kernel<<<(unsigned)((n_total + 255) / 256), 256, 0, st>>>(
-        n_total, p->rs.leafseg, p->rs.cnt, p->rs.off, p->rs.leaf_base, (int32_t*)nullptr, -1);
-    FEPLL_LAUNCH();
-  }
-  wiener_fp64_kernel<<<grid_for(n_total, kWienerWarps, 148 * 8), kWienerWarps * 32, 0, st>>>(
-      p->v, t, p->d_leaf_nodes, p->n_leaf_nodes, p->rs.cnt, p->rs.off, p->rs.leafseg, Z64, Zhat);
-  FEPLL_LAUNCH();
-  return kOk;
-}
-
 extern "C" int fepll_select_rescored(fepll_plan_t plan, int32_t* dst, void* stream) {
   Plan* p = reinterpret_cast<Plan*>(plan);
   FEPLL_REQUIRE(p != nullptr && dst != nullptr, "select_rescored: bad arguments");
   FEPLL_CUDA(cudaMemcpyAsync(dst, p->rs.queue_len, sizeof(int32_t) * kMaxDepth,
                              cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return kOk;
+}
+
+extern "C" int fepll_wiener(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32_t W,
+                            const int32_t* anchors, int32_t n_img, const double* dc,
+                            int64_t n_total, double* Zhat, void* stream) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  FEPLL_REQUIRE(p != nullptr && x != nullptr && anchors != nullptr && dc != nullptr &&
+                    Zhat != nullptr,
+                "wiener: bad arguments");
+  FEPLL_REQUIRE(t >= 0 && t < p->v.T, "wiener: iteration index outside the beta schedule");
+  FEPLL_REQUIRE(n_total == p->last_n_total, "wiener: must follow fepll_select on the same patches");
+  FEPLL_REQUIRE(p->n_leaf_nodes <= kMaxLevelNodes, "wiener: too many leaves");
+  if (n_total == 0) return kOk;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (p->child_count[0] == 0) {
+    // root is the only leaf: its bucket is the identity order
+    route_init_kernel<<<(unsigned)((n_total + 255) / 256), 256, 0, st>>>(
+        n_total, p->rs.leafseg, p->rs.cnt, p->rs.off, p->rs.leaf_base, (int32_t*)nullptr, -1);
+    FEPLL_LAUNCH();
+  }
+  PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P)};
+  const int P = p->v.P;
+  const int rmax = p->max_model_rank;
+  if (rmax <= 64) {
+    const size_t smem = ((sizeof(WienerSmemHead) + 15) & ~size_t(15)) +
+                        sizeof(double) * ((size_t)kWRows * (P + 1) + 2 * (size_t)P * rmax +
+                                          (size_t)kWRows * (rmax + 1) + rmax);
+    FEPLL_CUDA(cudaFuncSetAttribute(wiener_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+    wiener_tile_kernel<<<kSMs * 2, kWThreads, smem, st>>>(p->v, t, p->d_leaf_nodes, p->n_leaf_nodes,
+                                                          p->rs.cnt, p->rs.off, p->rs.leafseg, ps,
+                                                          Zhat, rmax);
+  } else {
+    wiener_fp64_kernel<<<grid_for(n_total, kWienerWarps, 148 * 8), kWienerWarps * 32, 0, st>>>(
+        p->v, t, p->d_leaf_nodes, p->n_leaf_nodes, p->rs.cnt, p->rs.off, p->rs.leafseg, ps, Zhat);
+  }
+  FEPLL_LAUNCH();
   return kOk;
 }

@@ -7,9 +7,8 @@
 //
 //   C (128 x N) = Z_tile (128 x P) . G_u (P x N)     N = sum of child ranks
 //
-// runs as 3xTF32 on tcgen05 (kind::tf32, M=128, K=8 per MMA, accumulators in
-// TMEM): D_main = Zhi.Ghi, D_corr = Zhi.Glo + Zlo.Ghi (separate TMEM
-// columns, summed in FP64 by the epilogue).  Operands are K-major,
+// runs as 3xTF32 on tcgen05 (kind::tf32, M=128, K=8 per MMA, FP32 accumulator
+// in TMEM): D = Zhi.Ghi + Zhi.Glo + Zlo.Ghi.  Operands are K-major,
 // 128-byte-swizzled: the group image G_u arrives pre-split/pre-swizzled by
 // the TMA bulk engine, the patch rows are gathered by the CTA's threads,
 // split hi/lo and stored swizzled.  The K dimension streams through two
@@ -24,6 +23,7 @@
 // equals the FP64 argmin.
 #include "route.cuh"
 #include "tc.cuh"
+#include "tc_epi.cuh"
 
 namespace fepll {
 
@@ -31,17 +31,11 @@ constexpr int kTcRows = 128;          // M
 constexpr int kTcThreads = 128;       // 4 warps: loaders + epilogue; thread 0 issues MMAs
 constexpr int kAtomFloats = 32;       // 128-byte K atom
 constexpr int kAtomBytesA = kTcRows * 128;
-constexpr uint32_t kTmemCols = 512;   // [0,256): D_main, [256,512): D_corr
+constexpr uint32_t kTmemCols = 256;   // one accumulator, N <= 256
 
 struct TcSmemTables {
-  int32_t tpre[kMaxLevelNodes + 1];   // tile prefix over depth-d nodes
-  int32_t cpre[kMaxLevelNodes + 1];   // count prefix
-  int64_t child_off[kMaxLevelNodes];  // next-level segment offsets of depth-(d+1) nodes
-  double w[kMaxGroupCols / 2];        // group column weights of the current tile's node
-  double cconst[kMaxChildren];
-  double cnut[kMaxChildren];
-  int32_t cend[kMaxChildren];         // exclusive end column of each child
-  int32_t cbfs[kMaxChildren];
+  LevelTables lv;
+  EpiChild ch;
   int32_t rows[kTcRows];
   int32_t key[kTcRows];
   int32_t lrank[kTcRows];
@@ -50,8 +44,6 @@ struct TcSmemTables {
   uint64_t mma_bar[2];
   uint64_t load_bar[2];
   uint32_t tmem_base;
-  int32_t total_tiles;
-  int32_t cur_node;
 };
 
 struct TcArgs {
@@ -65,46 +57,6 @@ struct TcArgs {
   int katoms;
   int bmax_rows;       // padded N of the stage buffers
 };
-
-__device__ __forceinline__ void tc_level_setup(const PlanView& pv, const LevelArgs& a,
-                                               TcSmemTables& s) {
-  const int nd = a.lvl_end - a.lvl_begin;
-  for (int k = threadIdx.x; k < nd; k += blockDim.x) {
-    const int u = a.lvl_begin + k;
-    s.cpre[k + 1] = pv.child_count[u] > 0 ? a.cnt[u] : 0;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    s.cpre[0] = 0;
-    s.tpre[0] = 0;
-    int64_t run_int = 0, run_leaf = 0;
-    const int64_t lb = a.leaf_base[a.depth];
-    for (int k = 0; k < nd; ++k) {
-      const int c = s.cpre[k + 1];
-      s.cpre[k + 1] = s.cpre[k] + c;
-      s.tpre[k + 1] = s.tpre[k] + (c + kTcRows - 1) / kTcRows;
-      const int u = a.lvl_begin + k;
-      const int nk = pv.child_count[u];
-      const int cs = pv.child_start[u];
-      for (int j = 0; j < nk; ++j) {
-        const int v = pv.child_list[cs + j];
-        if (pv.child_count[v] > 0) {
-          s.child_off[v - a.nxt_begin] = run_int;
-          run_int += c;
-        } else {
-          s.child_off[v - a.nxt_begin] = lb + run_leaf;
-          run_leaf += c;
-        }
-      }
-    }
-    s.total_tiles = s.tpre[nd];
-    if (blockIdx.x == 0) a.leaf_base[a.depth + 1] = lb + run_leaf;
-  }
-  __syncthreads();
-  if (blockIdx.x == 0)
-    for (int k = threadIdx.x; k < a.nxt_end - a.nxt_begin; k += blockDim.x)
-      a.off[a.nxt_begin + k] = s.child_off[k];
-}
 
 __global__ void __launch_bounds__(kTcThreads, 1)
 select_level_tc_kernel(PlanView pv, TcArgs args) {
@@ -131,39 +83,25 @@ select_level_tc_kernel(PlanView pv, TcArgs args) {
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = s.tmem_base;
-  tc_level_setup(pv, a, s);
+  level_tables(pv, a, s.lv, kTcRows);
 
   const int nd = a.lvl_end - a.lvl_begin;
   const int t = a.t;
   uint32_t uses[2] = {0, 0};  // completed-or-pending commits per stage (uniform across threads)
   const double guard = args.guard;
 
-  for (int tile = blockIdx.x; tile < s.total_tiles; tile += gridDim.x) {
+  for (int tile = blockIdx.x; tile < s.lv.total_tiles; tile += gridDim.x) {
     // tile -> node, row range
-    int lo = 0, hi = nd;
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (s.tpre[mid] <= tile) lo = mid; else hi = mid;
-    }
+    const int lo = prefix_find(s.lv.tpre, nd, tile);
     const int u = a.lvl_begin + lo;
-    const int first = (tile - s.tpre[lo]) * kTcRows;
-    const int cnt_u = s.cpre[lo + 1] - s.cpre[lo];
+    const int first = (tile - s.lv.tpre[lo]) * kTcRows;
+    const int cnt_u = s.lv.cpre[lo + 1] - s.lv.cpre[lo];
     const int m = min(kTcRows, cnt_u - first);
-    const int width = pv.grp_width[u];
     const int npad = pv.tc_npad[u];
     const int nk = pv.child_count[u];
     const int64_t seg0 = a.off[u] + first;
     // per-tile tables (previous tile's epilogue finished: trailing __syncthreads)
-    for (int j = tid; j < width; j += kTcThreads)
-      s.w[j] = pv.grp_sqw[(int64_t)t * pv.grp_cols_total + pv.grp_col_off[u] + j];
-    if (tid < nk) {
-      const int v = pv.child_list[pv.child_start[u] + tid];
-      const int64_t ti = (int64_t)t * pv.n_nodes + v;
-      s.cconst[tid] = pv.node_const[ti];
-      s.cnut[tid] = pv.node_nu_tail[ti];
-      s.cend[tid] = pv.child_col_off[v] + pv.node_rank[v];
-      s.cbfs[tid] = v;
-    }
+    epi_load_node(pv, t, u, s.ch, tid, kTcThreads);
     const int my_patch = tid < m ? a.seg_in[seg0 + tid] : -1;
     s.rows[tid] = my_patch;
     const float* zrow = my_patch >= 0 ? args.Z32 + (int64_t)my_patch * args.z32_pitch : nullptr;
@@ -216,8 +154,8 @@ select_level_tc_kernel(PlanView pv, TcArgs args) {
           const uint32_t ko = kk * 32;  // 8 tf32 = 32 bytes inside the swizzle atom
           const uint32_t acc = (ka > 0 || kk > 0) ? 1u : 0u;
           tc::mma_tf32(tmem, tc::desc_sw128(a_hi + ko), tc::desc_sw128(b_hi + ko), idesc, acc);
-          tc::mma_tf32(tmem + 256, tc::desc_sw128(a_hi + ko), tc::desc_sw128(b_lo + ko), idesc, acc);
-          tc::mma_tf32(tmem + 256, tc::desc_sw128(a_lo + ko), tc::desc_sw128(b_hi + ko), idesc, 1u);
+          tc::mma_tf32(tmem, tc::desc_sw128(a_hi + ko), tc::desc_sw128(b_lo + ko), idesc, 1u);
+          tc::mma_tf32(tmem, tc::desc_sw128(a_lo + ko), tc::desc_sw128(b_hi + ko), idesc, 1u);
         }
         tc::mma_commit(&s.mma_bar[st]);
       }
@@ -231,45 +169,9 @@ select_level_tc_kernel(PlanView pv, TcArgs args) {
     // ---- epilogue: thread tid owns TMEM lane tid == tile row tid
     const bool valid = tid < m;
     const double sqv = valid ? args.sq[my_patch] : 0.0;
-    const double zn = sqrt(sqv);
-    double best = INFINITY, best_err = 0.0, m1 = INFINITY, m2 = INFINITY;
-    int bi = 0, i1 = -1;
-    int ci = 0;
-    int cend = s.cend[0];
-    double acc_s = 0.0, acc_e = 0.0;
     const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
-    const int nchunks = (width + 31) >> 5;
-    for (int ch = 0; ch < nchunks; ++ch) {
-      uint32_t ra[32], rb[32];
-      tc::tmem_ld32(lane_base + ch * 32, ra);
-      tc::tmem_ld32(lane_base + 256 + ch * 32, rb);
-      tc::tmem_ld_wait();
-#pragma unroll
-      for (int q = 0; q < 32; ++q) {
-        const int j = ch * 32 + q;
-        if (j < width) {
-          const double c = (double)__uint_as_float(ra[q]) + (double)__uint_as_float(rb[q]);
-          const double w = s.w[j];
-          const double cw = c * w;
-          acc_s = fma(cw, c, acc_s);
-          acc_e += fabs(cw);
-          if (j + 1 == cend) {
-            const double sc = s.cconst[ci] + sqv / s.cnut[ci] + acc_s;
-            const double er = guard * zn * acc_e;
-            if (sc < best) { best = sc; bi = ci; best_err = er; }
-            const double lo_c = sc - er;
-            if (lo_c < m1) { m2 = m1; m1 = lo_c; i1 = ci; }
-            else if (lo_c < m2) { m2 = lo_c; }
-            ++ci;
-            cend = ci < nk ? s.cend[ci] : 0x7fffffff;
-            acc_s = 0.0;
-            acc_e = 0.0;
-          }
-        }
-      }
-    }
-    const double other = (i1 == bi) ? m2 : m1;
-    const bool flagged = !(other > best + best_err) || !isfinite(best);
+    bool flagged;
+    const int bi = epi_score_row(s.ch, nk, lane_base, sqv, guard, &flagged);
     // ---- routing (aggregated per tile: one global atomic per child)
     tc::fence_before_sync();
     if (tid <= kMaxChildren) s.bcnt[tid] = 0;
@@ -280,7 +182,7 @@ select_level_tc_kernel(PlanView pv, TcArgs args) {
       s.lrank[tid] = atomicAdd(&s.bcnt[key], 1);
     }
     __syncthreads();
-    if (tid < nk && s.bcnt[tid] > 0) s.bbase[tid] = atomicAdd(&a.cnt[s.cbfs[tid]], s.bcnt[tid]);
+    if (tid < nk && s.bcnt[tid] > 0) s.bbase[tid] = atomicAdd(&a.cnt[s.ch.bfs[tid]], s.bcnt[tid]);
     if (tid == kTcThreads - 1 && s.bcnt[kMaxChildren] > 0)
       s.bbase[kMaxChildren] = atomicAdd(&args.queue_len[a.depth], s.bcnt[kMaxChildren]);
     __syncthreads();
@@ -291,8 +193,8 @@ select_level_tc_kernel(PlanView pv, TcArgs args) {
         args.queue[2 * slot] = my_patch;
         args.queue[2 * slot + 1] = u;
       } else {
-        const int v = s.cbfs[key];
-        const int64_t b0 = s.child_off[v - a.nxt_begin];
+        const int v = s.ch.bfs[key];
+        const int64_t b0 = s.lv.child_off[v - a.nxt_begin];
         if (pv.child_count[v] > 0) {
           a.seg_out[b0 + slot] = my_patch;
         } else {
@@ -308,28 +210,23 @@ select_level_tc_kernel(PlanView pv, TcArgs args) {
   if (warp == 0) tc::tmem_dealloc(tmem, kTmemCols);
 }
 
-// exact re-scoring of the queued (patch, node) decisions (select.cu)
-int rescore_queue(Plan* p, const LevelArgs& a, const double* Z64, const double* sq,
-                  const int32_t* queue, const int32_t* queue_len, cudaStream_t st);
-
 static size_t tc_smem_bytes(int bmax_rows) {
   const size_t stage = 2 * (size_t)kAtomBytesA + 2 * (size_t)bmax_rows * 128;
   return 1024 + 2 * stage + sizeof(TcSmemTables);
 }
 
-int select_level_tc(Plan* p, const LevelArgs& a, const float* Z32, const double* Z64,
-                    const double* sq, double guard, cudaStream_t st) {
-  FEPLL_REQUIRE(Z64 != nullptr, "tensor mode needs FP64 patches for the re-scoring path");
-  FEPLL_REQUIRE(p->max_group_cols <= 256, "tensor mode supports nodes whose children ranks sum to <= 256");
+int select_level_tc(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
+                    cudaStream_t st) {
+  FEPLL_REQUIRE(p->max_tc_npad <= 256, "tensor mode supports nodes whose padded child ranks sum to <= 256");
   const int P = p->v.P;
   const int ppad = (P + 31) / 32 * 32;
-  const int bmax = std::max(16, (p->max_group_cols + 15) / 16 * 16);
+  const int bmax = std::max(16, p->max_tc_npad);
   TcArgs args;
   args.a = a;
   args.Z32 = Z32;
   args.z32_pitch = ppad;
   args.sq = sq;
-  args.guard = guard > 0 ? guard : 7.62939453125e-06;  // 2^-17
+  args.guard = guard > 0 ? guard : kDefaultGuard;
   args.queue = p->rs.queue;
   args.queue_len = p->rs.queue_len;
   args.katoms = ppad / 32;
@@ -339,7 +236,7 @@ int select_level_tc(Plan* p, const LevelArgs& a, const float* Z32, const double*
                                   (int)smem));
   select_level_tc_kernel<<<kSMs, kTcThreads, smem, st>>>(p->v, args);
   FEPLL_LAUNCH();
-  return rescore_queue(p, a, Z64, sq, p->rs.queue, p->rs.queue_len, st);
+  return kOk;
 }
 
 }  // namespace fepll

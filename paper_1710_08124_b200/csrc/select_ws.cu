@@ -1,0 +1,352 @@
+// Kernel (b), tensor-core path, warp-specialized pipeline (P <= 64).
+//
+// Same arithmetic as select_tc.cu (3xTF32 tcgen05 scoring of one tree level,
+// certified argmin, FP64 re-scoring of the rest; pkg/src/fepll/tree.py:416-428,
+// pkg/src/fepll/gmm.py:323-339), laid out as a persistent pipeline:
+//
+//   warps 0-7    producers: warp w owns K atom w/4 of the tile's 128 FP32
+//                patch rows (kernel (a) output).  Each thread prefetches its
+//                row of tile i+1 into registers (8 x 16-byte loads) while
+//                tile i is in flight, then splits TF32 hi/lo and stores it
+//                128B-swizzled into one of two A stages;
+//   warp 8       MMA issuer: keeps the current node's group image G_u resident
+//                in smem (reloaded by the TMA bulk engine only when the node
+//                changes — each CTA walks a contiguous, node-sorted tile
+//                range), issues 24 tcgen05.mma per tile into one of four
+//                128-column TMEM accumulators;
+//   warps 9-24   four epilogue groups (tile i -> group i % 4): tcgen05.ld,
+//                per-child scores (tc_epi.cuh), certified argmin,
+//                aggregated routing.
+//
+// smem (P=64, N<=128): 2 x 64 KB A stages + 64 KB B + tables; TMEM 512 cols.
+#include "route.cuh"
+#include "tc.cuh"
+#include "tc_epi.cuh"
+
+namespace fepll {
+
+namespace ws {
+
+constexpr int kRows = 128;
+constexpr int kProducerWarps = 8;
+constexpr int kMmaWarp = 8;
+constexpr int kGroups = 4;                 // epilogue groups == TMEM accumulators
+constexpr int kEpiWarps = 4 * kGroups;
+constexpr int kThreads = (kProducerWarps + 1 + kEpiWarps) * 32;
+constexpr int kStages = 2;
+constexpr int kAtomA = kRows * 128;     // bytes of one K atom of A (hi or lo)
+constexpr int kMaxKAtoms = 2;           // P <= 64
+constexpr int kMaxN = 128;              // padded group width == accumulator columns
+constexpr int kStageBytes = 2 * kMaxKAtoms * kAtomA;       // hi + lo, all atoms
+constexpr int kBBytes = 2 * kMaxKAtoms * kMaxN * 128;      // hi + lo, all atoms
+constexpr uint32_t kTmemCols = 512;
+
+struct EpiGroup {
+  EpiChild ch;
+  int node;
+  int32_t key[kRows];
+  int32_t lrank[kRows];
+  int32_t bcnt[kMaxChildren + 1];
+  int32_t bbase[kMaxChildren + 1];
+};
+
+struct Smem {
+  LevelTables lv;
+  EpiGroup epi[kGroups];
+  uint64_t a_full[kStages], a_empty[kStages], acc_full[kGroups], acc_empty[kGroups];
+  uint64_t b_full, drain;
+  uint32_t tmem_base;
+  int32_t t_begin, t_end;
+};
+
+struct Args {
+  LevelArgs a;
+  const float* Z32;      // [n_total][z32_pitch] FP32 patch rows (fepll_extract)
+  int z32_pitch;
+  const double* sq;
+  double guard;
+  int32_t* queue;
+  int32_t* queue_len;
+  int katoms;
+  uint64_t* trace;       // debug timeline: [CTA][64 tiles][8] globaltimer stamps (or NULL)
+};
+
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void stamp(const Args& a, int i, int slot) {
+  if (a.trace && i < 64) a.trace[((size_t)blockIdx.x * 64 + i) * 8 + slot] = gtimer();
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+
+struct TileInfo {
+  int u, first, m;
+};
+
+__device__ __forceinline__ TileInfo tile_info(const LevelArgs& a, const LevelTables& lv, int tile) {
+  TileInfo ti;
+  const int k = prefix_find(lv.tpre, a.lvl_end - a.lvl_begin, tile);
+  ti.u = a.lvl_begin + k;
+  ti.first = (tile - lv.tpre[k]) * kRows;
+  ti.m = min(kRows, (lv.cpre[k + 1] - lv.cpre[k]) - ti.first);
+  return ti;
+}
+
+// row r of tile `tile`, K atom ka: 8 float4 into registers (zeros past m)
+__device__ __forceinline__ void load_row(const Args& args, const LevelArgs& a, const LevelTables& lv,
+                                         int tile, int row, int ka, float4 (&v)[8]) {
+  const TileInfo ti = tile_info(a, lv, tile);
+  const int g = row < ti.m ? a.seg_in[a.off[ti.u] + ti.first + row] : -1;
+  if (g >= 0) {
+    const float4* src = reinterpret_cast<const float4*>(args.Z32 + (int64_t)g * args.z32_pitch) + ka * 8;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = __ldg(src + c);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+select_level_ws_kernel(PlanView pv, Args args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* stageA = base;
+  uint8_t* bbuf = base + kStages * kStageBytes;   // resident B (hi then lo)
+  Smem& s = *reinterpret_cast<Smem*>(bbuf + kBBytes);
+  const LevelArgs& a = args.a;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+
+  if (warp == kMmaWarp) tc::tmem_alloc(&s.tmem_base, kTmemCols);
+  if (tid == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      tc::mbar_init(&s.a_full[i], kProducerWarps);
+      tc::mbar_init(&s.a_empty[i], 1);
+    }
+    for (int i = 0; i < kGroups; ++i) {
+      tc::mbar_init(&s.acc_full[i], 1);
+      tc::mbar_init(&s.acc_empty[i], 4);
+    }
+    tc::mbar_init(&s.b_full, 1);
+    tc::mbar_init(&s.drain, 1);
+    tc::fence_mbar_init();
+  }
+  if (tid < kGroups) s.epi[tid].node = -1;
+  level_tables(pv, a, s.lv, kRows);  // contains __syncthreads
+  if (tid == 0) {
+    const int T = s.lv.total_tiles;
+    s.t_begin = (int)(((int64_t)T * blockIdx.x) / gridDim.x);
+    s.t_end = (int)(((int64_t)T * (blockIdx.x + 1)) / gridDim.x);
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = s.tmem_base;
+  if (tid == 0) stamp(args, 0, 7);
+  const int t_begin = s.t_begin, t_end = s.t_end;
+  const int ntile = t_end - t_begin;
+  const int t = a.t;
+
+  if (warp < kProducerWarps) {
+    // ------------------------------------------------------------ producers
+    const int row = tid & (kRows - 1);
+    const int ka = warp >> 2;          // K atom of this warp
+    const bool active = ka < args.katoms;
+    const int r8 = row & 7;
+    float4 v[8];
+    if (active && ntile > 0) load_row(args, a, s.lv, t_begin, row, ka, v);
+    for (int i = 0; i < ntile; ++i) {
+      const int st = i % kStages;
+      if (i >= kStages) tc::mbar_wait(&s.a_empty[st], ((i / kStages) - 1) & 1);
+      if (tid == 0) stamp(args, i, 0);
+      if (active) {
+        uint8_t* A = stageA + st * kStageBytes;
+        uint8_t* dhi = A + (2 * ka) * kAtomA + (row >> 3) * 1024 + r8 * 128;
+        uint8_t* dlo = A + (2 * ka + 1) * kAtomA + (row >> 3) * 1024 + r8 * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          float4 h, l;
+          h.x = tc::to_tf32(v[c].x); l.x = v[c].x - h.x;
+          h.y = tc::to_tf32(v[c].y); l.y = v[c].y - h.y;
+          h.z = tc::to_tf32(v[c].z); l.z = v[c].z - h.z;
+          h.w = tc::to_tf32(v[c].w); l.w = v[c].w - h.w;
+          *reinterpret_cast<float4*>(dhi + ((c ^ r8) << 4)) = h;
+          *reinterpret_cast<float4*>(dlo + ((c ^ r8) << 4)) = l;
+        }
+        tc::fence_proxy_async_smem();
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s.a_full[st]);
+      if (tid == 0) stamp(args, i, 1);
+      // prefetch the next tile's row while this one is consumed
+      if (active && i + 1 < ntile) load_row(args, a, s.lv, t_begin + i + 1, row, ka, v);
+    }
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int cur = -1;
+      uint32_t b_loads = 0, drains = 0;
+      for (int i = 0; i < ntile; ++i) {
+        const int st = i % kStages;
+        const int ac = i % kGroups;
+        const TileInfo ti = tile_info(a, s.lv, t_begin + i);
+        const int npad = pv.tc_npad[ti.u];
+        if (ti.u != cur) {
+          if (i > 0) {  // every MMA reading the old B must be done
+            tc::mma_commit(&s.drain);
+            tc::mbar_wait(&s.drain, drains & 1);
+            ++drains;
+          }
+          const uint32_t half = (uint32_t)args.katoms * npad * 128u;
+          tc::mbar_arrive_expect_tx(&s.b_full, 2 * half);
+          tc::bulk_g2s(bbuf, pv.tc_hi + pv.tc_off[ti.u], half, &s.b_full);
+          tc::bulk_g2s(bbuf + half, pv.tc_lo + pv.tc_off[ti.u], half, &s.b_full);
+          tc::mbar_wait(&s.b_full, b_loads & 1);
+          ++b_loads;
+          cur = ti.u;
+        }
+        if (i >= kGroups) tc::mbar_wait(&s.acc_empty[ac], ((i / kGroups) - 1) & 1);
+        tc::mbar_wait(&s.a_full[st], (i / kStages) & 1);
+        tc::fence_after_sync();
+        stamp(args, i, 2);
+        const uint32_t idesc = tc::idesc_tf32(kRows, npad);
+        const uint32_t d = tmem + ac * kMaxN;
+        const uint32_t A0 = tc::smem_u32(stageA + st * kStageBytes);
+        const uint32_t B0 = tc::smem_u32(bbuf);
+        const uint32_t bhalf = (uint32_t)args.katoms * npad * 128u;
+        for (int kq = 0; kq < args.katoms; ++kq) {
+          const uint32_t a_hi = A0 + (2 * kq) * kAtomA, a_lo = A0 + (2 * kq + 1) * kAtomA;
+          const uint32_t b_hi = B0 + kq * npad * 128, b_lo = B0 + bhalf + kq * npad * 128;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t ko = kk * 32;
+            const uint32_t acc = (kq > 0 || kk > 0) ? 1u : 0u;
+            tc::mma_tf32(d, tc::desc_sw128(a_lo + ko), tc::desc_sw128(b_hi + ko), idesc, acc);
+            tc::mma_tf32(d, tc::desc_sw128(a_hi + ko), tc::desc_sw128(b_lo + ko), idesc, 1u);
+            tc::mma_tf32(d, tc::desc_sw128(a_hi + ko), tc::desc_sw128(b_hi + ko), idesc, 1u);
+          }
+        }
+        tc::mma_commit(&s.a_empty[st]);
+        tc::mma_commit(&s.acc_full[ac]);
+        stamp(args, i, 3);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - (kMmaWarp + 1);  // 0..15
+    const int grp = ew >> 2;               // tiles with i % 4 == grp
+    const int row = 32 * (warp & 3) + lane;
+    const uint32_t d_acc = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + grp * kMaxN;
+    EpiGroup& E = s.epi[grp];
+    const int etid = (ew & 3) * 32 + lane;  // 0..127 inside the group
+    const int bar_id = 1 + grp;
+    const double guard = args.guard;
+    for (int i = grp; i < ntile; i += kGroups) {
+      const TileInfo ti = tile_info(a, s.lv, t_begin + i);
+      const int u = ti.u;
+      const int nk = pv.child_count[u];
+      const bool valid = row < ti.m;
+      const int g = valid ? a.seg_in[a.off[u] + ti.first + row] : -1;
+      const double sqv = valid ? args.sq[g] : 0.0;
+      if (u != E.node) {
+        named_bar(bar_id, 128);  // everyone done with the previous tables
+        epi_load_node(pv, t, u, E.ch, etid, 128);
+        named_bar(bar_id, 128);
+        if (etid == 0) E.node = u;
+      }
+      tc::mbar_wait(&s.acc_full[grp], (i / kGroups) & 1);
+      tc::fence_after_sync();
+      if (etid == 0) stamp(args, i, 4);
+      bool flagged;
+      const int bi = epi_score_row(E.ch, nk, d_acc, sqv, guard, &flagged);
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s.acc_empty[grp]);
+      if (etid == 0) stamp(args, i, 5);
+      // routing, aggregated over the group's 128 rows
+      if (etid <= kMaxChildren) E.bcnt[etid] = 0;
+      named_bar(bar_id, 128);
+      if (valid) {
+        const int key = flagged ? kMaxChildren : bi;
+        E.key[row] = key;
+        E.lrank[row] = atomicAdd(&E.bcnt[key], 1);
+      }
+      named_bar(bar_id, 128);
+      if (etid < nk && E.bcnt[etid] > 0) E.bbase[etid] = atomicAdd(&a.cnt[E.ch.bfs[etid]], E.bcnt[etid]);
+      if (etid == 127 && E.bcnt[kMaxChildren] > 0)
+        E.bbase[kMaxChildren] = atomicAdd(&args.queue_len[a.depth], E.bcnt[kMaxChildren]);
+      named_bar(bar_id, 128);
+      if (valid) {
+        const int key = E.key[row];
+        const int slot = E.bbase[key] + E.lrank[row];
+        if (key == kMaxChildren) {
+          args.queue[2 * slot] = g;
+          args.queue[2 * slot + 1] = u;
+        } else {
+          const int v = E.ch.bfs[key];
+          const int64_t b0 = s.lv.child_off[v - a.nxt_begin];
+          if (pv.child_count[v] > 0) {
+            a.seg_out[b0 + slot] = g;
+          } else {
+            a.leafseg[b0 + slot] = g;
+            a.labels[g] = pv.leaf_index[v];
+          }
+        }
+      }
+      if (etid == 0) stamp(args, i, 6);
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == kMmaWarp) tc::tmem_dealloc(tmem, kTmemCols);
+}
+
+}  // namespace ws
+
+uint64_t* g_ws_trace = nullptr;
+int g_ws_trace_level = -1;
+
+bool select_ws_supported(const Plan* p) {
+  return p->have_tc && p->v.P <= 64 && p->max_tc_npad <= ws::kMaxN;
+}
+
+int select_level_ws(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
+                    cudaStream_t st) {
+  ws::Args args;
+  args.a = a;
+  args.Z32 = Z32;
+  args.z32_pitch = (p->v.P + 31) / 32 * 32;
+  args.sq = sq;
+  args.guard = guard > 0 ? guard : kDefaultGuard;
+  args.queue = p->rs.queue;
+  args.queue_len = p->rs.queue_len;
+  args.katoms = (p->v.P + 31) / 32;
+  args.trace = (a.depth == g_ws_trace_level) ? g_ws_trace : nullptr;
+  const size_t smem = 1024 + ws::kStages * ws::kStageBytes + ws::kBBytes + sizeof(ws::Smem);
+  FEPLL_CUDA(cudaFuncSetAttribute(ws::select_level_ws_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ws::select_level_ws_kernel<<<kSMs, ws::kThreads, smem, st>>>(p->v, args);
+  FEPLL_LAUNCH();
+  return kOk;
+}
+
+}  // namespace fepll
+
+extern "C" int fepll_debug_ws_trace(void* device_buffer, int32_t level) {
+  fepll::g_ws_trace = static_cast<uint64_t*>(device_buffer);
+  fepll::g_ws_trace_level = level;
+  return 0;
+}

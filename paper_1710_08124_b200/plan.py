@@ -12,7 +12,8 @@ Layout in HBM (all FP64 unless stated):
   ``model_shrink[t]`` = gamma - gamma_tail per column and
   ``model_gamma_tail[t]``;
 * tcgen05 operand images (FP32, TF32 hi/lo split, K-major 128B-swizzled,
-  width padded to 16): see ``tc_images``.
+  each child padded to 16 columns) and their FP32 column weights: see
+  ``tc_images``.
 
 The whole beta schedule is packed once, so nothing is uploaded inside the
 restoration loop.
@@ -68,28 +69,60 @@ def swizzle128_kmajor(mat: np.ndarray) -> np.ndarray:
     return out
 
 
-def tc_images(grp_blocks: dict, P: int):
-    """B operands of the tcgen05 scorer: for internal node u the group
-    matrix transposed to (width_pad, P_pad) K-major, hi/lo TF32 split and
-    swizzled.  Returns (hi, lo, offsets, npad) for all nodes."""
+def tc_images(topo, comps, P: int, sqw_per_node: list):
+    """Operands of the tcgen05 scorer.
+
+    For internal node u the B image is the group matrix transposed to
+    (npad_u, P_pad) K-major — child v occupying rows
+    [tc_child_col[v], tc_child_col[v] + r_v), every child padded to a multiple
+    of 16 rows so each child starts on a 16-column TMEM chunk — then TF32
+    hi/lo split and 128B-swizzled.  ``sqw_per_node[t][v]`` (FP64 vectors)
+    become the FP32 per-column weights (0 on padding)."""
     Ppad = ((P + 31) // 32) * 32
+    n = topo.n_nodes
     his, los = [], []
-    off = {}
-    npad = {}
+    tc_off = np.zeros(n, np.int64)
+    tc_npad = np.zeros(n, np.int32)
+    tc_child_col = np.zeros(n, np.int32)
+    tc_w_off = np.zeros(n, np.int32)
     cur = 0
-    for u, G in grp_blocks.items():
-        width = G.shape[1]
-        wp = ((width + 15) // 16) * 16
-        Bt = np.zeros((wp, Ppad), dtype=np.float32)
-        Bt[:width, :P] = G.T.astype(np.float32)
+    wcols = 0
+    groups = []
+    for u in range(n):
+        nk = topo.child_count[u]
+        if nk == 0:
+            continue
+        kids = topo.child_list[topo.child_start[u]:topo.child_start[u] + nk]
+        col = 0
+        for v in kids:
+            tc_child_col[v] = col
+            col += ((comps[v].kept_basis.shape[1] + 15) // 16) * 16
+        npad = max(col, 16)
+        Bt = np.zeros((npad, Ppad), dtype=np.float32)
+        for v in kids:
+            r = comps[v].kept_basis.shape[1]
+            Bt[tc_child_col[v]:tc_child_col[v] + r, :P] = np.asarray(comps[v].kept_basis).T
         hi, lo = tf32_split(Bt)
-        his.append(swizzle128_kmajor(hi.reshape(wp, Ppad)))
-        los.append(swizzle128_kmajor(lo.reshape(wp, Ppad)))
-        off[u] = cur
-        npad[u] = wp
-        cur += wp * Ppad
-    return (np.concatenate(his) if his else np.zeros(0, np.float32),
-            np.concatenate(los) if los else np.zeros(0, np.float32), off, npad)
+        his.append(swizzle128_kmajor(hi.reshape(npad, Ppad)))
+        los.append(swizzle128_kmajor(lo.reshape(npad, Ppad)))
+        tc_off[u] = cur
+        tc_npad[u] = npad
+        tc_w_off[u] = wcols
+        cur += npad * Ppad
+        wcols += npad
+        groups.append((u, kids))
+    T = len(sqw_per_node)
+    tc_w = np.zeros((T, max(wcols, 1)), np.float32)
+    for t in range(T):
+        for u, kids in groups:
+            for v in kids:
+                a0 = tc_w_off[u] + tc_child_col[v]
+                w = sqw_per_node[t][v]
+                tc_w[t, a0:a0 + w.size] = w.astype(np.float32)
+    return dict(tc_hi=np.concatenate(his) if his else np.zeros(0, np.float32),
+                tc_lo=np.concatenate(los) if los else np.zeros(0, np.float32),
+                tc_off=tc_off, tc_npad=tc_npad, tc_child_col=tc_child_col,
+                tc_w=tc_w, tc_w_off=tc_w_off, tc_w_cols=max(wcols, 1))
 
 
 def pack_plan(model, tree, betas, with_tc: bool = True) -> dict:
@@ -140,8 +173,10 @@ def pack_plan(model, tree, betas, with_tc: bool = True) -> dict:
     mcols = int(mrank.sum())
     shrink = np.zeros((T, max(mcols, 1)))
     gtail = np.zeros((T, K))
+    sqw_nodes = []
     for t, beta in enumerate(betas):
         sc = score_constants(comps, float(beta))
+        sqw_nodes.append(sc.sq_weight)
         node_const[t] = sc.const
         node_nu_tail[t] = sc.nu_tail
         for u in bl:
@@ -159,13 +194,7 @@ def pack_plan(model, tree, betas, with_tc: bool = True) -> dict:
                node_nu_tail=node_nu_tail, grp_sqw=grp_sqw, mrank=mrank, mcol=mcol, moff=moff,
                mbasis=mbasis, mcols=mcols, shrink=shrink, gtail=gtail, blocks=bl)
     if with_tc:
-        hi, lo, off, npad = tc_images(bl, P)
-        tc_off = np.zeros(n, np.int64)
-        tc_npad = np.zeros(n, np.int32)
-        for u in off:
-            tc_off[u] = off[u]
-            tc_npad[u] = npad[u]
-        out.update(tc_hi=hi, tc_lo=lo, tc_off=tc_off, tc_npad=tc_npad)
+        out.update(tc_images(topo, comps, P, sqw_nodes))
     # per-leaf path costs for the reference's counters (tree.py:413-427)
     out["path_evals"], out["path_mults"] = _path_costs(topo, rank, P)
     return out
@@ -242,6 +271,10 @@ class DevicePlan:
             d.grp_tc_len = keep["th"].size
             d.grp_tc_off = _c(arr("to", h["tc_off"], np.int64), C.c_int64)
             d.grp_tc_npad = _c(arr("tn", h["tc_npad"], np.int32), C.c_int32)
+            d.grp_tc_child_col = _c(arr("tcc", h["tc_child_col"], np.int32), C.c_int32)
+            d.grp_tc_w = _c(arr("tw", h["tc_w"], np.float32), C.c_float)
+            d.grp_tc_w_off = _c(arr("two", h["tc_w_off"], np.int32), C.c_int32)
+            d.grp_tc_w_cols = int(h["tc_w_cols"])
         handle = C.c_void_p()
         N.call("fepll_plan_create", C.byref(d), C.byref(handle))
         self.handle = handle
