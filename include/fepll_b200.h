@@ -101,11 +101,13 @@ int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32
  * to exact FP64 re-scoring; dst: device int32[64]. */
 int fepll_select_rescored(fepll_plan_t plan, int32_t* dst, void* stream);
 
-/* gmm.py:352-359 / solver.py:233-241: Wiener estimates of the patches under
- * their labels, grouped by label (uses the segments of the last select). */
+/* gmm.py:352-359 / solver.py:233-241: FP64 Wiener estimates of the patches
+ * under their labels, grouped by label (the leaf buckets of the last select).
+ * With Z64 (the FP64 patch rows of fepll_extract) it runs on the FP64 tensor
+ * cores (DMMA); otherwise it re-extracts the patches from x. */
 int fepll_wiener(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32_t W,
-                 const int32_t* anchors, int32_t n_img, const double* dc, int64_t n_total,
-                 double* Zhat, void* stream);
+                 const int32_t* anchors, int32_t n_img, const double* dc, const double* Z64,
+                 int64_t n_total, double* Zhat, void* stream);
 
 /* patches.py:198-222 (+ operators.py:284-287 when kind==0):
  * per-pixel ordered gather of (Zhat + dc) over covering anchors.

@@ -48,7 +48,7 @@ _SIGS = {
     "fepll_plan_destroy": (i32, [vp]),
     "fepll_extract": (i32, [vp, i32, i32, i32, i32, vp, i32, vp, vp, i32, vp, vp, vp]),
     "fepll_select": (i32, [vp, i32, vp, i32, i32, vp, i32, vp, vp, vp, i64, i32, f64, vp, vp, vp]),
-    "fepll_wiener": (i32, [vp, i32, vp, i32, i32, vp, i32, vp, i64, vp, vp]),
+    "fepll_wiener": (i32, [vp, i32, vp, i32, i32, vp, i32, vp, vp, i64, vp, vp]),
     "fepll_select_rescored": (i32, [vp, vp, vp]),
     "fepll_aggregate": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, vp, vp, f64,
                               i32, vp, vp, vp, vp]),

@@ -371,6 +371,9 @@ int rescore_queue_x(Plan* p, const LevelArgs& a, const double* x, const int32_t*
   return kOk;
 }
 
+int wiener_dmma(Plan* p, int t, const double* Z64, double* Zhat, cudaStream_t st);
+bool wiener_dmma_supported(const Plan* p);
+
 LevelArgs make_level(Plan* p, int d, int t, int32_t* labels) {
   LevelArgs a;
   a.depth = d;
@@ -457,7 +460,8 @@ extern "C" int fepll_select_rescored(fepll_plan_t plan, int32_t* dst, void* stre
 
 extern "C" int fepll_wiener(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32_t W,
                             const int32_t* anchors, int32_t n_img, const double* dc,
-                            int64_t n_total, double* Zhat, void* stream) {
+                            const double* Z64, int64_t n_total, double* Zhat, void* stream) {
+  using namespace fepll;
   Plan* p = reinterpret_cast<Plan*>(plan);
   FEPLL_REQUIRE(p != nullptr && x != nullptr && anchors != nullptr && dc != nullptr &&
                     Zhat != nullptr,
@@ -473,6 +477,7 @@ extern "C" int fepll_wiener(fepll_plan_t plan, int32_t t, const double* x, int32
         n_total, p->rs.leafseg, p->rs.cnt, p->rs.off, p->rs.leaf_base, (int32_t*)nullptr, -1);
     FEPLL_LAUNCH();
   }
+  if (Z64 != nullptr && wiener_dmma_supported(p)) return wiener_dmma(p, t, Z64, Zhat, st);
   PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P)};
   const int P = p->v.P;
   const int rmax = p->max_model_rank;

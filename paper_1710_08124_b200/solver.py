@@ -189,6 +189,8 @@ class Restorer:
         f64 = torch.float64
         self.anchors = [torch.from_numpy(g[0]).to(dev) for g in self._grids]
         self.z32_pitch = ((P + 31) // 32) * 32
+        # FP64 patch rows (kernel (a) output) feed the DMMA Wiener kernel
+        self.Z64 = torch.empty((B * n, P), dtype=f64, device=dev)
         # FP32 patch rows (kernel (a) output) feed the tensor-core scorer
         self.Z32 = (torch.empty((B * n, self.z32_pitch), dtype=torch.float32, device=dev)
                     if mode == "tensor" else None)
@@ -284,7 +286,7 @@ class Restorer:
         mode = self.MODES[self.mode]
         self._mark(timer, "start")
         N.call("fepll_extract", N.ptr(self.x), B, H, W, side, N.ptr(anchors), n,
-               None, N.ptr(self.Z32), self.z32_pitch, N.ptr(self.dc), N.ptr(self.sq), st)
+               N.ptr(self.Z64), N.ptr(self.Z32), self.z32_pitch, N.ptr(self.dc), N.ptr(self.sq), st)
         self._mark(timer, "extract")
         N.call("fepll_select", self.plan.handle, t, N.ptr(self.x), H, W, N.ptr(anchors), n,
                N.ptr(self.dc), N.ptr(self.sq), N.ptr(self.Z32), nt, mode, float(self.guard),
@@ -292,7 +294,7 @@ class Restorer:
         N.call("fepll_select_rescored", self.plan.handle, N.ptr(self.rescored[t]), st)
         self._mark(timer, "select")
         N.call("fepll_wiener", self.plan.handle, t, N.ptr(self.x), H, W, N.ptr(anchors), n,
-               N.ptr(self.dc), nt, N.ptr(self.Zhat), st)
+               N.ptr(self.dc), N.ptr(self.Z64), nt, N.ptr(self.Zhat), st)
         self._mark(timer, "wiener")
         bs2 = float(self.betas[t]) * self.sigma * self.sigma
         N.call("fepll_aggregate", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(anchors), nr, nc,
