@@ -52,6 +52,13 @@ _SIGS = {
     "fepll_select_rescored": (i32, [vp, vp, vp]),
     "fepll_aggregate": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, vp, vp, f64,
                               i32, vp, vp, vp, vp]),
+    "fepll_op_create": (i32, [i32, i32, i32, i32, vp, i32, i32, vp, C.POINTER(vp)]),
+    "fepll_op_destroy": (i32, [vp]),
+    "fepll_op_adjoint": (i32, [vp, vp, vp, vp]),
+    "fepll_op_lambda": (i32, [vp, vp, f64, f64, C.POINTER(f64), C.POINTER(f64)]),
+    "fepll_op_init": (i32, [vp, vp, vp, f64, f64, f64, i32, vp, vp, vp]),
+    "fepll_op_solve": (i32, [vp, vp, vp, f64, f64, i32, vp, vp, vp, vp]),
+    "fepll_op_normal": (i32, [vp, vp, f64, vp, vp]),
 }
 
 _lib = None

@@ -28,6 +28,7 @@ from .errors import DataError, NumericalError
 from .gmm import score_flat_cost, wiener_flat_cost
 from .operators import CgConfig
 from .patches import axis_anchors, jitter_rng, jittered_grid, regular_grid
+from .device_ops import DeviceOperator
 from .plan import DevicePlan
 
 __all__ = ["RestorationConfig", "IterationStats", "SolverStats", "beta_schedule",
@@ -170,14 +171,18 @@ class Restorer:
         if not config.use_flat_tail and not bool(np.all(
                 [c.kept_basis.shape[1] == P for c in model.components])):
             raise DataError("flat tail disabled: a full-rank model is required")
-        if A.solve_strategy != "pixel_diagonal":
-            raise DataError(f"{A.kind} operators are not built on the device yet")
+        A.solve_strategy  # validates the kind
         self.P, self.side = P, side
         self.H, self.W = (int(v) for v in A.input_dims)
         self.mode = mode
         self.guard = guard
         self.sigma = max(config.sigma, SIGMA_FLOOR_8BIT) / 255.0
-        self.lam = float(lam) if lam is not None else self._lambda()
+        self.op = DeviceOperator(A)
+        self.l2sq = None
+        if lam is None:
+            self.lam, self.l2sq = self.op.lambda_param(self.sigma)
+        else:
+            self.lam = float(lam)
         self.betas = beta_schedule(self.sigma, self.lam, config.beta_multipliers)
         self.plan = DevicePlan(model, tree, self.betas, with_tc=(mode == "tensor"))
         self._grids = [self._grid(t) for t in range(config.iterations)]
@@ -208,29 +213,16 @@ class Restorer:
         self.diag = None
         if kind in ("mask", "gain"):
             pm = np.asarray(A.pixel_map, dtype=np.float64)
-            d = pm if kind == "mask" else pm * pm
+            d = (pm != 0).astype(np.float64) if kind == "mask" else pm * pm
             self.diag = torch.from_numpy(np.ascontiguousarray(np.broadcast_to(d, (B, H, W)))).to(dev)
-            self.pixel_map = torch.from_numpy(np.ascontiguousarray(pm)).to(dev)
         self.aty = torch.empty((B, H, W), dtype=f64, device=dev)
+        self.pixel_kind = A.solve_strategy == "pixel_diagonal"
+        # rhs of the FFT / CG image update and the solver infos
+        self.rhs = None if self.pixel_kind else torch.empty((B, H, W), dtype=f64, device=dev)
+        self.solve_info = torch.zeros((config.iterations, B, 4), dtype=f64, device=dev)
+        self.init_info = torch.zeros((B, 4), dtype=f64, device=dev)
 
     # ---------------------------------------------------------------- setup
-    def _lambda(self) -> float:
-        """lambda = min(||A^T A||_F^2 / (N ||A||_2^2), 250 sigma^2)
-        (`pkg/src/fepll/operators.py:342-355`).  Pixel-diagonal kinds: the
-        power iteration on diag(A^T A) converges to max(diag) after one
-        step from a dense start, so ||A||_2^2 = max(diag)."""
-        A = self.A
-        H, W = self.H, self.W
-        if A.kind == "identity":
-            frob, l2 = float(H * W), 1.0
-        else:
-            pm = np.asarray(A.pixel_map, dtype=np.float64)
-            d = pm if A.kind == "mask" else pm * pm
-            frob, l2 = float(np.sum(d ** 2)), float(d.max())
-        if frob == 0.0 or l2 <= 0.0:
-            raise DataError("zero operator has no coupling parameter")
-        return min(frob / (H * W * l2), 250.0 * self.sigma * self.sigma)
-
     def _grid(self, t: int):
         c = self.config
         H, W, P, s = self.H, self.W, self.P, c.spacing
@@ -251,13 +243,20 @@ class Restorer:
         torch = self.torch
         st = torch.cuda.current_stream(self.device).cuda_stream
         A = self.A
+        self.status.zero_()
+        self._mark(timer, "start")
         if A.kind == "identity":
+            # solver.py:195-196: x0 = y; A^T y = y
             self.aty.copy_(y_dev)
             self.x.copy_(y_dev)
         else:
-            torch.mul(y_dev, self.pixel_map, out=self.aty)
-            raise DataError("init_estimate for pixel kinds lands with the CG kernels")
-        self.status.zero_()
+            cg = self.config.cg
+            for b in range(self.batch):
+                self.op.adjoint(y_dev[b], self.aty[b], st)
+                # solver.py:198 -> operators.py:374-394
+                self.op.init(y_dev[b], self.aty[b], self.sigma, self.lam, cg.tolerance,
+                             cg.max_iterations, self.x[b], self.init_info[b], st)
+        self._mark(timer, "init")
         records = []
         for t in range(len(self.betas)):
             self._iteration(t, st, timer)
@@ -297,10 +296,22 @@ class Restorer:
                N.ptr(self.dc), N.ptr(self.Z64), nt, N.ptr(self.Zhat), st)
         self._mark(timer, "wiener")
         bs2 = float(self.betas[t]) * self.sigma * self.sigma
-        N.call("fepll_aggregate", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(anchors), nr, nc,
-               self.config.spacing, half, side, B, H, W, N.ptr(self.aty), N.ptr(self.diag),
-               bs2, 0, N.ptr(self.x), N.ptr(self.xt), N.ptr(self.status), st)
-        self._mark(timer, "aggregate")
+        if self.pixel_kind:
+            # reproject + pixel-diagonal update fused (patches.py:198-222, operators.py:281-287)
+            N.call("fepll_aggregate", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(anchors), nr, nc,
+                   self.config.spacing, half, side, B, H, W, N.ptr(self.aty), N.ptr(self.diag),
+                   bs2, 0, N.ptr(self.x), N.ptr(self.xt), N.ptr(self.status), st)
+            self._mark(timer, "aggregate")
+        else:
+            N.call("fepll_aggregate", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(anchors), nr, nc,
+                   self.config.spacing, half, side, B, H, W, N.ptr(self.aty), None,
+                   bs2, 1, N.ptr(self.rhs), N.ptr(self.xt), N.ptr(self.status), st)
+            self._mark(timer, "aggregate")
+            cg = self.config.cg
+            for b in range(B):
+                self.op.solve(self.rhs[b], self.xt[b], bs2, cg.tolerance, cg.max_iterations,
+                              self.x[b], self.solve_info[t, b], self.status, st)
+            self._mark(timer, "image_solve")
 
     @staticmethod
     def phase_times(timer: dict) -> dict:
@@ -332,6 +343,18 @@ class Restorer:
             raise DataError("reprojection target has uncovered pixels")
         if s & 2:
             raise NumericalError("non-finite image estimate")
+        if not self.pixel_kind and self.A.kind == "decimate":
+            finite = self.solve_info[:, :, 3].cpu().numpy()
+            if np.any(finite == 0):
+                raise NumericalError("non-finite image estimate")
+
+    def solve_infos(self):
+        """(converged, residual) per iteration (first image), the
+        `SolveInfo` fields the reference records (solver.py:252-253)."""
+        if self.pixel_kind or self.A.kind == "convolution":
+            return [(True, 0.0)] * len(self.betas)
+        si = self.solve_info.cpu().numpy()
+        return [(bool(si[t, 0, 2] > 0), float(si[t, 0, 1])) for t in range(si.shape[0])]
 
 
 def restore(y, A, model, tree=None, config=None, *, mode: str = "tensor", lam=None):
@@ -370,8 +393,10 @@ def restore_batch(ys, A, model, tree=None, config=None, *, mode: str = "tensor",
     r.check_status()
     stats = SolverStats(lam=r.lam)
     stats.init_seconds = t1 - t0
+    infos = r.solve_infos()
     for t, (npatch, ev, sm, em) in enumerate(r.counters()):
         it = IterationStats(beta=float(r.betas[t]), patches=npatch // max(r.batch, 1),
+                            image_solve_converged=infos[t][0], image_solve_residual=infos[t][1],
                             score_evaluations=ev, selection_multiplies=sm,
                             estimation_multiplies=em)
         stats.iterations.append(it)
