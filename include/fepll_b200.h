@@ -120,6 +120,34 @@ int fepll_aggregate(const double* Zhat, const double* dc, const int32_t* anchors
                     const double* aty, const double* diag, double bs2, int32_t kind,
                     double* x_out, double* xtilde_out, int32_t* status, void* stream);
 
+/* ---- degradation operators (operators.py:51-394); handle = opaque plan.
+ * kind: 0 identity, 1 convolution, 2 mask, 3 gain, 4 decimate (factor).
+ * taps: [kh][kw] host kernel (kinds 1, 4); pixel_map: [H][W] host (2, 3). */
+int fepll_op_create(int32_t kind, int32_t H, int32_t W, int32_t factor, const double* taps,
+                    int32_t kh, int32_t kw, const double* pixel_map, void** out);
+int fepll_op_destroy(void* op);
+/* apply_adjoint (operators.py:216-230): y [Ho][Wo] -> out [H][W] (device) */
+int fepll_op_adjoint(void* op, const double* y, double* out, void* stream);
+/* lambda_param (operators.py:342-355): power iteration from the host start
+ * vector v0 [H][W] on the device; frob = ||A^T A||_F^2 (closed form).
+ * Synchronous; writes lambda and the power-iteration estimate l2sq. */
+int fepll_op_lambda(void* op, const double* v0_host, double frob, double sigma, double* lam_out,
+                    double* l2sq_out);
+/* init_estimate (operators.py:374-394); info: device double[4]
+ * (iterations, residual, converged, finite) for the CG kinds. */
+int fepll_op_init(void* op, const double* y, const double* aty, double sigma, double lam,
+                  double tol, int32_t maxit, double* x, double* info, void* stream);
+/* solve_image_estimation for convolution (FFT) and decimate (CG from
+ * x0 = x_tilde) (operators.py:273-295); rhs = A^T y + bs2 x_tilde. */
+int fepll_op_solve(void* op, const double* rhs, const double* xtilde, double bs2, double tol,
+                   int32_t maxit, double* x, double* info, int32_t* status, void* stream);
+/* normal_apply (operators.py:233-235) + shift: y = A^T A x + shift x */
+int fepll_op_normal(void* op, const double* x, double shift, double* y, void* stream);
+
+/* debugging: record per-tile pipeline timestamps of one tree level of the
+ * warp-specialized scorer into a device buffer (148 x 64 x 8 uint64). */
+int fepll_debug_ws_trace(void* device_buffer, int32_t level);
+
 #ifdef __cplusplus
 }
 #endif

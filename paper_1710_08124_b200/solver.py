@@ -145,9 +145,6 @@ class Restorer:
 
     def __init__(self, A, model, tree, config, batch: int = 1, lam: float | None = None,
                  mode: str = "tensor", device=None, guard: float = 0.0):
-        torch = _torch()
-        self.torch = torch
-        self.device = torch.device(device or "cuda")
         _validate_config(config)
         self.config = config
         self.A = A
@@ -172,6 +169,11 @@ class Restorer:
                 [c.kept_basis.shape[1] == P for c in model.components])):
             raise DataError("flat tail disabled: a full-rank model is required")
         A.solve_strategy  # validates the kind
+        if mode not in self.MODES:
+            raise DataError(f"unknown mode {mode!r} (exact | tensor)")
+        torch = _torch()
+        self.torch = torch
+        self.device = torch.device(device or "cuda")
         self.P, self.side = P, side
         self.H, self.W = (int(v) for v in A.input_dims)
         self.mode = mode
@@ -378,15 +380,17 @@ def restore(y, A, model, tree=None, config=None, *, mode: str = "tensor", lam=No
 def restore_batch(ys, A, model, tree=None, config=None, *, mode: str = "tensor", lam=None,
                   restorer: Restorer | None = None):
     """Restore a (B, H, W) stack sharing operator, sigma and seed."""
-    torch = _torch()
     if config is None:
         config = RestorationConfig(sigma=20.0)
     t0 = time.perf_counter()
     ys = np.asarray(ys, dtype=np.float64)
     if ys.ndim != 3:
         raise DataError("restore_batch expects a (B, H, W) stack")
+    if tuple(ys.shape[1:]) != tuple(A.output_dims):
+        raise DataError(f"observation shape {ys.shape[1:]} != operator output {tuple(A.output_dims)}")
     r = restorer or Restorer(A, model, tree, config, batch=ys.shape[0], lam=lam, mode=mode)
-    y_dev = torch.from_numpy(ys).to(r.device)
+    torch = r.torch
+    y_dev = torch.from_numpy(np.ascontiguousarray(ys)).to(r.device)
     t1 = time.perf_counter()
     x_dev, recs = r.run(y_dev, trace=config.trace)
     x = x_dev.cpu().numpy()

@@ -1,38 +1,247 @@
-"""Device path vs the golden vectors and the live oracle (needs a B200)."""
+"""Device path vs the reference's golden vectors and the live CPU oracle.
+
+Parity bar (BASELINE.json north_star): >= 99.9% of selected labels,
+restored RMSE <= 1e-3 on the [0,255] scale, |dPSNR| <= 0.01 dB.  The exact
+(FP64) path must additionally reproduce every label and counter; the
+tensor path must too, because its argmin is certified (tc_epi.cuh) and the
+uncertified decisions are re-scored in FP64.
+"""
 
 import numpy as np
 import pytest
-from conftest import golden_inputs
+from conftest import golden_inputs, load_golden
 
 import fepll_oracle as O
 
 pytestmark = pytest.mark.gpu
 
+RMSE_TOL = 1e-3      # on [0, 255]
+PSNR_TOL = 0.01      # dB
+LABEL_TOL = 0.999
 
-def _rmse255(a, b):
+
+def rmse255(a, b):
     return 255.0 * float(np.sqrt(np.mean((np.asarray(a) - np.asarray(b)) ** 2)))
 
 
-def _psnr(x, ref):
-    mse = float(np.mean((np.clip(x, 0, 1) - ref) ** 2))
-    return 10 * np.log10(1.0 / mse)
+def psnr(x, ref):
+    return 10 * np.log10(1.0 / float(np.mean((np.clip(x, 0, 1) - ref) ** 2)))
+
+
+GOLDEN = ["cfg1", "regular48", "gain64", "inpaint96", "deblur96", "sr96"]
 
 
 @pytest.mark.parametrize("mode", ["exact", "tensor"])
-@pytest.mark.parametrize("name", ["cfg1", "gain64", "regular48"])
-def test_restore_matches_golden(name, mode, models):
+@pytest.mark.parametrize("name", GOLDEN)
+def test_restore_matches_reference_golden(name, mode, models):
     from paper_1710_08124_b200 import RestorationConfig, restore
 
     g, A, y, s8, s, P = golden_inputs(name)
-    meta = g["meta"]
     model, tree = models[P]
-    cfg = RestorationConfig(sigma=s8, spacing=s, seed=0, trace=True, sampling=meta["sampling"])
+    cfg = RestorationConfig(sigma=s8, spacing=s, seed=0, trace=True, sampling=g["meta"]["sampling"])
     x, st = restore(y, A, model, tree, cfg, mode=mode)
-    agree = [float(np.mean(rec["selected"] == g["labels"][t])) for t, rec in enumerate(st.trace)]
-    assert min(agree) >= 0.999, agree
-    assert _rmse255(x, g["x"]) <= 1e-3
-    if mode == "exact":
-        assert min(agree) == 1.0
-        assert [it.score_evaluations for it in st.iterations] == list(g["evals"])
-        assert [it.selection_multiplies for it in st.iterations] == list(g["sel_mults"])
-        assert [it.estimation_multiplies for it in st.iterations] == list(g["est_mults"])
+    assert st.lam == pytest.approx(float(g["lam"]), rel=1e-10)
+    for t, rec in enumerate(st.trace):
+        np.testing.assert_array_equal(rec["selected"], g["labels"][t])
+    assert rmse255(x, g["x"]) <= RMSE_TOL
+    assert [it.score_evaluations for it in st.iterations] == list(g["evals"])
+    assert [it.selection_multiplies for it in st.iterations] == list(g["sel_mults"])
+    assert [it.estimation_multiplies for it in st.iterations] == list(g["est_mults"])
+    assert [it.image_solve_converged for it in st.iterations] == list(g["converged"])
+    assert [it.patches for it in st.iterations] == list(g["patches"])
+
+
+@pytest.mark.parametrize("cfg_name", ["cfg2", "cfg4a", "cfg3", "cfg4b"])
+def test_full_size_configs_vs_live_oracle(cfg_name, models):
+    """BASELINE configs 2-4 at full size.  The oracle's lambda comes from its
+    own power iteration except for cfg3 (cap active, checked separately)."""
+    from paper_1710_08124_b200 import RestorationConfig, restore, synthetic
+
+    c = synthetic.baseline_case(cfg_name)
+    model, tree = models[c.patch_dim]
+    cfg = RestorationConfig(sigma=c.sigma8, spacing=c.spacing, seed=0, trace=True)
+    x, st = restore(c.y, c.A, model, tree, cfg, mode="tensor")
+    lam = st.lam if cfg_name == "cfg3" else None
+    xo, so = O.restore(c.y, c.A, model, tree, sigma=c.sigma8, spacing=c.spacing, seed=0,
+                       trace=True, lam=lam)
+    if lam is None:
+        assert st.lam == pytest.approx(so.lam, rel=1e-9)
+    else:
+        assert st.lam == pytest.approx(250.0 * (c.sigma8 / 255.0) ** 2, rel=1e-12)
+    agree = [float(np.mean(a["selected"] == b["selected"])) for a, b in zip(st.trace, so.trace)]
+    assert min(agree) >= LABEL_TOL, agree
+    assert rmse255(x, xo) <= RMSE_TOL
+    assert abs(psnr(x, c.clean) - psnr(xo, c.clean)) <= PSNR_TOL
+
+
+def test_same_seed_bit_identical_and_batch_equals_single(models):
+    from paper_1710_08124_b200 import RestorationConfig, restore, restore_batch, synthetic
+
+    model, tree = models[64]
+    cases = [synthetic.baseline_case("cfg1", 96, image_seed=i, noise_seed=10 + i) for i in range(3)]
+    cfg = RestorationConfig(sigma=20.0, spacing=4, seed=3)
+    singles = [restore(c.y, c.A, model, tree, cfg)[0] for c in cases]
+    again = restore(cases[0].y, cases[0].A, model, tree, cfg)[0]
+    assert np.array_equal(singles[0], again)
+    xb, _ = restore_batch(np.stack([c.y for c in cases]), cases[0].A, model, tree, cfg)
+    for i in range(3):
+        assert np.array_equal(xb[i], singles[i])
+
+
+@pytest.mark.parametrize("H,W,s", [(41, 53, 3), (40, 40, 8), (33, 47, 1), (8, 8, 6)])
+def test_edge_geometries_vs_oracle(H, W, s, models):
+    """Odd sizes, spacing == side (no jitter), spacing 1, a single anchor."""
+    from paper_1710_08124_b200 import RestorationConfig, identity_operator, restore, synthetic
+
+    model, tree = models[64]
+    img = synthetic.synthetic_image(H, W, 5) / 255.0
+    y = img + (20.0 / 255.0) * np.random.default_rng(7).standard_normal((H, W))
+    A = identity_operator((H, W))
+    cfg = RestorationConfig(sigma=20.0, spacing=s, seed=11, trace=True)
+    x, st = restore(y, A, model, tree, cfg)
+    xo, so = O.restore(y, A, model, tree, sigma=20.0, spacing=s, seed=11, trace=True)
+    for a, b in zip(st.trace, so.trace):
+        np.testing.assert_array_equal(a["selected"], b["selected"])
+    assert rmse255(x, xo) <= RMSE_TOL
+
+
+def test_noiseless_passthrough_and_unclamped(models):
+    """solver.py sigma floor: sigma=0 returns ~y; output is not clamped."""
+    from paper_1710_08124_b200 import RestorationConfig, identity_operator, restore, synthetic
+
+    model, tree = models[64]
+    y = synthetic.synthetic_image(48, 48, 1) / 255.0 + 0.5
+    A = identity_operator(y.shape)
+    x, st = restore(y, A, model, tree, RestorationConfig(sigma=0.0, spacing=4))
+    xo, so = O.restore(y, A, model, tree, sigma=0.0, spacing=4)
+    assert st.lam == pytest.approx(so.lam) and st.iterations[0].beta == pytest.approx(so.betas[0])
+    assert rmse255(x, xo) <= RMSE_TOL
+    assert np.sqrt(np.mean((x - y) ** 2)) < 5e-3   # floor sigma = 0.5/255: near pass-through
+    assert x.max() > 1.0
+
+
+def test_nonfinite_input_raises_numerical_error(models):
+    from paper_1710_08124_b200 import NumericalError, RestorationConfig, identity_operator, restore
+
+    model, tree = models[64]
+    y = np.full((32, 32), 0.5)
+    y[3, 4] = np.nan
+    with pytest.raises(NumericalError):
+        restore(y, identity_operator(y.shape), model, tree, RestorationConfig(sigma=20.0, spacing=4))
+
+
+# ---------------------------------------------------------------- kernel-level parity (C ABI)
+def _dev(a, dtype=None):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=dtype)).cuda()
+
+
+def test_extract_kernel_bitwise():
+    import torch
+    from paper_1710_08124_b200 import _native as N, jitter_rng, jittered_grid
+
+    for P, H, W, s in [(64, 70, 61, 3), (100, 64, 64, 6), (36, 30, 40, 2)]:
+        side = int(np.sqrt(P))
+        x = np.random.default_rng(P).random((H, W))
+        pos = jittered_grid(H, W, P, s, jitter_rng(1, 2)).positions.astype(np.int32)
+        n = pos.shape[0]
+        Zo, dco = O.extract(x, pos.astype(np.int64), side)
+        pitch = (P + 31) // 32 * 32
+        Z64 = torch.empty((n, P), dtype=torch.float64, device="cuda")
+        Z32 = torch.empty((n, pitch), dtype=torch.float32, device="cuda")
+        dc = torch.empty(n, dtype=torch.float64, device="cuda")
+        sq = torch.empty(n, dtype=torch.float64, device="cuda")
+        xd, pd = _dev(x), _dev(pos)  # keep the device inputs alive across the async launch
+        N.call("fepll_extract", N.ptr(xd), 1, H, W, side, N.ptr(pd), n, N.ptr(Z64),
+               N.ptr(Z32), pitch, N.ptr(dc), N.ptr(sq), torch.cuda.current_stream().cuda_stream)
+        np.testing.assert_array_equal(dc.cpu().numpy(), dco)           # pairwise fold, bitwise
+        np.testing.assert_array_equal(Z64.cpu().numpy(), Zo)
+        np.testing.assert_array_equal(Z32.cpu().numpy()[:, :P], Zo.astype(np.float32))
+        assert not Z32.cpu().numpy()[:, P:].any()
+        np.testing.assert_allclose(sq.cpu().numpy(), np.einsum("ij,ij->i", Zo, Zo), rtol=1e-13)
+
+
+def test_aggregate_kernel_bitwise_vs_bincount():
+    """Fed the reference's estimates, the ordered gather reproduces
+    np.bincount's sums bit for bit (patches.py:198-222)."""
+    import torch
+    from paper_1710_08124_b200 import _native as N, jitter_rng, jittered_grid
+    from paper_1710_08124_b200.patches import axis_anchors
+
+    for P, H, W, s in [(64, 70, 61, 3), (100, 64, 64, 6), (64, 40, 40, 1)]:
+        side = int(np.sqrt(P))
+        pos = jittered_grid(H, W, P, s, jitter_rng(4, 1)).positions.astype(np.int32)
+        n = pos.shape[0]
+        rng = np.random.default_rng(2)
+        est = rng.standard_normal((n, P))
+        dc = rng.standard_normal(n)
+        ref = O.reproject(est, dc, pos.astype(np.int64), side, H, W)
+        xt = torch.empty((1, H, W), dtype=torch.float64, device="cuda")
+        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        ed, dd, pd = _dev(est), _dev(dc), _dev(pos)
+        N.call("fepll_aggregate", N.ptr(ed), N.ptr(dd), N.ptr(pd),
+               axis_anchors(H, side, s).size, axis_anchors(W, side, s).size, s, (side - s) // 2,
+               side, 1, H, W, None, None, 1.0, 1, None, N.ptr(xt), N.ptr(status),
+               torch.cuda.current_stream().cuda_stream)
+        np.testing.assert_array_equal(xt.cpu().numpy()[0], ref)
+        assert int(status.item()) == 0
+
+
+def test_lo_eq_hi_rule_returns_common_value():
+    """Identical overlapping contributions come back verbatim (patches.py:221)."""
+    import torch
+    from paper_1710_08124_b200 import _native as N
+
+    H = W = 8
+    pos = np.array([[0, 0], [0, 0]], np.int32)
+    v = np.full((2, 64), 0.1)
+    dc = np.array([0.2, 0.2])
+    xt = torch.empty((1, H, W), dtype=torch.float64, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    # two anchors at the same place: nominal grid of 2 rows x 1 col, spacing 8
+    vd, dd, pd = _dev(v), _dev(dc), _dev(pos)
+    N.call("fepll_aggregate", N.ptr(vd), N.ptr(dd), N.ptr(pd), 1, 2, 8, 0, 8, 1,
+           H, W, None, None, 1.0, 1, None, N.ptr(xt), N.ptr(status),
+           torch.cuda.current_stream().cuda_stream)
+    assert np.all(xt.cpu().numpy() == 0.1 + 0.2)
+
+
+def test_uncovered_pixel_raises_data_error():
+    import torch
+    from paper_1710_08124_b200 import _native as N
+
+    H = W = 16
+    pos = np.array([[0, 0]], np.int32)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    xt = torch.empty((1, H, W), dtype=torch.float64, device="cuda")
+    zd, dd, pd = _dev(np.zeros((1, 16))), _dev(np.zeros(1)), _dev(pos)
+    N.call("fepll_aggregate", N.ptr(zd), N.ptr(dd), N.ptr(pd), 1, 1, 4, 0, 4, 1, H, W, None, None, 1.0, 1, None, N.ptr(xt),
+           N.ptr(status), torch.cuda.current_stream().cuda_stream)
+    assert int(status.item()) & 1
+
+
+@pytest.mark.parametrize("name", ["deblur96", "sr96", "inpaint96", "gain64"])
+def test_operator_adjoint_identity_and_normal(name):
+    """<A x, y> == <x, A^T y> through the device A^T, and A^T A vs the oracle."""
+    import torch
+    from paper_1710_08124_b200.device_ops import DeviceOperator
+
+    _, A, *_ = golden_inputs(name)
+    op = DeviceOperator(A)
+    o = O.Op(A)
+    rng = np.random.default_rng(5)
+    st = torch.cuda.current_stream().cuda_stream
+    for _ in range(5):
+        x = rng.standard_normal(A.input_dims)
+        y = rng.standard_normal(A.output_dims)
+        aty = torch.empty(A.input_dims, dtype=torch.float64, device="cuda")
+        yd, xd = _dev(y), _dev(x)
+        op.adjoint(yd, aty, st)
+        np.testing.assert_allclose(aty.cpu().numpy(), o.adjoint(y), rtol=0, atol=1e-12)
+        lhs = float(np.vdot(o.apply(x), y))
+        rhs = float(np.vdot(x, aty.cpu().numpy()))
+        assert abs(lhs - rhs) <= 1e-10 * max(1.0, abs(lhs))
+        nx = torch.empty(A.input_dims, dtype=torch.float64, device="cuda")
+        op.normal(xd, 0.5, nx, st)
+        np.testing.assert_allclose(nx.cpu().numpy(), o.normal(x) + 0.5 * x, rtol=0, atol=1e-12)
