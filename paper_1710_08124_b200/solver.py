@@ -261,6 +261,7 @@ class Restorer:
         self._mark(timer, "init")
         records = []
         for t in range(len(self.betas)):
+            self._want_xt = trace
             self._iteration(t, st, timer)
             if trace:
                 B, n = self.batch, self.n
@@ -302,7 +303,7 @@ class Restorer:
             # reproject + pixel-diagonal update fused (patches.py:198-222, operators.py:281-287)
             N.call("fepll_aggregate", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(anchors), nr, nc,
                    self.config.spacing, half, side, B, H, W, N.ptr(self.aty), N.ptr(self.diag),
-                   bs2, 0, N.ptr(self.x), N.ptr(self.xt), N.ptr(self.status), st)
+                   bs2, 0, N.ptr(self.x), N.ptr(self.xt) if self._want_xt else None, N.ptr(self.status), st)
             self._mark(timer, "aggregate")
         else:
             N.call("fepll_aggregate", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(anchors), nr, nc,
