@@ -77,8 +77,8 @@ static int create(const fepll_plan_desc* d, Plan** out) {
     return kDataError;
   }
   for (int dd = 0; dd <= maxd; ++dd) {
-    if (p->level_start[dd + 1] - p->level_start[dd] > 1024) {
-      set_error("a tree level holds more than 1024 nodes");
+    if (p->level_start[dd + 1] - p->level_start[dd] > 512) {
+      set_error("a tree level holds more than 512 nodes");
       delete p;
       return kDataError;
     }

@@ -14,7 +14,7 @@
 
 namespace fepll {
 
-constexpr int kMaxLevelNodes = 1024;  // nodes per depth handled in smem
+constexpr int kMaxLevelNodes = 512;  // nodes per depth handled in smem
 
 struct LevelArgs {
   int depth;

@@ -19,6 +19,8 @@
 //                aggregated routing.
 //
 // smem (P=64, N<=128): 2 x 64 KB A stages + 64 KB B + tables; TMEM 512 cols.
+#include <algorithm>
+
 #include "route.cuh"
 #include "tc.cuh"
 #include "tc_epi.cuh"
@@ -50,8 +52,18 @@ struct EpiGroup {
   int32_t bbase[kMaxChildren + 1];
 };
 
+constexpr int kMaxNodes = 256;  // internal nodes per level handled by this kernel
+
+constexpr int kIdxAhead = 4;   // tiles of row indices in flight per producer thread
+constexpr int kIdxRing = 5;
+constexpr int kL2Ahead = 3;    // tiles whose rows are prefetched into L2
+
 struct Smem {
+  int32_t idx_ring[2][kIdxRing][kRows];  // [K atom group][slot][row]
   LevelTables lv;
+  int64_t nd_off[kMaxNodes];      // segment offset of each depth-d node (a.off)
+  int16_t nd_npad[kMaxNodes];     // padded group width
+  int16_t nd_nk[kMaxNodes];       // child count
   EpiGroup epi[kGroups];
   uint64_t a_full[kStages], a_empty[kStages], acc_full[kGroups], acc_empty[kGroups];
   uint64_t b_full, drain;
@@ -69,11 +81,12 @@ struct Args {
   int32_t* queue_len;
   int katoms;
   uint64_t* trace;       // debug timeline: [CTA][64 tiles][8] globaltimer stamps (or NULL)
+  int debug;             // experiment flags: 1 skip epilogue math, 2 skip producer stores
 };
 
 __device__ __forceinline__ uint64_t gtimer() {
   uint64_t t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));  // SM cycles (per-CTA relative timing)
   return t;
 }
 
@@ -90,23 +103,27 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 struct TileInfo {
-  int u, first, m;
+  int k, u, first, m;
 };
 
+// tile -> (level-local node k, BFS id u, first row, rows): smem only
 __device__ __forceinline__ TileInfo tile_info(const LevelArgs& a, const LevelTables& lv, int tile) {
   TileInfo ti;
-  const int k = prefix_find(lv.tpre, a.lvl_end - a.lvl_begin, tile);
-  ti.u = a.lvl_begin + k;
-  ti.first = (tile - lv.tpre[k]) * kRows;
-  ti.m = min(kRows, (lv.cpre[k + 1] - lv.cpre[k]) - ti.first);
+  ti.k = prefix_find(lv.tpre, a.lvl_end - a.lvl_begin, tile);
+  ti.u = a.lvl_begin + ti.k;
+  ti.first = (tile - lv.tpre[ti.k]) * kRows;
+  ti.m = min(kRows, (lv.cpre[ti.k + 1] - lv.cpre[ti.k]) - ti.first);
   return ti;
 }
 
-// row r of tile `tile`, K atom ka: 8 float4 into registers (zeros past m)
-__device__ __forceinline__ void load_row(const Args& args, const LevelArgs& a, const LevelTables& lv,
-                                         int tile, int row, int ka, float4 (&v)[8]) {
-  const TileInfo ti = tile_info(a, lv, tile);
-  const int g = row < ti.m ? a.seg_in[a.off[ti.u] + ti.first + row] : -1;
+// patch index of row `row` of tile `tile` (-1 past the end)
+__device__ __forceinline__ int row_patch(const LevelArgs& a, const Smem& s, int tile, int row) {
+  const TileInfo ti = tile_info(a, s.lv, tile);
+  return row < ti.m ? a.seg_in[s.nd_off[ti.k] + ti.first + row] : -1;
+}
+
+// K atom ka of patch g: 8 float4 into registers (zeros for g < 0)
+__device__ __forceinline__ void load_row(const Args& args, int g, int ka, float4 (&v)[8]) {
   if (g >= 0) {
     const float4* src = reinterpret_cast<const float4*>(args.Z32 + (int64_t)g * args.z32_pitch) + ka * 8;
 #pragma unroll
@@ -146,6 +163,12 @@ select_level_ws_kernel(PlanView pv, Args args) {
   }
   if (tid < kGroups) s.epi[tid].node = -1;
   level_tables(pv, a, s.lv, kRows);  // contains __syncthreads
+  for (int k = tid; k < a.lvl_end - a.lvl_begin; k += blockDim.x) {
+    const int u = a.lvl_begin + k;
+    s.nd_off[k] = a.off[u];
+    s.nd_npad[k] = (int16_t)pv.tc_npad[u];
+    s.nd_nk[k] = (int16_t)pv.child_count[u];
+  }
   if (tid == 0) {
     const int T = s.lv.total_tiles;
     s.t_begin = (int)(((int64_t)T * blockIdx.x) / gridDim.x);
@@ -166,13 +189,37 @@ select_level_ws_kernel(PlanView pv, Args args) {
     const int ka = warp >> 2;          // K atom of this warp
     const bool active = ka < args.katoms;
     const int r8 = row & 7;
+    // Row indices arrive kIdxAhead tiles early by cp.async into a per-thread
+    // smem ring (no register dependency), row data one tile ahead in
+    // registers.
+    int32_t* ring = s.idx_ring[ka][0];
+    auto fetch_idx = [&](int j) {  // tile t_begin + j -> ring slot j % kIdxRing
+      if (j < ntile) {
+        const TileInfo ti = tile_info(a, s.lv, t_begin + j);
+        int32_t* dst = ring + (j % kIdxRing) * kRows + row;
+        if (row < ti.m) {
+          tc::cp_async4(dst, a.seg_in + s.nd_off[ti.k] + ti.first + row);
+        } else {
+          *dst = -1;
+        }
+      }
+      tc::cp_async_commit();
+    };
     float4 v[8];
-    if (active && ntile > 0) load_row(args, a, s.lv, t_begin, row, ka, v);
+    if (active) {
+      for (int j = 0; j < kIdxAhead; ++j) fetch_idx(j);
+      tc::cp_async_wait<0>();
+      for (int j = 1; j < kL2Ahead && j < ntile; ++j) {
+        const int gp = ring[(j % kIdxRing) * kRows + row];
+        if (gp >= 0) tc::prefetch_l2(args.Z32 + (int64_t)gp * args.z32_pitch + ka * 32);
+      }
+      load_row(args, ntile > 0 ? ring[row] : -1, ka, v);
+    }
     for (int i = 0; i < ntile; ++i) {
       const int st = i % kStages;
       if (i >= kStages) tc::mbar_wait(&s.a_empty[st], ((i / kStages) - 1) & 1);
       if (tid == 0) stamp(args, i, 0);
-      if (active) {
+      if (active && !(args.debug & 2)) {
         uint8_t* A = stageA + st * kStageBytes;
         uint8_t* dhi = A + (2 * ka) * kAtomA + (row >> 3) * 1024 + r8 * 128;
         uint8_t* dlo = A + (2 * ka + 1) * kAtomA + (row >> 3) * 1024 + r8 * 128;
@@ -192,57 +239,77 @@ select_level_ws_kernel(PlanView pv, Args args) {
       if (lane == 0) mbar_arrive(&s.a_full[st]);
       if (tid == 0) stamp(args, i, 1);
       // prefetch the next tile's row while this one is consumed
-      if (active && i + 1 < ntile) load_row(args, a, s.lv, t_begin + i + 1, row, ka, v);
+      if (active && i + 1 < ntile) {
+        fetch_idx(i + kIdxAhead);
+        tc::cp_async_wait<kIdxAhead - kL2Ahead>();  // indices through tile i+kL2Ahead landed
+        if (i + kL2Ahead < ntile) {
+          const int gp = ring[((i + kL2Ahead) % kIdxRing) * kRows + row];
+          if (gp >= 0) tc::prefetch_l2(args.Z32 + (int64_t)gp * args.z32_pitch + ka * 32);
+        }
+        load_row(args, ring[((i + 1) % kIdxRing) * kRows + row], ka, v);
+      }
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      int cur = -1;
-      uint32_t b_loads = 0, drains = 0;
-      for (int i = 0; i < ntile; ++i) {
-        const int st = i % kStages;
-        const int ac = i % kGroups;
-        const TileInfo ti = tile_info(a, s.lv, t_begin + i);
-        const int npad = pv.tc_npad[ti.u];
-        if (ti.u != cur) {
-          if (i > 0) {  // every MMA reading the old B must be done
-            tc::mma_commit(&s.drain);
-            tc::mbar_wait(&s.drain, drains & 1);
-            ++drains;
-          }
-          const uint32_t half = (uint32_t)args.katoms * npad * 128u;
-          tc::mbar_arrive_expect_tx(&s.b_full, 2 * half);
-          tc::bulk_g2s(bbuf, pv.tc_hi + pv.tc_off[ti.u], half, &s.b_full);
-          tc::bulk_g2s(bbuf + half, pv.tc_lo + pv.tc_off[ti.u], half, &s.b_full);
-          tc::mbar_wait(&s.b_full, b_loads & 1);
-          ++b_loads;
-          cur = ti.u;
+    // The whole warp runs this loop (uniform values); one elected lane
+    // issues each tcgen05 instruction (tc.cuh *_warp).
+    int cur = -1;
+    uint32_t b_loads = 0, drains = 0;
+    const uint64_t a_base = tc::desc_sw128(tc::smem_u32(stageA));
+    const uint64_t b_base = tc::desc_sw128(tc::smem_u32(bbuf));
+    for (int i = 0; i < ntile; ++i) {
+      const int st = i % kStages;
+      const int ac = i % kGroups;
+      const TileInfo ti = tile_info(a, s.lv, t_begin + i);
+      const int npad = s.nd_npad[ti.k];
+      const uint32_t bhalf = (uint32_t)args.katoms * npad * 128u;
+      if (ti.u != cur) {
+        if (i > 0) {  // every MMA reading the old B must be done
+          tc::mma_commit_warp(&s.drain);
+          tc::mbar_wait(&s.drain, drains & 1);
+          ++drains;
         }
-        if (i >= kGroups) tc::mbar_wait(&s.acc_empty[ac], ((i / kGroups) - 1) & 1);
-        tc::mbar_wait(&s.a_full[st], (i / kStages) & 1);
-        tc::fence_after_sync();
-        stamp(args, i, 2);
-        const uint32_t idesc = tc::idesc_tf32(kRows, npad);
-        const uint32_t d = tmem + ac * kMaxN;
-        const uint32_t A0 = tc::smem_u32(stageA + st * kStageBytes);
-        const uint32_t B0 = tc::smem_u32(bbuf);
-        const uint32_t bhalf = (uint32_t)args.katoms * npad * 128u;
-        for (int kq = 0; kq < args.katoms; ++kq) {
-          const uint32_t a_hi = A0 + (2 * kq) * kAtomA, a_lo = A0 + (2 * kq + 1) * kAtomA;
-          const uint32_t b_hi = B0 + kq * npad * 128, b_lo = B0 + bhalf + kq * npad * 128;
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint32_t ko = kk * 32;
-            const uint32_t acc = (kq > 0 || kk > 0) ? 1u : 0u;
-            tc::mma_tf32(d, tc::desc_sw128(a_lo + ko), tc::desc_sw128(b_hi + ko), idesc, acc);
-            tc::mma_tf32(d, tc::desc_sw128(a_hi + ko), tc::desc_sw128(b_lo + ko), idesc, 1u);
-            tc::mma_tf32(d, tc::desc_sw128(a_hi + ko), tc::desc_sw128(b_hi + ko), idesc, 1u);
-          }
+        if (lane == 0) {
+          tc::mbar_arrive_expect_tx(&s.b_full, 2 * bhalf);
+          tc::bulk_g2s(bbuf, pv.tc_hi + pv.tc_off[ti.u], bhalf, &s.b_full);
+          tc::bulk_g2s(bbuf + bhalf, pv.tc_lo + pv.tc_off[ti.u], bhalf, &s.b_full);
         }
-        tc::mma_commit(&s.a_empty[st]);
-        tc::mma_commit(&s.acc_full[ac]);
-        stamp(args, i, 3);
+        __syncwarp();
+        tc::mbar_wait(&s.b_full, b_loads & 1);
+        ++b_loads;
+        cur = ti.u;
       }
+      if (lane == 0 && (args.debug & 4)) stamp(args, i, 4);
+      if (i >= kGroups) tc::mbar_wait(&s.acc_empty[ac], ((i / kGroups) - 1) & 1);
+      if (lane == 0 && (args.debug & 4)) stamp(args, i, 5);
+      tc::mbar_wait(&s.a_full[st], (i / kStages) & 1);
+      tc::fence_after_sync();
+      if (lane == 0) stamp(args, i, 2);
+      const uint32_t idesc = tc::idesc_tf32(kRows, npad);
+      const uint32_t d = tmem + ac * kMaxN;
+      // descriptor start-address field counts 16-byte units
+      const uint64_t A0 = a_base + (uint64_t)((st * kStageBytes) >> 4);
+      for (int kq = 0; kq < args.katoms; ++kq) {
+        const uint64_t a_hi = A0 + (uint64_t)(((2 * kq) * kAtomA) >> 4);
+        const uint64_t a_lo = A0 + (uint64_t)(((2 * kq + 1) * kAtomA) >> 4);
+        const uint64_t b_hi = b_base + (uint64_t)((kq * npad * 128) >> 4);
+        const uint64_t b_lo = b_base + (uint64_t)((bhalf + kq * npad * 128) >> 4);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t ko = 2 * kk;  // 8 tf32 = 32 bytes inside the swizzle atom
+          const uint32_t acc = (kq > 0 || kk > 0) ? 1u : 0u;
+          tc::mma_tf32_warp(d, a_lo + ko, b_hi + ko, idesc, acc);
+          tc::mma_tf32_warp(d, a_hi + ko, b_lo + ko, idesc, 1u);
+          tc::mma_tf32_warp(d, a_hi + ko, b_hi + ko, idesc, 1u);
+        }
+      }
+      tc::mma_commit_warp(&s.a_empty[st]);
+      tc::mma_commit_warp(&s.acc_full[ac]);
+      if (args.debug & 8) {
+        tc::mbar_wait(&s.acc_full[ac], (i / kGroups) & 1);
+        if (lane == 0) stamp(args, i, 6);
+      }
+      if (lane == 0) stamp(args, i, 3);
     }
   } else {
     // ------------------------------------------------------------ epilogue
@@ -257,9 +324,9 @@ select_level_ws_kernel(PlanView pv, Args args) {
     for (int i = grp; i < ntile; i += kGroups) {
       const TileInfo ti = tile_info(a, s.lv, t_begin + i);
       const int u = ti.u;
-      const int nk = pv.child_count[u];
+      const int nk = s.nd_nk[ti.k];
       const bool valid = row < ti.m;
-      const int g = valid ? a.seg_in[a.off[u] + ti.first + row] : -1;
+      const int g = valid ? a.seg_in[s.nd_off[ti.k] + ti.first + row] : -1;
       const double sqv = valid ? args.sq[g] : 0.0;
       if (u != E.node) {
         named_bar(bar_id, 128);  // everyone done with the previous tables
@@ -269,13 +336,14 @@ select_level_ws_kernel(PlanView pv, Args args) {
       }
       tc::mbar_wait(&s.acc_full[grp], (i / kGroups) & 1);
       tc::fence_after_sync();
-      if (etid == 0) stamp(args, i, 4);
+      if (etid == 0 && !(args.debug & 4)) stamp(args, i, 4);
       bool flagged;
-      const int bi = epi_score_row(E.ch, nk, d_acc, sqv, guard, &flagged);
+      int bi = 0; flagged = false;
+      if (!(args.debug & 1)) bi = epi_score_row(E.ch, nk, d_acc, sqv, guard, &flagged);
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s.acc_empty[grp]);
-      if (etid == 0) stamp(args, i, 5);
+      if (etid == 0 && !(args.debug & 4)) stamp(args, i, 5);
       // routing, aggregated over the group's 128 rows
       if (etid <= kMaxChildren) E.bcnt[etid] = 0;
       named_bar(bar_id, 128);
@@ -306,7 +374,7 @@ select_level_ws_kernel(PlanView pv, Args args) {
           }
         }
       }
-      if (etid == 0) stamp(args, i, 6);
+      if (etid == 0 && !(args.debug & 8)) stamp(args, i, 6);
     }
   }
   tc::fence_before_sync();
@@ -318,9 +386,13 @@ select_level_ws_kernel(PlanView pv, Args args) {
 
 uint64_t* g_ws_trace = nullptr;
 int g_ws_trace_level = -1;
+int g_ws_debug = 0;
 
 bool select_ws_supported(const Plan* p) {
-  return p->have_tc && p->v.P <= 64 && p->max_tc_npad <= ws::kMaxN;
+  int widest = 0;
+  for (int d = 0; d < p->n_levels; ++d)
+    widest = std::max(widest, p->level_start[d + 1] - p->level_start[d]);
+  return p->have_tc && p->v.P <= 64 && p->max_tc_npad <= ws::kMaxN && widest <= ws::kMaxNodes;
 }
 
 int select_level_ws(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
@@ -335,6 +407,7 @@ int select_level_ws(Plan* p, const LevelArgs& a, const float* Z32, const double*
   args.queue_len = p->rs.queue_len;
   args.katoms = (p->v.P + 31) / 32;
   args.trace = (a.depth == g_ws_trace_level) ? g_ws_trace : nullptr;
+  args.debug = g_ws_debug;
   const size_t smem = 1024 + ws::kStages * ws::kStageBytes + ws::kBBytes + sizeof(ws::Smem);
   FEPLL_CUDA(cudaFuncSetAttribute(ws::select_level_ws_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -348,5 +421,10 @@ int select_level_ws(Plan* p, const LevelArgs& a, const float* Z32, const double*
 extern "C" int fepll_debug_ws_trace(void* device_buffer, int32_t level) {
   fepll::g_ws_trace = static_cast<uint64_t*>(device_buffer);
   fepll::g_ws_trace_level = level;
+  return 0;
+}
+
+extern "C" int fepll_debug_ws_flags(int32_t flags) {
+  fepll::g_ws_debug = flags;
   return 0;
 }

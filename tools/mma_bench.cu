@@ -1,0 +1,96 @@
+// Microbenchmark: back-to-back tcgen05.mma throughput (kind::tf32 and kind::f16)
+// with SWIZZLE_128B K-major operands resident in smem.  One CTA per SM.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1710_08124_b200/csrc tools/mma_bench.cu -o /tmp/mma_bench
+#include <cstdio>
+#include <cstdint>
+#include "tc.cuh"
+
+using namespace fepll;
+
+__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d), "l"(a), "l"(b),
+               "r"(idesc), "r"(acc) : "memory");
+}
+
+// whole warp executes; one elected lane issues
+__device__ __forceinline__ void mma_tf32_elect(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "elect.sync _|e, 0xffffffff;\n\t"
+               "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d), "l"(a), "l"(b),
+               "r"(idesc), "r"(acc) : "memory");
+}
+
+__global__ void bench(int kind, int N, int iters, unsigned long long* out, int nacc) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem;
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) ((float*)base)[i] = 0.001f * (i % 7);
+  if (threadIdx.x < 32) tc::tmem_alloc(&tmem, 512);
+  if (threadIdx.x == 0) { tc::mbar_init(&bar, 1); tc::fence_mbar_init(); }
+  tc::fence_proxy_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (kind == 2 && threadIdx.x < 32) {
+    const uint32_t A = tc::smem_u32(base), B = tc::smem_u32(base + 32768);
+    const uint32_t idt = tc::idesc_tf32(128, N);
+    const uint64_t da = tc::desc_sw128(A), db = tc::desc_sw128(B);
+    unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t d = tmem + ((kk % nacc) * 128);
+        mma_tf32_elect(d, da + 2 * kk, db + 2 * kk, idt, it | kk);
+      }
+    }
+    if (threadIdx.x == 0) { tc::mma_commit(&bar); tc::mbar_wait(&bar, 0); }
+    __syncwarp();
+    unsigned long long t1 = clock64();
+    if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  } else if (kind < 2 && threadIdx.x == 0) {
+    const uint32_t A = tc::smem_u32(base), B = tc::smem_u32(base + 32768);
+    const uint32_t idt = tc::idesc_tf32(128, N);
+    // f16: c_format F32 (1<<4), a/b format F16 (0), K-major
+    const uint32_t idh = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t d = tmem + ((it * 4 + kk) % nacc) * 128;
+        if (kind == 0)
+          tc::mma_tf32(d, tc::desc_sw128(A + kk * 32), tc::desc_sw128(B + kk * 32), idt, it | kk);
+        else
+          mma_f16(d, tc::desc_sw128(A + kk * 32), tc::desc_sw128(B + kk * 32), idh, it | kk);
+      }
+    }
+    tc::mma_commit(&bar);
+    tc::mbar_wait(&bar, 0);
+    unsigned long long t1 = clock64();
+    out[blockIdx.x] = t1 - t0;
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (threadIdx.x < 32) tc::tmem_dealloc(tmem, 512);
+}
+
+int main() {
+  unsigned long long* d;
+  cudaMalloc(&d, 148 * 8);
+  cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+  for (int nacc : {1, 2, 4})
+  for (int kind = 0; kind < 3; ++kind)
+    for (int N : {64, 128, 256}) {
+      if (N == 256 && nacc > 2) continue;
+      const int iters = 2000;
+      bench<<<148, 128, 80 * 1024>>>(kind, N, iters, d, N == 256 ? 1 : nacc);
+      cudaError_t e = cudaDeviceSynchronize();
+      unsigned long long h[148];
+      cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+      double cyc = (double)h[0] / (iters * 4);
+      double macs = 128.0 * N * (kind == 1 ? 16 : 8);
+      printf("nacc=%d %s N=%3d: %.1f cycles/MMA  -> %.0f MAC/clk/SM (%s)\n", nacc, kind == 0 ? "tf32" : (kind == 1 ? "f16 " : "tf32E"),
+             N, cyc, macs / cyc, cudaGetErrorString(e));
+    }
+  return 0;
+}

@@ -1,0 +1,25 @@
+import sys, os, ctypes
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_1710_08124_b200 import RestorationConfig, Restorer, synthetic, _native as N
+B = 16; level = int(sys.argv[1]) if len(sys.argv) > 1 else 6
+flags = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+c = synthetic.baseline_case("cfg5", 1024)
+ys = np.stack([c.y] * B)
+model = synthetic.synthetic_gmm(200, 64, 0, 0.95); tree = synthetic.baseline_tree(model)
+r = Restorer(c.A, model, tree, RestorationConfig(sigma=25.0, spacing=4, seed=0), batch=B, mode="tensor")
+y = torch.from_numpy(ys).cuda(); r.run(y)
+buf = torch.zeros(148 * 64 * 8, dtype=torch.int64, device="cuda")
+fn = N.lib().fepll_debug_ws_trace; fn.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+fl = N.lib().fepll_debug_ws_flags; fl.argtypes = [ctypes.c_int32]
+fl(flags); fn(buf.data_ptr(), level); r.run(y); torch.cuda.synchronize(); fn(None, -1); fl(0)
+tr = buf.view(148, 64, 8).cpu().numpy().astype(np.float64) / 1.965  # cycles -> ns
+cta = 30
+t0 = tr[cta, 0, 7]
+print("ns relative to CTA start: p0=after a_empty wait, p1=arrive a_full, m2=MMA start, m3=issued, e4=acc ready, e5=epi math done, e6=routed")
+for i in range(0, 14):
+    row = tr[cta, i] - t0
+    print(f"tile {i:2d}: p0 {row[0]:7.0f} p1 {row[1]:7.0f} | m2 {row[2]:7.0f} m3 {row[3]:7.0f} | e4 {row[4]:7.0f} e5 {row[5]:7.0f} e6 {row[6]:7.0f}")
+d = lambda a, b: np.median((tr[:, 2:40, b] - tr[:, 2:40, a])[tr[:, 2:40, 2] > 0])
+print("median ns: fill(p0->p1)", d(0, 1), "issue(m2->m3)", d(2, 3), "epi math(e4->e5)", d(4, 5), "route(e5->e6)", d(5, 6))
+st = np.diff(tr[:, 2:40, 2], axis=1); print("MMA start spacing median ns", np.median(st[st > 0]))
