@@ -30,14 +30,17 @@ struct LevelArgs {
   int t;
 };
 
-struct LevelTables {
-  int32_t cpre[kMaxLevelNodes + 1];   // prefix of counts over depth-d internal nodes
-  int32_t tpre[kMaxLevelNodes + 1];   // prefix of tiles (rows_per_tile) over the same
-  int64_t child_off[kMaxLevelNodes];  // next-level segment offsets of depth-(d+1) nodes
+template <int NMAX>
+struct LevelTablesN {
+  static constexpr int kCap = NMAX;
+  int32_t cpre[NMAX + 1];   // prefix of counts over depth-d internal nodes
+  int32_t tpre[NMAX + 1];   // prefix of tiles (rows_per_tile) over the same
+  int64_t child_off[NMAX];  // next-level segment offsets of depth-(d+1) nodes
   uint64_t scan_tmp[256];
   int32_t total_items;
   int32_t total_tiles;
 };
+using LevelTables = LevelTablesN<kMaxLevelNodes>;
 
 // in-place exclusive scan of data[0..n) (smem) by the first <=255 threads;
 // every thread of the block must call it.  Returns the total.
@@ -75,7 +78,8 @@ __device__ __forceinline__ T block_exscan(T* data, int n, uint64_t* tmp) {
 }
 
 // Every CTA: count/tile prefixes of level d and the offsets of level d+1.
-__device__ inline void level_tables(const PlanView& pv, const LevelArgs& a, LevelTables& s,
+template <class LT>
+__device__ inline void level_tables(const PlanView& pv, const LevelArgs& a, LT& s,
                                     int rows_per_tile) {
   const int nd = a.lvl_end - a.lvl_begin;
   const int nn = a.nxt_end - a.nxt_begin;
@@ -126,7 +130,8 @@ __device__ __forceinline__ int prefix_find(const int32_t* pre, int n, int x) {
 }
 
 // item -> (node, patch)
-__device__ __forceinline__ void level_item(const LevelArgs& a, const LevelTables& s, int item,
+template <class LT>
+__device__ __forceinline__ void level_item(const LevelArgs& a, const LT& s, int item,
                                            int& u, int& patch) {
   const int k = prefix_find(s.cpre, a.lvl_end - a.lvl_begin, item);
   u = a.lvl_begin + k;
@@ -134,8 +139,9 @@ __device__ __forceinline__ void level_item(const LevelArgs& a, const LevelTables
 }
 
 // append patch to child v's segment of the next level
+template <class LT>
 __device__ __forceinline__ void level_route(const PlanView& pv, const LevelArgs& a,
-                                            const LevelTables& s, int v, int patch) {
+                                            const LT& s, int v, int patch) {
   const int slot = atomicAdd(&a.cnt[v], 1);
   const int64_t base = s.child_off[v - a.nxt_begin];
   if (pv.child_count[v] > 0) {

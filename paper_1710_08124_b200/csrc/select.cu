@@ -42,6 +42,51 @@ __device__ __forceinline__ void load_patch(const PatchSrc& ps, int g, int P, dou
   __syncwarp();
 }
 
+// lane's columns (lane + 32k, k < NC) of z . G, p ascending per column (one
+// FMA chain each, the same order for every width); CH rows of G are loaded
+// before they are consumed so a warp keeps CH*NC loads in flight instead of
+// one L2 round trip per row.
+template <int NC, int CH>
+__device__ __forceinline__ void project_cols(const double* G, int width, int P, const double* zs,
+                                             int lane, double (&acc)[NC]) {
+  const int ncol = (width - lane + 31) >> 5;
+#pragma unroll
+  for (int k = 0; k < NC; ++k) acc[k] = 0.0;
+  int p = 0;
+  for (; p + CH <= P; p += CH) {
+    double g[CH][NC];
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+#pragma unroll
+      for (int k = 0; k < NC; ++k)
+        g[j][k] = k < ncol ? __ldg(G + (int64_t)(p + j) * width + lane + 32 * k) : 0.0;
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      const double zp = zs[p + j];
+#pragma unroll
+      for (int k = 0; k < NC; ++k) acc[k] = fma(zp, g[j][k], acc[k]);
+    }
+  }
+  for (; p < P; ++p) {
+    const double zp = zs[p];
+#pragma unroll
+    for (int k = 0; k < NC; ++k)
+      if (k < ncol) acc[k] = fma(zp, __ldg(G + (int64_t)p * width + lane + 32 * k), acc[k]);
+  }
+}
+
+template <int NC, int CH>
+__device__ __forceinline__ void child_terms(const double* G, const double* w, int width, int P,
+                                            const double* zs, int lane, double* tv) {
+  double acc[NC];
+  project_cols<NC, CH>(G, width, P, zs, lane, acc);
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    const int j = lane + 32 * k;
+    if (j < width) tv[j] = acc[k] * acc[k] * w[j];
+  }
+}
+
 // one warp: best child of node u for the patch in zs (smem); returns BFS id.
 __device__ __forceinline__ int score_children_fp64(const PlanView& pv, int t, int u,
                                                    const double* zs, double sqv, double* tv) {
@@ -50,23 +95,12 @@ __device__ __forceinline__ int score_children_fp64(const PlanView& pv, int t, in
   const int width = pv.grp_width[u];
   const double* G = pv.grp_basis + pv.grp_off64[u];
   const double* w = pv.grp_sqw + (int64_t)t * pv.grp_cols_total + pv.grp_col_off[u];
-  const int ncol = (width - lane + 31) >> 5;
-  double acc[kColsPerLane];
-#pragma unroll
-  for (int k = 0; k < kColsPerLane; ++k) acc[k] = 0.0;
-  for (int p = 0; p < P; ++p) {
-    const double zp = zs[p];
-    const double* row = G + (int64_t)p * width + lane;
-#pragma unroll
-    for (int k = 0; k < kColsPerLane; ++k)
-      if (k < ncol) acc[k] = fma(zp, __ldg(row + 32 * k), acc[k]);
-  }
-#pragma unroll
-  for (int k = 0; k < kColsPerLane; ++k)
-    if (k < ncol) {
-      const int j = lane + 32 * k;
-      tv[j] = acc[k] * acc[k] * w[j];
-    }
+  if (width <= 128)
+    child_terms<4, 8>(G, w, width, P, zs, lane, tv);
+  else if (width <= 256)
+    child_terms<8, 4>(G, w, width, P, zs, lane, tv);
+  else
+    child_terms<kColsPerLane, 2>(G, w, width, P, zs, lane, tv);
   __syncwarp();
   const int nk = pv.child_count[u];
   double best = INFINITY;

@@ -5,15 +5,20 @@
 // pkg/src/fepll/gmm.py:323-339), laid out as a persistent pipeline:
 //
 //   warps 0-7    producers: warp w owns K atom w/4 of the tile's 128 FP32
-//                patch rows (kernel (a) output).  Each thread prefetches its
-//                row of tile i+1 into registers (8 x 16-byte loads) while
-//                tile i is in flight, then splits TF32 hi/lo and stores it
-//                128B-swizzled into one of two A stages;
-//   warp 8       MMA issuer: keeps the current node's group image G_u resident
-//                in smem (reloaded by the TMA bulk engine only when the node
-//                changes — each CTA walks a contiguous, node-sorted tile
-//                range), issues 24 tcgen05.mma per tile into one of four
-//                128-column TMEM accumulators;
+//                patch rows (kernel (a) output).  Row indices arrive several
+//                tiles early by cp.async into a smem ring, rows are prefetched
+//                into L2 and then into registers one tile ahead; each thread
+//                splits TF32 hi/lo and stores 128B-swizzled into one of two A
+//                stages.  (A TMA tile::gather4 producer was measured and
+//                rejected: ~62 cycles per 512-byte gather4, ~2.3 TB/s chip-wide,
+//                tools/tma_rate.cu — below this loop, and it needs the split
+//                rows materialized, doubling kernel (a)'s writes.)
+//   warp 8       MMA issuer (warp-collective, elected lane): keeps the
+//                current node's group image G_u resident in smem (reloaded
+//                by the TMA bulk engine only when the node changes — each CTA
+//                walks a contiguous, node-sorted tile range), issues 24
+//                tcgen05.mma per tile into one of four 128-column TMEM
+//                accumulators;
 //   warps 9-24   four epilogue groups (tile i -> group i % 4): tcgen05.ld,
 //                per-child scores (tc_epi.cuh), certified argmin,
 //                aggregated routing.
@@ -32,9 +37,10 @@ namespace ws {
 constexpr int kRows = 128;
 constexpr int kProducerWarps = 8;
 constexpr int kMmaWarp = 8;
+constexpr int kEpiWarp0 = 9;
 constexpr int kGroups = 4;                 // epilogue groups == TMEM accumulators
 constexpr int kEpiWarps = 4 * kGroups;
-constexpr int kThreads = (kProducerWarps + 1 + kEpiWarps) * 32;
+constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
 constexpr int kStages = 2;
 constexpr int kAtomA = kRows * 128;     // bytes of one K atom of A (hi or lo)
 constexpr int kMaxKAtoms = 2;           // P <= 64
@@ -52,15 +58,16 @@ struct EpiGroup {
   int32_t bbase[kMaxChildren + 1];
 };
 
-constexpr int kMaxNodes = 256;  // internal nodes per level handled by this kernel
+constexpr int kMaxNodes = 128;  // internal nodes per level handled by this kernel
+using WsLevelTables = LevelTablesN<256>;  // next level <= 256 nodes
 
-constexpr int kIdxAhead = 4;   // tiles of row indices in flight per producer thread
-constexpr int kIdxRing = 5;
+constexpr int kIdxAhead = 6;   // tiles of row indices in flight per producer thread
+constexpr int kIdxRing = 7;
 constexpr int kL2Ahead = 3;    // tiles whose rows are prefetched into L2
 
 struct Smem {
   int32_t idx_ring[2][kIdxRing][kRows];  // [K atom group][slot][row]
-  LevelTables lv;
+  WsLevelTables lv;
   int64_t nd_off[kMaxNodes];      // segment offset of each depth-d node (a.off)
   int16_t nd_npad[kMaxNodes];     // padded group width
   int16_t nd_nk[kMaxNodes];       // child count
@@ -80,18 +87,15 @@ struct Args {
   int32_t* queue;
   int32_t* queue_len;
   int katoms;
-  uint64_t* trace;       // debug timeline: [CTA][64 tiles][8] globaltimer stamps (or NULL)
-  int debug;             // experiment flags: 1 skip epilogue math, 2 skip producer stores
+  uint64_t* trace;       // debug timeline: [CTA][64 tiles][8] clock64 stamps (or NULL)
 };
 
-__device__ __forceinline__ uint64_t gtimer() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));  // SM cycles (per-CTA relative timing)
-  return t;
-}
-
 __device__ __forceinline__ void stamp(const Args& a, int i, int slot) {
-  if (a.trace && i < 64) a.trace[((size_t)blockIdx.x * 64 + i) * 8 + slot] = gtimer();
+  if (a.trace && i < 64) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));  // SM cycles (per-CTA relative timing)
+    a.trace[((size_t)blockIdx.x * 64 + i) * 8 + slot] = t;
+  }
 }
 
 __device__ __forceinline__ void named_bar(int id, int n) {
@@ -107,19 +111,13 @@ struct TileInfo {
 };
 
 // tile -> (level-local node k, BFS id u, first row, rows): smem only
-__device__ __forceinline__ TileInfo tile_info(const LevelArgs& a, const LevelTables& lv, int tile) {
+__device__ __forceinline__ TileInfo tile_info(const LevelArgs& a, const WsLevelTables& lv, int tile) {
   TileInfo ti;
   ti.k = prefix_find(lv.tpre, a.lvl_end - a.lvl_begin, tile);
   ti.u = a.lvl_begin + ti.k;
   ti.first = (tile - lv.tpre[ti.k]) * kRows;
   ti.m = min(kRows, (lv.cpre[ti.k + 1] - lv.cpre[ti.k]) - ti.first);
   return ti;
-}
-
-// patch index of row `row` of tile `tile` (-1 past the end)
-__device__ __forceinline__ int row_patch(const LevelArgs& a, const Smem& s, int tile, int row) {
-  const TileInfo ti = tile_info(a, s.lv, tile);
-  return row < ti.m ? a.seg_in[s.nd_off[ti.k] + ti.first + row] : -1;
 }
 
 // K atom ka of patch g: 8 float4 into registers (zeros for g < 0)
@@ -178,7 +176,6 @@ select_level_ws_kernel(PlanView pv, Args args) {
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = s.tmem_base;
-  if (tid == 0) stamp(args, 0, 7);
   const int t_begin = s.t_begin, t_end = s.t_end;
   const int ntile = t_end - t_begin;
   const int t = a.t;
@@ -219,7 +216,7 @@ select_level_ws_kernel(PlanView pv, Args args) {
       const int st = i % kStages;
       if (i >= kStages) tc::mbar_wait(&s.a_empty[st], ((i / kStages) - 1) & 1);
       if (tid == 0) stamp(args, i, 0);
-      if (active && !(args.debug & 2)) {
+      if (active) {
         uint8_t* A = stageA + st * kStageBytes;
         uint8_t* dhi = A + (2 * ka) * kAtomA + (row >> 3) * 1024 + r8 * 128;
         uint8_t* dlo = A + (2 * ka + 1) * kAtomA + (row >> 3) * 1024 + r8 * 128;
@@ -279,9 +276,8 @@ select_level_ws_kernel(PlanView pv, Args args) {
         ++b_loads;
         cur = ti.u;
       }
-      if (lane == 0 && (args.debug & 4)) stamp(args, i, 4);
       if (i >= kGroups) tc::mbar_wait(&s.acc_empty[ac], ((i / kGroups) - 1) & 1);
-      if (lane == 0 && (args.debug & 4)) stamp(args, i, 5);
+
       tc::mbar_wait(&s.a_full[st], (i / kStages) & 1);
       tc::fence_after_sync();
       if (lane == 0) stamp(args, i, 2);
@@ -305,15 +301,11 @@ select_level_ws_kernel(PlanView pv, Args args) {
       }
       tc::mma_commit_warp(&s.a_empty[st]);
       tc::mma_commit_warp(&s.acc_full[ac]);
-      if (args.debug & 8) {
-        tc::mbar_wait(&s.acc_full[ac], (i / kGroups) & 1);
-        if (lane == 0) stamp(args, i, 6);
-      }
       if (lane == 0) stamp(args, i, 3);
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - (kMmaWarp + 1);  // 0..15
+    const int ew = warp - kEpiWarp0;       // 0..15
     const int grp = ew >> 2;               // tiles with i % 4 == grp
     const int row = 32 * (warp & 3) + lane;
     const uint32_t d_acc = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + grp * kMaxN;
@@ -336,14 +328,13 @@ select_level_ws_kernel(PlanView pv, Args args) {
       }
       tc::mbar_wait(&s.acc_full[grp], (i / kGroups) & 1);
       tc::fence_after_sync();
-      if (etid == 0 && !(args.debug & 4)) stamp(args, i, 4);
+      if (etid == 0) stamp(args, i, 4);
       bool flagged;
-      int bi = 0; flagged = false;
-      if (!(args.debug & 1)) bi = epi_score_row(E.ch, nk, d_acc, sqv, guard, &flagged);
+      const int bi = epi_score_row(E.ch, nk, d_acc, sqv, guard, &flagged);
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s.acc_empty[grp]);
-      if (etid == 0 && !(args.debug & 4)) stamp(args, i, 5);
+      if (etid == 0) stamp(args, i, 5);
       // routing, aggregated over the group's 128 rows
       if (etid <= kMaxChildren) E.bcnt[etid] = 0;
       named_bar(bar_id, 128);
@@ -374,7 +365,7 @@ select_level_ws_kernel(PlanView pv, Args args) {
           }
         }
       }
-      if (etid == 0 && !(args.debug & 8)) stamp(args, i, 6);
+      if (etid == 0) stamp(args, i, 6);
     }
   }
   tc::fence_before_sync();
@@ -386,15 +377,19 @@ select_level_ws_kernel(PlanView pv, Args args) {
 
 uint64_t* g_ws_trace = nullptr;
 int g_ws_trace_level = -1;
-int g_ws_debug = 0;
 
 bool select_ws_supported(const Plan* p) {
-  int widest = 0;
-  for (int d = 0; d < p->n_levels; ++d)
+  int widest = 0, widest_next = 0;
+  for (int d = 0; d < p->n_levels; ++d) {
     widest = std::max(widest, p->level_start[d + 1] - p->level_start[d]);
-  return p->have_tc && p->v.P <= 64 && p->max_tc_npad <= ws::kMaxN && widest <= ws::kMaxNodes;
+    widest_next = std::max(widest_next, p->level_start[d + 2] - p->level_start[d + 1]);
+  }
+  return p->have_tc && p->v.P <= 64 && p->max_tc_npad <= ws::kMaxN && widest <= ws::kMaxNodes &&
+         widest_next <= ws::WsLevelTables::kCap;
 }
 
+// 2-D tensor map over the [rows][pitch] FP32 patch rows: boxes of one
+// 128-byte K atom of one row, 128B swizzle (the UMMA K-major layout)
 int select_level_ws(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                     cudaStream_t st) {
   ws::Args args;
@@ -407,7 +402,6 @@ int select_level_ws(Plan* p, const LevelArgs& a, const float* Z32, const double*
   args.queue_len = p->rs.queue_len;
   args.katoms = (p->v.P + 31) / 32;
   args.trace = (a.depth == g_ws_trace_level) ? g_ws_trace : nullptr;
-  args.debug = g_ws_debug;
   const size_t smem = 1024 + ws::kStages * ws::kStageBytes + ws::kBBytes + sizeof(ws::Smem);
   FEPLL_CUDA(cudaFuncSetAttribute(ws::select_level_ws_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -421,10 +415,5 @@ int select_level_ws(Plan* p, const LevelArgs& a, const float* Z32, const double*
 extern "C" int fepll_debug_ws_trace(void* device_buffer, int32_t level) {
   fepll::g_ws_trace = static_cast<uint64_t*>(device_buffer);
   fepll::g_ws_trace_level = level;
-  return 0;
-}
-
-extern "C" int fepll_debug_ws_flags(int32_t flags) {
-  fepll::g_ws_debug = flags;
   return 0;
 }

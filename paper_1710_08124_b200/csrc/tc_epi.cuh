@@ -3,16 +3,18 @@
 // For every child c of the tile's node (pkg/src/fepll/tree.py:417-425) the
 // child's columns start on a 16-column boundary (plan.py tc_images), so the
 // thread streams them in 16-column TMEM chunks and accumulates
-// s_c = sum_j c_j^2 w_j and e_c = sum_j |c_j w_j| in FP32.
+// s_c = sum_j c_j^2 w_j with packed FP32x2 multiply/FMA (FMUL2/FFMA2).
 // score_c = const_c + ||z||^2 / nu_tail_c + s_c (FP64, gmm.py:335-338; the
 // division is a multiplication by the FP64 reciprocal, a 1-ulp change
 // covered by the bound's relative slack).
 //
 // Certification: the 3xTF32 projection (three FP32-accumulated tcgen05
-// passes) is within 2^-18 ||z|| of the exact coefficient, and the FP32
-// accumulation adds <= 64 * 2^-24 * sum|c^2 w| <= 2^-18 ||z|| sum|c w|;
-// err_c = guard * ||z|| * e_c + 2^-40 |score_c| with guard = 2^-16 covers
-// both with margin.  The argmin is certified when every other child
+// passes) is within gamma = 2^-18 ||z|| of the exact coefficient, so
+// |d s_c| <= 2 gamma ||z|| sum_j |c_j w_j| <= 2^-17 ||z||^2 ||w_c||
+// (Cauchy-Schwarz, ||c|| <= ||z||); the FP32 accumulation adds
+// <= 64 * 2^-24 * sum|c_j^2 w_j| <= 2^-18 ||z||^2 ||w_c||.
+// err_c = guard * ||z||^2 * ||w_c|| + 2^-40 |score_c| with guard = 2^-16
+// covers both.  The argmin is certified when every other child
 // satisfies score_c - err_c > score_best + err_best; otherwise the caller
 // queues the patch for exact FP64 re-scoring.
 #pragma once
@@ -26,6 +28,7 @@ constexpr double kDefaultGuard = 1.52587890625e-05;  // 2^-16
 struct EpiChild {
   double cconst[kMaxChildren];
   double cinvnut[kMaxChildren];   // 1 / nu_tail
+  double wnorm[kMaxChildren];     // ||w_c|| of the FP32 column weights
   int32_t col[kMaxChildren];     // 16-aligned first column in the node's image
   int32_t chunks[kMaxChildren];  // ceil(rank / 16)
   int32_t bfs[kMaxChildren];
@@ -54,40 +57,51 @@ __device__ __forceinline__ void epi_load_node(const PlanView& pv, int t, int u, 
     const int64_t ti = (int64_t)t * pv.n_nodes + v;
     E.cconst[tid] = pv.node_const[ti];
     E.cinvnut[tid] = 1.0 / pv.node_nu_tail[ti];
+    const float* wc = w + pv.tc_child_col[v];
+    double n2 = 0.0;
+    for (int j = 0; j < pv.node_rank[v]; ++j) n2 += (double)wc[j] * (double)wc[j];
+    E.wnorm[tid] = sqrt(n2);
     E.col[tid] = pv.tc_child_col[v];
     E.chunks[tid] = (pv.node_rank[v] + 15) >> 4;
     E.bfs[tid] = v;
   }
 }
 
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
 // Returns the best child index; *flagged when the decision is not certified.
 // d_acc: TMEM address (lane field set) of the tile's accumulator.
 __device__ __forceinline__ int epi_score_row(const EpiChild& E, int nk, uint32_t d_acc,
                                              double sqv, double guard, bool* flagged) {
-  const double zn = (double)sqrtf((float)sqv) * (1.0 + 1e-6);
   double best = INFINITY, best_err = 0.0, m1 = INFINITY, m2 = INFINITY;
   int bi = 0, i1 = -1;
   for (int ci = 0; ci < nk; ++ci) {
     const int c0 = E.col[ci];
-    float s0 = 0.f, s1 = 0.f, e0 = 0.f, e1 = 0.f;
+    uint64_t s2 = 0;  // two FP32 partial sums
     for (int q = 0; q < E.chunks[ci]; ++q) {
       uint32_t ra[16];
       tmem_ld16(d_acc + c0 + 16 * q, ra);
+      const uint64_t* w2 = reinterpret_cast<const uint64_t*>(E.w + c0 + 16 * q);
       tc::tmem_ld_wait();
-      const float* w = E.w + c0 + 16 * q;
 #pragma unroll
-      for (int j = 0; j < 16; j += 2) {
-        const float ca = __uint_as_float(ra[j]);
-        const float cb = __uint_as_float(ra[j + 1]);
-        const float wa = ca * w[j], wb = cb * w[j + 1];
-        s0 = fmaf(wa, ca, s0);
-        s1 = fmaf(wb, cb, s1);
-        e0 += fabsf(wa);
-        e1 += fabsf(wb);
+      for (int j = 0; j < 8; ++j) {
+        const uint64_t c2 = (uint64_t)ra[2 * j] | ((uint64_t)ra[2 * j + 1] << 32);
+        s2 = f2_fma(f2_mul(c2, w2[j]), c2, s2);
       }
     }
-    const double sc = E.cconst[ci] + sqv * E.cinvnut[ci] + ((double)s0 + (double)s1);
-    const double er = guard * zn * ((double)e0 + (double)e1) + 0x1p-40 * fabs(sc);
+    const float s_lo = __uint_as_float((uint32_t)s2), s_hi = __uint_as_float((uint32_t)(s2 >> 32));
+    const double sc = E.cconst[ci] + sqv * E.cinvnut[ci] + ((double)s_lo + (double)s_hi);
+    const double er = guard * sqv * E.wnorm[ci] + 0x1p-40 * fabs(sc);
     if (sc < best) { best = sc; bi = ci; best_err = er; }
     const double lo = sc - er;
     if (lo < m1) { m2 = m1; m1 = lo; i1 = ci; }
