@@ -61,10 +61,18 @@ static int create(const fepll_plan_desc* d, Plan** out) {
     p->max_group_cols = std::max(p->max_group_cols, d->grp_width[i]);
   }
   for (int k = 0; k < K; ++k) p->max_model_rank = std::max(p->max_model_rank, d->model_rank[k]);
-  if (p->max_children > kMaxChildren || p->max_group_cols > kMaxGroupCols) {
-    set_error("tree node exceeds device limits (children <= 32, sum of child ranks <= 512)");
-    delete p;
-    return kDataError;
+  // segment capacities: a child's segment holds up to its parent's count
+  // (leaf buckets of every depth share one array: sum the per-depth maxima)
+  {
+    std::vector<int> leaf_at_depth(maxd + 1, 0);
+    for (int u = 0; u < n; ++u) {
+      int inner = 0, leaves = 0;
+      for (int j = 0; j < d->child_count[u]; ++j)
+        (d->child_count[d->child_list[d->child_start[u] + j]] > 0 ? inner : leaves) += 1;
+      p->max_inner_children = std::max(p->max_inner_children, inner);
+      leaf_at_depth[d->depth[u]] = std::max(leaf_at_depth[d->depth[u]], leaves);
+    }
+    for (int x : leaf_at_depth) p->max_leaf_children += x;
   }
   p->level_start.assign(maxd + 2, 0);
   for (int dd = 0, i = 0; dd <= maxd + 1; ++dd) {
@@ -86,6 +94,16 @@ static int create(const fepll_plan_desc* d, Plan** out) {
   p->n_levels = 0;
   for (int i = 0; i < n; ++i)
     if (d->child_count[i] > 0) p->n_levels = std::max(p->n_levels, d->depth[i] + 1);
+  // "wide" levels hold a node beyond the single-pass scorers' limits (more
+  // than 32 children or 512 group columns — e.g. the exhaustive star tree);
+  // they are scored in sub-groups / column chunks
+  p->level_wide.assign(maxd + 1, 0);
+  p->level_tc_npad.assign(maxd + 1, 0);
+  for (int i = 0; i < n; ++i) {
+    if (d->child_count[i] > kMaxChildren || d->grp_width[i] > kMaxGroupCols) p->level_wide[d->depth[i]] = 1;
+    if (d->grp_tc_npad)
+      p->level_tc_npad[d->depth[i]] = std::max(p->level_tc_npad[d->depth[i]], d->grp_tc_npad[i]);
+  }
   UP(d->child_start, n, v.child_start);
   UP(d->child_count, n, v.child_count);
   UP(d->child_list, std::max(n - 1, 1), v.child_list);
@@ -165,10 +183,12 @@ static int reserve(Plan* p, int64_t max_patches) {
   if (max_patches <= p->rs.cap) return kOk;
   free_scratch(p);
   RouteScratch& r = p->rs;
-  const int64_t seg = std::max<int64_t>(1, max_patches) * std::max(2, p->max_children);
-  FEPLL_CUDA(cudaMalloc(&r.seg[0], sizeof(int32_t) * seg));
+  const int64_t np = std::max<int64_t>(1, max_patches);
+  const int64_t seg = np * std::max(1, p->max_inner_children);
+  const int64_t lseg = np * std::max(1, p->max_leaf_children);
+  FEPLL_CUDA(cudaMalloc(&r.seg[0], sizeof(int32_t) * std::max(seg, np)));  // level 0 = all patches
   FEPLL_CUDA(cudaMalloc(&r.seg[1], sizeof(int32_t) * seg));
-  FEPLL_CUDA(cudaMalloc(&r.leafseg, sizeof(int32_t) * seg));
+  FEPLL_CUDA(cudaMalloc(&r.leafseg, sizeof(int32_t) * lseg));
   r.queue_cap = std::max<int64_t>(1024, max_patches);
   FEPLL_CUDA(cudaMalloc(&r.queue, sizeof(int32_t) * 2 * r.queue_cap));
   r.cap = max_patches;

@@ -69,6 +69,10 @@ struct Plan {
   std::vector<int> max_group_cols_at_depth;
   int n_levels = 0;               // depth of the deepest internal node + 1
   int max_children = 0;
+  int max_inner_children = 0;     // internal children of one node
+  int max_leaf_children = 0;      // leaf-bucket capacity per patch (sum over depths)
+  std::vector<int> level_wide;    // per depth: a node needs the sub-group scorer
+  std::vector<int> level_tc_npad; // per depth: widest tcgen05 group image
   int max_group_cols = 0;
   int max_model_rank = 0;
   int max_tc_npad = 0;

@@ -42,14 +42,15 @@ __device__ __forceinline__ void load_patch(const PatchSrc& ps, int g, int P, dou
   __syncwarp();
 }
 
-// lane's columns (lane + 32k, k < NC) of z . G, p ascending per column (one
-// FMA chain each, the same order for every width); CH rows of G are loaded
+// lane's columns (lane + 32k, k < NC) of z . G for a P x ncols block of a
+// row-major matrix with row stride `stride`, p ascending per column (one FMA
+// chain each, the same order for every width); CH rows of G are loaded
 // before they are consumed so a warp keeps CH*NC loads in flight instead of
 // one L2 round trip per row.
 template <int NC, int CH>
-__device__ __forceinline__ void project_cols(const double* G, int width, int P, const double* zs,
-                                             int lane, double (&acc)[NC]) {
-  const int ncol = (width - lane + 31) >> 5;
+__device__ __forceinline__ void project_cols(const double* G, int stride, int ncols, int P,
+                                             const double* zs, int lane, double (&acc)[NC]) {
+  const int ncol = (ncols - lane + 31) >> 5;
 #pragma unroll
   for (int k = 0; k < NC; ++k) acc[k] = 0.0;
   int p = 0;
@@ -59,7 +60,7 @@ __device__ __forceinline__ void project_cols(const double* G, int width, int P, 
     for (int j = 0; j < CH; ++j)
 #pragma unroll
       for (int k = 0; k < NC; ++k)
-        g[j][k] = k < ncol ? __ldg(G + (int64_t)(p + j) * width + lane + 32 * k) : 0.0;
+        g[j][k] = k < ncol ? __ldg(G + (int64_t)(p + j) * stride + lane + 32 * k) : 0.0;
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
       const double zp = zs[p + j];
@@ -71,51 +72,53 @@ __device__ __forceinline__ void project_cols(const double* G, int width, int P, 
     const double zp = zs[p];
 #pragma unroll
     for (int k = 0; k < NC; ++k)
-      if (k < ncol) acc[k] = fma(zp, __ldg(G + (int64_t)p * width + lane + 32 * k), acc[k]);
+      if (k < ncol) acc[k] = fma(zp, __ldg(G + (int64_t)p * stride + lane + 32 * k), acc[k]);
   }
 }
 
+// tv[j] = c_j^2 w_j for the ncols columns of the block (c = z . G)
 template <int NC, int CH>
-__device__ __forceinline__ void child_terms(const double* G, const double* w, int width, int P,
-                                            const double* zs, int lane, double* tv) {
+__device__ __forceinline__ void child_terms(const double* G, const double* w, int stride, int ncols,
+                                            int P, const double* zs, int lane, double* tv) {
   double acc[NC];
-  project_cols<NC, CH>(G, width, P, zs, lane, acc);
+  project_cols<NC, CH>(G, stride, ncols, P, zs, lane, acc);
 #pragma unroll
   for (int k = 0; k < NC; ++k) {
     const int j = lane + 32 * k;
-    if (j < width) tv[j] = acc[k] * acc[k] * w[j];
+    if (j < ncols) tv[j] = acc[k] * acc[k] * w[j];
   }
 }
 
-// one warp: best child of node u for the patch in zs (smem); returns BFS id.
-__device__ __forceinline__ int score_children_fp64(const PlanView& pv, int t, int u,
-                                                   const double* zs, double sqv, double* tv) {
-  const int lane = lane_id();
-  const int P = pv.P;
-  const int width = pv.grp_width[u];
-  const double* G = pv.grp_basis + pv.grp_off64[u];
-  const double* w = pv.grp_sqw + (int64_t)t * pv.grp_cols_total + pv.grp_col_off[u];
-  if (width <= 128)
-    child_terms<4, 8>(G, w, width, P, zs, lane, tv);
-  else if (width <= 256)
-    child_terms<8, 4>(G, w, width, P, zs, lane, tv);
+__device__ __forceinline__ void block_terms(const double* G, const double* w, int stride, int ncols,
+                                            int P, const double* zs, int lane, double* tv) {
+  if (ncols <= 128)
+    child_terms<4, 8>(G, w, stride, ncols, P, zs, lane, tv);
+  else if (ncols <= 256)
+    child_terms<8, 4>(G, w, stride, ncols, P, zs, lane, tv);
   else
-    child_terms<kColsPerLane, 2>(G, w, width, P, zs, lane, tv);
+    child_terms<kColsPerLane, 2>(G, w, stride, ncols, P, zs, lane, tv);
   __syncwarp();
-  const int nk = pv.child_count[u];
-  double best = INFINITY;
-  int bestk = nk;
-  if (lane < nk) {
-    const int v = pv.child_list[pv.child_start[u] + lane];
-    const int c0 = pv.child_col_off[v];
+}
+
+// children [k0, k1) of node u (k1 - k0 <= 32, columns [col0, col0 + tv
+// width) already in tv): lane k - k0 scores child k; first minimum in child
+// order (np.argmin) over the block
+__device__ __forceinline__ void block_argmin(const PlanView& pv, int t, int u, int k0, int k1,
+                                             int col0, const double* tv, double sqv,
+                                             double& best, int& bestk) {
+  const int lane = lane_id();
+  best = INFINITY;
+  bestk = k1;
+  if (lane < k1 - k0) {
+    const int v = pv.child_list[pv.child_start[u] + k0 + lane];
+    const int c0 = pv.child_col_off[v] - col0;
     const int r = pv.node_rank[v];
-    double s = 0.0;
-    for (int j = 0; j < r; ++j) s += tv[c0 + j];
+    double sacc = 0.0;
+    for (int j = 0; j < r; ++j) sacc += tv[c0 + j];
     const int64_t ti = (int64_t)t * pv.n_nodes + v;
-    best = pv.node_const[ti] + sqv / pv.node_nu_tail[ti] + s;
-    bestk = lane;
+    best = pv.node_const[ti] + sqv / pv.node_nu_tail[ti] + sacc;
+    bestk = k0 + lane;
   }
-  // first minimum in child order (np.argmin)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const double ob = __shfl_xor_sync(0xffffffffu, best, o);
@@ -126,7 +129,40 @@ __device__ __forceinline__ int score_children_fp64(const PlanView& pv, int t, in
     }
   }
   __syncwarp();
-  return pv.child_list[pv.child_start[u] + bestk];
+}
+
+// one warp: best child of node u for the patch in zs (smem); returns BFS id.
+// A node within the single-pass limits (<= 32 children, <= 512 group
+// columns) is one block; a wider one (the exhaustive star root of
+// gmm.py:371-391, K children) is scanned in consecutive blocks with a
+// strict-less running minimum, so ties still go to the lowest child index.
+__device__ __forceinline__ int score_children_fp64(const PlanView& pv, int t, int u,
+                                                   const double* zs, double sqv, double* tv) {
+  const int lane = lane_id();
+  const int P = pv.P;
+  const int width = pv.grp_width[u];
+  const int nk = pv.child_count[u];
+  const double* G = pv.grp_basis + pv.grp_off64[u];
+  const double* w = pv.grp_sqw + (int64_t)t * pv.grp_cols_total + pv.grp_col_off[u];
+  const int32_t* kids = pv.child_list + pv.child_start[u];
+  double best = INFINITY;
+  int bestk = 0;
+  for (int k0 = 0; k0 < nk;) {
+    const int col0 = pv.child_col_off[kids[k0]];
+    int k1 = k0, cols = 0;
+    while (k1 < nk && k1 - k0 < 32 && cols + pv.node_rank[kids[k1]] <= kMaxGroupCols)
+      cols += pv.node_rank[kids[k1++]];
+    block_terms(G + col0, w + col0, width, cols, P, zs, lane, tv);
+    double b;
+    int bk;
+    block_argmin(pv, t, u, k0, k1, col0, tv, sqv, b, bk);
+    if (b < best || k0 == 0) {
+      best = b;
+      bestk = bk;
+    }
+    k0 = k1;
+  }
+  return kids[bestk];
 }
 
 __global__ void route_init_kernel(int64_t n_total, int32_t* seg0, int32_t* cnt, int64_t* off,
@@ -386,7 +422,7 @@ __global__ void leaf_counts_kernel(const int32_t* leaf_nodes, int n_leaf_nodes,
 // P <= 128; select_ws.cu: warp-specialized pipeline, P <= 64)
 int select_level_tc(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                     cudaStream_t st);
-bool select_ws_supported(const Plan* p);
+bool select_ws_supported(const Plan* p, int d);
 int select_level_ws(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                     cudaStream_t st);
 
@@ -441,10 +477,9 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
   FEPLL_REQUIRE(t >= 0 && t < p->v.T, "select: iteration index outside the beta schedule");
   FEPLL_REQUIRE(n_total >= 0 && n_total <= p->rs.cap, "select: patch count exceeds the reserved scratch");
   FEPLL_REQUIRE(n_img >= 1 && n_total % n_img == 0, "select: n_total must be a multiple of n_img");
-  FEPLL_REQUIRE(n_total * std::max(2, p->max_children) < (int64_t(1) << 32),
+  FEPLL_REQUIRE(n_total * std::max({1, p->max_inner_children, p->max_leaf_children}) < (int64_t(1) << 32),
                 "select: too many patches for 32-bit segment offsets");
   FEPLL_REQUIRE(mode == 0 || mode == 1, "select: unknown mode");
-  const bool use_ws = mode == 1 && select_ws_supported(p);
   FEPLL_REQUIRE(mode == 0 || (Z32 != nullptr && p->have_tc),
                 "select: tensor mode needs a tcgen05 plan and the FP32 patch rows");
   cudaStream_t st = (cudaStream_t)stream;
@@ -464,11 +499,11 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
     for (int d = 0; d < p->n_levels; ++d) {
       LevelArgs a = make_level(p, d, t, labels);
       int rc = kOk;
-      if (mode == 1) {
-        rc = use_ws ? select_level_ws(p, a, Z32, sq, guard, st)
-                    : select_level_tc(p, a, Z32, sq, guard, st);
+      if (mode == 1 && !p->level_wide[d] && p->level_tc_npad[d] <= 256) {
+        rc = select_ws_supported(p, d) ? select_level_ws(p, a, Z32, sq, guard, st)
+                                       : select_level_tc(p, a, Z32, sq, guard, st);
         if (!rc) rc = rescore_queue_x(p, a, x, anchors, n_img, H, W, dc, sq, st);
-      } else {
+      } else {  // exact mode, or a wide level (sub-group FP64 scan)
         select_level_fp64_kernel<<<grid_for(n_total, kSelWarps, 148 * 8), kSelWarps * 32, 0, st>>>(
             p->v, a, ps, sq);
         FEPLL_LAUNCH();

@@ -217,10 +217,11 @@ static size_t tc_smem_bytes(int bmax_rows) {
 
 int select_level_tc(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                     cudaStream_t st) {
-  FEPLL_REQUIRE(p->max_tc_npad <= 256, "tensor mode supports nodes whose padded child ranks sum to <= 256");
+  FEPLL_REQUIRE(!p->level_wide[a.depth] && p->level_tc_npad[a.depth] <= 256,
+                "tensor level kernel: node wider than 256 padded columns");
   const int P = p->v.P;
   const int ppad = (P + 31) / 32 * 32;
-  const int bmax = std::max(16, p->max_tc_npad);
+  const int bmax = std::max(16, p->level_tc_npad[a.depth]);
   TcArgs args;
   args.a = a;
   args.Z32 = Z32;

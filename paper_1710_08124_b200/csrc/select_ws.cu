@@ -378,14 +378,11 @@ select_level_ws_kernel(PlanView pv, Args args) {
 uint64_t* g_ws_trace = nullptr;
 int g_ws_trace_level = -1;
 
-bool select_ws_supported(const Plan* p) {
-  int widest = 0, widest_next = 0;
-  for (int d = 0; d < p->n_levels; ++d) {
-    widest = std::max(widest, p->level_start[d + 1] - p->level_start[d]);
-    widest_next = std::max(widest_next, p->level_start[d + 2] - p->level_start[d + 1]);
-  }
-  return p->have_tc && p->v.P <= 64 && p->max_tc_npad <= ws::kMaxN && widest <= ws::kMaxNodes &&
-         widest_next <= ws::WsLevelTables::kCap;
+bool select_ws_supported(const Plan* p, int d) {
+  const int width = p->level_start[d + 1] - p->level_start[d];
+  const int width_next = p->level_start[d + 2] - p->level_start[d + 1];
+  return p->have_tc && p->v.P <= 64 && !p->level_wide[d] && p->level_tc_npad[d] <= ws::kMaxN &&
+         width <= ws::kMaxNodes && width_next <= ws::WsLevelTables::kCap;
 }
 
 // 2-D tensor map over the [rows][pitch] FP32 patch rows: boxes of one

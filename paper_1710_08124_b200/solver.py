@@ -30,6 +30,7 @@ from .operators import CgConfig
 from .patches import axis_anchors, jitter_rng, jittered_grid, regular_grid
 from .device_ops import DeviceOperator
 from .plan import DevicePlan
+from .tree import star_tree
 
 __all__ = ["RestorationConfig", "IterationStats", "SolverStats", "beta_schedule",
            "restore", "restore_batch", "Restorer", "SIGMA_FLOOR_8BIT"]
@@ -164,7 +165,8 @@ class Restorer:
                 raise DataError(f"tree has {tree.n_leaves} leaves but the model has "
                                 f"{len(model.components)} components")
         else:
-            raise DataError("exhaustive (no-tree) selection is not built on the device yet")
+            # exhaustive scan (solver.py:154-157) == descent of the one-level star tree
+            tree = self.tree = star_tree(model)
         if not config.use_flat_tail and not bool(np.all(
                 [c.kept_basis.shape[1] == P for c in model.components])):
             raise DataError("flat tail disabled: a full-rank model is required")
@@ -216,7 +218,7 @@ class Restorer:
         if kind in ("mask", "gain"):
             pm = np.asarray(A.pixel_map, dtype=np.float64)
             d = (pm != 0).astype(np.float64) if kind == "mask" else pm * pm
-            self.diag = torch.from_numpy(np.ascontiguousarray(np.broadcast_to(d, (B, H, W)))).to(dev)
+            self.diag = torch.from_numpy(d).to(dev).expand(B, H, W).contiguous()
         self.aty = torch.empty((B, H, W), dtype=f64, device=dev)
         self.pixel_kind = A.solve_strategy == "pixel_diagonal"
         # rhs of the FFT / CG image update and the solver infos

@@ -24,7 +24,7 @@ from .errors import DataError
 from .gmm import eigen_from_covariance, flatten_component
 
 __all__ = ["TreeNode", "GmmTree", "TreeTopology", "tree_topology",
-           "tree_from_partitions", "tree_partitions"]
+           "tree_from_partitions", "tree_partitions", "star_tree"]
 
 
 @dataclass
@@ -94,6 +94,19 @@ class TreeTopology:
     leaf_index: np.ndarray  # -1 for internal nodes
     depth: np.ndarray
     parent: np.ndarray
+
+
+def star_tree(model) -> GmmTree:
+    """The exhaustive scan (gmm.py:371-391, select_exhaustive) as a one-level
+    tree: the root's children are every component in index order, so the
+    device descent takes the first minimum over all K scores — np.argmin's
+    tie-break — and its path costs reproduce the no-tree counters of
+    solver.py:154-157 (K evaluations, P + sum of score_flat_cost per patch).
+    The root's own component is never scored."""
+    comps = list(model.components)
+    leaves = [TreeNode(component=c, leaf_index=k) for k, c in enumerate(comps)]
+    return GmmTree(root=TreeNode(component=comps[0], children=leaves),
+                   level_sizes=(1, len(comps)), patch_dim=int(model.patch_dim))
 
 
 def tree_topology(tree) -> TreeTopology:

@@ -28,7 +28,7 @@ def psnr(x, ref):
     return 10 * np.log10(1.0 / float(np.mean((np.clip(x, 0, 1) - ref) ** 2)))
 
 
-GOLDEN = ["cfg1", "regular48", "gain64", "inpaint96", "deblur96", "sr96"]
+GOLDEN = ["cfg1", "regular48", "gain64", "inpaint96", "deblur96", "sr96", "notree64"]
 
 
 @pytest.mark.parametrize("mode", ["exact", "tensor"])
@@ -38,7 +38,8 @@ def test_restore_matches_reference_golden(name, mode, models):
 
     g, A, y, s8, s, P = golden_inputs(name)
     model, tree = models[P]
-    cfg = RestorationConfig(sigma=s8, spacing=s, seed=0, trace=True, sampling=g["meta"]["sampling"])
+    cfg = RestorationConfig(sigma=s8, spacing=s, seed=0, trace=True, sampling=g["meta"]["sampling"],
+                            use_tree=bool(g["meta"]["use_tree"]))
     x, st = restore(y, A, model, tree, cfg, mode=mode)
     assert st.lam == pytest.approx(float(g["lam"]), rel=1e-10)
     for t, rec in enumerate(st.trace):

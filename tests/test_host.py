@@ -17,7 +17,7 @@ from paper_1710_08124_b200 import (DataError, RestorationConfig, beta_schedule, 
 from paper_1710_08124_b200 import _native as N
 from paper_1710_08124_b200.device_ops import frobenius_norm_sq_ata
 from paper_1710_08124_b200.plan import pack_plan, swizzle128_kmajor, tf32_split
-from paper_1710_08124_b200.tree import tree_partitions, tree_topology
+from paper_1710_08124_b200.tree import star_tree, tree_partitions, tree_topology
 
 
 # ---------------------------------------------------------------- C ABI
@@ -94,6 +94,24 @@ def test_path_costs_reproduce_reference_counters(models):
     g = load_golden("cfg1")
     model, tree = models[64]
     h = pack_plan(model, tree, [1.0], with_tc=False)
+    for t in range(g["labels"].shape[0]):
+        hist = np.bincount(g["labels"][t], minlength=200)
+        assert int(hist @ h["path_evals"]) == int(g["evals"][t])
+        assert int(hist @ h["path_mults"]) == int(g["sel_mults"][t])
+
+
+def test_star_tree_reproduces_exhaustive_counters(models):
+    """No-tree profile (solver.py:154-157): the star tree's path costs give
+    K evaluations and P + sum_k score_flat_cost(r_k, P) multiplies per patch,
+    the golden notree64 counters."""
+    g = load_golden("notree64")
+    model, _ = models[64]
+    star = star_tree(model)
+    topo = tree_topology(star)
+    assert topo.n_nodes == 201 and topo.child_count[0] == 200
+    np.testing.assert_array_equal(topo.leaf_index[1:], np.arange(200))
+    h = pack_plan(model, star, [1.0], with_tc=True)
+    assert h["grp_width"][0] == sum(c.kept_basis.shape[1] for c in model.components)
     for t in range(g["labels"].shape[0]):
         hist = np.bincount(g["labels"][t], minlength=200)
         assert int(hist @ h["path_evals"]) == int(g["evals"][t])
