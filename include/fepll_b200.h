@@ -76,6 +76,20 @@ int fepll_plan_create(const fepll_plan_desc* desc, fepll_plan_t* out);
 int fepll_plan_reserve(fepll_plan_t plan, int64_t max_patches);
 int fepll_plan_destroy(fepll_plan_t plan);
 
+/* patches.py:89-132: the sampling plan of iteration t on the device,
+ * bit-identical to jittered_grid(H, W, side^2, spacing,
+ * Generator(Philox(key=[seed, t]))) (jittered != 0) or regular_grid.
+ * key0/key1: the Philox key words numpy derives from [seed, t].
+ * anchors: [n_rows*n_cols][2] int32 (row, col), nominal row-major order.
+ * scratch: device int32[fepll_grid_scratch_ints()].  status bit 4 is set if
+ * more draws were rejected than the fix-up list holds (never expected).
+ * threshold_override: 0, or a Lemire rejection threshold used instead of
+ * (2^32 - n) mod n (test hook exercising the rejection fix-up). */
+int fepll_grid_scratch_ints(void);
+int fepll_sample_grid(uint64_t key0, uint64_t key1, int32_t H, int32_t W, int32_t side,
+                      int32_t spacing, int32_t jittered, uint32_t threshold_override,
+                      int32_t* anchors, int32_t* scratch, int32_t* status, void* stream);
+
 /* patches.py:167-183 (extract + _row_mean pairwise fold):
  * x: [batch][H][W] fp64; anchors: [n][2] int32 (row, col);
  * outputs (any may be NULL): Z64 [batch*n][P], Z32 [batch*n][z32_pitch]

@@ -66,6 +66,97 @@ def jittered_grid(H, W, P, s, seed, t):
     return pos
 
 
+# Counter-indexed restatement of the draw stream behind jittered_grid, the
+# model of the device generator (csrc/grid.cu).  numpy's Philox bit generator
+# (numpy/random/src/philox/philox.h, the Random123 Philox4x64-10) bumps its
+# 256-bit counter BEFORE each block, so block b (b = 0, 1, ...) is
+# philox4x64_10(ctr=[b+1, 0, 0, 0], key=[seed, t]); its four uint64 words are
+# consumed in order, each as two uint32 draws (low half first — philox_next32).
+# Generator.integers(lo, hi) for int64 ranges below 2^32 is Lemire's bounded
+# multiply (distributions.c buffered_bounded_lemire_uint32): m = u * n,
+# accept iff (m mod 2^32) >= (2^32 - n) mod n, value = lo + (m >> 32); a
+# rejected draw is skipped and the next one tried, so the values are the
+# accepted draws of the stream in order.
+_PHILOX_M = (0xD2E7470EE14C6C93, 0xCA5A826395121157)
+_PHILOX_W = (0x9E3779B97F4A7C15, 0xBB67AE8584CAA73B)
+_M64 = (1 << 64) - 1
+
+
+def philox4x64_10(ctr, key):
+    """Random123 philox4x64 with 10 rounds (numpy philox.h philox4x64_R)."""
+    c = [int(v) & _M64 for v in ctr]
+    k = [int(v) & _M64 for v in key]
+    for r in range(10):
+        if r:
+            k = [(k[0] + _PHILOX_W[0]) & _M64, (k[1] + _PHILOX_W[1]) & _M64]
+        p0 = _PHILOX_M[0] * c[0]
+        p1 = _PHILOX_M[1] * c[2]
+        c = [(p1 >> 64) ^ c[1] ^ k[0], p1 & _M64, (p0 >> 64) ^ c[3] ^ k[1], p0 & _M64]
+    return c
+
+
+def philox_key(seed, t):
+    """Key words numpy's Philox derives from the list [seed & (2^64-1), t]
+    (patches.py:104; numpy converts the list, which matters for seeds >= 2^63)."""
+    k = np.random.Philox(key=[seed & _M64, t]).state["state"]["key"]
+    return int(k[0]), int(k[1])
+
+
+def philox_draw32(key, j, _cache={}):
+    """uint32 draw j of the stream with Philox key words `key`."""
+    q = j >> 1
+    blk = (key, q >> 2)
+    if blk not in _cache:
+        if len(_cache) > 4096:
+            _cache.clear()
+        _cache[blk] = philox4x64_10([(q >> 2) + 1, 0, 0, 0], key)
+    word = _cache[blk][q & 3]
+    return (word >> 32) if (j & 1) else (word & 0xFFFFFFFF)
+
+
+def lemire_threshold(n_excl):
+    return ((1 << 32) - n_excl) % n_excl
+
+
+def bounded_draws(seed, t, start, count, n_excl, threshold=None):
+    """`count` accepted Lemire draws over [0, n_excl) from stream position
+    `start`; returns (values, next position).  `threshold` overrides the
+    rejection threshold (test hook for the device fix-up path)."""
+    key = philox_key(seed, t)
+    th = lemire_threshold(n_excl) if threshold is None else threshold
+    out, j = [], start
+    while len(out) < count:
+        m = philox_draw32(key, j) * n_excl
+        j += 1
+        if (m & 0xFFFFFFFF) >= th:
+            out.append(m >> 32)
+    return np.asarray(out, dtype=np.int64), j
+
+
+def jittered_grid_counter(H, W, P, s, seed, t, threshold=None):
+    """jittered_grid recomputed from the counter-indexed stream (pinned to
+    numpy's Generator by tests/test_oracle_golden.py)."""
+    side = math.isqrt(P)
+    base = regular_grid(H, W, P, s)
+    half = (side - s) // 2
+    if half == 0:
+        return base
+    j = 0
+    if s > 1:
+        shift, j = bounded_draws(seed, t, 0, 2, s, threshold)
+    else:
+        shift = np.zeros(2, np.int64)
+    eff = shift % (2 * half + 1) - half
+    jit, _ = bounded_draws(seed, t, j, base.size, 2 * half + 1, threshold)
+    off = np.clip(eff[None, :] + (jit.reshape(base.shape) - half), -half, half)
+    off[(base[:, 0] == 0) | (base[:, 0] == H - side), 0] = 0
+    off[(base[:, 1] == 0) | (base[:, 1] == W - side), 1] = 0
+    pos = base + off
+    pos[:, 0] = np.clip(pos[:, 0], 0, H - side)
+    pos[:, 1] = np.clip(pos[:, 1], 0, W - side)
+    return pos
+
+
 # ---------------------------------------------------------------- extraction
 def pairwise_mean(rows):
     """pkg/src/fepll/patches.py:153-164: halve the width until one column

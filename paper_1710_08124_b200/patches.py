@@ -11,9 +11,9 @@ Two producers exist for the jittered plan:
 
 * :func:`jittered_grid` — host numpy (the same bit generator the reference
   uses); kept for plan inspection and the CPU tests;
-* the device generator ``fepll_jitter_grid`` in ``csrc/grid.cu`` — a
-  counter-indexed Philox4x64-10 + Lemire restatement that runs inside the
-  restoration loop (`plan_grid_device`).
+* the device generator ``fepll_sample_grid`` in ``csrc/grid.cu`` — a
+  counter-indexed Philox4x64-10 + Lemire restatement with a rejection
+  fix-up, which the solver uses (``Restorer._grid``).
 """
 
 from __future__ import annotations
@@ -26,7 +26,7 @@ import numpy as np
 from .errors import DataError
 
 __all__ = ["SampleGrid", "axis_anchors", "regular_grid", "jitter_rng", "jittered_grid",
-           "grid_draw_layout"]
+           "grid_draw_layout", "philox_key"]
 
 
 @dataclass
@@ -76,6 +76,13 @@ def regular_grid(H: int, W: int, patch_dim: int, spacing: int) -> SampleGrid:
 
 def jitter_rng(seed: int, iteration: int) -> np.random.Generator:
     return np.random.Generator(np.random.Philox(key=[seed & (2 ** 64 - 1), iteration]))
+
+
+def philox_key(seed: int, iteration: int) -> tuple:
+    """The two Philox key words numpy derives for jitter_rng(seed, iteration)
+    (fed to the device generator so numpy's key-list conversion carries over)."""
+    k = jitter_rng(seed, iteration).bit_generator.state["state"]["key"]
+    return int(k[0]), int(k[1])
 
 
 def jittered_grid(H: int, W: int, patch_dim: int, spacing: int,

@@ -27,7 +27,7 @@ from . import _native as N
 from .errors import DataError, NumericalError
 from .gmm import score_flat_cost, wiener_flat_cost
 from .operators import CgConfig
-from .patches import axis_anchors, jitter_rng, jittered_grid, regular_grid
+from .patches import axis_anchors, philox_key
 from .device_ops import DeviceOperator
 from .plan import DevicePlan
 from .tree import star_tree
@@ -189,14 +189,16 @@ class Restorer:
             self.lam = float(lam)
         self.betas = beta_schedule(self.sigma, self.lam, config.beta_multipliers)
         self.plan = DevicePlan(model, tree, self.betas, with_tc=(mode == "tensor"))
+        dev = self.device
+        # sampling plans: generated on the device (csrc/grid.cu), bitwise the
+        # reference's numpy Philox draws (patches.py:102-132)
         self._grids = [self._grid(t) for t in range(config.iterations)]
-        n = self._grids[0][0].shape[0]
+        self.anchors = [g[0] for g in self._grids]
+        n = int(self.anchors[0].shape[0])
         self.n = n
         self.plan.reserve(n * self.batch)
-        dev = self.device
         B, H, W = self.batch, self.H, self.W
         f64 = torch.float64
-        self.anchors = [torch.from_numpy(g[0]).to(dev) for g in self._grids]
         self.z32_pitch = ((P + 31) // 32) * 32
         # FP64 patch rows (kernel (a) output) feed the DMMA Wiener kernel
         self.Z64 = torch.empty((B * n, P), dtype=f64, device=dev)
@@ -228,16 +230,24 @@ class Restorer:
 
     # ---------------------------------------------------------------- setup
     def _grid(self, t: int):
+        """(device anchors [n][2] int32, n_rows, n_cols, half) of iteration t."""
+        torch = self.torch
         c = self.config
-        H, W, P, s = self.H, self.W, self.P, c.spacing
-        if c.sampling == "jittered":
-            pos = jittered_grid(H, W, P, s, jitter_rng(c.seed, t)).positions
-        else:
-            pos = regular_grid(H, W, P, s).positions
-        half = (self.side - s) // 2 if c.sampling == "jittered" else 0
-        nr = axis_anchors(H, self.side, s).size
-        nc = axis_anchors(W, self.side, s).size
-        return np.ascontiguousarray(pos, dtype=np.int32), nr, nc, half
+        H, W, s, side = self.H, self.W, c.spacing, self.side
+        jit = c.sampling == "jittered"
+        half = (side - s) // 2 if jit else 0
+        nr = axis_anchors(H, side, s).size
+        nc = axis_anchors(W, side, s).size
+        anchors = torch.empty((nr * nc, 2), dtype=torch.int32, device=self.device)
+        scratch = torch.empty(N.lib().fepll_grid_scratch_ints(), dtype=torch.int32, device=self.device)
+        status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        k0, k1 = philox_key(c.seed, t)
+        N.call("fepll_sample_grid", k0, k1, H, W, side, s, int(jit), 0,
+               N.ptr(anchors), N.ptr(scratch), N.ptr(status), st)
+        if int(status.item()) & 4:
+            raise NumericalError("sampling plan: more rejected Philox draws than the fix-up list holds")
+        return anchors, nr, nc, half
 
     # ---------------------------------------------------------------- loop
     def run(self, y_dev, trace: bool = False, timer: dict | None = None):
@@ -267,7 +277,8 @@ class Restorer:
             self._iteration(t, st, timer)
             if trace:
                 B, n = self.batch, self.n
-                records.append({"beta": float(self.betas[t]), "positions": self._grids[t][0],
+                records.append({"beta": float(self.betas[t]),
+                                "positions": self.anchors[t].cpu().numpy().astype(np.int64),
                                 "labels": self.labels.view(B, n).cpu().numpy().copy(),
                                 "dc": self.dc.view(B, n).cpu().numpy().copy(),
                                 "x_tilde": self.xt.cpu().numpy().copy(),
@@ -283,9 +294,8 @@ class Restorer:
 
     def _iteration(self, t: int, st, timer=None) -> None:
         B, H, W, P, side = self.batch, self.H, self.W, self.P, self.side
-        pos, nr, nc, half = self._grids[t]
-        anchors = self.anchors[t]
-        n = pos.shape[0]
+        anchors, nr, nc, half = self._grids[t]
+        n = self.n
         nt = B * n
         mode = self.MODES[self.mode]
         self._mark(timer, "start")

@@ -163,6 +163,49 @@ def test_extract_kernel_bitwise():
         np.testing.assert_allclose(sq.cpu().numpy(), np.einsum("ij,ij->i", Zo, Zo), rtol=1e-13)
 
 
+def _device_grid(H, W, P, s, seed, t, jittered=True, threshold=0):
+    import torch
+    from paper_1710_08124_b200 import _native as N
+    from paper_1710_08124_b200.patches import axis_anchors, philox_key
+
+    side = int(np.sqrt(P))
+    n = axis_anchors(H, side, s).size * axis_anchors(W, side, s).size
+    anchors = torch.empty((n, 2), dtype=torch.int32, device="cuda")
+    scratch = torch.empty(N.lib().fepll_grid_scratch_ints(), dtype=torch.int32, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    k0, k1 = philox_key(seed, t)
+    N.call("fepll_sample_grid", k0, k1, H, W, side, s, int(jittered), threshold, N.ptr(anchors),
+           N.ptr(scratch), N.ptr(status), torch.cuda.current_stream().cuda_stream)
+    assert int(status.item()) == 0
+    return anchors.cpu().numpy().astype(np.int64), int(scratch[3].item())
+
+
+def test_device_sampling_plan_bitwise_vs_numpy():
+    """csrc/grid.cu == jittered_grid(Generator(Philox(key=[seed, t]))) and
+    regular_grid, over sizes, spacings, P, seeds (incl. >= 2^63) and t."""
+    from paper_1710_08124_b200 import jitter_rng, jittered_grid, regular_grid
+
+    for (H, W, P, s) in [(64, 64, 64, 4), (41, 53, 64, 3), (96, 96, 100, 6), (33, 47, 64, 1),
+                         (512, 512, 64, 4), (1024, 768, 64, 2), (510, 510, 100, 5), (8, 8, 64, 6)]:
+        for seed, t in [(0, 0), (0, 4), (11, 2), (2 ** 64 - 1, 3), (987654321987, 1)]:
+            want = jittered_grid(H, W, P, s, jitter_rng(seed, t)).positions
+            got, _ = _device_grid(H, W, P, s, seed, t)
+            np.testing.assert_array_equal(got, want)
+        np.testing.assert_array_equal(_device_grid(H, W, P, s, 0, 0, jittered=False)[0],
+                                      regular_grid(H, W, P, s).positions)
+
+
+def test_device_sampling_plan_rejection_fixup():
+    """Forced Lemire rejections (threshold override, ~1% of draws) follow the
+    counter-indexed oracle stream, whose unforced form is pinned to numpy."""
+    for (H, W, P, s, seed, t) in [(96, 96, 64, 4, 5, 1), (64, 80, 100, 6, 0, 3), (48, 48, 64, 2, 9, 0)]:
+        th = 1 << 25
+        want = O.jittered_grid_counter(H, W, P, s, seed, t, threshold=th)
+        got, rejects = _device_grid(H, W, P, s, seed, t, threshold=th)
+        assert rejects > 0
+        np.testing.assert_array_equal(got, want)
+
+
 def test_aggregate_kernel_bitwise_vs_bincount():
     """Fed the reference's estimates, the ordered gather reproduces
     np.bincount's sums bit for bit (patches.py:198-222)."""

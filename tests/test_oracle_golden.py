@@ -64,3 +64,26 @@ def test_grids_match_reference():
         np.testing.assert_array_equal(opos, pos)
         if f"pos_{i}" in d.files:
             np.testing.assert_array_equal(d[f"pos_{i}"], pos)
+
+
+def test_counter_indexed_philox_stream_pinned_to_numpy():
+    """The device generator's model (counter-indexed Philox4x64-10 blocks,
+    low/high uint32 halves, Lemire acceptance) reproduces numpy's Generator:
+    raw blocks, bounded draws, and whole grids — the golden ones included."""
+    for seed, t in [(0, 0), (11, 3), (2 ** 64 - 1, 7), (123456789012345, 2)]:
+        raw = np.random.Philox(key=[seed, t]).random_raw(12)
+        for b in range(3):
+            assert O.philox4x64_10([b + 1, 0, 0, 0], O.philox_key(seed, t)) == \
+                [int(v) for v in raw[4 * b:4 * b + 4]]
+        g = np.random.Generator(np.random.Philox(key=[seed, t]))
+        a = g.integers(0, 4, size=2)
+        b_ = g.integers(-2, 3, size=50)
+        va, j = O.bounded_draws(seed, t, 0, 2, 4)
+        vb, _ = O.bounded_draws(seed, t, j, 50, 5)
+        np.testing.assert_array_equal(a, va)
+        np.testing.assert_array_equal(b_, vb - 2)
+    d = np.load(GOLDEN / "grids.npz")
+    for key in d["keys"]:
+        H, W, P, s, seed, t = (int(v) for v in key)
+        np.testing.assert_array_equal(O.jittered_grid_counter(H, W, P, s, seed, t),
+                                      O.jittered_grid(H, W, P, s, seed, t))
