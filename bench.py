@@ -44,6 +44,8 @@ sys.path.insert(0, str(ROOT))
 WORKLOADS = {
     # name: (config key, images, size)
     "cfg5-batch": ("cfg5", 64, 1024),
+    # one 8192^2 image split by pixel rows across ranks (halo exchange per iteration)
+    "cfg5-strip": ("cfg5", 1, 8192),
     "cfg2": ("cfg2", 1, 512),
     "cfg1": ("cfg1", 1, 256),
 }
@@ -214,19 +216,31 @@ def main():
     from paper_1710_08124_b200 import _native as N
 
     key, n_images, size = WORKLOADS[args.workload]
-    if n_images % world and n_images > 1:
-        raise SystemExit(f"{n_images} images do not split over {world} ranks")
-    per = max(1, n_images // world)
-    mine = list(range(rank * per, rank * per + per)) if n_images > 1 else [0]
+    from paper_1710_08124_b200.strips import StripRestorer, batch_shard
+    strip = args.workload == "cfg5-strip"
+    mine = batch_shard(n_images, world, rank) if n_images > 1 else [0]
     A, ys, clean, spec = inputs(args.workload, mine)
     P = spec["patch_dim"]
     model = synthetic.synthetic_gmm(200, P, 0, 0.95)
     tree = synthetic.baseline_tree(model)
     cfg = RestorationConfig(sigma=spec["sigma"], spacing=spec["spacing"], seed=0)
     t_setup = time.perf_counter()
-    r = Restorer(A, model, tree, cfg, batch=len(mine), mode=args.mode, device=dev)
+    if strip:
+        sr = StripRestorer(size, size, model, tree, cfg, rank, world, mode=args.mode, device=dev)
+        r = sr.restorer
+        sp = sr.spec
+        # this rank's slab of the observation; owned rows come back
+        ys, clean = ys[:, sp.slab_lo:sp.slab_hi], clean[:, sp.r0:sp.r1]
+
+        def run(y, timer=None):
+            return sr.run(y, timer=timer)[None]
+    else:
+        r = Restorer(A, model, tree, cfg, batch=len(mine), mode=args.mode, device=dev)
+
+        def run(y, timer=None):
+            return r.run(y, timer=timer)[0]
     setup_s = time.perf_counter() - t_setup
-    y_dev = torch.from_numpy(ys).to(dev)
+    y_dev = torch.from_numpy(np.ascontiguousarray(ys)).to(dev)
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -235,7 +249,7 @@ def main():
         torch.cuda.synchronize(dev)
 
     for _ in range(args.warmup):
-        r.run(y_dev)
+        run(y_dev)
     barrier()
     launches0 = N.lib().fepll_launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -244,7 +258,7 @@ def main():
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
-            r.run(y_dev)
+            run(y_dev)
         e1.record(stream)
         barrier()
     launches = (N.lib().fepll_launch_count() - launches0) // args.steps
@@ -258,15 +272,14 @@ def main():
 
     # ---- end to end through the public API on host buffers
     pin_in = torch.from_numpy(ys.astype(np.float32)).pin_memory()
-    pin_out = torch.empty(pin_in.shape, dtype=torch.float32).pin_memory()
+    pin_out = torch.empty(clean.shape, dtype=torch.float32).pin_memory()
     y32 = torch.empty(pin_in.shape, dtype=torch.float32, device=dev)
     y64 = torch.empty(pin_in.shape, dtype=torch.float64, device=dev)
 
     def e2e_step():
         y32.copy_(pin_in, non_blocking=True)
         y64.copy_(y32)
-        x, _ = r.run(y64)
-        pin_out.copy_(x, non_blocking=True)
+        pin_out.copy_(run(y64), non_blocking=True)
 
     e2e_step()
     barrier()
@@ -282,12 +295,13 @@ def main():
         dist.all_reduce(ms_e2e, op=dist.ReduceOp.MAX)
     e2e_value = total_mp / (float(ms_e2e.item()) / 1e3)
     out = pin_out.numpy().astype(np.float64)
-    psnr_in = [10 * np.log10(1 / np.mean((np.clip(ys[i], 0, 1) - clean[i]) ** 2)) for i in range(len(mine))]
+    y_owned = ys[:, sp.r0 - sp.slab_lo:sp.r1 - sp.slab_lo] if strip else ys
+    psnr_in = [10 * np.log10(1 / np.mean((np.clip(y_owned[i], 0, 1) - clean[i]) ** 2)) for i in range(len(mine))]
     psnr_out = [10 * np.log10(1 / np.mean((np.clip(out[i], 0, 1) - clean[i]) ** 2)) for i in range(len(mine))]
 
     # ---- phase profile (one extra step with events between phases)
     timer: dict = {}
-    r.run(y_dev, timer=timer)
+    run(y_dev, timer=timer)
     torch.cuda.synchronize(dev)
     phases = Restorer.phase_times(timer)
     counters = r.counters()
@@ -325,14 +339,17 @@ def main():
         sys.path.insert(0, str(ROOT / "oracle"))
         import fepll_oracle as O
 
-        k = min(args.cpu_sample_images, len(mine))
+        # a 1024^2 crop per sample image for the strip workload (bounded CPU time)
+        k = min(args.cpu_sample_images, len(mine)) if not strip else 1
+        crop = 1024 if strip else size
+        A_s = A if not strip else synthetic.baseline_case("cfg5", crop).A
         t0 = time.perf_counter()
         for i in range(k):
-            cpu_reference_step(A, ys[i], model, tree, spec, 1.0, 1)
+            cpu_reference_step(A_s, np.ascontiguousarray(ys[i][:crop, :crop]), model, tree, spec, 1.0, 1)
         dt = time.perf_counter() - t0
-        cpu = {"value": k * size * size / 1e6 / dt, "unit": "MP/s", "cores": 1, "kind": "port",
-               "sample": f"{k} of the {n_images} images ({size}^2), single worker like the "
-                         f"reference default (host has {O.host_threads()} threads)"}
+        cpu = {"value": k * crop * crop / 1e6 / dt, "unit": "MP/s", "cores": 1, "kind": "port",
+               "sample": f"{k} x {crop}^2 {'crop of the image' if strip else 'of the images'}, "
+                         f"single worker like the reference default (host has {O.host_threads()} threads)"}
 
     if rank == 0:
         clocks = clk.summary()
@@ -343,8 +360,10 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64+tf32x3",
             "data": "synthetic (BASELINE piecewise-smooth images, seeded K=200 GMM + reference tree)",
             "config": {"workload": f"{args.workload}: {n_images} x {size}x{size} denoise sigma="
-                                   f"{spec['sigma']}, P={P}, stride {spec['spacing']} jittered, 5 HQS iterations",
-                       "images_per_rank": len(mine), "mode": args.mode,
+                                   f"{spec['sigma']}, P={P}, stride {spec['spacing']} jittered, 5 HQS iterations"
+                                   + (f", {world} row strips with halo exchange" if strip else ""),
+                       "images_per_rank": len(mine) if not strip else f"1/{world} (rows {sp.r0}-{sp.r1})",
+                       "mode": args.mode,
                        "l2": "inputs larger than L2 (state 8 MB/image x batch)",
                        "setup_s_excluded": round(setup_s, 3)},
             "roofline": roof,

@@ -134,6 +134,20 @@ int fepll_aggregate(const double* Zhat, const double* dc, const int32_t* anchors
                     const double* aty, const double* diag, double bs2, int32_t kind,
                     double* x_out, double* xtilde_out, int32_t* status, void* stream);
 
+/* Strip form of fepll_aggregate (one image split by pixel rows across
+ * ranks): the local image ([batch][H][W]) is global rows [row0, row0+H) of an
+ * image with H_glob rows; Zhat/dc/anchors hold the patches of global nominal
+ * anchor rows [a_first, a_first + n_local_rows) (anchor rows local to the
+ * strip); n_rows is the global nominal row count.  Only local rows
+ * [r_begin, r_end) are written, each bit-identical to the unsplit result. */
+int fepll_aggregate_strip(const double* Zhat, const double* dc, const int32_t* anchors,
+                          int32_t n_rows, int32_t n_cols, int32_t spacing, int32_t half,
+                          int32_t side, int32_t batch, int32_t H, int32_t W,
+                          int32_t row0, int32_t H_glob, int32_t a_first,
+                          int32_t n_local_rows, int32_t r_begin, int32_t r_end,
+                          const double* aty, const double* diag, double bs2, int32_t kind,
+                          double* x_out, double* xtilde_out, int32_t* status, void* stream);
+
 /* ---- degradation operators (operators.py:51-394); handle = opaque plan.
  * kind: 0 identity, 1 convolution, 2 mask, 3 gain, 4 decimate (factor).
  * taps: [kh][kw] host kernel (kinds 1, 4); pixel_map: [H][W] host (2, 3). */

@@ -54,6 +54,8 @@ _SIGS = {
     "fepll_select_rescored": (i32, [vp, vp, vp]),
     "fepll_aggregate": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, vp, vp, f64,
                               i32, vp, vp, vp, vp]),
+    "fepll_aggregate_strip": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32,
+                                    i32, i32, i32, i32, i32, i32, vp, vp, f64, i32, vp, vp, vp, vp]),
     "fepll_op_create": (i32, [i32, i32, i32, i32, vp, i32, i32, vp, C.POINTER(vp)]),
     "fepll_op_destroy": (i32, [vp]),
     "fepll_op_adjoint": (i32, [vp, vp, vp, vp]),

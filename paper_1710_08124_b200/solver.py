@@ -145,8 +145,16 @@ class Restorer:
     MODES = {"exact": 0, "tensor": 1}
 
     def __init__(self, A, model, tree, config, batch: int = 1, lam: float | None = None,
-                 mode: str = "tensor", device=None, guard: float = 0.0):
+                 mode: str = "tensor", device=None, guard: float = 0.0, strip=None):
         _validate_config(config)
+        # strip mode (strips.StripSpec): A covers the strip's slab of a larger
+        # image; only the owned rows are aggregated (denoise, batch 1)
+        self.strip = strip
+        if strip is not None:
+            if A.kind != "identity" or int(batch) != 1:
+                raise DataError("strip mode restores one denoising image (identity operator, batch 1)")
+            if tuple(A.input_dims) != (strip.slab_hi - strip.slab_lo, strip.W):
+                raise DataError("strip operator dims differ from the strip's slab")
         self.config = config
         self.A = A
         self.model = model
@@ -238,6 +246,10 @@ class Restorer:
         half = (side - s) // 2 if jit else 0
         nr = axis_anchors(H, side, s).size
         nc = axis_anchors(W, side, s).size
+        sp = self.strip
+        if sp is not None:  # the global grid; this strip keeps nominal rows a_lo..a_hi
+            H = sp.H
+            nr = axis_anchors(H, side, s).size
         anchors = torch.empty((nr * nc, 2), dtype=torch.int32, device=self.device)
         scratch = torch.empty(N.lib().fepll_grid_scratch_ints(), dtype=torch.int32, device=self.device)
         status = torch.zeros(1, dtype=torch.int32, device=self.device)
@@ -247,13 +259,27 @@ class Restorer:
                N.ptr(anchors), N.ptr(scratch), N.ptr(status), st)
         if int(status.item()) & 4:
             raise NumericalError("sampling plan: more rejected Philox draws than the fix-up list holds")
+        if sp is not None:
+            anchors = anchors[sp.a_lo * nc:(sp.a_hi + 1) * nc].clone()
+            anchors[:, 0] -= sp.slab_lo
         return anchors, nr, nc, half
 
     # ---------------------------------------------------------------- loop
-    def run(self, y_dev, trace: bool = False, timer: dict | None = None):
+    def run(self, y_dev, trace: bool = False, timer: dict | None = None, exchange=None):
         """y_dev: (B, Ho, Wo) float64 device tensor.  Returns x (B, H, W) on
         the device and the per-iteration records.  ``timer`` (optional dict)
-        collects CUDA-event pairs per phase for profiling."""
+        collects CUDA-event pairs per phase for profiling; ``exchange(t)``
+        (strip mode) refreshes the halo rows after iteration t."""
+        self.start(y_dev, timer)
+        records = []
+        for t in range(len(self.betas)):
+            records.extend(self.iterate(t, trace, timer))
+            if exchange is not None and t + 1 < len(self.betas):
+                exchange(t)
+        return self.x, records
+
+    def start(self, y_dev, timer: dict | None = None) -> None:
+        """x0 (solver.py:195-198) for a device-resident observation batch."""
         torch = self.torch
         st = torch.cuda.current_stream(self.device).cuda_stream
         A = self.A
@@ -271,19 +297,22 @@ class Restorer:
                 self.op.init(y_dev[b], self.aty[b], self.sigma, self.lam, cg.tolerance,
                              cg.max_iterations, self.x[b], self.init_info[b], st)
         self._mark(timer, "init")
-        records = []
-        for t in range(len(self.betas)):
-            self._want_xt = trace
-            self._iteration(t, st, timer)
-            if trace:
-                B, n = self.batch, self.n
-                records.append({"beta": float(self.betas[t]),
-                                "positions": self.anchors[t].cpu().numpy().astype(np.int64),
-                                "labels": self.labels.view(B, n).cpu().numpy().copy(),
-                                "dc": self.dc.view(B, n).cpu().numpy().copy(),
-                                "x_tilde": self.xt.cpu().numpy().copy(),
-                                "x": self.x.cpu().numpy().copy()})
-        return self.x, records
+
+    def iterate(self, t: int, trace: bool = False, timer: dict | None = None) -> list:
+        """One HQS iteration (solver.py:200-262); returns its trace record
+        (empty unless ``trace``)."""
+        st = self.torch.cuda.current_stream(self.device).cuda_stream
+        self._want_xt = trace
+        self._iteration(t, st, timer)
+        if not trace:
+            return []
+        B, n = self.batch, self.n
+        return [{"beta": float(self.betas[t]),
+                 "positions": self.anchors[t].cpu().numpy().astype(np.int64),
+                 "labels": self.labels.view(B, n).cpu().numpy().copy(),
+                 "dc": self.dc.view(B, n).cpu().numpy().copy(),
+                 "x_tilde": self.xt.cpu().numpy().copy(),
+                 "x": self.x.cpu().numpy().copy()}]
 
     def _mark(self, timer, name):
         if timer is None:
@@ -311,7 +340,15 @@ class Restorer:
                N.ptr(self.dc), N.ptr(self.Z64), nt, N.ptr(self.Zhat), st)
         self._mark(timer, "wiener")
         bs2 = float(self.betas[t]) * self.sigma * self.sigma
-        if self.pixel_kind:
+        if self.strip is not None:
+            sp = self.strip
+            N.call("fepll_aggregate_strip", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(anchors), nr, nc,
+                   self.config.spacing, half, side, B, H, W, sp.slab_lo, sp.H, sp.a_lo,
+                   sp.a_hi - sp.a_lo + 1, sp.r0 - sp.slab_lo, sp.r1 - sp.slab_lo, N.ptr(self.aty),
+                   N.ptr(self.diag), bs2, 0, N.ptr(self.x), N.ptr(self.xt) if self._want_xt else None,
+                   N.ptr(self.status), st)
+            self._mark(timer, "aggregate")
+        elif self.pixel_kind:
             # reproject + pixel-diagonal update fused (patches.py:198-222, operators.py:281-287)
             N.call("fepll_aggregate", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(anchors), nr, nc,
                    self.config.spacing, half, side, B, H, W, N.ptr(self.aty), N.ptr(self.diag),

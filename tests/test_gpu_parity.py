@@ -163,6 +163,23 @@ def test_extract_kernel_bitwise():
         np.testing.assert_allclose(sq.cpu().numpy(), np.einsum("ij,ij->i", Zo, Zo), rtol=1e-13)
 
 
+@pytest.mark.parametrize("mode", ["tensor", "exact"])
+@pytest.mark.parametrize("H,W,world,s", [(160, 96, 3, 4), (130, 77, 2, 3), (96, 64, 4, 2)])
+def test_strip_mode_bitwise_equals_unsplit(H, W, world, s, mode, models):
+    """SURVEY §8(e) strip mode: world strips with halo exchange between HQS
+    iterations reproduce the single-image run bit for bit."""
+    from paper_1710_08124_b200 import RestorationConfig, identity_operator, restore, synthetic
+    from paper_1710_08124_b200.strips import restore_strips_single_process
+
+    model, tree = models[64]
+    img = synthetic.synthetic_image(H, W, 3) / 255.0
+    y = img + (25.0 / 255.0) * np.random.default_rng(5).standard_normal((H, W))
+    cfg = RestorationConfig(sigma=25.0, spacing=s, seed=2)
+    x_full, _ = restore(y, identity_operator((H, W)), model, tree, cfg, mode=mode)
+    x_strips = restore_strips_single_process(y, model, tree, cfg, world, mode=mode)
+    assert np.array_equal(x_strips, x_full)
+
+
 def _device_grid(H, W, P, s, seed, t, jittered=True, threshold=0):
     import torch
     from paper_1710_08124_b200 import _native as N
