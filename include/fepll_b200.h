@@ -92,10 +92,12 @@ int fepll_sample_grid(uint64_t key0, uint64_t key1, int32_t H, int32_t W, int32_
 
 /* patches.py:167-183 (extract + _row_mean pairwise fold):
  * x: [batch][H][W] fp64; anchors: [n][2] int32 (row, col);
+ * grid_cols: anchors per nominal grid row when anchors is a row-major grid
+ * (enables the shared-memory tiled kernel), else 0;
  * outputs (any may be NULL): Z64 [batch*n][P], Z32 [batch*n][z32_pitch]
  * (zero-padded past P; the tcgen05 scorer reads 128-byte K atoms), dc, sq. */
 int fepll_extract(const double* x, int32_t batch, int32_t H, int32_t W, int32_t side,
-                  const int32_t* anchors, int32_t n, double* Z64, float* Z32,
+                  const int32_t* anchors, int32_t n, int32_t grid_cols, double* Z64, float* Z32,
                   int32_t z32_pitch, double* dc, double* sq, void* stream);
 
 /* tree.py:387-434 (greedy descent, first-min tie break) over n_total =
@@ -145,6 +147,29 @@ int fepll_aggregate_strip(const double* Zhat, const double* dc, const int32_t* a
                           int32_t side, int32_t batch, int32_t H, int32_t W,
                           int32_t row0, int32_t H_glob, int32_t a_first,
                           int32_t n_local_rows, int32_t r_begin, int32_t r_end,
+                          const double* aty, const double* diag, double bs2, int32_t kind,
+                          double* x_out, double* xtilde_out, int32_t* status, void* stream);
+
+/* Cover lists (CSR) of a sampling plan: for local rows [r_begin, r_end) of a
+ * (strip of an) image, the anchors covering each pixel in ascending patch
+ * order (the np.bincount order of patches.py:213-220), entry = local patch
+ * index << 8 | (dr*side + dcol).  The plan is shared by all images of a
+ * batch, so this is built once per iteration's grid.  ptr: [npx + 1],
+ * entries: >= n_local_rows*n_cols*side^2, scratch: int32
+ * [fepll_cover_scratch_ints(npx)], npx = (r_end - r_begin) * W.
+ * Geometry arguments as fepll_aggregate_strip. */
+int64_t fepll_cover_scratch_ints(int64_t n_pixels);
+int fepll_cover_build(const int32_t* anchors, int32_t n_rows, int32_t n_cols, int32_t spacing,
+                      int32_t half, int32_t side, int32_t W, int32_t row0, int32_t H_glob,
+                      int32_t a_first, int32_t n_local_rows, int32_t r_begin, int32_t r_end,
+                      int32_t* ptr, int32_t* entries, int64_t entries_cap, int32_t* scratch,
+                      void* stream);
+
+/* fepll_aggregate over cover lists (bit-identical results): Zhat/dc hold
+ * n_local patches per image, images [batch][H][W]; rows [r_begin, r_end). */
+int fepll_aggregate_cover(const double* Zhat, const double* dc, const int32_t* ptr,
+                          const int32_t* entries, int32_t P, int32_t n_local, int32_t batch,
+                          int32_t H, int32_t W, int32_t r_begin, int32_t r_end,
                           const double* aty, const double* diag, double bs2, int32_t kind,
                           double* x_out, double* xtilde_out, int32_t* status, void* stream);
 

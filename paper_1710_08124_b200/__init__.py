@@ -12,7 +12,7 @@ from .model_io import model_read, model_write, tree_read, tree_write
 from .operators import (CgConfig, DegradationOperator, SolveInfo, convolution_operator,
                         decimate_operator, gain_operator, gaussian_kernel, identity_operator,
                         mask_operator, radial_gain_map)
-from .patches import SampleGrid, jitter_rng, jittered_grid, regular_grid
+from .patches import SampleGrid, axis_anchors, jitter_rng, jittered_grid, regular_grid
 from .solver import (IterationStats, RestorationConfig, Restorer, SolverStats, beta_schedule,
                      restore, restore_batch)
 from .tree import GmmTree, TreeNode

@@ -18,6 +18,8 @@
 // pkg/src/fepll/operators.py:281-287 (x = (A^T y + bs2 x~) / (diag + bs2)) is
 // applied in the same pass with explicit round-to-nearest multiply/add (no
 // FMA contraction) so it is bit-identical to numpy's two-step evaluation.
+#include <climits>
+
 #include "common.cuh"
 
 namespace fepll {
@@ -26,52 +28,45 @@ __device__ __forceinline__ int ceil_div_floor0(int num, int s) {
   return num <= 0 ? 0 : (num + s - 1) / s;
 }
 
-__global__ void __launch_bounds__(256)
-aggregate_kernel(const double* __restrict__ Zhat, const double* __restrict__ dc,
-                 const int32_t* __restrict__ anchors, int n_rows, int n_cols, int s, int half,
-                 int side, int batch, int H, int W, const double* __restrict__ aty,
-                 const double* __restrict__ diag, double bs2, int kind,
-                 double* __restrict__ x_out, double* __restrict__ xt_out, int32_t* status,
-                 int row0, int H_glob, int a_first, int n_local_rows, int r_begin) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r_loc = r_begin + blockIdx.y;
-  const int r = row0 + r_loc;  // global row
-  const int b = blockIdx.z;
-  if (c >= W) return;
-  const int P = side * side;
-  const int n = n_local_rows * n_cols;  // local patches per image
-  const int last_r = H_glob - side, last_c = W - side;
-  // candidate nominal rows a with R_a in [r-side+1-half, r+half]
+struct GridGeo {
+  const int32_t* anchors;
+  int n_rows, n_cols, s, half, side, W;
+  int row0, H_glob, a_first;
+};
+
+// Visit the anchors covering global pixel (r, c) in ascending patch index —
+// np.bincount's accumulation order (patches.py:213-220): candidate nominal
+// rows a with a*s in [r-side+1-half, r+half] (a <= n_rows-2), then the
+// clamped last row; within a row the candidate columns likewise, then the
+// last column.  fn(local patch index, dr, dcol).
+template <class F>
+__device__ __forceinline__ void for_each_cover(const GridGeo& g, int r, int c, F&& fn) {
+  const int side = g.side, s = g.s, half = g.half;
+  const int last_r = g.H_glob - side, last_c = g.W - side;
   const int a_lo = ceil_div_floor0(r - side + 1 - half, s);
-  const int a_hi = min(n_rows - 2, (r + half) / s);
+  const int a_hi = min(g.n_rows - 2, (r + half) / s);
   const int b_lo = ceil_div_floor0(c - side + 1 - half, s);
-  const int b_hi = min(n_cols - 2, (c + half) / s);
+  const int b_hi = min(g.n_cols - 2, (c + half) / s);
   const bool last_row_ok = last_r <= r + half;  // always >= r-side+1-half
   const bool last_col_ok = last_c <= c + half;
-  const int64_t gbase = (int64_t)b * n;
-  double sum = 0.0, lo = INFINITY, hi = -INFINITY;
-  int count = 0;
   auto visit = [&](int ia, int ib) {
-    const int i = (ia - a_first) * n_cols + ib;  // local patch index
-    const int pr = row0 + anchors[2 * i], pc = anchors[2 * i + 1];
-    const int dr = r - pr, dcol = c - pc;
-    if ((unsigned)dr < (unsigned)side && (unsigned)dcol < (unsigned)side) {
-      const int64_t g = gbase + i;
-      const double v = __dadd_rn(Zhat[g * P + dr * side + dcol], dc[g]);
-      sum += v;
-      lo = fmin(lo, v);
-      hi = fmax(hi, v);
-      ++count;
-    }
+    const int i = (ia - g.a_first) * g.n_cols + ib;  // local patch index
+    const int dr = r - (g.row0 + g.anchors[2 * i]), dcol = c - g.anchors[2 * i + 1];
+    if ((unsigned)dr < (unsigned)side && (unsigned)dcol < (unsigned)side) fn(i, dr, dcol);
   };
   auto visit_row = [&](int ia) {
     for (int ib = b_lo; ib <= b_hi; ++ib) visit(ia, ib);
-    if (last_col_ok) visit(ia, n_cols - 1);
+    if (last_col_ok) visit(ia, g.n_cols - 1);
   };
-  // ascending patch index == np.bincount's accumulation order
   for (int ia = a_lo; ia <= a_hi; ++ia) visit_row(ia);
-  if (last_row_ok) visit_row(n_rows - 1);
-  const int64_t pix = ((int64_t)b * H + r_loc) * W + c;
+  if (last_row_ok) visit_row(g.n_rows - 1);
+}
+
+// x~ (with the lo == hi rule) and the fused pixel update for one pixel
+__device__ __forceinline__ void finish_pixel(double sum, double lo, double hi, int count,
+                                             int64_t pix, const double* aty, const double* diag,
+                                             double bs2, int kind, double* x_out, double* xt_out,
+                                             int32_t* status) {
   double xt;
   if (count == 0) {
     atomicOr(status, 1);
@@ -89,6 +84,193 @@ aggregate_kernel(const double* __restrict__ Zhat, const double* __restrict__ dc,
     if (x_out) x_out[pix] = x;
   } else if (x_out) {
     x_out[pix] = rhs;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+aggregate_kernel(const double* __restrict__ Zhat, const double* __restrict__ dc, GridGeo geo,
+                 int batch, int H, const double* __restrict__ aty,
+                 const double* __restrict__ diag, double bs2, int kind,
+                 double* __restrict__ x_out, double* __restrict__ xt_out, int32_t* status,
+                 int n_local_rows, int r_begin) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r_loc = r_begin + blockIdx.y;
+  const int b = blockIdx.z;
+  const int W = geo.W;
+  if (c >= W) return;
+  const int P = geo.side * geo.side;
+  const int64_t gbase = (int64_t)b * n_local_rows * geo.n_cols;
+  double sum = 0.0, lo = INFINITY, hi = -INFINITY;
+  int count = 0;
+  for_each_cover(geo, geo.row0 + r_loc, c, [&](int i, int dr, int dcol) {
+    const int64_t g = gbase + i;
+    const double v = __dadd_rn(Zhat[g * P + dr * geo.side + dcol], dc[g]);
+    sum += v;
+    lo = fmin(lo, v);
+    hi = fmax(hi, v);
+    ++count;
+  });
+  finish_pixel(sum, lo, hi, count, ((int64_t)b * H + r_loc) * W + c, aty, diag, bs2, kind, x_out,
+               xt_out, status);
+}
+
+// ---- cover lists: the grid is shared by every image of a batch, so the
+// covering (patch, offset) entries of each pixel are enumerated once per
+// sampling plan, as CSR in ascending patch order: entry = i << 8 | offset.
+__global__ void cover_count_kernel(GridGeo geo, int r_begin, int rows, int32_t* __restrict__ counts) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (int64_t)rows * geo.W) return;
+  const int r_loc = r_begin + (int)(p / geo.W), c = (int)(p % geo.W);
+  int k = 0;
+  for_each_cover(geo, geo.row0 + r_loc, c, [&](int, int, int) { ++k; });
+  counts[p] = k;
+}
+
+__global__ void cover_fill_kernel(GridGeo geo, int r_begin, int rows, const int32_t* __restrict__ ptr,
+                                  int32_t* __restrict__ entries) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (int64_t)rows * geo.W) return;
+  const int r_loc = r_begin + (int)(p / geo.W), c = (int)(p % geo.W);
+  int32_t* out = entries + ptr[p];
+  for_each_cover(geo, geo.row0 + r_loc, c, [&](int i, int dr, int dcol) {
+    *out++ = (i << 8) | (dr * geo.side + dcol);
+  });
+}
+
+// exclusive scan of counts[0..n) into ptr[0..n] (ptr[n] = total): block
+// sums, one-block scan of the sums, block-local scans
+__global__ void scan_blocks_kernel(const int32_t* __restrict__ counts, int64_t n, int32_t* __restrict__ bsum) {
+  __shared__ int32_t red[32];
+  const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  int v = i < n ? counts[i] : 0;
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int w = red[threadIdx.x];
+    w = warp_sum(w);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = w;
+  }
+}
+
+__global__ void scan_sums_kernel(int32_t* bsum, int nb) {
+  // single block of 1024 threads, sequential chunks
+  __shared__ int32_t carry;
+  __shared__ int32_t tmp[1024];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nb; base += 1024) {
+    const int i = base + threadIdx.x;
+    tmp[threadIdx.x] = i < nb ? bsum[i] : 0;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+      const int v = threadIdx.x >= off ? tmp[threadIdx.x - off] : 0;
+      __syncthreads();
+      tmp[threadIdx.x] += v;
+      __syncthreads();
+    }
+    if (i < nb) bsum[i] = carry + tmp[threadIdx.x] - (i < nb ? bsum[i] : 0);
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += tmp[1023];
+    __syncthreads();
+  }
+}
+
+__global__ void scan_apply_kernel(const int32_t* __restrict__ counts, int64_t n,
+                                  const int32_t* __restrict__ bsum, int32_t* __restrict__ ptr) {
+  __shared__ int32_t tmp[1024];
+  const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  const int v = i < n ? counts[i] : 0;
+  tmp[threadIdx.x] = v;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const int u = threadIdx.x >= off ? tmp[threadIdx.x - off] : 0;
+    __syncthreads();
+    tmp[threadIdx.x] += u;
+    __syncthreads();
+  }
+  if (i < n) ptr[i] = bsum[blockIdx.x] + tmp[threadIdx.x] - v;
+  if (i == n - 1) ptr[n] = bsum[blockIdx.x] + tmp[threadIdx.x];
+}
+
+// Gather over the cover list.  A block owns 256 pixels of one row for the
+// whole batch: their cover entries are staged in shared memory once (the
+// plan is the batch's), then every image's Zhat / dc loads issue straight
+// from them — one dependent global round trip per pixel and image, two
+// images in flight per thread.  Per image the operations are exactly
+// aggregate_kernel's.
+constexpr int kCoverThreads = 256;
+constexpr int kCoverMaxEntries = 16;  // per pixel, staged (more: read from global)
+
+__global__ void __launch_bounds__(kCoverThreads)
+aggregate_cover_kernel(const double* __restrict__ Zhat, const double* __restrict__ dc,
+                       const int32_t* __restrict__ ptr, const int32_t* __restrict__ entries, int P,
+                       int n_local, int batch, int H, int W, int r_begin,
+                       const double* __restrict__ aty, const double* __restrict__ diag, double bs2,
+                       int kind, double* __restrict__ x_out, double* __restrict__ xt_out,
+                       int32_t* status) {
+  __shared__ int32_t s_ent[kCoverThreads * kCoverMaxEntries];
+  __shared__ int32_t s_ptr[kCoverThreads + 1];
+  const int c0 = blockIdx.x * kCoverThreads;
+  const int c = c0 + threadIdx.x;
+  const int r_loc = r_begin + blockIdx.y;
+  const int64_t p0 = (int64_t)blockIdx.y * W + c0;
+  const int npx = min(kCoverThreads, W - c0);
+  if (threadIdx.x < npx) s_ptr[threadIdx.x] = __ldg(ptr + p0 + threadIdx.x);
+  if (threadIdx.x == 0) s_ptr[npx] = __ldg(ptr + p0 + npx);
+  __syncthreads();
+  const int base = s_ptr[0];
+  const int span = s_ptr[npx] - base;
+  const bool staged = span <= kCoverThreads * kCoverMaxEntries;
+  if (staged)
+    for (int k = threadIdx.x; k < span; k += kCoverThreads) s_ent[k] = __ldg(entries + base + k);
+  __syncthreads();
+  if (c >= W) return;
+  const int e0 = s_ptr[threadIdx.x] - base, e1 = s_ptr[threadIdx.x + 1] - base;
+  const int32_t* ent = entries + base;
+  auto entry = [&](int e) {
+    int v;
+    if (staged)
+      v = s_ent[e];
+    else
+      v = ent[e];  // (a plain load: a select between the two address spaces must stay generic)
+    return v;
+  };
+  const int64_t pix0 = (int64_t)r_loc * W + c;
+  const int64_t img = (int64_t)H * W;
+  for (int b = 0; b < batch; b += 2) {
+    const bool two = b + 1 < batch;
+    double sum[2] = {0.0, 0.0}, lo[2] = {INFINITY, INFINITY}, hi[2] = {-INFINITY, -INFINITY};
+    for (int e = e0; e < e1; e += 4) {
+      double z[2][4], d[2][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (e + q < e1) {
+          const int v = entry(e + q);
+#pragma unroll
+          for (int bb = 0; bb < 2; ++bb)
+            if (bb == 0 || two) {
+              const int64_t g = (int64_t)(b + bb) * n_local + (v >> 8);
+              z[bb][q] = __ldg(Zhat + g * P + (v & 255));
+              d[bb][q] = __ldg(dc + g);
+            }
+        }
+#pragma unroll
+      for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if ((bb == 0 || two) && e + q < e1) {
+            const double v = __dadd_rn(z[bb][q], d[bb][q]);
+            sum[bb] += v;
+            lo[bb] = fmin(lo[bb], v);
+            hi[bb] = fmax(hi[bb], v);
+          }
+    }
+    finish_pixel(sum[0], lo[0], hi[0], e1 - e0, b * img + pix0, aty, diag, bs2, kind, x_out, xt_out,
+                 status);
+    if (two)
+      finish_pixel(sum[1], lo[1], hi[1], e1 - e0, (b + 1) * img + pix0, aty, diag, bs2, kind, x_out,
+                   xt_out, status);
   }
 }
 
@@ -114,9 +296,10 @@ extern "C" int fepll_aggregate_strip(const double* Zhat, const double* dc, const
   FEPLL_REQUIRE(H <= 65535 && batch <= 65535, "aggregate: image too tall for the launch grid");
   if (r_end == r_begin) return kOk;
   dim3 grid((W + 255) / 256, r_end - r_begin, batch);
+  const GridGeo geo{anchors, n_rows, n_cols, spacing, half, side, W, row0, H_glob, a_first};
   aggregate_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
-      Zhat, dc, anchors, n_rows, n_cols, spacing, half, side, batch, H, W, aty, diag, bs2, kind,
-      x_out, xtilde_out, status, row0, H_glob, a_first, n_local_rows, r_begin);
+      Zhat, dc, geo, batch, H, aty, diag, bs2, kind, x_out, xtilde_out, status, n_local_rows,
+      r_begin);
   FEPLL_LAUNCH();
   return kOk;
 }
@@ -129,4 +312,69 @@ extern "C" int fepll_aggregate(const double* Zhat, const double* dc, const int32
   return fepll_aggregate_strip(Zhat, dc, anchors, n_rows, n_cols, spacing, half, side, batch, H, W,
                                0, H, 0, n_rows, 0, H, aty, diag, bs2, kind, x_out, xtilde_out,
                                status, stream);
+}
+
+extern "C" int64_t fepll_cover_scratch_ints(int64_t n_pixels) {
+  return n_pixels + (n_pixels + 1023) / 1024 + 1;
+}
+
+extern "C" int fepll_cover_build(const int32_t* anchors, int32_t n_rows, int32_t n_cols,
+                                 int32_t spacing, int32_t half, int32_t side, int32_t W,
+                                 int32_t row0, int32_t H_glob, int32_t a_first,
+                                 int32_t n_local_rows, int32_t r_begin, int32_t r_end,
+                                 int32_t* ptr, int32_t* entries, int64_t entries_cap,
+                                 int32_t* scratch, void* stream) {
+  using namespace fepll;
+  FEPLL_REQUIRE(anchors && ptr && entries && scratch, "cover_build: bad arguments");
+  FEPLL_REQUIRE(side * side <= 256 && side >= 1 && spacing >= 1 && half >= 0,
+                "cover_build: bad grid geometry");
+  FEPLL_REQUIRE((int64_t)n_local_rows * n_cols < (int64_t(1) << 23),
+                "cover_build: more than 2^23 patches per image");
+  FEPLL_REQUIRE(0 <= r_begin && r_begin <= r_end && row0 >= 0 && row0 + r_end <= H_glob,
+                "cover_build: rows outside the image");
+  const int rows = r_end - r_begin;
+  const int64_t npx = (int64_t)rows * W;
+  if (npx == 0) return kOk;
+  cudaStream_t st = (cudaStream_t)stream;
+  const GridGeo geo{anchors, n_rows, n_cols, spacing, half, side, W, row0, H_glob, a_first};
+  int32_t* counts = scratch;
+  int32_t* bsum = scratch + npx;
+  const int64_t nb = (npx + 1023) / 1024;
+  FEPLL_REQUIRE(nb < (int64_t(1) << 31), "cover_build: image too large");
+  cover_count_kernel<<<(unsigned)((npx + 255) / 256), 256, 0, st>>>(geo, r_begin, rows, counts);
+  FEPLL_LAUNCH();
+  scan_blocks_kernel<<<(unsigned)nb, 1024, 0, st>>>(counts, npx, bsum);
+  FEPLL_LAUNCH();
+  scan_sums_kernel<<<1, 1024, 0, st>>>(bsum, (int)nb);
+  FEPLL_LAUNCH();
+  scan_apply_kernel<<<(unsigned)nb, 1024, 0, st>>>(counts, npx, bsum, ptr);
+  FEPLL_LAUNCH();
+  // every patch covers exactly P pixels of the full image; a strip holds
+  // at most its patches' P each
+  FEPLL_REQUIRE(entries_cap >= (int64_t)n_local_rows * n_cols * side * side,
+                "cover_build: entry buffer below n_local * P");
+  cover_fill_kernel<<<(unsigned)((npx + 255) / 256), 256, 0, st>>>(geo, r_begin, rows, ptr, entries);
+  FEPLL_LAUNCH();
+  return kOk;
+}
+
+extern "C" int fepll_aggregate_cover(const double* Zhat, const double* dc, const int32_t* ptr,
+                                     const int32_t* entries, int32_t P, int32_t n_local,
+                                     int32_t batch, int32_t H, int32_t W, int32_t r_begin,
+                                     int32_t r_end, const double* aty, const double* diag,
+                                     double bs2, int32_t kind, double* x_out, double* xtilde_out,
+                                     int32_t* status, void* stream) {
+  using namespace fepll;
+  FEPLL_REQUIRE(Zhat && dc && ptr && entries && status, "aggregate_cover: bad arguments");
+  FEPLL_REQUIRE(kind == 0 || kind == 1, "aggregate_cover: unknown kind");
+  FEPLL_REQUIRE(0 <= r_begin && r_begin <= r_end && r_end <= H && batch >= 1,
+                "aggregate_cover: bad rows");
+  if (r_end == r_begin) return kOk;
+  FEPLL_REQUIRE(r_end - r_begin <= 65535, "aggregate_cover: strip taller than the launch grid");
+  dim3 grid((unsigned)((W + kCoverThreads - 1) / kCoverThreads), r_end - r_begin);
+  aggregate_cover_kernel<<<grid, kCoverThreads, 0, (cudaStream_t)stream>>>(
+      Zhat, dc, ptr, entries, P, n_local, batch, H, W, r_begin, aty, diag, bs2, kind, x_out,
+      xtilde_out, status);
+  FEPLL_LAUNCH();
+  return kOk;
 }

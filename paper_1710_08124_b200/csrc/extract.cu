@@ -6,6 +6,8 @@
 // per patch; the fold runs in a per-warp shared-memory row so its addition
 // order is exactly the reference's for any P (odd widths fold their trailing
 // column into the last slot).
+#include <climits>
+
 #include "common.cuh"
 
 namespace fepll {
@@ -159,11 +161,163 @@ extract_pow2_kernel(const double* __restrict__ x, int batch, int H, int W,
   }
 }
 
+// Tiled variant for power-of-two sides on a row-major anchor grid: a block
+// takes PB consecutive anchors of one nominal row (grid_cols anchors per
+// row), stages the image window they touch in shared memory with coalesced
+// loads, runs the same shuffle fold per patch (bitwise-equal dc), stages the
+// patch rows, and writes the block's contiguous Z64 / Z32 span with 16-byte
+// stores — the per-lane 8-byte global accesses of extract_pow2_kernel were
+// LSU-issue bound.  Blocks whose window exceeds the staging area (irregular
+// anchors) read the image directly.
+template <int SIDE>
+__global__ void __launch_bounds__(256)
+extract_tile_kernel(const double* __restrict__ x, int batch, int H, int W,
+                    const int32_t* __restrict__ anchors, int n, int grid_cols, int win_cap,
+                    double* __restrict__ Z64, float* __restrict__ Z32, int z32_pitch,
+                    double* __restrict__ dc_out, double* __restrict__ sq_out) {
+  constexpr int P = SIDE * SIDE;
+  constexpr int PER_WARP = 32 / SIDE;
+  constexpr int PB = 8 * PER_WARP;  // patches per block
+  extern __shared__ __align__(16) double sm[];
+  double* zs = sm;                       // [PB][P] staged FP64 rows
+  double* win = sm + PB * P;             // [rows][cols] image window (win_cap doubles)
+  __shared__ int s_pr[PB], s_pc[PB];
+  __shared__ int s_lo[2], s_hi[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int col_blocks = (grid_cols + PB - 1) / PB;
+  const int rows_total = n / grid_cols;
+  for (int64_t blk = blockIdx.x; blk < (int64_t)batch * rows_total * col_blocks; blk += gridDim.x) {
+    const int b = (int)(blk / ((int64_t)rows_total * col_blocks));
+    const int rem = (int)(blk - (int64_t)b * rows_total * col_blocks);
+    const int a = rem / col_blocks, cb = rem - a * col_blocks;
+    const int i0 = a * grid_cols + cb * PB;
+    const int m = min(PB, grid_cols - cb * PB);
+    const int64_t g0 = (int64_t)b * n + i0;
+    if (tid < 2) {
+      s_lo[tid] = INT_MAX;
+      s_hi[tid] = INT_MIN;
+    }
+    __syncthreads();
+    if (tid < m) {
+      const int pr = anchors[2 * (i0 + tid)], pc = anchors[2 * (i0 + tid) + 1];
+      s_pr[tid] = pr;
+      s_pc[tid] = pc;
+      atomicMin(&s_lo[0], pr);
+      atomicMax(&s_hi[0], pr);
+      atomicMin(&s_lo[1], pc);
+      atomicMax(&s_hi[1], pc);
+    }
+    __syncthreads();
+    const int r_lo = s_lo[0], c_lo = s_lo[1];
+    const int wr = s_hi[0] - r_lo + SIDE, wc = s_hi[1] - c_lo + SIDE;
+    const bool staged = wr * wc <= win_cap;
+    const double* img = x + (int64_t)b * H * W;
+    if (staged) {
+      for (int r = warp; r < wr; r += 8) {
+        const double* src = img + (int64_t)(r_lo + r) * W + c_lo;
+        for (int c = lane; c < wc; c += 32) win[r * wc + c] = __ldg(src + c);
+      }
+    }
+    __syncthreads();
+    // one lane group per patch, lane r = window row r (extract_pow2_kernel)
+    const int p = warp * PER_WARP + lane / SIDE;
+    const int r = lane % SIDE;
+    const bool valid = p < m;
+    double v[SIDE];
+    if (valid) {
+      const int pr = s_pr[p], pc = s_pc[p];
+      if (staged) {
+        const double* src = win + (pr - r_lo + r) * wc + (pc - c_lo);
+#pragma unroll
+        for (int c = 0; c < SIDE; ++c) v[c] = src[c];
+      } else {
+        const double* src = img + (int64_t)(pr + r) * W + pc;
+#pragma unroll
+        for (int c = 0; c < SIDE; ++c) v[c] = __ldg(src + c);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < SIDE; ++c) v[c] = 0.0;
+    }
+    double acc[SIDE];
+#pragma unroll
+    for (int c = 0; c < SIDE; ++c) acc[c] = v[c];
+#pragma unroll
+    for (int h = SIDE / 2; h >= 1; h >>= 1) {
+#pragma unroll
+      for (int c = 0; c < SIDE; ++c) {
+        const double o = __shfl_down_sync(0xffffffffu, acc[c], h, SIDE);
+        if (r < h) acc[c] = acc[c] + o;
+      }
+    }
+#pragma unroll
+    for (int h = SIDE / 2; h >= 1; h >>= 1)
+#pragma unroll
+      for (int c = 0; c < h; ++c) acc[c] = acc[c] + acc[c + h];
+    const double dc = __shfl_sync(0xffffffffu, acc[0], 0, SIDE) / (double)P;
+    double sq = 0.0;
+    if (valid) {
+      double* zrow = zs + p * P + r * SIDE;
+#pragma unroll
+      for (int c = 0; c < SIDE; ++c) {
+        const double z = v[c] - dc;
+        sq = fma(z, z, sq);
+        zrow[c] = z;
+      }
+    }
+#pragma unroll
+    for (int h = SIDE / 2; h >= 1; h >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, h, SIDE);
+    if (valid && r == 0) {
+      if (dc_out) dc_out[g0 + p] = dc;
+      if (sq_out) sq_out[g0 + p] = sq;
+    }
+    __syncthreads();
+    // contiguous spans: m rows of Z64 (P doubles), m rows of Z32 (z32_pitch floats)
+    if (Z64) {
+      const double2* src = reinterpret_cast<const double2*>(zs);
+      double2* dst = reinterpret_cast<double2*>(Z64 + g0 * P);
+      for (int k = tid; k < m * P / 2; k += 256) dst[k] = src[k];
+    }
+    if (Z32) {
+      const int q4 = z32_pitch / 4;
+      float4* dst = reinterpret_cast<float4*>(Z32 + g0 * z32_pitch);
+      for (int k = tid; k < m * q4; k += 256) {
+        const int row = k / q4, col = (k - row * q4) * 4;
+        float4 f;
+        f.x = col + 0 < P ? (float)zs[row * P + col + 0] : 0.0f;
+        f.y = col + 1 < P ? (float)zs[row * P + col + 1] : 0.0f;
+        f.z = col + 2 < P ? (float)zs[row * P + col + 2] : 0.0f;
+        f.w = col + 3 < P ? (float)zs[row * P + col + 3] : 0.0f;
+        dst[k] = f;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int SIDE>
+static void launch_tile(const double* x, int batch, int H, int W, const int32_t* anchors, int n,
+                        int grid_cols, double* Z64, float* Z32, int z32_pitch, double* dc, double* sq,
+                        cudaStream_t st) {
+  constexpr int P = SIDE * SIDE;
+  constexpr int PB = 8 * (32 / SIDE);
+  const int win_cap = SIDE == 16 ? 8192 : 2048;  // staged window (doubles)
+  const size_t smem = sizeof(double) * ((size_t)PB * P + win_cap);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(extract_tile_kernel<SIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const int64_t blocks = (int64_t)batch * (n / grid_cols) * ((grid_cols + PB - 1) / PB);
+  extract_tile_kernel<SIDE><<<grid_for(blocks, 1, kSMs * 8), 256, smem, st>>>(
+      x, batch, H, W, anchors, n, grid_cols, win_cap, Z64, Z32, z32_pitch, dc, sq);
+}
+
 }  // namespace fepll
 
 extern "C" int fepll_extract(const double* x, int32_t batch, int32_t H, int32_t W, int32_t side,
-                             const int32_t* anchors, int32_t n, double* Z64, float* Z32,
-                             int32_t z32_pitch, double* dc, double* sq, void* stream) {
+                             const int32_t* anchors, int32_t n, int32_t grid_cols, double* Z64,
+                             float* Z32, int32_t z32_pitch, double* dc, double* sq, void* stream) {
   using namespace fepll;
   FEPLL_REQUIRE(x && anchors && batch >= 1 && n >= 0, "extract: bad arguments");
   FEPLL_REQUIRE(side >= 1 && side * side <= kMaxP, "extract: patch side out of range");
@@ -172,7 +326,15 @@ extern "C" int fepll_extract(const double* x, int32_t batch, int32_t H, int32_t 
   if (n == 0) return kOk;
   const int64_t total = (int64_t)batch * n;
   cudaStream_t st = (cudaStream_t)stream;
-  if (side == 8 || side == 4 || side == 16) {
+  if (grid_cols > 0 && n % grid_cols == 0 && (side == 8 || side == 4 || side == 16) &&
+      (Z32 == nullptr || z32_pitch % 4 == 0)) {
+    if (side == 8)
+      launch_tile<8>(x, batch, H, W, anchors, n, grid_cols, Z64, Z32, z32_pitch, dc, sq, st);
+    else if (side == 4)
+      launch_tile<4>(x, batch, H, W, anchors, n, grid_cols, Z64, Z32, z32_pitch, dc, sq, st);
+    else
+      launch_tile<16>(x, batch, H, W, anchors, n, grid_cols, Z64, Z32, z32_pitch, dc, sq, st);
+  } else if (side == 8 || side == 4 || side == 16) {
     const int per_warp = 32 / side;
     const int64_t warps = (total + per_warp - 1) / per_warp;
     const int grid = grid_for(warps, 8, 148 * 32);

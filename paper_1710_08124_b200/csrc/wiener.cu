@@ -7,34 +7,44 @@
 // in FP64 — the estimates become the next iteration's image, whose tree
 // decisions must stay the FP64 reference's, so no reduced precision here.
 //
-// A CTA (8 warps) walks a contiguous range of 64-patch tiles in leaf order:
+// A CTA (MT/8 warps) walks a contiguous range of MT-patch tiles in leaf order:
 // U_k is staged in smem once per leaf, the FP64 patch rows (kernel (a)
 // output, 512 B each) arrive by cp.async into a double buffer while the
-// previous tile computes.  Both products run as mma.sync m8n8k4 f64:
-// warp w owns rows 8w..8w+7 of the tile.
+// previous tile computes.  Both products run as mma.sync m16n8k8 f64
+// (37.2 TFLOP/s FP64 peak measured on B200 for every f64 shape,
+// tools/dmma_bench.cu; the k8 shape halves the B-fragment loads per FLOP of
+// m8n8k4): warp w owns rows 16w..16w+15 of the tile.
 #include "route.cuh"
 
 namespace fepll {
 
 namespace wn {
 
-constexpr int kRows = 64;
-constexpr int kWarps = 8;
-constexpr int kThreads = kWarps * 32;
 constexpr int kMaxP = 128;
 constexpr int kMaxR = 64;
+constexpr int kMaxRows = 128;
 
+// tile rows MT: 64 (8 warps) for small buckets, 128 (16 warps, twice the
+// independent DMMA chains per SM) when the buckets are large
 struct Head {
   int32_t tpre[kMaxLevelNodes + 1];
   uint64_t scan_tmp[256];
-  int32_t rows[2][kRows];
+  int32_t leaf_v[kMaxLevelNodes];   // leaf BFS id, bucket count and offset
+  int32_t leaf_cnt[kMaxLevelNodes];
+  int64_t leaf_off[kMaxLevelNodes];
+  int32_t rows[8][kMaxRows];        // patch-index ring (2 x stages slots)
   int32_t t_begin, t_end;
 };
 
-__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d[0]), "+d"(d[1])
-               : "d"(a), "d"(b));
+// D(16x8) += A(16x8) B(8x8); lane (g = lane/4, t = lane%4) holds
+// a = {A[g][t], A[g+8][t], A[g][t+4], A[g+8][t+4]}, b = {B[t][g], B[t+4][g]},
+// d = {D[g][2t], D[g][2t+1], D[g+8][2t], D[g+8][2t+1]}
+__device__ __forceinline__ void dmma16(double (&d)[4], const double (&a)[4], const double (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
 }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -43,40 +53,65 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
                "l"(src)
                : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 // Row strides (in doubles) are chosen so every fragment load is two
 // conflict-free shared-memory wavefronts: A-side tiles (rows g, 4
 // consecutive k) use ld = 4 mod 16, B-side tiles (4 rows k, 8 consecutive n)
 // use ld = 8 mod 16.
 struct Geo {
-  int P, Pn;     // P, P rounded up to 8 (phase-2 N)
-  int zld;       // Zs [64][zld]
+  int P, Pn;     // P, P rounded up to 8 (phase-1 K, phase-2 N)
+  int zld;       // Zs [MT][zld], columns P..Pn-1 zero
   int R8;        // rank rounded up to 8
   int uld;       // Us [Pn][uld]  (phase-1 B: k = p, n = j)
   int utld;      // UT [R8][utld] (phase-2 B: k = j, n = p)
   int cld;       // Cs [64][cld]
 };
 
-template <int NT2>  // phase-2 n-tiles (P/8 rounded up): 8 for P=64, 13 for P=100
-__global__ void __launch_bounds__(kThreads)
+// NT2: phase-2 n-tiles (P/8 rounded up): 8 for P=64, 13 for P=100.
+// MT rows per tile, NS row buffers (NS - 1 tiles of rows in flight).
+template <int NT2, int MT, int NS>
+__global__ void __launch_bounds__(MT * 2)
 wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, int n_leaf_nodes,
                    const int32_t* __restrict__ cnt, const int64_t* __restrict__ off,
                    const int32_t* __restrict__ leafseg, const double* __restrict__ Z64,
                    double* __restrict__ Zhat, Geo geo) {
   extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int kRows = MT;
+  constexpr int kThreads = MT * 2;  // one warp per 16 rows
   Head& h = *reinterpret_cast<Head*>(smem);
+  constexpr int kRing = 2 * NS;      // index ring slots
+  constexpr int kLead = 2 * NS - 2;  // tiles of indices fetched ahead of their rows' issue
   double* Zs0 = reinterpret_cast<double*>(smem + ((sizeof(Head) + 127) & ~size_t(127)));
-  double* Zs1 = Zs0 + kRows * geo.zld;
-  double* Us = Zs1 + kRows * geo.zld;          // [Pn][uld]   (p, j)
+  double* Us = Zs0 + NS * kRows * geo.zld;     // [Pn][uld]   (p, j)
   double* UT = Us + geo.Pn * geo.uld;          // [R8][utld]  (j, p)
   double* Cs = UT + geo.R8 * geo.utld;         // [64][cld]
   double* sh = Cs + kRows * geo.cld;           // [R8]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int P = geo.P;
-  for (int k = tid; k < n_leaf_nodes; k += kThreads)
-    h.tpre[k] = (cnt[leaf_nodes[k]] + kRows - 1) / kRows;
+  // K padding columns of the row buffers stay zero (cp.async fills [0, P))
+  for (int e = tid; e < NS * kRows * (geo.Pn - P); e += kThreads) {
+    const int w = geo.Pn - P, i = e / w;  // row i of the adjacent buffers
+    Zs0[i * geo.zld + P + (e - i * w)] = 0.0;
+  }
+  for (int k = tid; k < n_leaf_nodes; k += kThreads) {
+    const int v = leaf_nodes[k];
+    h.leaf_v[k] = v;
+    h.leaf_cnt[k] = cnt[v];
+    h.leaf_off[k] = off[v];
+    h.tpre[k] = (cnt[v] + kRows - 1) / kRows;
+  }
   __syncthreads();
   const int tiles = block_exscan(h.tpre, n_leaf_nodes, h.scan_tmp);
   if (tid == 0) {
@@ -88,19 +123,29 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
   const int t_begin = h.t_begin, t_end = h.t_end;
   if (t_begin >= t_end) return;
 
-  // stage the rows of tile `tile` into buffer b (cp.async, 16-byte chunks)
-  auto issue_tile = [&](int tile, int b) {
-    const int li = prefix_find(h.tpre, n_leaf_nodes, tile);
-    const int v = leaf_nodes[li];
-    const int first = (tile - h.tpre[li]) * kRows;
-    const int m = min(kRows, cnt[v] - first);
-    if (tid < kRows) h.rows[b][tid] = tid < m ? leafseg[off[v] + first + tid] : -1;
-    __syncthreads();
-    double* Zs = b ? Zs1 : Zs0;
+  // Pipeline (all cp.async): the rows of tile j land in buffer j % NS,
+  // issued NS - 1 tiles ahead of its compute; its patch indices land in ring
+  // slot j % kRing another NS - 1 tiles earlier — no global round trip on
+  // the compute path, NS - 1 tiles of random 8P-byte row reads in flight.
+  auto fetch_rows = [&](int j) {
+    if (j < t_end && tid < kRows) {
+      const int li = prefix_find(h.tpre, n_leaf_nodes, j);
+      const int first = (j - h.tpre[li]) * kRows;
+      int32_t* dst = &h.rows[(j - t_begin) % kRing][tid];
+      if (tid < h.leaf_cnt[li] - first)
+        cp_async4(dst, leafseg + h.leaf_off[li] + first + tid);
+      else
+        *dst = -1;
+    }
+  };
+  auto fetch_z = [&](int j) {
+    if (j >= t_end) return;
+    const int32_t* rows = h.rows[(j - t_begin) % kRing];
+    double* Zs = Zs0 + ((j - t_begin) % NS) * kRows * geo.zld;
     const int chunks = P / 2;  // 16-byte chunks per row (P even)
     for (int e = tid; e < kRows * chunks; e += kThreads) {
       const int i = e / chunks, c = e - i * chunks;
-      const int g = h.rows[b][i];
+      const int g = rows[i];
       double* dst = Zs + i * geo.zld + 2 * c;
       if (g >= 0) {
         cp_async16(dst, Z64 + (int64_t)g * P + 2 * c);
@@ -109,20 +154,28 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
         dst[1] = 0.0;
       }
     }
-    cp_async_commit();
   };
 
   int cur_leaf = -1;
-  issue_tile(t_begin, 0);
+  for (int j = 0; j < kLead; ++j) fetch_rows(t_begin + j);
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  for (int j = 0; j < NS - 1; ++j) {
+    fetch_z(t_begin + j);
+    cp_async_commit();
+  }
   for (int tile = t_begin; tile < t_end; ++tile) {
-    const int b = (tile - t_begin) & 1;
+    const int i = tile - t_begin;
+    const int slot = i % kRing;
     const int li = prefix_find(h.tpre, n_leaf_nodes, tile);
-    const int v = leaf_nodes[li];
-    const int comp = pv.leaf_index[v];
+    const int comp = pv.leaf_index[h.leaf_v[li]];
     const int r = pv.model_rank[comp];
-    cp_async_wait_all();
-    __syncthreads();  // tile rows landed; previous tile's compute finished
-    if (tile + 1 < t_end) issue_tile(tile + 1, b ^ 1);
+    cp_async_wait_group<NS - 2>();
+    __syncthreads();  // this tile's rows landed; the buffer refilled next is free
+    fetch_z(tile + NS - 1);
+    fetch_rows(tile + kLead);
+    cp_async_commit();
     if (comp != cur_leaf) {
       const double* U = pv.model_basis + pv.model_off64[comp];
       for (int e = tid; e < geo.Pn * geo.R8; e += kThreads) {
@@ -136,55 +189,84 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       cur_leaf = comp;
       __syncthreads();
     }
-    const double* Zs = b ? Zs1 : Zs0;
+    const double* Zs = Zs0 + (i % NS) * kRows * geo.zld;
     const int g4 = lane >> 2, t4 = lane & 3;
-    const int m0 = warp * 8;
-    // ---- phase 1: C[m0..m0+7][0..R8) = Z . U
+    const int m0 = warp * 16;
+    const double* za = Zs + (m0 + g4) * geo.zld + t4;       // rows g, g+8 of the warp
+    const double* zb = za + 8 * geo.zld;
+    // ---- phase 1: C[m0..m0+15][0..R8) = (Z . U) * shrink
     {
-      double acc[kMaxR / 8][2];
-      const int nt = geo.R8 / 8;
+      double acc[kMaxR / 8][4];
+      const int nt = (r + 7) / 8;  // this leaf's rank, not the model's widest
 #pragma unroll
-      for (int n = 0; n < kMaxR / 8; ++n) acc[n][0] = acc[n][1] = 0.0;
-      for (int k0 = 0; k0 < P; k0 += 4) {
-        const double a = Zs[(m0 + g4) * geo.zld + k0 + t4];
+      for (int n = 0; n < kMaxR / 8; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0;
+      for (int k0 = 0; k0 < geo.Pn; k0 += 8) {
+        const double a[4] = {za[k0], zb[k0], za[k0 + 4], zb[k0 + 4]};
+        const double* u0 = Us + (k0 + t4) * geo.uld + g4;
+        const double* u1 = u0 + 4 * geo.uld;
 #pragma unroll
         for (int n = 0; n < kMaxR / 8; ++n)
-          if (n < nt) dmma(acc[n], a, Us[(k0 + t4) * geo.uld + n * 8 + g4]);
+          if (n < nt) {
+            const double bb[2] = {u0[n * 8], u1[n * 8]};
+            dmma16(acc[n], a, bb);
+          }
       }
 #pragma unroll
       for (int n = 0; n < kMaxR / 8; ++n)
         if (n < nt) {
           const int col = n * 8 + 2 * t4;
-          Cs[(m0 + g4) * geo.cld + col] = acc[n][0] * sh[col];
-          Cs[(m0 + g4) * geo.cld + col + 1] = acc[n][1] * sh[col + 1];
+          double* c0 = Cs + (m0 + g4) * geo.cld + col;
+          double* c1 = c0 + 8 * geo.cld;
+          c0[0] = acc[n][0] * sh[col];
+          c0[1] = acc[n][1] * sh[col + 1];
+          c1[0] = acc[n][2] * sh[col];
+          c1[1] = acc[n][3] * sh[col + 1];
         }
     }
     __syncwarp();  // each warp only reads its own rows of Cs
-    // ---- phase 2: Zhat[m0..m0+7][0..P) = C . U^T + gamma_tail Z
+    const int nt1 = (r + 7) / 8;
+    // ---- phase 2: Zhat[m0..m0+15][0..P) = C . U^T + gamma_tail Z
     {
-      double acc[NT2][2];
+      double acc[NT2][4];
 #pragma unroll
-      for (int n = 0; n < NT2; ++n) acc[n][0] = acc[n][1] = 0.0;
-      for (int k0 = 0; k0 < geo.R8; k0 += 4) {
-        const double a = Cs[(m0 + g4) * geo.cld + k0 + t4];
+      for (int n = 0; n < NT2; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0;
+      const double* ca = Cs + (m0 + g4) * geo.cld + t4;
+      const double* cb = ca + 8 * geo.cld;
+      for (int k0 = 0; k0 < nt1 * 8; k0 += 8) {
+        const double a[4] = {ca[k0], cb[k0], ca[k0 + 4], cb[k0 + 4]};
+        const double* u0 = UT + (k0 + t4) * geo.utld + g4;
+        const double* u1 = u0 + 4 * geo.utld;
 #pragma unroll
-        for (int n = 0; n < NT2; ++n) dmma(acc[n], a, UT[(k0 + t4) * geo.utld + n * 8 + g4]);
+        for (int n = 0; n < NT2; ++n) {
+          const double bb[2] = {u0[n * 8], u1[n * 8]};
+          dmma16(acc[n], a, bb);
+        }
       }
       const double gt = pv.model_gamma_tail[(int64_t)t * pv.K + comp];
-      const int row = m0 + g4;
-      const int gidx = h.rows[b][row];
-      if (gidx >= 0) {
-        double* out = Zhat + (int64_t)gidx * P;
+      // Zhat = acc + gamma_tail z, written over this warp's own rows of Zs
+      // (each element read and written by the same lane)...
+      double* zw = const_cast<double*>(Zs);
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        double* zr = zw + (m0 + g4 + 8 * half) * geo.zld;
 #pragma unroll
         for (int n = 0; n < NT2; ++n) {
           const int col = n * 8 + 2 * t4;
           if (col < P) {
-            double2 o;
-            o.x = acc[n][0] + gt * Zs[row * geo.zld + col];
-            o.y = acc[n][1] + gt * Zs[row * geo.zld + col + 1];
-            *reinterpret_cast<double2*>(out + col) = o;
+            zr[col] = acc[n][2 * half] + gt * zr[col];
+            zr[col + 1] = acc[n][2 * half + 1] + gt * zr[col + 1];
           }
         }
+      }
+      __syncwarp();
+      // ... then stored as whole 8P-byte rows (coalesced 16-byte lanes)
+      const int32_t* rows = h.rows[slot];
+      for (int i = 0; i < 16; ++i) {
+        const int gidx = rows[m0 + i];
+        if (gidx < 0) continue;
+        const double2* src = reinterpret_cast<const double2*>(zw + (m0 + i) * geo.zld);
+        double2* dst = reinterpret_cast<double2*>(Zhat + (int64_t)gidx * P);
+        for (int c = lane; c < P / 2; c += 32) dst[c] = src[c];
       }
     }
   }
@@ -198,38 +280,53 @@ int wiener_dmma(Plan* p, int t, const double* Z64, double* Zhat, cudaStream_t st
   geo.P = P;
   geo.Pn = (P + 7) / 8 * 8;
   auto ld = [](int n, int rem) { int v = n; while (v % 16 != rem) ++v; return v; };
-  geo.zld = ld(P, 4);
+  geo.zld = ld(geo.Pn, 4);
   geo.R8 = (p->max_model_rank + 7) / 8 * 8;
   geo.uld = ld(geo.R8, 8);
   geo.utld = ld(geo.Pn, 8);
   geo.cld = ld(geo.R8, 4);
-  const size_t smem = ((sizeof(wn::Head) + 127) & ~size_t(127)) +
-                      sizeof(double) * (2 * (size_t)wn::kRows * geo.zld + (size_t)geo.Pn * geo.uld +
-                                        (size_t)geo.R8 * geo.utld + (size_t)wn::kRows * geo.cld +
-                                        geo.R8);
+  auto smem_for = [&](int mt, int ns) {
+    return ((sizeof(wn::Head) + 127) & ~size_t(127)) +
+           sizeof(double) * (ns * (size_t)mt * geo.zld + (size_t)geo.Pn * geo.uld +
+                             (size_t)geo.R8 * geo.utld + (size_t)mt * geo.cld + geo.R8);
+  };
+  // 128-row tiles (16 warps) once the average leaf bucket is large enough
+  // that the extra padding rows do not matter, and the tile fits in smem
+  const int64_t n_total = p->last_n_total;
+  const bool big = n_total >= (int64_t)1024 * std::max(1, p->n_leaf_nodes) &&
+                   smem_for(128, 2) <= 227 * 1024;
+  const int mt = big ? 128 : 64;
+  const int ns = big ? 2 : (smem_for(64, 4) <= 227 * 1024 ? 4 : 2);
+  const size_t smem = smem_for(mt, ns);
   const int nt2 = geo.Pn / 8;
   auto launch = [&](auto kernel) -> int {
     FEPLL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, wn::kThreads, smem);
-    kernel<<<kSMs * std::max(1, per_sm), wn::kThreads, smem, st>>>(
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, mt * 2, smem);
+    kernel<<<kSMs * std::max(1, per_sm), mt * 2, smem, st>>>(
         p->v, t, p->d_leaf_nodes, p->n_leaf_nodes, p->rs.cnt, p->rs.off, p->rs.leafseg, Z64, Zhat,
         geo);
     FEPLL_LAUNCH();
     return kOk;
   };
+#define FEPLL_WN_CASE(N)                                                   \
+  case N:                                                                  \
+    return big ? launch(wn::wiener_dmma_kernel<N, 128, 2>)                 \
+               : ns == 4 ? launch(wn::wiener_dmma_kernel<N, 64, 4>)        \
+                         : launch(wn::wiener_dmma_kernel<N, 64, 2>);
   switch (nt2) {
-    case 1: return launch(wn::wiener_dmma_kernel<1>);
-    case 2: return launch(wn::wiener_dmma_kernel<2>);
-    case 4: return launch(wn::wiener_dmma_kernel<4>);
-    case 5: return launch(wn::wiener_dmma_kernel<5>);
-    case 7: return launch(wn::wiener_dmma_kernel<7>);
-    case 8: return launch(wn::wiener_dmma_kernel<8>);
-    case 11: return launch(wn::wiener_dmma_kernel<11>);
-    case 13: return launch(wn::wiener_dmma_kernel<13>);
-    case 16: return launch(wn::wiener_dmma_kernel<16>);
+    FEPLL_WN_CASE(1)
+    FEPLL_WN_CASE(2)
+    FEPLL_WN_CASE(4)
+    FEPLL_WN_CASE(5)
+    FEPLL_WN_CASE(7)
+    FEPLL_WN_CASE(8)
+    FEPLL_WN_CASE(11)
+    FEPLL_WN_CASE(13)
+    FEPLL_WN_CASE(16)
     default: break;
   }
+#undef FEPLL_WN_CASE
   set_error("wiener: unsupported patch size for the DMMA kernel");
   return kDataError;
 }

@@ -204,6 +204,8 @@ class Restorer:
         self.anchors = [g[0] for g in self._grids]
         n = int(self.anchors[0].shape[0])
         self.n = n
+        # per-pixel cover lists of each plan (shared by the whole batch)
+        self._covers = [self._cover(t) for t in range(config.iterations)]
         self.plan.reserve(n * self.batch)
         B, H, W = self.batch, self.H, self.W
         f64 = torch.float64
@@ -263,6 +265,29 @@ class Restorer:
             anchors = anchors[sp.a_lo * nc:(sp.a_hi + 1) * nc].clone()
             anchors[:, 0] -= sp.slab_lo
         return anchors, nr, nc, half
+
+    def _cover(self, t: int):
+        """CSR cover lists (ptr, entries) of iteration t's plan for the rows
+        this restorer produces (csrc/aggregate.cu fepll_cover_build)."""
+        torch = self.torch
+        anchors, nr, nc, half = self._grids[t]
+        sp = self.strip
+        if sp is None:
+            row0, H_glob, a_first, n_loc_rows, r0, r1 = 0, self.H, 0, nr, 0, self.H
+        else:
+            row0, H_glob, a_first = sp.slab_lo, sp.H, sp.a_lo
+            n_loc_rows, r0, r1 = sp.a_hi - sp.a_lo + 1, sp.r0 - sp.slab_lo, sp.r1 - sp.slab_lo
+        npx = (r1 - r0) * self.W
+        cap = n_loc_rows * nc * self.P
+        dev = self.device
+        ptr = torch.empty(npx + 1, dtype=torch.int32, device=dev)
+        entries = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        scratch = torch.empty(int(N.lib().fepll_cover_scratch_ints(npx)), dtype=torch.int32, device=dev)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        N.call("fepll_cover_build", N.ptr(anchors), nr, nc, self.config.spacing, half, self.side,
+               self.W, row0, H_glob, a_first, n_loc_rows, r0, r1, N.ptr(ptr), N.ptr(entries), cap,
+               N.ptr(scratch), st)
+        return ptr, entries, r0, r1
 
     # ---------------------------------------------------------------- loop
     def run(self, y_dev, trace: bool = False, timer: dict | None = None, exchange=None):
@@ -328,7 +353,7 @@ class Restorer:
         nt = B * n
         mode = self.MODES[self.mode]
         self._mark(timer, "start")
-        N.call("fepll_extract", N.ptr(self.x), B, H, W, side, N.ptr(anchors), n,
+        N.call("fepll_extract", N.ptr(self.x), B, H, W, side, N.ptr(anchors), n, nc,
                N.ptr(self.Z64), N.ptr(self.Z32), self.z32_pitch, N.ptr(self.dc), N.ptr(self.sq), st)
         self._mark(timer, "extract")
         N.call("fepll_select", self.plan.handle, t, N.ptr(self.x), H, W, N.ptr(anchors), n,
@@ -340,24 +365,19 @@ class Restorer:
                N.ptr(self.dc), N.ptr(self.Z64), nt, N.ptr(self.Zhat), st)
         self._mark(timer, "wiener")
         bs2 = float(self.betas[t]) * self.sigma * self.sigma
-        if self.strip is not None:
-            sp = self.strip
-            N.call("fepll_aggregate_strip", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(anchors), nr, nc,
-                   self.config.spacing, half, side, B, H, W, sp.slab_lo, sp.H, sp.a_lo,
-                   sp.a_hi - sp.a_lo + 1, sp.r0 - sp.slab_lo, sp.r1 - sp.slab_lo, N.ptr(self.aty),
-                   N.ptr(self.diag), bs2, 0, N.ptr(self.x), N.ptr(self.xt) if self._want_xt else None,
-                   N.ptr(self.status), st)
-            self._mark(timer, "aggregate")
-        elif self.pixel_kind:
-            # reproject + pixel-diagonal update fused (patches.py:198-222, operators.py:281-287)
-            N.call("fepll_aggregate", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(anchors), nr, nc,
-                   self.config.spacing, half, side, B, H, W, N.ptr(self.aty), N.ptr(self.diag),
-                   bs2, 0, N.ptr(self.x), N.ptr(self.xt) if self._want_xt else None, N.ptr(self.status), st)
+        # reproject (patches.py:198-222) over the cover lists; pixel-diagonal
+        # kinds fuse the image update (operators.py:281-287), the others get
+        # rhs = A^T y + bs2 x~ for the FFT / CG solve
+        ptr, entries, r0, r1 = self._covers[t]
+        if self.pixel_kind:
+            N.call("fepll_aggregate_cover", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(ptr),
+                   N.ptr(entries), P, n, B, H, W, r0, r1, N.ptr(self.aty), N.ptr(self.diag), bs2, 0,
+                   N.ptr(self.x), N.ptr(self.xt) if self._want_xt else None, N.ptr(self.status), st)
             self._mark(timer, "aggregate")
         else:
-            N.call("fepll_aggregate", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(anchors), nr, nc,
-                   self.config.spacing, half, side, B, H, W, N.ptr(self.aty), None,
-                   bs2, 1, N.ptr(self.rhs), N.ptr(self.xt), N.ptr(self.status), st)
+            N.call("fepll_aggregate_cover", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(ptr),
+                   N.ptr(entries), P, n, B, H, W, r0, r1, N.ptr(self.aty), None, bs2, 1,
+                   N.ptr(self.rhs), N.ptr(self.xt), N.ptr(self.status), st)
             self._mark(timer, "aggregate")
             cg = self.config.cg
             for b in range(B):

@@ -142,11 +142,16 @@ def test_extract_kernel_bitwise():
     import torch
     from paper_1710_08124_b200 import _native as N, jitter_rng, jittered_grid
 
-    for P, H, W, s in [(64, 70, 61, 3), (100, 64, 64, 6), (36, 30, 40, 2)]:
+    from paper_1710_08124_b200 import axis_anchors
+
+    for P, H, W, s, tiled in [(64, 70, 61, 3, 1), (64, 70, 61, 3, 0), (100, 64, 64, 6, 1),
+                              (36, 30, 40, 2, 1), (16, 50, 47, 1, 1), (256, 64, 80, 16, 1),
+                              (64, 300, 280, 1, 1), (64, 300, 280, 8, 1), (256, 90, 70, 3, 1)]:
         side = int(np.sqrt(P))
         x = np.random.default_rng(P).random((H, W))
         pos = jittered_grid(H, W, P, s, jitter_rng(1, 2)).positions.astype(np.int32)
         n = pos.shape[0]
+        grid_cols = axis_anchors(W, side, s).size if tiled else 0
         Zo, dco = O.extract(x, pos.astype(np.int64), side)
         pitch = (P + 31) // 32 * 32
         Z64 = torch.empty((n, P), dtype=torch.float64, device="cuda")
@@ -154,7 +159,7 @@ def test_extract_kernel_bitwise():
         dc = torch.empty(n, dtype=torch.float64, device="cuda")
         sq = torch.empty(n, dtype=torch.float64, device="cuda")
         xd, pd = _dev(x), _dev(pos)  # keep the device inputs alive across the async launch
-        N.call("fepll_extract", N.ptr(xd), 1, H, W, side, N.ptr(pd), n, N.ptr(Z64),
+        N.call("fepll_extract", N.ptr(xd), 1, H, W, side, N.ptr(pd), n, grid_cols, N.ptr(Z64),
                N.ptr(Z32), pitch, N.ptr(dc), N.ptr(sq), torch.cuda.current_stream().cuda_stream)
         np.testing.assert_array_equal(dc.cpu().numpy(), dco)           # pairwise fold, bitwise
         np.testing.assert_array_equal(Z64.cpu().numpy(), Zo)
@@ -247,6 +252,19 @@ def test_aggregate_kernel_bitwise_vs_bincount():
                torch.cuda.current_stream().cuda_stream)
         np.testing.assert_array_equal(xt.cpu().numpy()[0], ref)
         assert int(status.item()) == 0
+        # the same gather over the plan's cover lists (the solver's path)
+        nr, nc = axis_anchors(H, side, s).size, axis_anchors(W, side, s).size
+        ptr = torch.empty(H * W + 1, dtype=torch.int32, device="cuda")
+        ent = torch.empty(n * P, dtype=torch.int32, device="cuda")
+        scr = torch.empty(int(N.lib().fepll_cover_scratch_ints(H * W)), dtype=torch.int32, device="cuda")
+        st = torch.cuda.current_stream().cuda_stream
+        N.call("fepll_cover_build", N.ptr(pd), nr, nc, s, (side - s) // 2, side, W, 0, H, 0, nr, 0, H,
+               N.ptr(ptr), N.ptr(ent), n * P, N.ptr(scr), st)
+        assert int(ptr[-1].item()) == n * P  # every patch covers exactly P pixels
+        xc = torch.empty((1, H, W), dtype=torch.float64, device="cuda")
+        N.call("fepll_aggregate_cover", N.ptr(ed), N.ptr(dd), N.ptr(ptr), N.ptr(ent), P, n, 1, H, W,
+               0, H, None, None, 1.0, 1, None, N.ptr(xc), N.ptr(status), st)
+        np.testing.assert_array_equal(xc.cpu().numpy()[0], ref)
 
 
 def test_lo_eq_hi_rule_returns_common_value():
