@@ -87,7 +87,10 @@ def inputs(workload: str, images: list):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons, sampled every 20 ms from before
+    the warm-up; :meth:`summary` reports the samples inside the timed window
+    (falling back to the loaded warm-up samples when the window is shorter
+    than the sampling period)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -97,25 +100,29 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.lines = []       # (perf_counter, line)
+        self.window = None
+        self._first = threading.Event()
 
-    def __enter__(self):
+    def start(self, wait_s: float = 10.0):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            self._first.wait(wait_s)
         except Exception:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+            self._first.set()
 
-    def __exit__(self, *exc):
+    def stop(self):
         if self.proc:
             self.proc.terminate()
             try:
@@ -124,9 +131,12 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0, t1 = self.window or (0.0, float("inf"))
+        inside = [ln for t, ln in self.lines if t0 - 0.03 <= t <= t1 + 0.03]
+        used = inside if len(inside) >= 2 else [ln for _, ln in self.lines]
+        sm, mx, reasons = [], [], set()
+        for ln in used:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -142,7 +152,18 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.lines)}
+                "reasons": sorted(reasons), "samples": len(used),
+                "samples_in_timed_window": len(inside)}
+
+
+def traffic_per_launch(n_patches: int):
+    """DRAM bytes (read + write) of one tree-level launch, scaled from the
+    per-patch figure of the committed ncu --set full capture, or None."""
+    f = ROOT / "profiles" / "select_ws_traffic.json"
+    if not f.exists():
+        return None
+    d = json.loads(f.read_text())
+    return d["dram_bytes_per_patch_level"] * n_patches
 
 
 def peaks():
@@ -248,19 +269,29 @@ def main():
             dist.barrier()
         torch.cuda.synchronize(dev)
 
+    clk = ClockSampler(local).start()
     for _ in range(args.warmup):
         run(y_dev)
     barrier()
     launches0 = N.lib().fepll_launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        barrier()
-        e0.record(stream)
-        for _ in range(args.steps):
-            run(y_dev)
-        e1.record(stream)
-        barrier()
+    # level kernels of kernel (b) bracketed by CUDA events on the launch stream
+    levels = int(getattr(r.tree, "depth", 64))
+    N.call("fepll_plan_profile", r.plan.handle, args.steps * len(r.betas) * levels + 64)
+    barrier()
+    tw0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        run(y_dev)
+    e1.record(stream)
+    barrier()
+    clk.window = (tw0, time.perf_counter())
+    clk.stop()
+    import ctypes
+    lvl_ms, lvl_n = ctypes.c_double(), ctypes.c_int32()
+    N.call("fepll_plan_profile_read", r.plan.handle, ctypes.byref(lvl_ms), ctypes.byref(lvl_n))
+    N.call("fepll_plan_profile", r.plan.handle, 0)
     launches = (N.lib().fepll_launch_count() - launches0) // args.steps
     ms = e0.elapsed_time(e1) / args.steps
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -311,17 +342,32 @@ def main():
     dominant = max(phases, key=phases.get)
     n_patch = sum(c[0] for c in counters)
     PB = P * 8
-    if dominant == "select":
-        achieved = sel_flops / (phases["select"] / 1e3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": bf16 / 2, "unit": "TFLOP/s",
-                "frac": achieved / (bf16 / 2), "traffic": None,
-                "kernel": "select_level_tc_kernel (+ rescore_fp64_kernel)",
-                "work": "2 x reference selection_multiplies per step (tree.py:413-427)",
-                "peak_note": f"TF32 dense = {src} bf16 {bf16} / 2; 3xTF32 issues 3 MMAs per "
-                             "algorithmic MMA so frac <= 1/3"}
+    ppad = (P + 31) // 32 * 32
+    n_step = n_patch // max(1, len(r.betas))  # patches per iteration = per level launch
+    if dominant == "select" and lvl_n.value > 0:
+        # kernel (b)'s tree-level kernel: every launch walks all n_step patches one
+        # level down, reading each FP32 patch row (4 P_pad bytes) plus its segment
+        # index and writing the routed index — algorithmic bytes per launch
+        launch_ms = lvl_ms.value / lvl_n.value
+        per_patch = 4 * ppad + 8
+        achieved = n_step * per_patch / (launch_ms / 1e3) / 1e9
+        flops_launch = sel_flops / max(1, lvl_n.value // args.steps)
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic_per_launch(n_step),
+                "kernel": "select_level_ws_kernel (tcgen05 3xTF32 tree level)",
+                "launch_ms": launch_ms, "launches_timed": int(lvl_n.value),
+                "bytes_per_launch": n_step * per_patch,
+                "work": f"{per_patch} B per patch-level: FP32 row gather + index in/out",
+                "peak_note": f"{src} HBM copy bandwidth; the rows are gathered in node order "
+                             "(random 256 B rows: measured gather ceiling ~2.5 TB/s, tools/tma_rate.cu)",
+                "tensor_view": {"achieved_tflops": flops_launch / (launch_ms / 1e3) / 1e12,
+                                "peak_tflops": bf16 / 2,
+                                "frac": flops_launch / (launch_ms / 1e3) / 1e12 / (bf16 / 2),
+                                "note": "2 x reference selection_multiplies (tree.py:413-427) vs TF32 "
+                                        "dense (= bf16/2); 3xTF32 issues 3 MMAs per algorithmic MMA"}}
     else:
         per_phase_bytes = {
-            "extract": n_patch * (PB + 4 * ((P + 31) // 32 * 32) + 16) + 8 * ys.size * 5,
+            "extract": n_patch * (PB + 4 * ppad + 16) + 8 * ys.size * 5,
             "aggregate": n_patch * (PB + 8) + 8 * 3 * ys.size * 5,
             "wiener": n_patch * 2 * PB,
         }

@@ -75,6 +75,12 @@ int fepll_plan_create(const fepll_plan_desc* desc, fepll_plan_t* out);
 /* scratch for up to max_patches patches per select call */
 int fepll_plan_reserve(fepll_plan_t plan, int64_t max_patches);
 int fepll_plan_destroy(fepll_plan_t plan);
+/* Timing of the tree-level kernels (kernel (b)): with capacity > 0 the next
+ * `capacity` level launches of fepll_select are bracketed by CUDA events on
+ * the caller's stream; _read returns their summed duration and count and
+ * resets.  capacity 0 turns it off. */
+int fepll_plan_profile(fepll_plan_t plan, int32_t capacity);
+int fepll_plan_profile_read(fepll_plan_t plan, double* total_ms, int32_t* launches);
 
 /* patches.py:89-132: the sampling plan of iteration t on the device,
  * bit-identical to jittered_grid(H, W, side^2, spacing,

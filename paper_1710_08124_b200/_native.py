@@ -46,6 +46,8 @@ _SIGS = {
     "fepll_plan_create": (i32, [C.POINTER(PlanDesc), C.POINTER(vp)]),
     "fepll_plan_reserve": (i32, [vp, i64]),
     "fepll_plan_destroy": (i32, [vp]),
+    "fepll_plan_profile": (i32, [vp, i32]),
+    "fepll_plan_profile_read": (i32, [vp, C.POINTER(f64), C.POINTER(i32)]),
     "fepll_grid_scratch_ints": (i32, []),
     "fepll_sample_grid": (i32, [C.c_uint64, C.c_uint64, i32, i32, i32, i32, i32, C.c_uint32, vp, vp, vp, vp]),
     "fepll_extract": (i32, [vp, i32, i32, i32, i32, vp, i32, i32, vp, vp, i32, vp, vp, vp]),

@@ -220,9 +220,36 @@ int fepll_plan_reserve(fepll_plan_t plan, int64_t max_patches) {
   return fepll::reserve(reinterpret_cast<Plan*>(plan), max_patches);
 }
 
+int fepll_plan_profile(fepll_plan_t plan, int32_t capacity) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  FEPLL_REQUIRE(p != nullptr && capacity >= 0, "plan_profile: bad arguments");
+  for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
+  p->prof_ev.assign(2 * (size_t)capacity, nullptr);
+  for (auto& e : p->prof_ev) FEPLL_CUDA(cudaEventCreate(&e));
+  p->prof_used = 0;
+  return fepll::kOk;
+}
+
+int fepll_plan_profile_read(fepll_plan_t plan, double* total_ms, int32_t* launches) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  FEPLL_REQUIRE(p != nullptr && total_ms && launches, "plan_profile_read: bad arguments");
+  double sum = 0.0;
+  if (p->prof_used > 0) FEPLL_CUDA(cudaEventSynchronize(p->prof_ev[2 * p->prof_used - 1]));
+  for (int i = 0; i < p->prof_used; ++i) {
+    float ms = 0.f;
+    FEPLL_CUDA(cudaEventElapsedTime(&ms, p->prof_ev[2 * i], p->prof_ev[2 * i + 1]));
+    sum += ms;
+  }
+  *total_ms = sum;
+  *launches = p->prof_used;
+  p->prof_used = 0;
+  return fepll::kOk;
+}
+
 int fepll_plan_destroy(fepll_plan_t plan) {
   Plan* p = reinterpret_cast<Plan*>(plan);
   if (!p) return fepll::kOk;
+  for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
   fepll::free_scratch(p);
   for (void* m : p->owned) cudaFree(m);
   delete p;

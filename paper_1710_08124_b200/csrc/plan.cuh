@@ -81,6 +81,9 @@ struct Plan {
   int n_leaf_nodes = 0;
   RouteScratch rs;
   int last_n_total = 0;
+  // optional timing of the level kernels (fepll_plan_profile): event pairs
+  std::vector<cudaEvent_t> prof_ev;
+  int prof_used = 0;
 };
 
 }  // namespace fepll
