@@ -423,6 +423,8 @@ __global__ void leaf_counts_kernel(const int32_t* leaf_nodes, int n_leaf_nodes,
 int select_level_tc(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                     cudaStream_t st);
 bool select_ws_supported(const Plan* p, int d);
+int select_level_wide(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
+                      cudaStream_t st);
 int select_level_ws(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                     cudaStream_t st);
 
@@ -501,12 +503,15 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
       int rc = kOk;
       const bool prof = p->prof_used < (int)p->prof_ev.size() / 2;
       if (prof) FEPLL_CUDA(cudaEventRecord(p->prof_ev[2 * p->prof_used], st));
-      if (mode == 1 && !p->level_wide[d] && p->level_tc_npad[d] <= 256) {
-        rc = select_ws_supported(p, d) ? select_level_ws(p, a, Z32, sq, guard, st)
-                                       : select_level_tc(p, a, Z32, sq, guard, st);
+      if (mode == 1) {
+        // wide levels (the exhaustive star root) stream their columns in chunks
+        const bool wide = p->level_wide[d] || p->level_tc_npad[d] > 256;
+        rc = wide ? select_level_wide(p, a, Z32, sq, guard, st)
+             : select_ws_supported(p, d) ? select_level_ws(p, a, Z32, sq, guard, st)
+                                         : select_level_tc(p, a, Z32, sq, guard, st);
         if (prof) FEPLL_CUDA(cudaEventRecord(p->prof_ev[2 * p->prof_used++ + 1], st));
         if (!rc) rc = rescore_queue_x(p, a, x, anchors, n_img, H, W, dc, sq, st);
-      } else {  // exact mode, or a wide level (sub-group FP64 scan)
+      } else {  // exact mode (wide nodes: block-wise FP64 scan)
         select_level_fp64_kernel<<<grid_for(n_total, kSelWarps, 148 * 8), kSelWarps * 32, 0, st>>>(
             p->v, a, ps, sq);
         FEPLL_LAUNCH();

@@ -79,12 +79,18 @@ __device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
   return d;
 }
 
-// Returns the best child index; *flagged when the decision is not certified.
-// d_acc: TMEM address (lane field set) of the tile's accumulator.
-__device__ __forceinline__ int epi_score_row(const EpiChild& E, int nk, uint32_t d_acc,
-                                             double sqv, double guard, bool* flagged) {
+// Running certified argmin over children scored chunk by chunk (wide nodes
+// stream their columns through TMEM in several chunks; a normal node is one
+// chunk).  m1/m2: the two smallest lower bounds score - err seen so far.
+struct EpiRun {
   double best = INFINITY, best_err = 0.0, m1 = INFINITY, m2 = INFINITY;
   int bi = 0, i1 = -1;
+};
+
+// Score children 0..nk-1 of the chunk in E (TMEM columns E.col[ci] of
+// d_acc); k_base: index of E's first child among the node's children.
+__device__ __forceinline__ void epi_run_chunk(const EpiChild& E, int nk, int k_base, uint32_t d_acc,
+                                              double sqv, double guard, EpiRun& R) {
   for (int ci = 0; ci < nk; ++ci) {
     const int c0 = E.col[ci];
     uint64_t s2 = 0;  // two FP32 partial sums
@@ -102,14 +108,28 @@ __device__ __forceinline__ int epi_score_row(const EpiChild& E, int nk, uint32_t
     const float s_lo = __uint_as_float((uint32_t)s2), s_hi = __uint_as_float((uint32_t)(s2 >> 32));
     const double sc = E.cconst[ci] + sqv * E.cinvnut[ci] + ((double)s_lo + (double)s_hi);
     const double er = guard * sqv * E.wnorm[ci] + 0x1p-40 * fabs(sc);
-    if (sc < best) { best = sc; bi = ci; best_err = er; }
+    const int k = k_base + ci;
+    if (sc < R.best) { R.best = sc; R.bi = k; R.best_err = er; }
     const double lo = sc - er;
-    if (lo < m1) { m2 = m1; m1 = lo; i1 = ci; }
-    else if (lo < m2) { m2 = lo; }
+    if (lo < R.m1) { R.m2 = R.m1; R.m1 = lo; R.i1 = k; }
+    else if (lo < R.m2) { R.m2 = lo; }
   }
-  const double other = (i1 == bi) ? m2 : m1;
-  *flagged = !(other > best + best_err) || !isfinite(best);
-  return bi;
+}
+
+// certified iff every other child's lower bound clears the best's upper one
+__device__ __forceinline__ bool epi_run_flagged(const EpiRun& R) {
+  const double other = (R.i1 == R.bi) ? R.m2 : R.m1;
+  return !(other > R.best + R.best_err) || !isfinite(R.best);
+}
+
+// Returns the best child index; *flagged when the decision is not certified.
+// d_acc: TMEM address (lane field set) of the tile's accumulator.
+__device__ __forceinline__ int epi_score_row(const EpiChild& E, int nk, uint32_t d_acc,
+                                             double sqv, double guard, bool* flagged) {
+  EpiRun R;
+  epi_run_chunk(E, nk, 0, d_acc, sqv, guard, R);
+  *flagged = epi_run_flagged(R);
+  return R.bi;
 }
 
 }  // namespace fepll

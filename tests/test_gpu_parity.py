@@ -75,6 +75,29 @@ def test_full_size_configs_vs_live_oracle(cfg_name, models):
     assert abs(psnr(x, c.clean) - psnr(xo, c.clean)) <= PSNR_TOL
 
 
+@pytest.mark.parametrize("P,H,s", [(64, 128, 4), (100, 96, 6)])
+def test_exhaustive_scan_tensor_vs_exact_and_oracle(P, H, s, models):
+    """No-tree profile (gmm.py:371-391) at sizes beyond the golden case: the
+    tcgen05 chunked scan (select_wide.cu) and the FP64 block scan give the
+    oracle's labels; counters follow solver.py:154-157."""
+    from paper_1710_08124_b200 import RestorationConfig, identity_operator, restore, synthetic
+
+    model, _ = models[P]
+    img = synthetic.synthetic_image(H, H, 9) / 255.0
+    y = img + (20.0 / 255.0) * np.random.default_rng(3).standard_normal((H, H))
+    cfg = RestorationConfig(sigma=20.0, spacing=s, seed=1, trace=True, use_tree=False)
+    A = identity_operator((H, H))
+    xt, st = restore(y, A, model, None, cfg, mode="tensor")
+    xe, se = restore(y, A, model, None, cfg, mode="exact")
+    xo, so = O.restore(y, A, model, None, sigma=20.0, spacing=s, seed=1, use_tree=False, trace=True)
+    for a, b, c in zip(st.trace, se.trace, so.trace):
+        np.testing.assert_array_equal(a["selected"], c["selected"])
+        np.testing.assert_array_equal(b["selected"], c["selected"])
+    assert rmse255(xt, xo) <= RMSE_TOL and rmse255(xe, xo) <= RMSE_TOL
+    n = st.iterations[0].patches
+    assert all(it.score_evaluations == n * 200 for it in st.iterations)
+
+
 def test_same_seed_bit_identical_and_batch_equals_single(models):
     from paper_1710_08124_b200 import RestorationConfig, restore, restore_batch, synthetic
 
