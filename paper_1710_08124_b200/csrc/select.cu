@@ -117,6 +117,7 @@ __device__ __forceinline__ void block_argmin(const PlanView& pv, int t, int u, i
     for (int j = 0; j < r; ++j) sacc += tv[c0 + j];
     const int64_t ti = (int64_t)t * pv.n_nodes + v;
     best = pv.node_const[ti] + sqv / pv.node_nu_tail[ti] + sacc;
+    if (best != best) best = INFINITY;  // non-finite patch: still a valid child (status flags it)
     bestk = k0 + lane;
   }
 #pragma unroll

@@ -66,10 +66,10 @@ __device__ __forceinline__ void cp_async_wait_group() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Row strides (in doubles) are chosen so every fragment load is two
-// conflict-free shared-memory wavefronts: A-side tiles (rows g, 4
-// consecutive k) use ld = 4 mod 16, B-side tiles (4 rows k, 8 consecutive n)
-// use ld = 8 mod 16.
+// Row strides (in doubles): A-side tiles (lane (g, t) reads row g, col t)
+// use ld = 4 mod 16 — conflict-free; B-side tiles (row t, col g) use
+// ld = 8 mod 16, which costs a 2-way conflict on half the fragment loads but
+// keeps P = 100 within shared memory (ld = 4 measured no faster at P = 64).
 struct Geo {
   int P, Pn;     // P, P rounded up to 8 (phase-1 K, phase-2 N)
   int zld;       // Zs [MT][zld], columns P..Pn-1 zero
@@ -293,10 +293,14 @@ int wiener_dmma(Plan* p, int t, const double* Z64, double* Zhat, cudaStream_t st
   // 128-row tiles (16 warps) once the average leaf bucket is large enough
   // that the extra padding rows do not matter, and the tile fits in smem
   const int64_t n_total = p->last_n_total;
-  const bool big = n_total >= (int64_t)1024 * std::max(1, p->n_leaf_nodes) &&
-                   smem_for(128, 2) <= 227 * 1024;
+  int dev = 0, optin = 0;
+  FEPLL_CUDA(cudaGetDevice(&dev));
+  FEPLL_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const size_t cap = (size_t)optin;
+  const bool big = n_total >= (int64_t)1024 * std::max(1, p->n_leaf_nodes) && smem_for(128, 2) <= cap;
   const int mt = big ? 128 : 64;
-  const int ns = big ? 2 : (smem_for(64, 4) <= 227 * 1024 ? 4 : 2);
+  const int ns = big ? 2 : (smem_for(64, 4) <= cap ? 4 : 2);
+  FEPLL_REQUIRE(smem_for(mt, ns) <= cap, "wiener: tile buffers exceed shared memory");
   const size_t smem = smem_for(mt, ns);
   const int nt2 = geo.Pn / 8;
   auto launch = [&](auto kernel) -> int {
