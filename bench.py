@@ -301,16 +301,27 @@ def main():
     total_mp = n_images * size * size / 1e6 if n_images > 1 else size * size / 1e6
     value = total_mp / (ms_max / 1e3)
 
-    # ---- end to end through the public API on host buffers
+    # ---- end to end through the public API on host buffers: pinned float32
+    # observations in, restored float32 images out, copies inside the timed
+    # region (HostPipeline overlaps them with compute, 4 chunks on 2 streams)
     pin_in = torch.from_numpy(ys.astype(np.float32)).pin_memory()
     pin_out = torch.empty(clean.shape, dtype=torch.float32).pin_memory()
-    y32 = torch.empty(pin_in.shape, dtype=torch.float32, device=dev)
-    y64 = torch.empty(pin_in.shape, dtype=torch.float64, device=dev)
+    chunks = 4 if (not strip and len(mine) % 4 == 0 and len(mine) >= 8) else 1
+    if not strip and chunks > 1:
+        from paper_1710_08124_b200 import HostPipeline
+        hp = HostPipeline(A, model, tree, cfg, batch=len(mine), chunks=chunks, lam=r.lam,
+                          mode=args.mode, device=dev)
 
-    def e2e_step():
-        y32.copy_(pin_in, non_blocking=True)
-        y64.copy_(y32)
-        pin_out.copy_(run(y64), non_blocking=True)
+        def e2e_step():
+            hp.run(pin_in, pin_out)
+    else:
+        y32 = torch.empty(pin_in.shape, dtype=torch.float32, device=dev)
+        y64 = torch.empty(pin_in.shape, dtype=torch.float64, device=dev)
+
+        def e2e_step():
+            y32.copy_(pin_in, non_blocking=True)
+            y64.copy_(y32)
+            pin_out.copy_(run(y64), non_blocking=True)
 
     e2e_step()
     barrier()

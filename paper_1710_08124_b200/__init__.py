@@ -13,6 +13,6 @@ from .operators import (CgConfig, DegradationOperator, SolveInfo, convolution_op
                         decimate_operator, gain_operator, gaussian_kernel, identity_operator,
                         mask_operator, radial_gain_map)
 from .patches import SampleGrid, axis_anchors, jitter_rng, jittered_grid, regular_grid
-from .solver import (IterationStats, RestorationConfig, Restorer, SolverStats, beta_schedule,
-                     restore, restore_batch)
+from .solver import (HostPipeline, IterationStats, RestorationConfig, Restorer, SolverStats,
+                     beta_schedule, restore, restore_batch)
 from .tree import GmmTree, TreeNode

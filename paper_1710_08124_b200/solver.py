@@ -429,6 +429,62 @@ class Restorer:
         return [(bool(si[t, 0, 2] > 0), float(si[t, 0, 1])) for t in range(si.shape[0])]
 
 
+class HostPipeline:
+    """Batch restoration from and to pinned host buffers with the copies
+    overlapped: the batch is cut into ``chunks`` equal parts that alternate
+    between two restorers on two CUDA streams, so the upload of chunk c+1 and
+    the download of chunk c-1 run on the copy engines while chunk c computes.
+    Results are identical to :class:`Restorer` on the whole batch (every
+    image is restored independently)."""
+
+    def __init__(self, A, model, tree, config, batch: int, chunks: int = 4, lam: float | None = None,
+                 mode: str = "tensor", device=None):
+        torch = _torch()
+        if batch % chunks:
+            raise DataError(f"batch {batch} does not split into {chunks} chunks")
+        self.torch = torch
+        self.batch, self.chunks = int(batch), int(chunks)
+        self.per = self.batch // self.chunks
+        k = min(2, self.chunks)
+        self.restorers = [Restorer(A, model, tree, config, batch=self.per, lam=lam, mode=mode,
+                                   device=device) for _ in range(k)]
+        dev = self.restorers[0].device
+        self.device = dev
+        self.streams = [torch.cuda.Stream(dev) for _ in range(k)]
+        Ho, Wo = (int(v) for v in A.output_dims)
+        H, W = (int(v) for v in A.input_dims)
+        self.y32 = [torch.empty((self.per, Ho, Wo), dtype=torch.float32, device=dev) for _ in range(k)]
+        self.y64 = [torch.empty((self.per, Ho, Wo), dtype=torch.float64, device=dev) for _ in range(k)]
+        self.x32 = [torch.empty((self.per, H, W), dtype=torch.float32, device=dev) for _ in range(k)]
+        self.status = [torch.zeros(1, dtype=torch.int32, device=dev) for _ in range(k)]
+
+    def run(self, y_host, x_host) -> None:
+        """y_host: pinned (batch, Ho, Wo) float32 observations; x_host: pinned
+        (batch, H, W) float32 output.  Returns after both are complete."""
+        torch = self.torch
+        main = torch.cuda.current_stream(self.device)
+        for s, st in zip(self.streams, self.status):
+            s.wait_stream(main)
+            st.zero_()
+        for c in range(self.chunks):
+            k = c % len(self.restorers)
+            r, s = self.restorers[k], self.streams[k]
+            lo, hi = c * self.per, (c + 1) * self.per
+            with torch.cuda.stream(s):
+                self.y32[k].copy_(y_host[lo:hi], non_blocking=True)
+                self.y64[k].copy_(self.y32[k])
+                x, _ = r.run(self.y64[k])
+                self.x32[k].copy_(x)
+                x_host[lo:hi].copy_(self.x32[k], non_blocking=True)
+                self.status[k].bitwise_or_(r.status)  # run() clears it per chunk
+        for s in self.streams:
+            main.wait_stream(s)
+        main.synchronize()
+        for r, st in zip(self.restorers, self.status):
+            r.status.copy_(st)
+            r.check_status()
+
+
 def restore(y, A, model, tree=None, config=None, *, mode: str = "tensor", lam=None):
     """GPU drop-in for `pkg/src/fepll/solver.py:161-274`."""
     if config is None:

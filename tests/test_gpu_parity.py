@@ -98,6 +98,24 @@ def test_exhaustive_scan_tensor_vs_exact_and_oracle(P, H, s, models):
     assert all(it.score_evaluations == n * 200 for it in st.iterations)
 
 
+def test_host_pipeline_equals_batch_restore(models):
+    """HostPipeline (chunks on two streams, pinned float32 buffers) gives the
+    float32 of the whole-batch restore, image for image."""
+    import torch
+    from paper_1710_08124_b200 import HostPipeline, RestorationConfig, restore_batch, synthetic
+
+    model, tree = models[64]
+    cases = [synthetic.baseline_case("cfg1", 80, image_seed=i, noise_seed=30 + i) for i in range(4)]
+    ys = np.stack([c.y for c in cases]).astype(np.float32)
+    cfg = RestorationConfig(sigma=20.0, spacing=4, seed=5)
+    hp = HostPipeline(cases[0].A, model, tree, cfg, batch=4, chunks=2)
+    pin_in = torch.from_numpy(ys).pin_memory()
+    pin_out = torch.empty(ys.shape, dtype=torch.float32).pin_memory()
+    hp.run(pin_in, pin_out)
+    xb, _ = restore_batch(ys.astype(np.float64), cases[0].A, model, tree, cfg)
+    np.testing.assert_array_equal(pin_out.numpy(), xb.astype(np.float32))
+
+
 def test_same_seed_bit_identical_and_batch_equals_single(models):
     from paper_1710_08124_b200 import RestorationConfig, restore, restore_batch, synthetic
 
