@@ -204,10 +204,10 @@ select_level_fp64_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __
 __global__ void __launch_bounds__(kSelWarps * 32)
 rescore_fp64_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restrict__ sq,
                     const int32_t* __restrict__ queue, const int32_t* __restrict__ queue_len) {
-  __shared__ LevelTables s;
+  // The level kernel already published the next level's segment offsets in
+  // a.off (route.cuh level_tables, CTA 0), so no per-CTA table rebuild here.
   __shared__ double zbuf[kSelWarps][kMaxP];
   __shared__ double tbuf[kSelWarps][kMaxGroupCols];
-  level_tables(pv, a, s, 1);
   const int lane = lane_id();
   double* zs = zbuf[warp_id()];
   double* tv = tbuf[warp_id()];
@@ -217,7 +217,15 @@ rescore_fp64_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restr
     const int u = queue[2 * item + 1];
     load_patch(ps, patch, pv.P, zs);
     const int v = score_children_fp64(pv, a.t, u, zs, sq[patch], tv);
-    if (lane == 0) level_route(pv, a, s, v, patch);
+    if (lane == 0) {
+      const int slot = atomicAdd(&a.cnt[v], 1);
+      if (pv.child_count[v] > 0) {
+        a.seg_out[a.off[v] + slot] = patch;
+      } else {
+        a.leafseg[a.off[v] + slot] = patch;
+        a.labels[patch] = pv.leaf_index[v];
+      }
+    }
     __syncwarp();
   }
 }
