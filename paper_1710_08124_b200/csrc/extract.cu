@@ -219,55 +219,58 @@ extract_tile_kernel(const double* __restrict__ x, int batch, int H, int W,
       }
     }
     __syncthreads();
-    // one lane group per patch, lane r = window row r (extract_pow2_kernel)
+    // one lane group per patch, lane c = window COLUMN c: the reference's
+    // halvings of the flattened row (patches.py:156-163) first add row r + h
+    // to row r elementwise — in-register adds down this lane's column — and
+    // then halve the surviving row across the group's lanes: the same FP64
+    // additions in the same order as extract_pow2_kernel, a fraction of its
+    // shuffles
     const int p = warp * PER_WARP + lane / SIDE;
-    const int r = lane % SIDE;
+    const int c = lane % SIDE;
     const bool valid = p < m;
-    double v[SIDE];
+    double v[SIDE];  // v[r] = window(r, c)
     if (valid) {
       const int pr = s_pr[p], pc = s_pc[p];
       if (staged) {
-        const double* src = win + (pr - r_lo + r) * wc + (pc - c_lo);
+        const double* src = win + (pr - r_lo) * wc + (pc - c_lo + c);
 #pragma unroll
-        for (int c = 0; c < SIDE; ++c) v[c] = src[c];
+        for (int r = 0; r < SIDE; ++r) v[r] = src[r * wc];
       } else {
-        const double* src = img + (int64_t)(pr + r) * W + pc;
+        const double* src = img + (int64_t)pr * W + pc + c;
 #pragma unroll
-        for (int c = 0; c < SIDE; ++c) v[c] = __ldg(src + c);
+        for (int r = 0; r < SIDE; ++r) v[r] = __ldg(src + (int64_t)r * W);
       }
     } else {
 #pragma unroll
-      for (int c = 0; c < SIDE; ++c) v[c] = 0.0;
+      for (int r = 0; r < SIDE; ++r) v[r] = 0.0;
     }
     double acc[SIDE];
 #pragma unroll
-    for (int c = 0; c < SIDE; ++c) acc[c] = v[c];
-#pragma unroll
-    for (int h = SIDE / 2; h >= 1; h >>= 1) {
-#pragma unroll
-      for (int c = 0; c < SIDE; ++c) {
-        const double o = __shfl_down_sync(0xffffffffu, acc[c], h, SIDE);
-        if (r < h) acc[c] = acc[c] + o;
-      }
-    }
+    for (int r = 0; r < SIDE; ++r) acc[r] = v[r];
 #pragma unroll
     for (int h = SIDE / 2; h >= 1; h >>= 1)
 #pragma unroll
-      for (int c = 0; c < h; ++c) acc[c] = acc[c] + acc[c + h];
-    const double dc = __shfl_sync(0xffffffffu, acc[0], 0, SIDE) / (double)P;
+      for (int r = 0; r < h; ++r) acc[r] = acc[r] + acc[r + h];
+    double col = acc[0];  // row 0 of the halved rows, column c
+#pragma unroll
+    for (int h = SIDE / 2; h >= 1; h >>= 1) {
+      const double o = __shfl_down_sync(0xffffffffu, col, h, SIDE);
+      if (c < h) col = col + o;
+    }
+    const double dc = __shfl_sync(0xffffffffu, col, 0, SIDE) / (double)P;
     double sq = 0.0;
     if (valid) {
-      double* zrow = zs + p * P + r * SIDE;
+      double* zcol = zs + p * P + c;
 #pragma unroll
-      for (int c = 0; c < SIDE; ++c) {
-        const double z = v[c] - dc;
+      for (int r = 0; r < SIDE; ++r) {
+        const double z = v[r] - dc;
         sq = fma(z, z, sq);
-        zrow[c] = z;
+        zcol[r * SIDE] = z;
       }
     }
 #pragma unroll
     for (int h = SIDE / 2; h >= 1; h >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, h, SIDE);
-    if (valid && r == 0) {
+    if (valid && c == 0) {
       if (dc_out) dc_out[g0 + p] = dc;
       if (sq_out) sq_out[g0 + p] = sq;
     }
@@ -278,7 +281,14 @@ extract_tile_kernel(const double* __restrict__ x, int batch, int H, int W,
       double2* dst = reinterpret_cast<double2*>(Z64 + g0 * P);
       for (int k = tid; k < m * P / 2; k += 256) dst[k] = src[k];
     }
-    if (Z32) {
+    if (Z32 && z32_pitch == P) {  // no padding: a flat conversion
+      const double2* src = reinterpret_cast<const double2*>(zs);
+      float4* dst = reinterpret_cast<float4*>(Z32 + g0 * P);
+      for (int k = tid; k < m * P / 4; k += 256) {
+        const double2 a0 = src[2 * k], a1 = src[2 * k + 1];
+        dst[k] = make_float4((float)a0.x, (float)a0.y, (float)a1.x, (float)a1.y);
+      }
+    } else if (Z32) {
       const int q4 = z32_pitch / 4;
       float4* dst = reinterpret_cast<float4*>(Z32 + g0 * z32_pitch);
       for (int k = tid; k < m * q4; k += 256) {
