@@ -200,7 +200,8 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       const int nt = (r + 7) / 8;  // this leaf's rank, not the model's widest
 #pragma unroll
       for (int n = 0; n < kMaxR / 8; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0;
-      for (int k0 = 0; k0 < geo.Pn; k0 += 8) {
+#pragma unroll
+      for (int k0 = 0; k0 < NT2 * 8; k0 += 8) {  // NT2 * 8 == Pn
         const double a[4] = {za[k0], zb[k0], za[k0 + 4], zb[k0 + 4]};
         const double* u0 = Us + (k0 + t4) * geo.uld + g4;
         const double* u1 = u0 + 4 * geo.uld;
@@ -232,7 +233,9 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       for (int n = 0; n < NT2; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0;
       const double* ca = Cs + (m0 + g4) * geo.cld + t4;
       const double* cb = ca + 8 * geo.cld;
-      for (int k0 = 0; k0 < nt1 * 8; k0 += 8) {
+#pragma unroll
+      for (int k0 = 0; k0 < kMaxR; k0 += 8) {
+        if (k0 >= nt1 * 8) break;
         const double a[4] = {ca[k0], cb[k0], ca[k0 + 4], cb[k0 + 4]};
         const double* u0 = UT + (k0 + t4) * geo.utld + g4;
         const double* u1 = u0 + 4 * geo.utld;
