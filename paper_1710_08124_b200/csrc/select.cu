@@ -434,6 +434,13 @@ int select_level_tc(Plan* p, const LevelArgs& a, const float* Z32, const double*
 bool select_ws_supported(const Plan* p, int d);
 int select_level_wide(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                       cudaStream_t st);
+int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
+                     cudaStream_t st);
+// 0: select_ws.cu, 1: select_ws2.cu (deep staging, TMEM lo), 2: per level —
+// ws2 on levels of <= 16 nodes (measured faster there: three tiles of row
+// loads in flight), ws on wider levels (its four epilogue groups keep up
+// with the larger child sets)
+int g_select_variant = 2;
 int select_level_ws(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                     cudaStream_t st);
 
@@ -516,8 +523,12 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
         // wide levels (the exhaustive star root) stream their columns in chunks
         const bool wide = p->level_wide[d] || p->level_tc_npad[d] > 256;
         rc = wide ? select_level_wide(p, a, Z32, sq, guard, st)
-             : select_ws_supported(p, d) ? select_level_ws(p, a, Z32, sq, guard, st)
-                                         : select_level_tc(p, a, Z32, sq, guard, st);
+             : select_ws_supported(p, d)
+                 ? ((g_select_variant == 1 ||
+                     (g_select_variant == 2 && p->level_start[d + 1] - p->level_start[d] <= 16))
+                        ? select_level_ws2(p, a, Z32, sq, guard, st)
+                        : select_level_ws(p, a, Z32, sq, guard, st))
+                 : select_level_tc(p, a, Z32, sq, guard, st);
         if (prof) FEPLL_CUDA(cudaEventRecord(p->prof_ev[2 * p->prof_used++ + 1], st));
         if (!rc) rc = rescore_queue_x(p, a, x, anchors, n_img, H, W, dc, sq, st);
       } else {  // exact mode (wide nodes: block-wise FP64 scan)
@@ -535,6 +546,11 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
     FEPLL_LAUNCH();
   }
   return kOk;
+}
+
+extern "C" int fepll_debug_select_variant(int32_t v) {
+  fepll::g_select_variant = v;
+  return 0;
 }
 
 extern "C" int fepll_select_rescored(fepll_plan_t plan, int32_t* dst, void* stream) {
