@@ -2,7 +2,8 @@ import sys, os, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_1710_08124_b200 import RestorationConfig, Restorer, synthetic, _native as N
-B = 16; level = int(sys.argv[1]) if len(sys.argv) > 1 else 6
+level = int(sys.argv[1]) if len(sys.argv) > 1 else 6
+B = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 c = synthetic.baseline_case("cfg5", 1024)
 ys = np.stack([c.y] * B)
 model = synthetic.synthetic_gmm(200, 64, 0, 0.95); tree = synthetic.baseline_tree(model)
