@@ -62,8 +62,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 select_level_tc_kernel(PlanView pv, TcArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-align the operand region (SWIZZLE_128B atoms)
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  uint8_t* base = tc::align1024(smem_raw);
   const int bstage = args.bmax_rows * 128;               // bytes of one B half per stage
   const int stage_bytes = 2 * kAtomBytesA + 2 * bstage;
   TcSmemTables& s = *reinterpret_cast<TcSmemTables*>(base + 2 * stage_bytes);

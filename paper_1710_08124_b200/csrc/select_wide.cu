@@ -51,8 +51,7 @@ struct Args {
 __global__ void __launch_bounds__(kThreads, 1)
 select_level_wide_kernel(PlanView pv, Args args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  uint8_t* base = tc::align1024(smem_raw);
   uint8_t* A = base;                                          // [katoms][hi, lo][128 rows]
   uint8_t* Bst = A + 2 * args.katoms * kAtomBytes;            // [2 stages][hi, lo][nw rows]
   const int bhalf = args.nw * 128;

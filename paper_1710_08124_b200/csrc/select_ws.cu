@@ -135,8 +135,7 @@ __device__ __forceinline__ void load_row(const Args& args, int g, int ka, float4
 __global__ void __launch_bounds__(kThreads, 1)
 select_level_ws_kernel(PlanView pv, Args args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  uint8_t* base = tc::align1024(smem_raw);
   uint8_t* stageA = base;
   uint8_t* bbuf = base + kStages * kStageBytes;   // resident B (hi then lo)
   Smem& s = *reinterpret_cast<Smem*>(bbuf + kBBytes);

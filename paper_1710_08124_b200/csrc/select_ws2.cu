@@ -122,8 +122,7 @@ __device__ __forceinline__ TileInfo tile_info(const LevelArgs& a, const WsLevelT
 __global__ void __launch_bounds__(kThreads, 1)
 select_level_ws2_kernel(PlanView pv, Args args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  uint8_t* base = tc::align1024(smem_raw);
   uint8_t* stageA = base;
   uint8_t* bbuf = base + kStages * kStageBytes;   // resident B (hi then lo)
   Smem& s = *reinterpret_cast<Smem*>(bbuf + kBBytes);

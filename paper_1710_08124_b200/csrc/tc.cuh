@@ -11,6 +11,14 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// 1024-byte aligned pointer into dynamic shared memory, derived by pointer
+// arithmetic so the compiler keeps the shared address space (an integer
+// round trip would turn every later access into a generic LD/ST)
+__device__ __forceinline__ uint8_t* align1024(uint8_t* smem) {
+  const uint32_t off = (1024u - (smem_u32(smem) & 1023u)) & 1023u;
+  return smem + off;
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
