@@ -39,6 +39,15 @@ struct Head {
 // D(16x8) += A(16x8) B(8x8); lane (g = lane/4, t = lane%4) holds
 // a = {A[g][t], A[g+8][t], A[g][t+4], A[g+8][t+4]}, b = {B[t][g], B[t+4][g]},
 // d = {D[g][2t], D[g][2t+1], D[g+8][2t], D[g+8][2t+1]}
+// D(8x8) += A(8x4) B(4x8): lane (g, t) holds a = A[g][t], b = B[t][g],
+// d = {D[g][2t], D[g][2t+1]}.  Not volatile: ptxas may interleave the
+// independent accumulators (each m16n8k8 is four of these).
+__device__ __forceinline__ void dmma8(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
 __device__ __forceinline__ void dmma16(double (&d)[4], const double (&a)[4], const double (&b)[2]) {
   asm volatile(
       "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -205,11 +214,26 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
         const double a[4] = {za[k0], zb[k0], za[k0 + 4], zb[k0 + 4]};
         const double* u0 = Us + (k0 + t4) * geo.uld + g4;
         const double* u1 = u0 + 4 * geo.uld;
+        // the m16n8k8 product as four m8n8k4 steps, ordered so consecutive
+        // DMMAs write different accumulators (k 0-3 for every n, then k 4-7)
+        double b0[kMaxR / 8], b1[kMaxR / 8];
 #pragma unroll
         for (int n = 0; n < kMaxR / 8; ++n)
           if (n < nt) {
-            const double bb[2] = {u0[n * 8], u1[n * 8]};
-            dmma16(acc[n], a, bb);
+            b0[n] = u0[n * 8];
+            b1[n] = u1[n * 8];
+          }
+#pragma unroll
+        for (int n = 0; n < kMaxR / 8; ++n)
+          if (n < nt) {
+            dmma8(acc[n][0], acc[n][1], a[0], b0[n]);
+            dmma8(acc[n][2], acc[n][3], a[1], b0[n]);
+          }
+#pragma unroll
+        for (int n = 0; n < kMaxR / 8; ++n)
+          if (n < nt) {
+            dmma8(acc[n][0], acc[n][1], a[2], b1[n]);
+            dmma8(acc[n][2], acc[n][3], a[3], b1[n]);
           }
       }
 #pragma unroll
@@ -239,10 +263,21 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
         const double a[4] = {ca[k0], cb[k0], ca[k0 + 4], cb[k0 + 4]};
         const double* u0 = UT + (k0 + t4) * geo.utld + g4;
         const double* u1 = u0 + 4 * geo.utld;
+        double b0[NT2], b1[NT2];
 #pragma unroll
         for (int n = 0; n < NT2; ++n) {
-          const double bb[2] = {u0[n * 8], u1[n * 8]};
-          dmma16(acc[n], a, bb);
+          b0[n] = u0[n * 8];
+          b1[n] = u1[n * 8];
+        }
+#pragma unroll
+        for (int n = 0; n < NT2; ++n) {
+          dmma8(acc[n][0], acc[n][1], a[0], b0[n]);
+          dmma8(acc[n][2], acc[n][3], a[1], b0[n]);
+        }
+#pragma unroll
+        for (int n = 0; n < NT2; ++n) {
+          dmma8(acc[n][0], acc[n][1], a[2], b1[n]);
+          dmma8(acc[n][2], acc[n][3], a[3], b1[n]);
         }
       }
       const double gt = pv.model_gamma_tail[(int64_t)t * pv.K + comp];
