@@ -20,6 +20,16 @@ namespace fepll {
 
 namespace wn {
 
+// debug timeline (fepll_debug_wiener_trace): [CTA][64 tiles][8] clock64
+__device__ uint64_t* g_trace = nullptr;
+__device__ __forceinline__ void wstamp(int i, int slot) {
+  if (g_trace && i < 64 && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+    g_trace[((size_t)blockIdx.x * 64 + i) * 8 + slot] = t;
+  }
+}
+
 constexpr int kMaxP = 128;
 constexpr int kMaxR = 64;
 constexpr int kMaxRows = 128;
@@ -68,6 +78,19 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
                "l"(src)
                : "memory");
 }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(static_cast<uint32_t>(__cvta_generic_to_shared(src))), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 template <int N>
@@ -90,6 +113,51 @@ struct Geo {
 
 // NT2: phase-2 n-tiles (P/8 rounded up): 8 for P=64, 13 for P=100.
 // MT rows per tile, NS row buffers (NS - 1 tiles of rows in flight).
+// phase 1 of one warp's 16 rows: C = (Z . U) * shrink for NT1 n-tiles of 8
+// rank columns; za / zb: this lane's A rows (g, g + 8) at column t; cw: the
+// warp's Cs rows
+template <int NT2, int NT1>
+__device__ __forceinline__ void phase1(const double* za, const double* zb, const double* Us, int uld,
+                                       double* cw, int cld, const double* sh, int t4, int g4) {
+  double acc[NT1][4];
+#pragma unroll
+  for (int n = 0; n < NT1; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0;
+#pragma unroll
+  for (int k0 = 0; k0 < NT2 * 8; k0 += 8) {  // NT2 * 8 == Pn
+    const double a0 = za[k0], a1 = zb[k0], a2 = za[k0 + 4], a3 = zb[k0 + 4];
+    const double* u0 = Us + (k0 + t4) * uld + g4;
+    const double* u1 = u0 + 4 * uld;
+    double b0[NT1], b1[NT1];
+#pragma unroll
+    for (int n = 0; n < NT1; ++n) {
+      b0[n] = u0[n * 8];
+      b1[n] = u1[n * 8];
+    }
+    // the m16n8k8 product as four m8n8k4 steps, consecutive DMMAs on
+    // different accumulators (k 0-3 for every n, then k 4-7)
+#pragma unroll
+    for (int n = 0; n < NT1; ++n) {
+      dmma8(acc[n][0], acc[n][1], a0, b0[n]);
+      dmma8(acc[n][2], acc[n][3], a1, b0[n]);
+    }
+#pragma unroll
+    for (int n = 0; n < NT1; ++n) {
+      dmma8(acc[n][0], acc[n][1], a2, b1[n]);
+      dmma8(acc[n][2], acc[n][3], a3, b1[n]);
+    }
+  }
+#pragma unroll
+  for (int n = 0; n < NT1; ++n) {
+    const int col = n * 8 + 2 * t4;
+    double* c0 = cw + col;
+    double* c1 = c0 + 8 * cld;
+    c0[0] = acc[n][0] * sh[col];
+    c0[1] = acc[n][1] * sh[col + 1];
+    c1[0] = acc[n][2] * sh[col];
+    c1[1] = acc[n][3] * sh[col + 1];
+  }
+}
+
 template <int NT2, int MT, int NS>
 __global__ void __launch_bounds__(MT * 2)
 wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, int n_leaf_nodes,
@@ -151,16 +219,16 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
     if (j >= t_end) return;
     const int32_t* rows = h.rows[(j - t_begin) % kRing];
     double* Zs = Zs0 + ((j - t_begin) % NS) * kRows * geo.zld;
-    const int chunks = P / 2;  // 16-byte chunks per row (P even)
-    for (int e = tid; e < kRows * chunks; e += kThreads) {
-      const int i = e / chunks, c = e - i * chunks;
-      const int g = rows[i];
-      double* dst = Zs + i * geo.zld + 2 * c;
+    // two threads per row, alternate 16-byte chunks (P even)
+    const int i = tid >> 1;
+    const int g = rows[i];
+    double* drow = Zs + i * geo.zld;
+    for (int c = tid & 1; c < P / 2; c += 2) {
       if (g >= 0) {
-        cp_async16(dst, Z64 + (int64_t)g * P + 2 * c);
+        cp_async16(drow + 2 * c, Z64 + (int64_t)g * P + 2 * c);
       } else {
-        dst[0] = 0.0;
-        dst[1] = 0.0;
+        drow[2 * c] = 0.0;
+        drow[2 * c + 1] = 0.0;
       }
     }
   };
@@ -180,8 +248,11 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
     const int li = prefix_find(h.tpre, n_leaf_nodes, tile);
     const int comp = pv.leaf_index[h.leaf_v[li]];
     const int r = pv.model_rank[comp];
+    wstamp(i, 0);
+    bulk_wait_read();  // the previous tile's row stores have left its buffer
     cp_async_wait_group<NS - 2>();
     __syncthreads();  // this tile's rows landed; the buffer refilled next is free
+    wstamp(i, 1);
     fetch_z(tile + NS - 1);
     fetch_rows(tile + kLead);
     cp_async_commit();
@@ -198,58 +269,28 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       cur_leaf = comp;
       __syncthreads();
     }
+    wstamp(i, 2);
     const double* Zs = Zs0 + (i % NS) * kRows * geo.zld;
     const int g4 = lane >> 2, t4 = lane & 3;
     const int m0 = warp * 16;
     const double* za = Zs + (m0 + g4) * geo.zld + t4;       // rows g, g+8 of the warp
     const double* zb = za + 8 * geo.zld;
-    // ---- phase 1: C[m0..m0+15][0..R8) = (Z . U) * shrink
-    {
-      double acc[kMaxR / 8][4];
-      const int nt = (r + 7) / 8;  // this leaf's rank, not the model's widest
-#pragma unroll
-      for (int n = 0; n < kMaxR / 8; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0;
-#pragma unroll
-      for (int k0 = 0; k0 < NT2 * 8; k0 += 8) {  // NT2 * 8 == Pn
-        const double a[4] = {za[k0], zb[k0], za[k0 + 4], zb[k0 + 4]};
-        const double* u0 = Us + (k0 + t4) * geo.uld + g4;
-        const double* u1 = u0 + 4 * geo.uld;
-        // the m16n8k8 product as four m8n8k4 steps, ordered so consecutive
-        // DMMAs write different accumulators (k 0-3 for every n, then k 4-7)
-        double b0[kMaxR / 8], b1[kMaxR / 8];
-#pragma unroll
-        for (int n = 0; n < kMaxR / 8; ++n)
-          if (n < nt) {
-            b0[n] = u0[n * 8];
-            b1[n] = u1[n * 8];
-          }
-#pragma unroll
-        for (int n = 0; n < kMaxR / 8; ++n)
-          if (n < nt) {
-            dmma8(acc[n][0], acc[n][1], a[0], b0[n]);
-            dmma8(acc[n][2], acc[n][3], a[1], b0[n]);
-          }
-#pragma unroll
-        for (int n = 0; n < kMaxR / 8; ++n)
-          if (n < nt) {
-            dmma8(acc[n][0], acc[n][1], a[2], b1[n]);
-            dmma8(acc[n][2], acc[n][3], a[3], b1[n]);
-          }
-      }
-#pragma unroll
-      for (int n = 0; n < kMaxR / 8; ++n)
-        if (n < nt) {
-          const int col = n * 8 + 2 * t4;
-          double* c0 = Cs + (m0 + g4) * geo.cld + col;
-          double* c1 = c0 + 8 * geo.cld;
-          c0[0] = acc[n][0] * sh[col];
-          c0[1] = acc[n][1] * sh[col + 1];
-          c1[0] = acc[n][2] * sh[col];
-          c1[1] = acc[n][3] * sh[col + 1];
-        }
+    // ---- phase 1: C[m0..m0+15][0..R8) = (Z . U) * shrink, with the
+    // leaf's n-tile count as a compile-time constant (predicated-off DMMAs
+    // would still occupy the pipe)
+    switch ((r + 7) / 8) {
+      case 1: phase1<NT2, 1>(za, zb, Us, geo.uld, Cs + (m0 + g4) * geo.cld, geo.cld, sh, t4, g4); break;
+      case 2: phase1<NT2, 2>(za, zb, Us, geo.uld, Cs + (m0 + g4) * geo.cld, geo.cld, sh, t4, g4); break;
+      case 3: phase1<NT2, 3>(za, zb, Us, geo.uld, Cs + (m0 + g4) * geo.cld, geo.cld, sh, t4, g4); break;
+      case 4: phase1<NT2, 4>(za, zb, Us, geo.uld, Cs + (m0 + g4) * geo.cld, geo.cld, sh, t4, g4); break;
+      case 5: phase1<NT2, 5>(za, zb, Us, geo.uld, Cs + (m0 + g4) * geo.cld, geo.cld, sh, t4, g4); break;
+      case 6: phase1<NT2, 6>(za, zb, Us, geo.uld, Cs + (m0 + g4) * geo.cld, geo.cld, sh, t4, g4); break;
+      case 7: phase1<NT2, 7>(za, zb, Us, geo.uld, Cs + (m0 + g4) * geo.cld, geo.cld, sh, t4, g4); break;
+      default: phase1<NT2, 8>(za, zb, Us, geo.uld, Cs + (m0 + g4) * geo.cld, geo.cld, sh, t4, g4); break;
     }
     __syncwarp();  // each warp only reads its own rows of Cs
     const int nt1 = (r + 7) / 8;
+    wstamp(i, 3);
     // ---- phase 2: Zhat[m0..m0+15][0..P) = C . U^T + gamma_tail Z
     {
       double acc[NT2][4];
@@ -280,6 +321,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
           dmma8(acc[n][2], acc[n][3], a[3], b1[n]);
         }
       }
+      wstamp(i, 4);
       const double gt = pv.model_gamma_tail[(int64_t)t * pv.K + comp];
       // Zhat = acc + gamma_tail z, written over this warp's own rows of Zs
       // (each element read and written by the same lane)...
@@ -296,18 +338,20 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
           }
         }
       }
+      // ... then each of the warp's 16 rows leaves as one TMA bulk store
+      // (smem -> global, 8P bytes); the buffer is reused only after the
+      // stores have read it (wait_group.read before the next tile's barrier)
+      fence_proxy_async_smem();
       __syncwarp();
-      // ... then stored as whole 8P-byte rows (coalesced 16-byte lanes)
-      const int32_t* rows = h.rows[slot];
-      for (int i = 0; i < 16; ++i) {
-        const int gidx = rows[m0 + i];
-        if (gidx < 0) continue;
-        const double2* src = reinterpret_cast<const double2*>(zw + (m0 + i) * geo.zld);
-        double2* dst = reinterpret_cast<double2*>(Zhat + (int64_t)gidx * P);
-        for (int c = lane; c < P / 2; c += 32) dst[c] = src[c];
+      if (lane < 16) {
+        const int gidx = h.rows[slot][m0 + lane];
+        if (gidx >= 0) bulk_s2g(Zhat + (int64_t)gidx * P, zw + (m0 + lane) * geo.zld, P * 8);
+        bulk_commit();
       }
+      wstamp(i, 5);
     }
   }
+  bulk_wait_all();  // the last rows' stores are complete before the kernel ends
 }
 
 }  // namespace wn
@@ -382,3 +426,8 @@ bool wiener_dmma_supported(const Plan* p) {
 }
 
 }  // namespace fepll
+
+extern "C" int fepll_debug_wiener_trace(void* device_buffer) {
+  uint64_t* p = static_cast<uint64_t*>(device_buffer);
+  return cudaMemcpyToSymbol(fepll::wn::g_trace, &p, sizeof(p)) == cudaSuccess ? 0 : 5;
+}
