@@ -519,7 +519,7 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
       int rc = kOk;
       const bool prof = p->prof_used < (int)p->prof_ev.size() / 2;
       if (prof) FEPLL_CUDA(cudaEventRecord(p->prof_ev[2 * p->prof_used], st));
-      if (mode == 1) {
+      if (mode == 1 && p->v.P <= 128) {
         // wide levels (the exhaustive star root) stream their columns in chunks
         const bool wide = p->level_wide[d] || p->level_tc_npad[d] > 256;
         rc = wide ? select_level_wide(p, a, Z32, sq, guard, st)
@@ -531,7 +531,8 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
                  : select_level_tc(p, a, Z32, sq, guard, st);
         if (prof) FEPLL_CUDA(cudaEventRecord(p->prof_ev[2 * p->prof_used++ + 1], st));
         if (!rc) rc = rescore_queue_x(p, a, x, anchors, n_img, H, W, dc, sq, st);
-      } else {  // exact mode (wide nodes: block-wise FP64 scan)
+      } else {  // exact mode, or P > 128 (beyond the tcgen05 kernels' K atoms):
+                // FP64 scoring (wide nodes: block-wise scan) — the same labels
         select_level_fp64_kernel<<<grid_for(n_total, kSelWarps, 148 * 8), kSelWarps * 32, 0, st>>>(
             p->v, a, ps, sq);
         FEPLL_LAUNCH();

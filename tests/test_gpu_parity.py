@@ -98,6 +98,26 @@ def test_exhaustive_scan_tensor_vs_exact_and_oracle(P, H, s, models):
     assert all(it.score_evaluations == n * 200 for it in st.iterations)
 
 
+@pytest.mark.parametrize("P,H,s", [(16, 40, 2), (36, 48, 3), (144, 60, 6), (256, 64, 8)])
+def test_other_patch_sizes_no_tree_vs_oracle(P, H, s):
+    """Patch sides 4, 6, 12, 16 (power-of-two and generic extraction, K atoms
+    1..8; P > 128 scores on the FP64 path in tensor mode) through the no-tree
+    profile, which needs no reference-built tree: labels equal the oracle's."""
+    from paper_1710_08124_b200 import RestorationConfig, identity_operator, restore, synthetic
+
+    model = synthetic.synthetic_gmm(20, P, 0, 0.95)
+    img = synthetic.synthetic_image(H, H, 4) / 255.0
+    y = img + (20 / 255) * np.random.default_rng(1).standard_normal((H, H))
+    cfg = RestorationConfig(sigma=20.0, spacing=s, seed=1, trace=True, use_tree=False)
+    A = identity_operator((H, H))
+    xo, so = O.restore(y, A, model, None, sigma=20.0, spacing=s, seed=1, use_tree=False, trace=True)
+    for mode in ("exact", "tensor"):
+        x, st = restore(y, A, model, None, cfg, mode=mode)
+        for a, b in zip(st.trace, so.trace):
+            np.testing.assert_array_equal(a["selected"], b["selected"])
+        assert rmse255(x, xo) <= RMSE_TOL
+
+
 def test_host_pipeline_equals_batch_restore(models):
     """HostPipeline (chunks on two streams, pinned float32 buffers) gives the
     float32 of the whole-batch restore, image for image."""
