@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--workload", default="cfg5-batch", choices=sorted(WORKLOADS))
     ap.add_argument("--mode", default="tensor", choices=["tensor", "exact"])
     ap.add_argument("--cpu-sample-images", type=int, default=2)
+    ap.add_argument("--e2e-chunks", type=int, default=2,
+                    help="HostPipeline chunks for the end-to-end leg (copies overlap compute)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -303,10 +305,11 @@ def main():
 
     # ---- end to end through the public API on host buffers: pinned float32
     # observations in, restored float32 images out, copies inside the timed
-    # region (HostPipeline overlaps them with compute, 4 chunks on 2 streams)
+    # region (HostPipeline overlaps them with compute: 2 chunks on 2 streams)
     pin_in = torch.from_numpy(ys.astype(np.float32)).pin_memory()
     pin_out = torch.empty(clean.shape, dtype=torch.float32).pin_memory()
-    chunks = 4 if (not strip and len(mine) % 4 == 0 and len(mine) >= 8) else 1
+    chunks = args.e2e_chunks if (not strip and len(mine) % args.e2e_chunks == 0
+                                 and len(mine) >= 2 * args.e2e_chunks) else 1
     if not strip and chunks > 1:
         from paper_1710_08124_b200 import HostPipeline
         hp = HostPipeline(A, model, tree, cfg, batch=len(mine), chunks=chunks, lam=r.lam,
