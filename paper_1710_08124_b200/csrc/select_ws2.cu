@@ -32,16 +32,16 @@ constexpr int kRows = 128;
 constexpr int kProducerWarps = 8;       // warp w: K atom w/4, TMEM lane quarter w%4
 constexpr int kMmaWarp = 8;
 constexpr int kEpiWarp0 = 9;
-constexpr int kGroups = 3;                 // epilogue groups == TMEM accumulators
-constexpr int kEpiWarps = 4 * kGroups;
-constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
+// epilogue groups (== TMEM accumulators) and accumulator width are template
+// parameters: <3, 128> for levels with nodes up to 128 padded columns,
+// <4, 96> where every node fits 96 (four groups keep up with the MMAs)
+constexpr int threads_for(int ng) { return (9 + 4 * ng) * 32; }
 constexpr int kStages = 4;              // raw row stages (hi operand)
 constexpr int kLoBufs = 2;              // TMEM lo buffers
 constexpr int kAtomA = kRows * 128;     // bytes of one K atom of A
 constexpr int kMaxKAtoms = 2;           // P <= 64
 constexpr int kMaxN = 128;              // padded group width == accumulator columns
 constexpr int kStageBytes = kMaxKAtoms * kAtomA;           // raw rows, all atoms
-constexpr uint32_t kLoCol0 = kGroups * kMaxN;              // TMEM column of lo buffer 0
 constexpr int kBBytes = 2 * kMaxKAtoms * kMaxN * 128;      // hi + lo, all atoms
 constexpr uint32_t kTmemCols = 512;
 
@@ -63,15 +63,16 @@ constexpr int kIdxAhead = 8;   // tiles of row indices in flight (>= 2 * kStages
 constexpr int kIdxRing = 9;
 constexpr int kRawAhead = kStages - 1;  // raw loads issued this many tiles ahead
 
+template <int NG>
 struct Smem {
   int32_t idx_ring[2][kIdxRing][kRows];  // [K atom][slot][row]
   WsLevelTables lv;
   int64_t nd_off[kMaxNodes];      // segment offset of each depth-d node (a.off)
   int16_t nd_npad[kMaxNodes];     // padded group width
   int16_t nd_nk[kMaxNodes];       // child count
-  EpiGroup epi[kGroups];
+  EpiGroup epi[NG];
   uint64_t raw_empty[kStages], lo_full[kLoBufs], lo_empty[kLoBufs];
-  uint64_t acc_full[kGroups], acc_empty[kGroups];
+  uint64_t acc_full[NG], acc_empty[NG];
   uint64_t b_full, drain;
   uint32_t tmem_base;
   int32_t t_begin, t_end;
@@ -119,13 +120,18 @@ __device__ __forceinline__ TileInfo tile_info(const LevelArgs& a, const WsLevelT
   return ti;
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+template <int NG, int ACC>
+__global__ void __launch_bounds__(threads_for(NG), 1)
 select_level_ws2_kernel(PlanView pv, Args args) {
+  constexpr int kGroups = NG;
+  constexpr int kAcc = ACC;                          // accumulator columns (>= node width)
+  constexpr uint32_t kLoCol0 = NG * ACC;             // TMEM column of lo buffer 0
+  static_assert(NG * ACC + kLoBufs * 64 <= 512, "TMEM: accumulators + lo buffers");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = tc::align1024(smem_raw);
   uint8_t* stageA = base;
   uint8_t* bbuf = base + kStages * kStageBytes;   // resident B (hi then lo)
-  Smem& s = *reinterpret_cast<Smem*>(bbuf + kBBytes);
+  Smem<NG>& s = *reinterpret_cast<Smem<NG>*>(bbuf + kBBytes);
   const LevelArgs& a = args.a;
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -282,7 +288,7 @@ select_level_ws2_kernel(PlanView pv, Args args) {
       tc::fence_after_sync();
       if (lane == 0) stamp(args, i, 2);
       const uint32_t idesc = tc::idesc_tf32(kRows, npad);
-      const uint32_t d = tmem + ac * kMaxN;
+      const uint32_t d = tmem + ac * kAcc;
       // descriptor start-address field counts 16-byte units
       const uint64_t A0 = a_base + (uint64_t)((st * kStageBytes) >> 4);
       for (int kq = 0; kq < args.katoms; ++kq) {
@@ -309,7 +315,7 @@ select_level_ws2_kernel(PlanView pv, Args args) {
     const int ew = warp - kEpiWarp0;       // 0..11
     const int grp = ew >> 2;               // tiles with i % kGroups == grp
     const int row = 32 * (warp & 3) + lane;
-    const uint32_t d_acc = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + grp * kMaxN;
+    const uint32_t d_acc = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + grp * kAcc;
     EpiGroup& E = s.epi[grp];
     const int etid = (ew & 3) * 32 + lane;  // 0..127 inside the group
     const int bar_id = 1 + grp;
@@ -427,10 +433,16 @@ int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double
   args.queue_len = p->rs.queue_len;
   args.katoms = (p->v.P + 31) / 32;
   args.trace = (a.depth == g_ws_trace_level) ? g_ws_trace : nullptr;
-  const size_t smem = 1024 + ws2::kStages * ws2::kStageBytes + ws2::kBBytes + sizeof(ws2::Smem);
-  FEPLL_CUDA(cudaFuncSetAttribute(ws2::select_level_ws2_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  ws2::select_level_ws2_kernel<<<kSMs, ws2::kThreads, smem, st>>>(p->v, args);
+  auto launch = [&](auto kernel, size_t tables, int threads) -> int {
+    const size_t smem = 1024 + ws2::kStages * ws2::kStageBytes + ws2::kBBytes + tables;
+    FEPLL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kernel<<<kSMs, threads, smem, st>>>(p->v, args);
+    return kOk;
+  };
+  if (p->level_tc_npad[a.depth] <= 96)
+    launch(ws2::select_level_ws2_kernel<4, 96>, sizeof(ws2::Smem<4>), ws2::threads_for(4));
+  else
+    launch(ws2::select_level_ws2_kernel<3, 128>, sizeof(ws2::Smem<3>), ws2::threads_for(3));
   FEPLL_LAUNCH();
   return kOk;
 }
