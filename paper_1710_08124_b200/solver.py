@@ -205,7 +205,8 @@ class Restorer:
         n = int(self.anchors[0].shape[0])
         self.n = n
         # per-pixel cover lists of each plan (shared by the whole batch)
-        self._covers = [self._cover(t) for t in range(config.iterations)]
+        self._covers = [self._cover(t) if self.batch > 1 else self._cover_rows()
+                        for t in range(config.iterations)]
         self.plan.reserve(n * self.batch)
         B, H, W = self.batch, self.H, self.W
         f64 = torch.float64
@@ -265,6 +266,13 @@ class Restorer:
             anchors = anchors[sp.a_lo * nc:(sp.a_hi + 1) * nc].clone()
             anchors[:, 0] -= sp.slab_lo
         return anchors, nr, nc, half
+
+    def _cover_rows(self):
+        """(None, None, r0, r1): the produced rows, for the single-image path."""
+        sp = self.strip
+        if sp is None:
+            return None, None, 0, self.H
+        return None, None, sp.r0 - sp.slab_lo, sp.r1 - sp.slab_lo
 
     def _cover(self, t: int):
         """CSR cover lists (ptr, entries) of iteration t's plan for the rows
@@ -365,20 +373,29 @@ class Restorer:
                N.ptr(self.dc), N.ptr(self.Z64), nt, N.ptr(self.Zhat), st)
         self._mark(timer, "wiener")
         bs2 = float(self.betas[t]) * self.sigma * self.sigma
-        # reproject (patches.py:198-222) over the cover lists; pixel-diagonal
-        # kinds fuse the image update (operators.py:281-287), the others get
-        # rhs = A^T y + bs2 x~ for the FFT / CG solve
+        # reproject (patches.py:198-222); pixel-diagonal kinds fuse the image
+        # update (operators.py:281-287), the others get rhs = A^T y + bs2 x~ for
+        # the FFT / CG solve.  Batches gather over the plan's cover lists
+        # (shared by all images); a single image (strip mode included) has
+        # nothing to amortize them over and searches its candidates directly.
         ptr, entries, r0, r1 = self._covers[t]
-        if self.pixel_kind:
-            N.call("fepll_aggregate_cover", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(ptr),
-                   N.ptr(entries), P, n, B, H, W, r0, r1, N.ptr(self.aty), N.ptr(self.diag), bs2, 0,
-                   N.ptr(self.x), N.ptr(self.xt) if self._want_xt else None, N.ptr(self.status), st)
-            self._mark(timer, "aggregate")
+        kind = 0 if self.pixel_kind else 1
+        out = self.x if self.pixel_kind else self.rhs
+        diag = self.diag if self.pixel_kind else None
+        xt = self.xt if (self._want_xt or not self.pixel_kind) else None
+        if B == 1:
+            sp = self.strip
+            row0, H_glob, a_first, n_loc = ((sp.slab_lo, sp.H, sp.a_lo, sp.a_hi - sp.a_lo + 1)
+                                            if sp is not None else (0, H, 0, nr))
+            N.call("fepll_aggregate_strip", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(anchors), nr, nc,
+                   self.config.spacing, half, side, B, H, W, row0, H_glob, a_first, n_loc, r0, r1,
+                   N.ptr(self.aty), N.ptr(diag), bs2, kind, N.ptr(out), N.ptr(xt), N.ptr(self.status), st)
         else:
             N.call("fepll_aggregate_cover", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(ptr),
-                   N.ptr(entries), P, n, B, H, W, r0, r1, N.ptr(self.aty), None, bs2, 1,
-                   N.ptr(self.rhs), N.ptr(self.xt), N.ptr(self.status), st)
-            self._mark(timer, "aggregate")
+                   N.ptr(entries), P, n, B, H, W, r0, r1, N.ptr(self.aty), N.ptr(diag), bs2, kind,
+                   N.ptr(out), N.ptr(xt), N.ptr(self.status), st)
+        self._mark(timer, "aggregate")
+        if not self.pixel_kind:
             cg = self.config.cg
             for b in range(B):
                 self.op.solve(self.rhs[b], self.xt[b], bs2, cg.tolerance, cg.max_iterations,
