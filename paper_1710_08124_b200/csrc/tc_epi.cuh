@@ -5,8 +5,8 @@
 // thread streams them in 16-column TMEM chunks and accumulates
 // s_c = sum_j c_j^2 w_j with packed FP32x2 multiply/FMA (FMUL2/FFMA2).
 // score_c = const_c + ||z||^2 / nu_tail_c + s_c (FP64, gmm.py:335-338; the
-// division is a multiplication by the FP64 reciprocal, a 1-ulp change
-// covered by the bound's relative slack).
+// division is a multiplication by the FP64 reciprocal fused with the add, a
+// few-ulp change covered by the bound's 2^-40 relative slack).
 //
 // Certification: the 3xTF32 projection (three FP32-accumulated tcgen05
 // passes) is within gamma = 2^-18 ||z|| of the exact coefficient, so
@@ -91,6 +91,7 @@ struct EpiRun {
 // d_acc); k_base: index of E's first child among the node's children.
 __device__ __forceinline__ void epi_run_chunk(const EpiChild& E, int nk, int k_base, uint32_t d_acc,
                                               double sqv, double guard, EpiRun& R) {
+  const double gs = guard * sqv;  // per-row part of the bound
   for (int ci = 0; ci < nk; ++ci) {
     const int c0 = E.col[ci];
     uint64_t s2 = 0;  // two FP32 partial sums
@@ -105,9 +106,11 @@ __device__ __forceinline__ void epi_run_chunk(const EpiChild& E, int nk, int k_b
         s2 = f2_fma(f2_mul(c2, w2[j]), c2, s2);
       }
     }
-    const float s_lo = __uint_as_float((uint32_t)s2), s_hi = __uint_as_float((uint32_t)(s2 >> 32));
-    const double sc = E.cconst[ci] + sqv * E.cinvnut[ci] + ((double)s_lo + (double)s_hi);
-    const double er = guard * sqv * E.wnorm[ci] + 0x1p-40 * fabs(sc);
+    // the two FP32 partial sums meet in FP32 (one more rounding, inside the
+    // accumulation budget), the score and its bound in fused FP64 ops
+    const float sf = __uint_as_float((uint32_t)s2) + __uint_as_float((uint32_t)(s2 >> 32));
+    const double sc = fma(sqv, E.cinvnut[ci], E.cconst[ci]) + (double)sf;
+    const double er = fma(0x1p-40, fabs(sc), gs * E.wnorm[ci]);
     const int k = k_base + ci;
     if (sc < R.best) { R.best = sc; R.bi = k; R.best_err = er; }
     const double lo = sc - er;
