@@ -138,6 +138,8 @@ static int create(const fepll_plan_desc* d, Plan** out) {
     UP(d->grp_tc_w, (int64_t)T * d->grp_tc_w_cols, v.tc_w);
     UP(d->grp_tc_w_off, n, v.tc_w_off);
     v.tc_w_cols = d->grp_tc_w_cols;
+    FEPLL_REQUIRE(d->grp_tc_len % T == 0, "plan: tcgen05 images must hold one block per iteration");
+    v.tc_tstride = d->grp_tc_len / T;
     p->have_tc = true;
     for (int i = 0; i < n; ++i) p->max_tc_npad = std::max(p->max_tc_npad, d->grp_tc_npad[i]);
   }

@@ -41,6 +41,7 @@ struct PlanView {
   const float* tc_w;
   const int32_t* tc_w_off;
   int tc_w_cols;
+  int64_t tc_tstride;          // floats between consecutive iterations' B images
 };
 
 // Routing scratch: ping-pong patch-index segments per level plus the leaf

@@ -104,8 +104,8 @@ select_level_tc_kernel(PlanView pv, TcArgs args) {
     const int my_patch = tid < m ? a.seg_in[seg0 + tid] : -1;
     s.rows[tid] = my_patch;
     const float* zrow = my_patch >= 0 ? args.Z32 + (int64_t)my_patch * args.z32_pitch : nullptr;
-    const float* bhi = pv.tc_hi + pv.tc_off[u];
-    const float* blo = pv.tc_lo + pv.tc_off[u];
+    const float* bhi = pv.tc_hi + (int64_t)t * pv.tc_tstride + pv.tc_off[u];
+    const float* blo = pv.tc_lo + (int64_t)t * pv.tc_tstride + pv.tc_off[u];
     const uint32_t bbytes = (uint32_t)npad * 128u;
     const uint32_t idesc = tc::idesc_tf32(kTcRows, npad);
 

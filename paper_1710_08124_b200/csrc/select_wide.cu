@@ -155,7 +155,7 @@ select_level_wide_kernel(PlanView pv, Args args) {
           uint8_t* bhi = Bst + st * 2 * bhalf;
           uint8_t* blo = bhi + bhalf;
           // rows [col0, col0 + width) of atom ka: contiguous 128-byte rows, 16-row aligned
-          const int64_t off = pv.tc_off[u] + ((int64_t)ka * npad + col0) * 32;
+          const int64_t off = (int64_t)t * pv.tc_tstride + pv.tc_off[u] + ((int64_t)ka * npad + col0) * 32;
           tc::mbar_arrive_expect_tx(&s.load_bar[st], 2 * bbytes);
           tc::bulk_g2s(bhi, pv.tc_hi + off, bbytes, &s.load_bar[st]);
           tc::bulk_g2s(blo, pv.tc_lo + off, bbytes, &s.load_bar[st]);

@@ -273,8 +273,9 @@ select_level_ws2_kernel(PlanView pv, Args args) {
         }
         if (lane == 0) {
           tc::mbar_arrive_expect_tx(&s.b_full, 2 * bhalf);
-          tc::bulk_g2s(bbuf, pv.tc_hi + pv.tc_off[ti.u], bhalf, &s.b_full);
-          tc::bulk_g2s(bbuf + bhalf, pv.tc_lo + pv.tc_off[ti.u], bhalf, &s.b_full);
+          const int64_t boff = (int64_t)t * pv.tc_tstride + pv.tc_off[ti.u];
+          tc::bulk_g2s(bbuf, pv.tc_hi + boff, bhalf, &s.b_full);
+          tc::bulk_g2s(bbuf + bhalf, pv.tc_lo + boff, bhalf, &s.b_full);
         }
         __syncwarp();
         tc::mbar_wait(&s.b_full, b_loads & 1);

@@ -2,17 +2,20 @@
 //
 // For every child c of the tile's node (pkg/src/fepll/tree.py:417-425) the
 // child's columns start on a 16-column boundary (plan.py tc_images), so the
-// thread streams them in 16-column TMEM chunks and accumulates
-// s_c = sum_j c_j^2 w_j with packed FP32x2 multiply/FMA (FMUL2/FFMA2).
+// thread streams them in 16-column TMEM chunks.  The B columns carry
+// sqrt(-w_j) (w = sq_weight <= 0 at the iteration's beta), so the
+// accumulators hold c'_j = c_j sqrt(-w_j) and s_c = sum_j c_j^2 w_j =
+// -sum_j c'_j^2: one packed FP32x2 FMA (FFMA2) per two columns.
 // score_c = const_c + ||z||^2 / nu_tail_c + s_c (FP64, gmm.py:335-338; the
 // division is a multiplication by the FP64 reciprocal fused with the add, a
 // few-ulp change covered by the bound's 2^-40 relative slack).
 //
 // Certification: the 3xTF32 projection (three FP32-accumulated tcgen05
-// passes) is within gamma = 2^-18 ||z|| of the exact coefficient, so
-// |d s_c| <= 2 gamma ||z|| sum_j |c_j w_j| <= 2^-17 ||z||^2 ||w_c||
-// (Cauchy-Schwarz, ||c|| <= ||z||); the FP32 accumulation adds
-// <= 64 * 2^-24 * sum|c_j^2 w_j| <= 2^-18 ||z||^2 ||w_c||.
+// passes) is within gamma = 2^-18 ||z|| ||b_j|| of the exact c'_j (b_j the
+// scaled column, ||b_j|| = sqrt|w_j|), so
+// |d s_c| <= 2 gamma sum_j |c'_j| sqrt|w_j| ||z|| = 2^-17 ||z|| sum_j |c_j w_j|
+// <= 2^-17 ||z||^2 ||w_c|| (Cauchy-Schwarz, ||c|| <= ||z||); the FP32
+// accumulation adds <= 65 * 2^-24 * sum_j c'_j^2 <= 2^-18 ||z||^2 ||w_c||.
 // err_c = guard * ||z||^2 * ||w_c|| + 2^-40 |score_c| with guard = 2^-16
 // covers both.  The argmin is certified when every other child
 // satisfies score_c - err_c > score_best + err_best; otherwise the caller
@@ -98,18 +101,18 @@ __device__ __forceinline__ void epi_run_chunk(const EpiChild& E, int nk, int k_b
     for (int q = 0; q < E.chunks[ci]; ++q) {
       uint32_t ra[16];
       tmem_ld16(d_acc + c0 + 16 * q, ra);
-      const uint64_t* w2 = reinterpret_cast<const uint64_t*>(E.w + c0 + 16 * q);
       tc::tmem_ld_wait();
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const uint64_t c2 = (uint64_t)ra[2 * j] | ((uint64_t)ra[2 * j + 1] << 32);
-        s2 = f2_fma(f2_mul(c2, w2[j]), c2, s2);
+        s2 = f2_fma(c2, c2, s2);
       }
     }
     // the two FP32 partial sums meet in FP32 (one more rounding, inside the
     // accumulation budget), the score and its bound in fused FP64 ops
     const float sf = __uint_as_float((uint32_t)s2) + __uint_as_float((uint32_t)(s2 >> 32));
-    const double sc = fma(sqv, E.cinvnut[ci], E.cconst[ci]) + (double)sf;
+    // the B columns carry sqrt(-w_j) (plan.py tc_images): sum_j c_j^2 w_j = -sum_j c'_j^2
+    const double sc = fma(sqv, E.cinvnut[ci], E.cconst[ci]) - (double)sf;
     const double er = fma(0x1p-40, fabs(sc), gs * E.wnorm[ci]);
     const int k = k_base + ci;
     if (sc < R.best) { R.best = sc; R.bi = k; R.best_err = er; }

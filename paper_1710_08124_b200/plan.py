@@ -70,17 +70,22 @@ def swizzle128_kmajor(mat: np.ndarray) -> np.ndarray:
 
 
 def tc_images(topo, comps, P: int, sqw_per_node: list):
-    """Operands of the tcgen05 scorer.
+    """Operands of the tcgen05 scorer, one set per beta_t.
 
-    For internal node u the B image is the group matrix transposed to
+    For internal node u and iteration t the B image is the group matrix with
+    every column scaled by sqrt(-w_t) (w_t = sq_weight at beta_t, <= 0 for a
+    flat-tail model: kept eigenvalues >= the tail value), transposed to
     (npad_u, P_pad) K-major — child v occupying rows
     [tc_child_col[v], tc_child_col[v] + r_v), every child padded to a multiple
     of 16 rows so each child starts on a 16-column TMEM chunk — then TF32
-    hi/lo split and 128B-swizzled.  ``sqw_per_node[t][v]`` (FP64 vectors)
-    become the FP32 per-column weights (0 on padding)."""
+    hi/lo split and 128B-swizzled.  The scorer's epilogue then needs only
+    -sum_j c'_j^2 per child (c' = z . B'), no per-column weights.  Images are
+    laid out [T][nodes]; ``tc_off`` is the offset within one iteration's
+    block.  ``sqw_per_node[t][v]`` (FP64 vectors) also become the FP32
+    per-column weights ``tc_w`` (0 on padding) that the error bound's
+    ||w_c|| is taken from.  Returns None if some weight is positive."""
     Ppad = ((P + 31) // 32) * 32
     n = topo.n_nodes
-    his, los = [], []
     tc_off = np.zeros(n, np.int64)
     tc_npad = np.zeros(n, np.int32)
     tc_child_col = np.zeros(n, np.int32)
@@ -98,13 +103,6 @@ def tc_images(topo, comps, P: int, sqw_per_node: list):
             tc_child_col[v] = col
             col += ((comps[v].kept_basis.shape[1] + 15) // 16) * 16
         npad = max(col, 16)
-        Bt = np.zeros((npad, Ppad), dtype=np.float32)
-        for v in kids:
-            r = comps[v].kept_basis.shape[1]
-            Bt[tc_child_col[v]:tc_child_col[v] + r, :P] = np.asarray(comps[v].kept_basis).T
-        hi, lo = tf32_split(Bt)
-        his.append(swizzle128_kmajor(hi.reshape(npad, Ppad)))
-        los.append(swizzle128_kmajor(lo.reshape(npad, Ppad)))
         tc_off[u] = cur
         tc_npad[u] = npad
         tc_w_off[u] = wcols
@@ -112,6 +110,23 @@ def tc_images(topo, comps, P: int, sqw_per_node: list):
         wcols += npad
         groups.append((u, kids))
     T = len(sqw_per_node)
+    for t in range(T):
+        for u, kids in groups:
+            for v in kids:
+                if np.any(np.asarray(sqw_per_node[t][v]) > 0):
+                    return None
+    his, los = [], []
+    for t in range(T):
+        for u, kids in groups:
+            Bt = np.zeros((tc_npad[u], Ppad), dtype=np.float64)
+            for v in kids:
+                r = comps[v].kept_basis.shape[1]
+                scale = np.sqrt(-np.asarray(sqw_per_node[t][v], dtype=np.float64))
+                Bt[tc_child_col[v]:tc_child_col[v] + r, :P] = (np.asarray(comps[v].kept_basis)
+                                                               * scale[None, :]).T
+            hi, lo = tf32_split(Bt.astype(np.float32))
+            his.append(swizzle128_kmajor(hi.reshape(tc_npad[u], Ppad)))
+            los.append(swizzle128_kmajor(lo.reshape(tc_npad[u], Ppad)))
     tc_w = np.zeros((T, max(wcols, 1)), np.float32)
     for t in range(T):
         for u, kids in groups:
@@ -122,7 +137,7 @@ def tc_images(topo, comps, P: int, sqw_per_node: list):
     return dict(tc_hi=np.concatenate(his) if his else np.zeros(0, np.float32),
                 tc_lo=np.concatenate(los) if los else np.zeros(0, np.float32),
                 tc_off=tc_off, tc_npad=tc_npad, tc_child_col=tc_child_col,
-                tc_w=tc_w, tc_w_off=tc_w_off, tc_w_cols=max(wcols, 1))
+                tc_w=tc_w, tc_w_off=tc_w_off, tc_w_cols=max(wcols, 1), tc_tstride=cur)
 
 
 def pack_plan(model, tree, betas, with_tc: bool = True) -> dict:
@@ -194,7 +209,9 @@ def pack_plan(model, tree, betas, with_tc: bool = True) -> dict:
                node_nu_tail=node_nu_tail, grp_sqw=grp_sqw, mrank=mrank, mcol=mcol, moff=moff,
                mbasis=mbasis, mcols=mcols, shrink=shrink, gtail=gtail, blocks=bl)
     if with_tc:
-        out.update(tc_images(topo, comps, P, sqw_nodes))
+        tc = tc_images(topo, comps, P, sqw_nodes)
+        if tc is not None:  # (a positive sq_weight leaves tensor mode unavailable)
+            out.update(tc)
     # per-leaf path costs for the reference's counters (tree.py:413-427)
     out["path_evals"], out["path_mults"] = _path_costs(topo, rank, P)
     return out
@@ -265,7 +282,8 @@ class DevicePlan:
         d.model_cols_total = max(h["mcols"], 1)
         d.model_shrink = _c(arr("ms", h["shrink"], np.float64), C.c_double)
         d.model_gamma_tail = _c(arr("mg", h["gtail"], np.float64), C.c_double)
-        if with_tc and h["tc_hi"].size:
+        self.has_tc = bool(with_tc and "tc_hi" in h and h["tc_hi"].size)
+        if self.has_tc:
             d.grp_tc_hi = _c(arr("th", h["tc_hi"], np.float32), C.c_float)
             d.grp_tc_lo = _c(arr("tl", h["tc_lo"], np.float32), C.c_float)
             d.grp_tc_len = keep["th"].size

@@ -197,6 +197,9 @@ class Restorer:
             self.lam = float(lam)
         self.betas = beta_schedule(self.sigma, self.lam, config.beta_multipliers)
         self.plan = DevicePlan(model, tree, self.betas, with_tc=(mode == "tensor"))
+        # a model with a positive score weight has no pre-scaled tcgen05 images:
+        # its tree walk runs on the exact FP64 scorer (the same labels)
+        self._select_mode = self.MODES[mode] if (mode == "exact" or self.plan.has_tc) else 0
         dev = self.device
         # sampling plans: generated on the device (csrc/grid.cu), bitwise the
         # reference's numpy Philox draws (patches.py:102-132)
@@ -359,7 +362,7 @@ class Restorer:
         anchors, nr, nc, half = self._grids[t]
         n = self.n
         nt = B * n
-        mode = self.MODES[self.mode]
+        mode = self._select_mode
         self._mark(timer, "start")
         N.call("fepll_extract", N.ptr(self.x), B, H, W, side, N.ptr(anchors), n, nc,
                N.ptr(self.Z64), N.ptr(self.Z32), self.z32_pitch, N.ptr(self.dc), N.ptr(self.sq), st)
