@@ -437,10 +437,9 @@ int select_level_wide(Plan* p, const LevelArgs& a, const float* Z32, const doubl
 int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                      cudaStream_t st);
 // 0: select_ws.cu, 1: select_ws2.cu (deep staging, TMEM lo), 2: per level —
-// ws2 on levels of <= 16 nodes or whose nodes fit 96 columns (measured
-// faster there: three tiles of row loads in flight; 96-column levels get
-// four epilogue groups), ws on the remaining wide levels (its four 128-column
-// epilogue groups keep up with the larger child sets)
+// ws2 on levels of <= 16 nodes (measured faster there: three tiles of row
+// loads in flight; levels whose nodes fit 96 columns get its four-group
+// form), ws on the wider levels (measured faster at 32 and 64 nodes)
 int g_select_variant = 2;
 int select_level_ws(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                     cudaStream_t st);
@@ -526,8 +525,7 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
         rc = wide ? select_level_wide(p, a, Z32, sq, guard, st)
              : select_ws_supported(p, d)
                  ? ((g_select_variant == 1 ||
-                     (g_select_variant == 2 && (p->level_start[d + 1] - p->level_start[d] <= 16 ||
-                                                p->level_tc_npad[d] <= 96)))
+                     (g_select_variant == 2 && p->level_start[d + 1] - p->level_start[d] <= 16))
                         ? select_level_ws2(p, a, Z32, sq, guard, st)
                         : select_level_ws(p, a, Z32, sq, guard, st))
                  : select_level_tc(p, a, Z32, sq, guard, st);
