@@ -436,11 +436,10 @@ int select_level_wide(Plan* p, const LevelArgs& a, const float* Z32, const doubl
                       cudaStream_t st);
 int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                      cudaStream_t st);
-// 0: select_ws.cu, 1: select_ws2.cu (deep staging, TMEM lo), 2: per level —
-// ws2 on levels of <= 16 nodes (measured faster there: three tiles of row
-// loads in flight; levels whose nodes fit 96 columns get its four-group
-// form), ws on the wider levels (measured faster at 32 and 64 nodes)
-int g_select_variant = 2;
+// 0: select_ws.cu, 1: select_ws2.cu (deep staging, TMEM lo; measured faster
+// on every level of the cfg5 tree once both load whole 128-byte row atoms per
+// instruction), 2: ws2 on levels of <= 16 nodes, ws on the wider ones
+int g_select_variant = 1;
 int select_level_ws(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                     cudaStream_t st);
 

@@ -7,9 +7,10 @@
 //   warps 0-7    producers: warp w owns K atom w/4 of the tile's 128 FP32
 //                patch rows (kernel (a) output).  Row indices arrive several
 //                tiles early by cp.async into a smem ring, rows are prefetched
-//                into L2 and then into registers one tile ahead; each thread
-//                splits TF32 hi/lo and stores 128B-swizzled into one of two A
-//                stages.  (A TMA tile::gather4 producer was measured and
+//                into L2 and then into registers one tile ahead (each load
+//                instruction covers four whole 128-byte row atoms); each
+//                thread splits TF32 hi/lo and stores 128B-swizzled into one
+//                of two A stages.  (A TMA tile::gather4 producer was measured and
 //                rejected: ~62 cycles per 512-byte gather4, ~2.3 TB/s chip-wide,
 //                tools/tma_rate.cu — below this loop, and it needs the split
 //                rows materialized, doubling kernel (a)'s writes.)
@@ -120,15 +121,17 @@ __device__ __forceinline__ TileInfo tile_info(const LevelArgs& a, const WsLevelT
   return ti;
 }
 
-// K atom ka of patch g: 8 float4 into registers (zeros for g < 0)
-__device__ __forceinline__ void load_row(const Args& args, int g, int ka, float4 (&v)[8]) {
-  if (g >= 0) {
-    const float4* src = reinterpret_cast<const float4*>(args.Z32 + (int64_t)g * args.z32_pitch) + ka * 8;
+// K atom ka of the warp's 32 rows (ring entries rg[0..31]): lane L holds the
+// 16-byte chunk L & 7 of rows 4q + L / 8, q = 0..7, so each load instruction
+// covers four whole 128-byte row atoms (zeros for g < 0)
+__device__ __forceinline__ void load_rows(const Args& args, const int32_t* rg, int ka, int lane,
+                                          float4 (&v)[8]) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) v[c] = __ldg(src + c);
-  } else {
-#pragma unroll
-    for (int c = 0; c < 8; ++c) v[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int q = 0; q < 8; ++q) {
+    const int g = rg[4 * q + (lane >> 3)];
+    v[q] = g >= 0 ? __ldg(reinterpret_cast<const float4*>(args.Z32 + (int64_t)g * args.z32_pitch) +
+                          ka * 8 + (lane & 7))
+                  : make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
 
@@ -184,7 +187,6 @@ select_level_ws_kernel(PlanView pv, Args args) {
     const int row = tid & (kRows - 1);
     const int ka = warp >> 2;          // K atom of this warp
     const bool active = ka < args.katoms;
-    const int r8 = row & 7;
     // Row indices arrive kIdxAhead tiles early by cp.async into a per-thread
     // smem ring (no register dependency), row data one tile ahead in
     // registers.
@@ -205,29 +207,31 @@ select_level_ws_kernel(PlanView pv, Args args) {
     if (active) {
       for (int j = 0; j < kIdxAhead; ++j) fetch_idx(j);
       tc::cp_async_wait<0>();
+      __syncwarp();  // the other lanes' ring entries
       for (int j = 1; j < kL2Ahead && j < ntile; ++j) {
         const int gp = ring[(j % kIdxRing) * kRows + row];
         if (gp >= 0) tc::prefetch_l2(args.Z32 + (int64_t)gp * args.z32_pitch + ka * 32);
       }
-      load_row(args, ntile > 0 ? ring[row] : -1, ka, v);
+      if (ntile > 0) load_rows(args, ring + 32 * (warp & 3), ka, lane, v);
     }
     for (int i = 0; i < ntile; ++i) {
       const int st = i % kStages;
       if (i >= kStages) tc::mbar_wait(&s.a_empty[st], ((i / kStages) - 1) & 1);
       if (tid == 0) stamp(args, i, 0);
       if (active) {
-        uint8_t* A = stageA + st * kStageBytes;
-        uint8_t* dhi = A + (2 * ka) * kAtomA + (row >> 3) * 1024 + r8 * 128;
-        uint8_t* dlo = A + (2 * ka + 1) * kAtomA + (row >> 3) * 1024 + r8 * 128;
+        uint8_t* A = stageA + st * kStageBytes + (warp & 3) * 4096;
+        const int c = lane & 7;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int q = 0; q < 8; ++q) {
+          const int r = 4 * q + (lane >> 3);  // row inside the warp's 32
+          const int o = (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4);
           float4 h, l;
-          h.x = tc::to_tf32(v[c].x); l.x = v[c].x - h.x;
-          h.y = tc::to_tf32(v[c].y); l.y = v[c].y - h.y;
-          h.z = tc::to_tf32(v[c].z); l.z = v[c].z - h.z;
-          h.w = tc::to_tf32(v[c].w); l.w = v[c].w - h.w;
-          *reinterpret_cast<float4*>(dhi + ((c ^ r8) << 4)) = h;
-          *reinterpret_cast<float4*>(dlo + ((c ^ r8) << 4)) = l;
+          h.x = tc::to_tf32(v[q].x); l.x = v[q].x - h.x;
+          h.y = tc::to_tf32(v[q].y); l.y = v[q].y - h.y;
+          h.z = tc::to_tf32(v[q].z); l.z = v[q].z - h.z;
+          h.w = tc::to_tf32(v[q].w); l.w = v[q].w - h.w;
+          *reinterpret_cast<float4*>(A + (2 * ka) * kAtomA + o) = h;
+          *reinterpret_cast<float4*>(A + (2 * ka + 1) * kAtomA + o) = l;
         }
         tc::fence_proxy_async_smem();
       }
@@ -238,11 +242,12 @@ select_level_ws_kernel(PlanView pv, Args args) {
       if (active && i + 1 < ntile) {
         fetch_idx(i + kIdxAhead);
         tc::cp_async_wait<kIdxAhead - kL2Ahead>();  // indices through tile i+kL2Ahead landed
+        __syncwarp();
         if (i + kL2Ahead < ntile) {
           const int gp = ring[((i + kL2Ahead) % kIdxRing) * kRows + row];
           if (gp >= 0) tc::prefetch_l2(args.Z32 + (int64_t)gp * args.z32_pitch + ka * 32);
         }
-        load_row(args, ring[((i + 1) % kIdxRing) * kRows + row], ka, v);
+        load_rows(args, ring + ((i + 1) % kIdxRing) * kRows + 32 * (warp & 3), ka, lane, v);
       }
     }
   } else if (warp == kMmaWarp) {

@@ -191,18 +191,23 @@ select_level_ws2_kernel(PlanView pv, Args args) {
         else *dst = -1;
       }
     };
-    auto issue_raw = [&](int j) {  // raw row chunk of tile j -> stage j % kStages
+    // raw K atom of the warp's 32 rows of tile j -> stage j % kStages.  Each
+    // instruction moves four whole 128-byte row atoms (lanes 8r..8r+7: the
+    // 16-byte chunks of one row), so every request is a full line; the
+    // indices come from the ring entries other lanes fetched (landed and
+    // made warp-visible by the wait + __syncwarp of an earlier iteration).
+    const int c16 = lane & 7;
+    auto issue_raw = [&](int j) {
       if (j < ntile && active) {
-        const int g = ring[(j % kIdxRing) * kRows + row];
-        uint8_t* dst = stageA + (j % kStages) * kStageBytes + ka * kAtomA + (row >> 3) * 1024 + r8 * 128;
-        if (g >= 0) {
-          const float* src = args.Z32 + (int64_t)g * args.z32_pitch + ka * 32;
+        const int* rg = ring + (j % kIdxRing) * kRows + 32 * (warp & 3);
+        uint8_t* stg = stageA + (j % kStages) * kStageBytes + ka * kAtomA + (warp & 3) * 4096;
 #pragma unroll
-          for (int c = 0; c < 8; ++c) tc::cp_async16(dst + ((c ^ r8) << 4), src + 4 * c);
-        } else {
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            *reinterpret_cast<float4*>(dst + ((c ^ r8) << 4)) = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = 0; q < 8; ++q) {
+          const int r = 4 * q + (lane >> 3);  // row inside the warp's 32
+          const int g = rg[r];
+          uint8_t* dst = stg + (r >> 3) * 1024 + (r & 7) * 128 + ((c16 ^ (r & 7)) << 4);
+          if (g >= 0) tc::cp_async16(dst, args.Z32 + (int64_t)g * args.z32_pitch + ka * 32 + 4 * c16);
+          else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
     };
@@ -211,6 +216,7 @@ select_level_ws2_kernel(PlanView pv, Args args) {
     for (int j = 0; j < kIdxAhead; ++j) issue_idx(j);
     tc::cp_async_commit();
     tc::cp_async_wait<0>();
+    __syncwarp();
     for (int j = 0; j < kRawAhead; ++j) {
       issue_raw(j);
       tc::cp_async_commit();
@@ -220,6 +226,7 @@ select_level_ws2_kernel(PlanView pv, Args args) {
     for (int i = 0; i < ntile; ++i) {
       const int st = i % kStages, lb = i % kLoBufs;
       tc::cp_async_wait<kRawAhead - 1>();  // raw(i) (and idx through i + kIdxAhead - kRawAhead) landed
+      __syncwarp();                         // ... including the lanes' parts of this thread's row
       if (tid == 0) stamp(args, i, 0);
       // lo = z - trunc(z) of this row's K atom -> TMEM lo buffer lb
       if (i >= kLoBufs) tc::mbar_wait(&s.lo_empty[lb], ((i / kLoBufs) - 1) & 1);

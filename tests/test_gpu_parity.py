@@ -150,6 +150,34 @@ def test_same_seed_bit_identical_and_batch_equals_single(models):
         assert np.array_equal(xb[i], singles[i])
 
 
+def test_select_kernel_variants_agree(models):
+    """Both tensor-core level kernels (select_ws.cu, select_ws2.cu) and the
+    per-level hybrid route every patch identically, and equal the FP64 path."""
+    import ctypes
+    from paper_1710_08124_b200 import RestorationConfig, _native as N, restore_batch, synthetic
+
+    model, tree = models[64]
+    cases = [synthetic.baseline_case("cfg5", 192, image_seed=i, noise_seed=40 + i) for i in range(3)]
+    ys = np.stack([c.y for c in cases])
+    cfg = RestorationConfig(sigma=25.0, spacing=4, seed=9, trace=True)
+    f = N.lib().fepll_debug_select_variant
+    f.argtypes = [ctypes.c_int32]
+    outs = []
+    try:
+        for v in (0, 1, 2):
+            f(v)
+            outs.append(restore_batch(ys, cases[0].A, model, tree, cfg, mode="tensor"))
+    finally:
+        f(1)
+    xe, se = restore_batch(ys, cases[0].A, model, tree, cfg, mode="exact")
+    for x, st in outs:
+        np.testing.assert_array_equal(x, outs[0][0])
+        assert len(st.trace) == len(se.trace) == 5
+        for a, b in zip(st.trace, se.trace):
+            np.testing.assert_array_equal(a["labels"], b["labels"])
+        assert rmse255(x, xe) <= 1e-9
+
+
 @pytest.mark.parametrize("H,W,s", [(41, 53, 3), (40, 40, 8), (33, 47, 1), (8, 8, 6)])
 def test_edge_geometries_vs_oracle(H, W, s, models):
     """Odd sizes, spacing == side (no jitter), spacing 1, a single anchor."""
