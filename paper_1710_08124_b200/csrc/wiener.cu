@@ -219,16 +219,18 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
     if (j >= t_end) return;
     const int32_t* rows = h.rows[(j - t_begin) % kRing];
     double* Zs = Zs0 + ((j - t_begin) % NS) * kRows * geo.zld;
-    // two threads per row, alternate 16-byte chunks (P even)
-    const int i = tid >> 1;
-    const int g = rows[i];
-    double* drow = Zs + i * geo.zld;
-    for (int c = tid & 1; c < P / 2; c += 2) {
+    // consecutive threads take consecutive 16-byte chunks of a row (P even),
+    // so each instruction reads whole lines of one or two rows
+    const int C = P / 2;
+    for (int e = tid; e < kRows * C; e += kThreads) {
+      const int i = e / C, c = e - i * C;
+      const int g = rows[i];
+      double* d = Zs + i * geo.zld + 2 * c;
       if (g >= 0) {
-        cp_async16(drow + 2 * c, Z64 + (int64_t)g * P + 2 * c);
+        cp_async16(d, Z64 + (int64_t)g * P + 2 * c);
       } else {
-        drow[2 * c] = 0.0;
-        drow[2 * c + 1] = 0.0;
+        d[0] = 0.0;
+        d[1] = 0.0;
       }
     }
   };
