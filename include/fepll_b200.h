@@ -63,6 +63,9 @@ typedef struct fepll_plan_desc {
   const float* grp_tc_w;        /* [T][grp_tc_w_cols] FP32 column weights (0 on padding) */
   const int32_t* grp_tc_w_off;  /* [n_nodes] first weight column of a node's image */
   int32_t grp_tc_w_cols;
+  /* bf16 [lo | hi] images of the mixed-precision scorer, same layout and
+   * length as grp_tc_hi (may be NULL: the level kernel then uses 3xTF32) */
+  const float* grp_tc_x;
 } fepll_plan_desc;
 
 int fepll_abi_version(void);

@@ -35,6 +35,7 @@ class PlanDesc(C.Structure):
         ("grp_tc_off", P_i64), ("grp_tc_npad", P_i32),
         ("grp_tc_child_col", P_i32), ("grp_tc_w", P_f32), ("grp_tc_w_off", P_i32),
         ("grp_tc_w_cols", i32),
+        ("grp_tc_x", P_f32),
     ]
 
 

@@ -132,6 +132,7 @@ static int create(const fepll_plan_desc* d, Plan** out) {
   if (d->grp_tc_hi && d->grp_tc_lo && d->grp_tc_len > 0) {
     UP(d->grp_tc_hi, d->grp_tc_len, v.tc_hi);
     UP(d->grp_tc_lo, d->grp_tc_len, v.tc_lo);
+    if (d->grp_tc_x) UP(d->grp_tc_x, d->grp_tc_len, v.tc_x);
     UP(d->grp_tc_off, n, v.tc_off);
     UP(d->grp_tc_npad, n, v.tc_npad);
     UP(d->grp_tc_child_col, n, v.tc_child_col);

@@ -35,6 +35,7 @@ struct PlanView {
   const double* model_gamma_tail;
   const float* tc_hi;
   const float* tc_lo;
+  const float* tc_x;    // bf16 [lo | hi] cross-pass images (NULL if absent)
   const int64_t* tc_off;
   const int32_t* tc_npad;
   const int32_t* tc_child_col;

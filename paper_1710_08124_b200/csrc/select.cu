@@ -201,7 +201,7 @@ select_level_fp64_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __
 
 // exact FP64 re-scoring of decisions the tensor-core epilogue could not
 // certify: queue entries are (patch, node) pairs of level d.
-__global__ void __launch_bounds__(kSelWarps * 32)
+__global__ void __launch_bounds__(kSelWarps * 32, 4)
 rescore_fp64_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restrict__ sq,
                     const int32_t* __restrict__ queue, const int32_t* __restrict__ queue_len) {
   // The level kernel already published the next level's segment offsets in
@@ -436,9 +436,9 @@ int select_level_wide(Plan* p, const LevelArgs& a, const float* Z32, const doubl
                       cudaStream_t st);
 int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                      cudaStream_t st);
-// 0: select_ws.cu, 1: select_ws2.cu (deep staging, TMEM lo; measured faster
-// on every level of the cfg5 tree once both load whole 128-byte row atoms per
-// instruction), 2: ws2 on levels of <= 16 nodes, ws on the wider ones
+// 0: select_ws.cu (3xTF32), 1: select_ws2.cu (tf32 + bf16 cross pass, split
+// loader / converter warps; measured faster on every level of the cfg5
+// tree), 2: ws2 on levels of <= 16 nodes, ws on the wider ones
 int g_select_variant = 1;
 int select_level_ws(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                     cudaStream_t st);
@@ -452,7 +452,7 @@ static int side_of(int P) {
 int rescore_queue_x(Plan* p, const LevelArgs& a, const double* x, const int32_t* anchors, int n_img,
                     int H, int W, const double* dc, const double* sq, cudaStream_t st) {
   PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P)};
-  rescore_fp64_kernel<<<2 * kSMs, kSelWarps * 32, 0, st>>>(p->v, a, ps, sq, p->rs.queue,
+  rescore_fp64_kernel<<<4 * kSMs, kSelWarps * 32, 0, st>>>(p->v, a, ps, sq, p->rs.queue,
                                                            p->rs.queue_len);
   FEPLL_LAUNCH();
   return kOk;
@@ -523,8 +523,9 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
         const bool wide = p->level_wide[d] || p->level_tc_npad[d] > 256;
         rc = wide ? select_level_wide(p, a, Z32, sq, guard, st)
              : select_ws_supported(p, d)
-                 ? ((g_select_variant == 1 ||
-                     (g_select_variant == 2 && p->level_start[d + 1] - p->level_start[d] <= 16))
+                 ? ((p->v.tc_x != nullptr &&
+                     (g_select_variant == 1 ||
+                      (g_select_variant == 2 && p->level_start[d + 1] - p->level_start[d] <= 16)))
                         ? select_level_ws2(p, a, Z32, sq, guard, st)
                         : select_level_ws(p, a, Z32, sq, guard, st))
                  : select_level_tc(p, a, Z32, sq, guard, st);

@@ -88,14 +88,14 @@ struct Args {
   int32_t* queue;
   int32_t* queue_len;
   int katoms;
-  uint64_t* trace;       // debug timeline: [CTA][64 tiles][8] clock64 stamps (or NULL)
+  uint64_t* trace;       // debug timeline: [CTA][64 tiles][16] clock64 stamps (or NULL)
 };
 
 __device__ __forceinline__ void stamp(const Args& a, int i, int slot) {
   if (a.trace && i < 64) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));  // SM cycles (per-CTA relative timing)
-    a.trace[((size_t)blockIdx.x * 64 + i) * 8 + slot] = t;
+    a.trace[((size_t)blockIdx.x * 64 + i) * 16 + slot] = t;
   }
 }
 

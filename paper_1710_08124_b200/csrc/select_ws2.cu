@@ -7,18 +7,31 @@
 //
 //   * tcgen05 kind::tf32 reads only the top 19 bits of an FP32 operand
 //     (truncation, tools/tf32_trunc_test.cu), so the raw FP32 patch row is
-//     the hi operand as is.  Rows land by cp.async in one of four 32 KB
-//     raw stages — three tiles of loads in flight, no register staging;
-//   * only lo = z - trunc(z) is computed (per producer thread: one 128-byte
-//     K atom of one row) and written to tensor memory with tcgen05.st; the
-//     lo x B_hi pass takes its A operand from TMEM (two 64-column lo
-//     buffers), hi x B_hi and hi x B_lo read the raw stage;
-//   * three 128-column TMEM accumulators / epilogue groups (512 columns in
-//     all with the lo buffers).
+//     the hi operand as is.  Two loader warps pull the rows by cp.async
+//     (every instruction moves four whole 128-byte row atoms) into one of
+//     four 32 KB raw stages and signal the stage's mbarrier when the copies
+//     land (cp.async.mbarrier.arrive) — three tiles of loads in flight, no
+//     register staging, no loader waiting on anything but a free stage;
+//   * the score is z . b = z_hi . b_hi + (z_hi . b_lo + z_lo . b_hi) with
+//     z_hi = trunc_tf32(z) (what kind::tf32 reads from the raw stage), b_hi
+//     = rne_tf32(b): the main term is one kind::tf32 pass (A = raw stage),
+//     the two small cross terms one kind::f16 pass in bf16 with K doubled —
+//     A' = [bf16(z_hi) | bf16(z_lo)] against B' = [bf16(b_lo) | bf16(b_hi)]
+//     (plan.py bf16_cross_image).  A bf16 MMA of K = 16 costs what a tf32
+//     MMA of K = 8 does, so the pair costs 2 tf32 passes instead of 3xTF32's
+//     three, and the cross pass reads only B from shared memory;
+//   * eight converter warps build A' (per thread: one 128-byte K atom of one
+//     row) and write it to tensor memory with tcgen05.st (two 64-column
+//     buffers);
+//   * NG accumulators of ACC columns / epilogue groups (512 TMEM columns in
+//     all with the A' buffers).
 //
-// Error budget of the split (tc_epi.cuh): |lo| < 2^-10 |z|, its TF32
-// truncation error < 2^-20 |z|; with B's RNE split and the FP32 accumulation
-// the projection stays within the 2^-18 ||z|| the guard assumes.
+// Error budget (per element, |z_lo| < 2^-10 |z|, |b_lo| <= 2^-11 |b|, bf16
+// rounding <= 2^-9 relative): z_hi b_lo in bf16 <= 2^-19 |z||b|, z_lo b_hi
+// in bf16 <= 2^-18 |z||b|, the dropped z_lo b_lo <= 2^-21 |z||b|, FP32
+// accumulation over 16 MMAs <= 2^-19: in all < 2^-17 ||z|| ||b|| by
+// Cauchy-Schwarz — twice the 3xTF32 projection bound of tc_epi.cuh, so this
+// kernel certifies with twice the guard (2^-15 by default).
 #include <algorithm>
 
 #include "route.cuh"
@@ -29,13 +42,16 @@ namespace fepll {
 
 namespace ws2 {
 constexpr int kRows = 128;
-constexpr int kProducerWarps = 8;       // warp w: K atom w/4, TMEM lane quarter w%4
-constexpr int kMmaWarp = 8;
-constexpr int kEpiWarp0 = 9;
+constexpr int kLoaderWarps = 2;         // warp w: rows 64w .. 64w+63, both K atoms
+constexpr int kLoaderThreads = 32 * kLoaderWarps;
+constexpr int kConvWarp0 = 2;           // warps 2..9: K atom (w-2)/4, TMEM lane quarter w%4
+constexpr int kConvWarps = 8;
+constexpr int kMmaWarp = 10;
+constexpr int kEpiWarp0 = 11;
 // epilogue groups (== TMEM accumulators) and accumulator width are template
 // parameters: <3, 128> for levels with nodes up to 128 padded columns,
 // <4, 96> where every node fits 96 (four groups keep up with the MMAs)
-constexpr int threads_for(int ng) { return (9 + 4 * ng) * 32; }
+constexpr int threads_for(int ng) { return (kEpiWarp0 + 4 * ng) * 32; }
 constexpr int kStages = 4;              // raw row stages (hi operand)
 constexpr int kLoBufs = 2;              // TMEM lo buffers
 constexpr int kAtomA = kRows * 128;     // bytes of one K atom of A
@@ -59,19 +75,20 @@ struct EpiGroup {
 constexpr int kMaxNodes = 128;  // internal nodes per level handled by this kernel
 using WsLevelTables = LevelTablesN<256>;  // next level <= 256 nodes
 
-constexpr int kIdxAhead = 8;   // tiles of row indices in flight (>= 2 * kStages)
-constexpr int kIdxRing = 9;
-constexpr int kRawAhead = kStages - 1;  // raw loads issued this many tiles ahead
+constexpr int kIdxAhead = 6;   // tiles of row indices in flight ahead of their rows
+constexpr int kIdxRing = kIdxAhead + 1;
 
 template <int NG>
 struct Smem {
-  int32_t idx_ring[2][kIdxRing][kRows];  // [K atom][slot][row]
+  int32_t idx_ring[kIdxRing][kRows];     // [slot][row]
   WsLevelTables lv;
   int64_t nd_off[kMaxNodes];      // segment offset of each depth-d node (a.off)
   int16_t nd_npad[kMaxNodes];     // padded group width
   int16_t nd_nk[kMaxNodes];       // child count
   EpiGroup epi[NG];
-  uint64_t raw_empty[kStages], lo_full[kLoBufs], lo_empty[kLoBufs];
+  // mma_done[i % kStages]: tile i's MMAs finished — frees its raw stage and
+  // its lo buffer (kLoBufs divides kStages)
+  uint64_t raw_full[kStages], mma_done[kStages], lo_full[kLoBufs];
   uint64_t acc_full[NG], acc_empty[NG];
   uint64_t b_full, drain;
   uint32_t tmem_base;
@@ -87,14 +104,14 @@ struct Args {
   int32_t* queue;
   int32_t* queue_len;
   int katoms;
-  uint64_t* trace;       // debug timeline: [CTA][64 tiles][8] clock64 stamps (or NULL)
+  uint64_t* trace;       // debug timeline: [CTA][64 tiles][16] clock64 stamps (or NULL)
 };
 
 __device__ __forceinline__ void stamp(const Args& a, int i, int slot) {
   if (a.trace && i < 64) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));  // SM cycles (per-CTA relative timing)
-    a.trace[((size_t)blockIdx.x * 64 + i) * 8 + slot] = t;
+    a.trace[((size_t)blockIdx.x * 64 + i) * 16 + slot] = t;
   }
 }
 
@@ -110,23 +127,33 @@ struct TileInfo {
   int k, u, first, m;
 };
 
-// tile -> (level-local node k, BFS id u, first row, rows): smem only
-__device__ __forceinline__ TileInfo tile_info(const LevelArgs& a, const WsLevelTables& lv, int tile) {
-  TileInfo ti;
-  ti.k = prefix_find(lv.tpre, a.lvl_end - a.lvl_begin, tile);
-  ti.u = a.lvl_begin + ti.k;
-  ti.first = (tile - lv.tpre[ti.k]) * kRows;
-  ti.m = min(kRows, (lv.cpre[ti.k + 1] - lv.cpre[ti.k]) - ti.first);
-  return ti;
-}
+// tile -> (level-local node k, BFS id u, first row, rows): smem only.  Every
+// role walks its tiles in increasing order, so the node index advances
+// instead of being searched for (the MMA warp's per-tile bookkeeping sits
+// between its MMA batches, where the tensor pipe would idle).
+struct TileCursor {
+  int k = -1;
+  __device__ __forceinline__ TileInfo at(const LevelArgs& a, const WsLevelTables& lv, int tile) {
+    const int n = a.lvl_end - a.lvl_begin;
+    if (k < 0) k = prefix_find(lv.tpre, n, tile);
+    while (k + 1 < n && lv.tpre[k + 1] <= tile) ++k;
+    TileInfo ti;
+    ti.k = k;
+    ti.u = a.lvl_begin + k;
+    ti.first = (tile - lv.tpre[k]) * kRows;
+    ti.m = min(kRows, (lv.cpre[k + 1] - lv.cpre[k]) - ti.first);
+    return ti;
+  }
+};
 
 template <int NG, int ACC>
 __global__ void __launch_bounds__(threads_for(NG), 1)
 select_level_ws2_kernel(PlanView pv, Args args) {
   constexpr int kGroups = NG;
   constexpr int kAcc = ACC;                          // accumulator columns (>= node width)
-  constexpr uint32_t kLoCol0 = NG * ACC;             // TMEM column of lo buffer 0
-  static_assert(NG * ACC + kLoBufs * 64 <= 512, "TMEM: accumulators + lo buffers");
+  constexpr uint32_t kXCol0 = NG * ACC;              // TMEM column of A' buffer 0
+  static_assert(NG * ACC + kLoBufs * 64 <= 512, "TMEM: accumulators + A' buffers");
+  static_assert(kStages % kLoBufs == 0, "mma_done serves both rings");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = tc::align1024(smem_raw);
   uint8_t* stageA = base;
@@ -139,10 +166,12 @@ select_level_ws2_kernel(PlanView pv, Args args) {
 
   if (warp == kMmaWarp) tc::tmem_alloc(&s.tmem_base, kTmemCols);
   if (tid == 0) {
-    for (int i = 0; i < kStages; ++i) tc::mbar_init(&s.raw_empty[i], 1);
+    for (int i = 0; i < kStages; ++i) {
+      tc::mbar_init(&s.raw_full[i], kLoaderThreads);
+      tc::mbar_init(&s.mma_done[i], 1);
+    }
     for (int i = 0; i < kLoBufs; ++i) {
-      tc::mbar_init(&s.lo_full[i], kProducerWarps);
-      tc::mbar_init(&s.lo_empty[i], 1);
+      tc::mbar_init(&s.lo_full[i], kConvWarps);
     }
     for (int i = 0; i < kGroups; ++i) {
       tc::mbar_init(&s.acc_full[i], 1);
@@ -173,90 +202,108 @@ select_level_ws2_kernel(PlanView pv, Args args) {
   const int ntile = t_end - t_begin;
   const int t = a.t;
 
-  if (warp < kProducerWarps) {
-    // ------------------------------------------------------------ producers
-    // thread = one 128-byte K atom of one row; warp w: atom w/4, TMEM lane
-    // quarter w%4 (rows 32*(w%4) .. +31)
-    const int row = tid & (kRows - 1);
-    const int ka = warp >> 2;
-    const bool active = ka < args.katoms;
-    const int r8 = row & 7;
-    const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
-    int32_t* ring = s.idx_ring[ka][0];
-    auto issue_idx = [&](int j) {  // patch index of this row of tile j -> ring
+  if (warp < kLoaderWarps) {
+    // ------------------------------------------------------------ loaders
+    // Row indices arrive kIdxAhead tiles early (cp.async into the ring, one
+    // commit group per tile); each lane then issues 32 cp.async of 16 bytes
+    // (the warp's 64 rows x 2 K atoms, four whole row atoms per instruction)
+    // and arrives on raw_full once they land.
+    const int r0 = 64 * warp;
+    TileCursor cur_idx;
+    auto issue_idx = [&](int j) {
       if (j < ntile) {
-        const TileInfo ti = tile_info(a, s.lv, t_begin + j);
-        int32_t* dst = ring + (j % kIdxRing) * kRows + row;
-        if (row < ti.m) tc::cp_async4(dst, a.seg_in + s.nd_off[ti.k] + ti.first + row);
-        else *dst = -1;
-      }
-    };
-    // raw K atom of the warp's 32 rows of tile j -> stage j % kStages.  Each
-    // instruction moves four whole 128-byte row atoms (lanes 8r..8r+7: the
-    // 16-byte chunks of one row), so every request is a full line; the
-    // indices come from the ring entries other lanes fetched (landed and
-    // made warp-visible by the wait + __syncwarp of an earlier iteration).
-    const int c16 = lane & 7;
-    auto issue_raw = [&](int j) {
-      if (j < ntile && active) {
-        const int* rg = ring + (j % kIdxRing) * kRows + 32 * (warp & 3);
-        uint8_t* stg = stageA + (j % kStages) * kStageBytes + ka * kAtomA + (warp & 3) * 4096;
+        const TileInfo ti = cur_idx.at(a, s.lv, t_begin + j);
+        int32_t* ring = s.idx_ring[j % kIdxRing];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int r = 4 * q + (lane >> 3);  // row inside the warp's 32
-          const int g = rg[r];
-          uint8_t* dst = stg + (r >> 3) * 1024 + (r & 7) * 128 + ((c16 ^ (r & 7)) << 4);
-          if (g >= 0) tc::cp_async16(dst, args.Z32 + (int64_t)g * args.z32_pitch + ka * 32 + 4 * c16);
-          else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int h = 0; h < 2; ++h) {
+          const int row = r0 + 32 * h + lane;
+          if (row < ti.m) tc::cp_async4(ring + row, a.seg_in + s.nd_off[ti.k] + ti.first + row);
+          else ring[row] = -1;
         }
       }
     };
-    // prologue: indices of the first kIdxAhead tiles (one group, waited),
-    // then raw rows of tiles 0 .. kRawAhead-1 (one group each)
-    for (int j = 0; j < kIdxAhead; ++j) issue_idx(j);
-    tc::cp_async_commit();
-    tc::cp_async_wait<0>();
-    __syncwarp();
-    for (int j = 0; j < kRawAhead; ++j) {
-      issue_raw(j);
+    const int c16 = lane & 7;
+    const int64_t pitch = args.z32_pitch;
+    for (int j = 0; j < kIdxAhead; ++j) {
+      issue_idx(j);
       tc::cp_async_commit();
     }
-    // iteration i commits one group {idx(i + kIdxAhead), raw(i + kRawAhead)};
-    // raw(i) then always has exactly kRawAhead - 1 younger groups
+    for (int i = 0; i < ntile; ++i) {
+      const int st = i % kStages;
+      if (i >= kStages) tc::mbar_wait(&s.mma_done[st], ((i / kStages) - 1) & 1);
+      if (tid == 0) stamp(args, i, 8);
+      tc::cp_async_wait<kIdxAhead - 1>();  // idx(i) landed (one group per tile)
+      __syncwarp();                         // ... including the other lanes' entries
+      const int32_t* rg = s.idx_ring[i % kIdxRing] + r0;
+      int g[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) g[q] = rg[4 * q + (lane >> 3)];
+      uint8_t* stg = stageA + st * kStageBytes + (r0 >> 3) * 1024;
+#pragma unroll
+      for (int ka = 0; ka < kMaxKAtoms; ++ka) {
+        if (ka < args.katoms) {
+          const float* zb = args.Z32 + ka * 32 + 4 * c16;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int r = 4 * q + (lane >> 3);  // row inside the warp's 64
+            uint8_t* dst = stg + ka * kAtomA + (r >> 3) * 1024 + (r & 7) * 128 + ((c16 ^ (r & 7)) << 4);
+            // rows past the tile's end land as zeros (no bytes read)
+            tc::cp_async16_zfill(dst, g[q] >= 0 ? zb + g[q] * pitch : args.Z32, g[q] >= 0 ? 16u : 0u);
+          }
+        }
+      }
+      issue_idx(i + kIdxAhead);
+      tc::cp_async_commit();
+      tc::cp_async_mbar_arrive(&s.raw_full[st]);
+      if (tid == 0) stamp(args, i, 7);
+    }
+    tc::cp_async_wait<0>();
+  } else if (warp < kConvWarp0 + kConvWarps) {
+    // ------------------------------------------------------------ converters
+    // thread = one 128-byte K atom of one row; TMEM lane quarter = warp % 4
+    const int cw = warp - kConvWarp0;
+    const int ka = cw >> 2;
+    const int quarter = warp & 3;
+    const int row = 32 * quarter + lane;
+    const bool active = ka < args.katoms;
+    const int r8 = row & 7;
+    const uint32_t lane_off = (uint32_t)(32 * quarter) << 16;
     for (int i = 0; i < ntile; ++i) {
       const int st = i % kStages, lb = i % kLoBufs;
-      tc::cp_async_wait<kRawAhead - 1>();  // raw(i) (and idx through i + kIdxAhead - kRawAhead) landed
-      __syncwarp();                         // ... including the lanes' parts of this thread's row
-      if (tid == 0) stamp(args, i, 0);
-      // lo = z - trunc(z) of this row's K atom -> TMEM lo buffer lb
-      if (i >= kLoBufs) tc::mbar_wait(&s.lo_empty[lb], ((i / kLoBufs) - 1) & 1);
+      tc::mbar_wait(&s.raw_full[st], (i / kStages) & 1);
+      if (cw == 0 && lane == 0) stamp(args, i, 0);
+      if (i >= kLoBufs) {  // tile i - kLoBufs's MMAs have read lo buffer lb
+        const int j = i - kLoBufs;
+        tc::mbar_wait(&s.mma_done[j % kStages], (j / kStages) & 1);
+      }
       tc::fence_after_sync();
       if (active) {
         const uint8_t* src = stageA + st * kStageBytes + ka * kAtomA + (row >> 3) * 1024 + r8 * 128;
-        uint32_t lo[32];
+        uint32_t xh[16], xl[16];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const float4 x = *reinterpret_cast<const float4*>(src + ((c ^ r8) << 4));
-          lo[4 * c + 0] = __float_as_uint(x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u));
-          lo[4 * c + 1] = __float_as_uint(x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u));
-          lo[4 * c + 2] = __float_as_uint(x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u));
-          lo[4 * c + 3] = __float_as_uint(x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u));
+          const float h0 = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+          const float h1 = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+          const float h2 = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+          const float h3 = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+          xh[2 * c] = tc::pack_bf16x2(h0, h1);
+          xh[2 * c + 1] = tc::pack_bf16x2(h2, h3);
+          xl[2 * c] = tc::pack_bf16x2(x.x - h0, x.y - h1);  // exact differences
+          xl[2 * c + 1] = tc::pack_bf16x2(x.z - h2, x.w - h3);
         }
-        tc::tmem_st32(tmem + lane_off + kLoCol0 + lb * 64 + ka * 32, lo);
+        // A' columns: bf16(z_hi) pairs of atom ka at 16 ka, bf16(z_lo) at
+        // 16 (katoms + ka)
+        const uint32_t xb = tmem + lane_off + kXCol0 + lb * 64;
+        tc::tmem_st16(xb + 16 * ka, xh);
+        tc::tmem_st16(xb + 16 * (args.katoms + ka), xl);
         tc::tmem_st_wait();
       }
-      tc::fence_proxy_async_smem();  // the raw stage (cp.async writes) for the MMAs
+      tc::fence_proxy_async_smem();  // the landed raw stage, for the MMAs' async-proxy reads
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s.lo_full[lb]);
-      if (tid == 0) stamp(args, i, 1);
-      // refill: tile i + kRawAhead into the stage tile i - 1 used
-      const int nx = i + kRawAhead;
-      if (nx < ntile && nx >= kStages)
-        tc::mbar_wait(&s.raw_empty[nx % kStages], ((nx / kStages) - 1) & 1);
-      issue_idx(i + kIdxAhead);
-      issue_raw(nx);
-      tc::cp_async_commit();
+      if (cw == 0 && lane == 0) stamp(args, i, 1);
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
@@ -264,12 +311,13 @@ select_level_ws2_kernel(PlanView pv, Args args) {
     // issues each tcgen05 instruction (tc.cuh *_warp).
     int cur = -1;
     uint32_t b_loads = 0, drains = 0;
+    TileCursor tcur;
     const uint64_t a_base = tc::desc_sw128(tc::smem_u32(stageA));
     const uint64_t b_base = tc::desc_sw128(tc::smem_u32(bbuf));
     for (int i = 0; i < ntile; ++i) {
       const int st = i % kStages;
       const int ac = i % kGroups;
-      const TileInfo ti = tile_info(a, s.lv, t_begin + i);
+      const TileInfo ti = tcur.at(a, s.lv, t_begin + i);
       const int npad = s.nd_npad[ti.k];
       const uint32_t bhalf = (uint32_t)args.katoms * npad * 128u;
       if (ti.u != cur) {
@@ -282,45 +330,55 @@ select_level_ws2_kernel(PlanView pv, Args args) {
           tc::mbar_arrive_expect_tx(&s.b_full, 2 * bhalf);
           const int64_t boff = (int64_t)t * pv.tc_tstride + pv.tc_off[ti.u];
           tc::bulk_g2s(bbuf, pv.tc_hi + boff, bhalf, &s.b_full);
-          tc::bulk_g2s(bbuf + bhalf, pv.tc_lo + boff, bhalf, &s.b_full);
+          tc::bulk_g2s(bbuf + bhalf, pv.tc_x + boff, bhalf, &s.b_full);
         }
         __syncwarp();
         tc::mbar_wait(&s.b_full, b_loads & 1);
         ++b_loads;
         cur = ti.u;
       }
+      if (lane == 0) stamp(args, i, 10);
       if (i >= kGroups) tc::mbar_wait(&s.acc_empty[ac], ((i / kGroups) - 1) & 1);
-
-      const int lb = i % kLoBufs;
-      tc::mbar_wait(&s.lo_full[lb], (i / kLoBufs) & 1);
+      if (lane == 0) stamp(args, i, 9);
+      const uint32_t d = tmem + ac * kAcc;
+      // main term: z_hi . b_hi, A = the raw stage (cp.async writes: proxy
+      // fence after observing them land)
+      tc::mbar_wait(&s.raw_full[st], (i / kStages) & 1);
       tc::fence_after_sync();
+      tc::fence_proxy_async_smem();
       if (lane == 0) stamp(args, i, 2);
       const uint32_t idesc = tc::idesc_tf32(kRows, npad);
-      const uint32_t d = tmem + ac * kAcc;
       // descriptor start-address field counts 16-byte units
       const uint64_t A0 = a_base + (uint64_t)((st * kStageBytes) >> 4);
       for (int kq = 0; kq < args.katoms; ++kq) {
-        const uint64_t a_hi = A0 + (uint64_t)((kq * kAtomA) >> 4);   // raw rows
-        const uint32_t a_lo = tmem + kLoCol0 + lb * 64 + kq * 32;     // TMEM lo
+        const uint64_t a_hi = A0 + (uint64_t)((kq * kAtomA) >> 4);
         const uint64_t b_hi = b_base + (uint64_t)((kq * npad * 128) >> 4);
-        const uint64_t b_lo = b_base + (uint64_t)((bhalf + kq * npad * 128) >> 4);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
           const uint64_t ko = 2 * kk;  // 8 tf32 = 32 bytes inside the swizzle atom
-          const uint32_t acc = (kq > 0 || kk > 0) ? 1u : 0u;
-          tc::mma_tf32_tmemA_warp(d, a_lo + 8 * kk, b_hi + ko, idesc, acc);
-          tc::mma_tf32_warp(d, a_hi + ko, b_lo + ko, idesc, 1u);
-          tc::mma_tf32_warp(d, a_hi + ko, b_hi + ko, idesc, 1u);
+          tc::mma_tf32_warp(d, a_hi + ko, b_hi + ko, idesc, (kq > 0 || kk > 0) ? 1u : 0u);
         }
       }
-      tc::mma_commit_warp(&s.raw_empty[st]);
-      tc::mma_commit_warp(&s.lo_empty[lb]);
+      // cross terms: A' (TMEM, bf16 pairs) . B' (bf16, K = 2 Ppad)
+      const int lb = i % kLoBufs;
+      tc::mbar_wait(&s.lo_full[lb], (i / kLoBufs) & 1);
+      tc::fence_after_sync();
+      const uint32_t idesc16 = tc::idesc_bf16(kRows, npad);
+      const uint32_t a_x = tmem + kXCol0 + lb * 64;
+      const uint64_t b_x = b_base + (uint64_t)(bhalf >> 4);
+      for (int kq = 0; kq < args.katoms; ++kq) {  // B' atom kq: 64 bf16 of K
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)             // K = 16 = 32 bytes per MMA
+          tc::mma_bf16_tmemA_warp(d, a_x + 32 * kq + 8 * kk,
+                                  b_x + (uint64_t)((kq * npad * 128 + 32 * kk) >> 4), idesc16, 1u);
+      }
+      tc::mma_commit_warp(&s.mma_done[st]);
       tc::mma_commit_warp(&s.acc_full[ac]);
       if (lane == 0) stamp(args, i, 3);
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - kEpiWarp0;       // 0..11
+    const int ew = warp - kEpiWarp0;       // 0 .. 4 NG - 1
     const int grp = ew >> 2;               // tiles with i % kGroups == grp
     const int row = 32 * (warp & 3) + lane;
     const uint32_t d_acc = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + grp * kAcc;
@@ -349,9 +407,10 @@ select_level_ws2_kernel(PlanView pv, Args args) {
         a.labels[p_g] = p_leaf;
       }
     };
+    TileCursor tcur;
     for (int i = grp; i < ntile; i += kGroups, ++it) {
       const int cb = it % 3, pb = (it + 2) % 3, nb = (it + 1) % 3;
-      const TileInfo ti = tile_info(a, s.lv, t_begin + i);
+      const TileInfo ti = tcur.at(a, s.lv, t_begin + i);
       const int u = ti.u;
       const int nk = s.nd_nk[ti.k];
       const bool valid = row < ti.m;
@@ -436,7 +495,8 @@ int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double
   args.Z32 = Z32;
   args.z32_pitch = (p->v.P + 31) / 32 * 32;
   args.sq = sq;
-  args.guard = guard > 0 ? guard : kDefaultGuard;
+  // the mixed-precision projection error is twice 3xTF32's (header)
+  args.guard = 2.0 * (guard > 0 ? guard : kDefaultGuard);
   args.queue = p->rs.queue;
   args.queue_len = p->rs.queue_len;
   args.katoms = (p->v.P + 31) / 32;

@@ -48,6 +48,23 @@ def tf32_split(a: np.ndarray):
     return hi, lo
 
 
+def bf16_rne(a: np.ndarray) -> np.ndarray:
+    """FP32 -> bfloat16 bit patterns (uint16), round to nearest even."""
+    bits = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    return ((bits + 0x7FFF + ((bits >> 16) & 1)) >> 16).astype(np.uint16)
+
+
+def bf16_cross_image(hi: np.ndarray, lo: np.ndarray) -> np.ndarray:
+    """B operand of the bf16 cross pass: rows x (2 Ppad) bfloat16 K-major
+    [bf16(lo) | bf16(hi)] (it meets A = [bf16(z_hi) | bf16(z_lo)], so the
+    pass adds z_hi . b_lo + z_lo . b_hi), packed two per 32-bit word (lower K
+    in the low half) and 128B-swizzled like the FP32 images — same bytes."""
+    rows, Ppad = hi.shape
+    x = np.concatenate([bf16_rne(lo), bf16_rne(hi)], axis=1).astype(np.uint32)  # (rows, 2 Ppad)
+    words = (x[:, 0::2] | (x[:, 1::2] << 16)).astype(np.uint32)                   # (rows, Ppad)
+    return swizzle128_kmajor(words.view(np.float32))
+
+
 def swizzle128_kmajor(mat: np.ndarray) -> np.ndarray:
     """Rows x 64-float (256 B) K-major matrix -> the byte image tcgen05
     expects for SWIZZLE_128B K-major operands: K split in 32-float (128 B)
@@ -78,7 +95,8 @@ def tc_images(topo, comps, P: int, sqw_per_node: list):
     (npad_u, P_pad) K-major — child v occupying rows
     [tc_child_col[v], tc_child_col[v] + r_v), every child padded to a multiple
     of 16 rows so each child starts on a 16-column TMEM chunk — then TF32
-    hi/lo split and 128B-swizzled.  The scorer's epilogue then needs only
+    hi/lo split and 128B-swizzled (``tc_x``: the bf16 [lo | hi] image of the
+    mixed-precision scorer, select_ws2.cu).  The scorer's epilogue then needs only
     -sum_j c'_j^2 per child (c' = z . B'), no per-column weights.  Images are
     laid out [T][nodes]; ``tc_off`` is the offset within one iteration's
     block.  ``sqw_per_node[t][v]`` (FP64 vectors) also become the FP32
@@ -115,7 +133,7 @@ def tc_images(topo, comps, P: int, sqw_per_node: list):
             for v in kids:
                 if np.any(np.asarray(sqw_per_node[t][v]) > 0):
                     return None
-    his, los = [], []
+    his, los, xs = [], [], []
     for t in range(T):
         for u, kids in groups:
             Bt = np.zeros((tc_npad[u], Ppad), dtype=np.float64)
@@ -125,8 +143,11 @@ def tc_images(topo, comps, P: int, sqw_per_node: list):
                 Bt[tc_child_col[v]:tc_child_col[v] + r, :P] = (np.asarray(comps[v].kept_basis)
                                                                * scale[None, :]).T
             hi, lo = tf32_split(Bt.astype(np.float32))
-            his.append(swizzle128_kmajor(hi.reshape(tc_npad[u], Ppad)))
-            los.append(swizzle128_kmajor(lo.reshape(tc_npad[u], Ppad)))
+            hi = hi.reshape(tc_npad[u], Ppad)
+            lo = lo.reshape(tc_npad[u], Ppad)
+            his.append(swizzle128_kmajor(hi))
+            los.append(swizzle128_kmajor(lo))
+            xs.append(bf16_cross_image(hi, lo))
     tc_w = np.zeros((T, max(wcols, 1)), np.float32)
     for t in range(T):
         for u, kids in groups:
@@ -136,6 +157,7 @@ def tc_images(topo, comps, P: int, sqw_per_node: list):
                 tc_w[t, a0:a0 + w.size] = w.astype(np.float32)
     return dict(tc_hi=np.concatenate(his) if his else np.zeros(0, np.float32),
                 tc_lo=np.concatenate(los) if los else np.zeros(0, np.float32),
+                tc_x=np.concatenate(xs) if xs else np.zeros(0, np.float32),
                 tc_off=tc_off, tc_npad=tc_npad, tc_child_col=tc_child_col,
                 tc_w=tc_w, tc_w_off=tc_w_off, tc_w_cols=max(wcols, 1), tc_tstride=cur)
 
@@ -293,6 +315,7 @@ class DevicePlan:
             d.grp_tc_w = _c(arr("tw", h["tc_w"], np.float32), C.c_float)
             d.grp_tc_w_off = _c(arr("two", h["tc_w_off"], np.int32), C.c_int32)
             d.grp_tc_w_cols = int(h["tc_w_cols"])
+            d.grp_tc_x = _c(arr("tx", h["tc_x"], np.float32), C.c_float)
         handle = C.c_void_p()
         N.call("fepll_plan_create", C.byref(d), C.byref(handle))
         self.handle = handle
