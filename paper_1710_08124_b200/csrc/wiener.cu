@@ -23,7 +23,7 @@ namespace wn {
 // debug timeline (fepll_debug_wiener_trace): [CTA][64 tiles][8] clock64
 __device__ uint64_t* g_trace = nullptr;
 __device__ __forceinline__ void wstamp(int i, int slot) {
-  if (g_trace && i < 64 && threadIdx.x == 0) {
+  if (g_trace && i < 64 && threadIdx.x == 0 && blockIdx.x < 148) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
     g_trace[((size_t)blockIdx.x * 64 + i) * 8 + slot] = t;
@@ -98,32 +98,38 @@ __device__ __forceinline__ void cp_async_wait_group() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Row strides (in doubles): A-side tiles (lane (g, t) reads row g, col t)
-// use ld = 4 mod 16 — conflict-free; B-side tiles (row t, col g) use
-// ld = 8 mod 16, which costs a 2-way conflict on half the fragment loads but
-// keeps P = 100 within shared memory (ld = 4 measured no faster at P = 64).
+// Row strides (in doubles) are 4 mod 16: a lane (g, t) fragment load of
+// row g, col t (A side) or of row t, col g (phase 1's B side, Us[p][j]) and
+// phase 2's B side read straight from Us (row 8n + g, col k + t) all hit 16
+// distinct 8-byte banks per half-warp — one basis copy serves both phases.
 struct Geo {
   int P, Pn;     // P, P rounded up to 8 (phase-1 K, phase-2 N)
   int zld;       // Zs [MT][zld], columns P..Pn-1 zero
   int R8;        // rank rounded up to 8
-  int uld;       // Us [Pn][uld]  (phase-1 B: k = p, n = j)
-  int utld;      // UT [R8][utld] (phase-2 B: k = j, n = p)
-  int cld;       // Cs [64][cld]
+  int uld;       // Us [Pn][uld]  (phase-1 B: k = p, n = j; phase-2 B: k = j, n = p)
 };
 
 // NT2: phase-2 n-tiles (P/8 rounded up): 8 for P=64, 13 for P=100.
 // MT rows per tile, NS row buffers (NS - 1 tiles of rows in flight).
-// phase 1 of one warp's 16 rows: C = (Z . U) * shrink for NT1 n-tiles of 8
-// rank columns; za / zb: this lane's A rows (g, g + 8) at column t; cw: the
-// warp's Cs rows
-template <int NT2, int NT1>
-__device__ __forceinline__ void phase1(const double* za, const double* zb, const double* Us, int uld,
-                                       double* cw, int cld, const double* sh, int t4, int g4) {
+// One warp's 16 rows, NT1 = rank n-tiles of 8 (compile time: predicated-off
+// DMMAs would still occupy the pipe):
+//   phase 1: C = (Z . U) * shrink, accumulators in registers;
+//   phase 2: acc2 = C . U^T, its A fragments taken from phase 1's
+//            accumulators by quad shuffles (no shared-memory round trip).
+// za / zb: this lane's A rows (g, g + 8) at column t.  step(s), s = 0 ..
+// NT2-1, runs before phase-1 k-step s: the caller issues the next tile's row
+// copies there, so their issue shares the SM with the DMMAs instead of
+// preceding them.
+template <int NT2, int NT1, class Step>
+__device__ __forceinline__ void wiener_rows(const double* za, const double* zb, const double* Us, int uld,
+                                            const double* sh, int t4, int g4, Step&& step,
+                                            double (&acc2)[NT2][4]) {
   double acc[NT1][4];
 #pragma unroll
   for (int n = 0; n < NT1; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0;
 #pragma unroll
   for (int k0 = 0; k0 < NT2 * 8; k0 += 8) {  // NT2 * 8 == Pn
+    step(k0 / 8);
     const double a0 = za[k0], a1 = zb[k0], a2 = za[k0 + 4], a3 = zb[k0 + 4];
     const double* u0 = Us + (k0 + t4) * uld + g4;
     const double* u1 = u0 + 4 * uld;
@@ -146,15 +152,53 @@ __device__ __forceinline__ void phase1(const double* za, const double* zb, const
       dmma8(acc[n][2], acc[n][3], a3, b1[n]);
     }
   }
+  // C = acc * shrink: lane (g, t) holds C[g][8n + 2t + e] (acc[n][e]) and
+  // C[g + 8][8n + 2t + e] (acc[n][2 + e])
 #pragma unroll
   for (int n = 0; n < NT1; ++n) {
     const int col = n * 8 + 2 * t4;
-    double* c0 = cw + col;
-    double* c1 = c0 + 8 * cld;
-    c0[0] = acc[n][0] * sh[col];
-    c0[1] = acc[n][1] * sh[col + 1];
-    c1[0] = acc[n][2] * sh[col];
-    c1[1] = acc[n][3] * sh[col + 1];
+    acc[n][0] *= sh[col];
+    acc[n][1] *= sh[col + 1];
+    acc[n][2] *= sh[col];
+    acc[n][3] *= sh[col + 1];
+  }
+#pragma unroll
+  for (int n = 0; n < NT2; ++n) acc2[n][0] = acc2[n][1] = acc2[n][2] = acc2[n][3] = 0.0;
+  // phase-2 A fragment of k-tile kb: a = {C[g][8kb + t], C[g+8][8kb + t],
+  // C[g][8kb + 4 + t], C[g+8][8kb + 4 + t]}; column 8kb + c sits in lane
+  // (g, c / 2), element c % 2
+  const int q0 = (g4 << 2) | (t4 >> 1), q1 = q0 + 2;
+  const bool odd = t4 & 1;
+#pragma unroll
+  for (int kb = 0; kb < NT1; ++kb) {
+    double a[4];
+    {
+      const double e0 = __shfl_sync(0xffffffffu, acc[kb][0], q0), e1 = __shfl_sync(0xffffffffu, acc[kb][1], q0);
+      const double f0 = __shfl_sync(0xffffffffu, acc[kb][2], q0), f1 = __shfl_sync(0xffffffffu, acc[kb][3], q0);
+      const double h0 = __shfl_sync(0xffffffffu, acc[kb][0], q1), h1 = __shfl_sync(0xffffffffu, acc[kb][1], q1);
+      const double j0 = __shfl_sync(0xffffffffu, acc[kb][2], q1), j1 = __shfl_sync(0xffffffffu, acc[kb][3], q1);
+      a[0] = odd ? e1 : e0;
+      a[1] = odd ? f1 : f0;
+      a[2] = odd ? h1 : h0;
+      a[3] = odd ? j1 : j0;
+    }
+    const double* u0 = Us + g4 * uld + 8 * kb + t4;  // U[8n + g][k + t] = U^T[k][n]
+    double b0[NT2], b1[NT2];
+#pragma unroll
+    for (int n = 0; n < NT2; ++n) {
+      b0[n] = u0[n * 8 * uld];
+      b1[n] = u0[n * 8 * uld + 4];
+    }
+#pragma unroll
+    for (int n = 0; n < NT2; ++n) {
+      dmma8(acc2[n][0], acc2[n][1], a[0], b0[n]);
+      dmma8(acc2[n][2], acc2[n][3], a[1], b0[n]);
+    }
+#pragma unroll
+    for (int n = 0; n < NT2; ++n) {
+      dmma8(acc2[n][0], acc2[n][1], a[2], b1[n]);
+      dmma8(acc2[n][2], acc2[n][3], a[3], b1[n]);
+    }
   }
 }
 
@@ -172,9 +216,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
   constexpr int kLead = 2 * NS - 2;  // tiles of indices fetched ahead of their rows' issue
   double* Zs0 = reinterpret_cast<double*>(smem + ((sizeof(Head) + 127) & ~size_t(127)));
   double* Us = Zs0 + NS * kRows * geo.zld;     // [Pn][uld]   (p, j)
-  double* UT = Us + geo.Pn * geo.uld;          // [R8][utld]  (j, p)
-  double* Cs = UT + geo.R8 * geo.utld;         // [64][cld]
-  double* sh = Cs + kRows * geo.cld;           // [R8]
+  double* sh = Us + geo.Pn * geo.uld;          // [R8]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int P = geo.P;
   // K padding columns of the row buffers stay zero (cp.async fills [0, P))
@@ -215,14 +257,18 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
         *dst = -1;
     }
   };
-  auto fetch_z = [&](int j) {
+  // consecutive threads take consecutive 16-byte chunks of a row (P even),
+  // so each instruction reads whole lines of one or two rows; slice s of a
+  // tile's copy is e in [s kThreads, (s + 1) kThreads)
+  const int C = P / 2;
+  const int n_slices = (kRows * C + kThreads - 1) / kThreads;
+  constexpr int kWarps = kThreads / 32;
+  constexpr bool kInterleave = NT2 == 8;  // P = 64 layout below: 16 slices, 8 k-steps
+  auto fetch_z_slices = [&](int j, int s0, int s1) {
     if (j >= t_end) return;
     const int32_t* rows = h.rows[(j - t_begin) % kRing];
     double* Zs = Zs0 + ((j - t_begin) % NS) * kRows * geo.zld;
-    // consecutive threads take consecutive 16-byte chunks of a row (P even),
-    // so each instruction reads whole lines of one or two rows
-    const int C = P / 2;
-    for (int e = tid; e < kRows * C; e += kThreads) {
+    for (int e = tid + s0 * kThreads; e < min(s1 * kThreads, kRows * C); e += kThreads) {
       const int i = e / C, c = e - i * C;
       const int g = rows[i];
       double* d = Zs + i * geo.zld + 2 * c;
@@ -241,7 +287,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
   cp_async_wait_all();
   __syncthreads();
   for (int j = 0; j < NS - 1; ++j) {
-    fetch_z(t_begin + j);
+    fetch_z_slices(t_begin + j, 0, n_slices);
     cp_async_commit();
   }
   for (int tile = t_begin; tile < t_end; ++tile) {
@@ -255,16 +301,13 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
     cp_async_wait_group<NS - 2>();
     __syncthreads();  // this tile's rows landed; the buffer refilled next is free
     wstamp(i, 1);
-    fetch_z(tile + NS - 1);
-    fetch_rows(tile + kLead);
-    cp_async_commit();
+    fetch_rows(tile + kLead);  // committed with the row copies below (one group per tile)
     if (comp != cur_leaf) {
       const double* U = pv.model_basis + pv.model_off64[comp];
       for (int e = tid; e < geo.Pn * geo.R8; e += kThreads) {
         const int p = e / geo.R8, j = e - p * geo.R8;
         const double u = (p < P && j < r) ? U[(int64_t)p * r + j] : 0.0;
         Us[p * geo.uld + j] = u;
-        UT[j * geo.utld + p] = u;
       }
       const double* shrink = pv.model_shrink + (int64_t)t * pv.model_cols_total + pv.model_col_off[comp];
       for (int j = tid; j < geo.R8; j += kThreads) sh[j] = j < r ? shrink[j] : 0.0;
@@ -280,49 +323,49 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
     // ---- phase 1: C[m0..m0+15][0..R8) = (Z . U) * shrink, with the
     // leaf's n-tile count as a compile-time constant (predicated-off DMMAs
     // would still occupy the pipe)
-    switch ((r + 7) / 8) {
-      case 1: phase1<NT2, 1>(za, zb, Us, geo.uld, Cs + (m0 + g4) * geo.cld, geo.cld, sh, t4, g4); break;
-      case 2: phase1<NT2, 2>(za, zb, Us, geo.uld, Cs + (m0 + g4) * geo.cld, geo.cld, sh, t4, g4); break;
-      case 3: phase1<NT2, 3>(za, zb, Us, geo.uld, Cs + (m0 + g4) * geo.cld, geo.cld, sh, t4, g4); break;
-      case 4: phase1<NT2, 4>(za, zb, Us, geo.uld, Cs + (m0 + g4) * geo.cld, geo.cld, sh, t4, g4); break;
-      case 5: phase1<NT2, 5>(za, zb, Us, geo.uld, Cs + (m0 + g4) * geo.cld, geo.cld, sh, t4, g4); break;
-      case 6: phase1<NT2, 6>(za, zb, Us, geo.uld, Cs + (m0 + g4) * geo.cld, geo.cld, sh, t4, g4); break;
-      case 7: phase1<NT2, 7>(za, zb, Us, geo.uld, Cs + (m0 + g4) * geo.cld, geo.cld, sh, t4, g4); break;
-      default: phase1<NT2, 8>(za, zb, Us, geo.uld, Cs + (m0 + g4) * geo.cld, geo.cld, sh, t4, g4); break;
+    // The next tile's row copies.  P = 64: thread (w, l) copies chunk l of
+    // rows w + kWarps s, s = 0..15, two per phase-1 k-step, with
+    // the patch indices read up front (an index load feeding each copy would
+    // stall the warp's in-order DMMA issue behind it); other shapes issue
+    // the whole copy here.
+    const int jn = tile + NS - 1;
+    const bool inter = kInterleave && P == 64 && jn < t_end;
+    int gsl[16];
+    double* zn = Zs0 + ((jn - t_begin) % NS) * kRows * geo.zld + 2 * lane;
+    if (inter) {
+      const int32_t* rn = h.rows[(jn - t_begin) % kRing];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) gsl[q] = rn[warp + kWarps * q];
+    } else {
+      fetch_z_slices(jn, 0, n_slices);
     }
-    __syncwarp();  // each warp only reads its own rows of Cs
-    const int nt1 = (r + 7) / 8;
-    wstamp(i, 3);
-    // ---- phase 2: Zhat[m0..m0+15][0..P) = C . U^T + gamma_tail Z
-    {
-      double acc[NT2][4];
+    auto zstep = [&](int st) {
+      if (!inter) return;
 #pragma unroll
-      for (int n = 0; n < NT2; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0;
-      const double* ca = Cs + (m0 + g4) * geo.cld + t4;
-      const double* cb = ca + 8 * geo.cld;
-#pragma unroll
-      for (int k0 = 0; k0 < kMaxR; k0 += 8) {
-        if (k0 >= nt1 * 8) break;
-        const double a[4] = {ca[k0], cb[k0], ca[k0 + 4], cb[k0 + 4]};
-        const double* u0 = UT + (k0 + t4) * geo.utld + g4;
-        const double* u1 = u0 + 4 * geo.utld;
-        double b0[NT2], b1[NT2];
-#pragma unroll
-        for (int n = 0; n < NT2; ++n) {
-          b0[n] = u0[n * 8];
-          b1[n] = u1[n * 8];
-        }
-#pragma unroll
-        for (int n = 0; n < NT2; ++n) {
-          dmma8(acc[n][0], acc[n][1], a[0], b0[n]);
-          dmma8(acc[n][2], acc[n][3], a[1], b0[n]);
-        }
-#pragma unroll
-        for (int n = 0; n < NT2; ++n) {
-          dmma8(acc[n][0], acc[n][1], a[2], b1[n]);
-          dmma8(acc[n][2], acc[n][3], a[3], b1[n]);
+      for (int q = 2 * st; q < 2 * st + 2; ++q) {
+        double* d = zn + (warp + kWarps * q) * geo.zld;
+        if (gsl[q] >= 0) {
+          cp_async16(d, Z64 + (int64_t)gsl[q] * 64 + 2 * lane);
+        } else {
+          d[0] = 0.0;
+          d[1] = 0.0;
         }
       }
+    };
+    double acc[NT2][4];
+    switch ((r + 7) / 8) {
+      case 1: wiener_rows<NT2, 1>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 2: wiener_rows<NT2, 2>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 3: wiener_rows<NT2, 3>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 4: wiener_rows<NT2, 4>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 5: wiener_rows<NT2, 5>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 6: wiener_rows<NT2, 6>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 7: wiener_rows<NT2, 7>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      default: wiener_rows<NT2, 8>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+    }
+    cp_async_commit();
+    wstamp(i, 3);
+    {
       wstamp(i, 4);
       const double gt = pv.model_gamma_tail[(int64_t)t * pv.K + comp];
       // Zhat = acc + gamma_tail z, written over this warp's own rows of Zs
@@ -342,7 +385,8 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       }
       // ... then each of the warp's 16 rows leaves as one TMA bulk store
       // (smem -> global, 8P bytes); the buffer is reused only after the
-      // stores have read it (wait_group.read before the next tile's barrier)
+      // stores have read it (wait_group.read before the next tile's barrier;
+      // coalesced 16-byte stores from the same rows measured slower)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane < 16) {
@@ -358,6 +402,8 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
 
 }  // namespace wn
 
+int g_wiener_pair = 1;
+
 int wiener_dmma(Plan* p, int t, const double* Z64, double* Zhat, cudaStream_t st) {
   const int P = p->v.P;
   wn::Geo geo;
@@ -366,13 +412,11 @@ int wiener_dmma(Plan* p, int t, const double* Z64, double* Zhat, cudaStream_t st
   auto ld = [](int n, int rem) { int v = n; while (v % 16 != rem) ++v; return v; };
   geo.zld = ld(geo.Pn, 4);
   geo.R8 = (p->max_model_rank + 7) / 8 * 8;
-  geo.uld = ld(geo.R8, 8);
-  geo.utld = ld(geo.Pn, 8);
-  geo.cld = ld(geo.R8, 4);
+  geo.uld = ld(geo.R8, 4);
   auto smem_for = [&](int mt, int ns) {
     return ((sizeof(wn::Head) + 127) & ~size_t(127)) +
            sizeof(double) * (ns * (size_t)mt * geo.zld + (size_t)geo.Pn * geo.uld +
-                             (size_t)geo.R8 * geo.utld + (size_t)mt * geo.cld + geo.R8);
+                             geo.R8);
   };
   // 128-row tiles (16 warps) once the average leaf bucket is large enough
   // that the extra padding rows do not matter, and the tile fits in smem
@@ -381,9 +425,15 @@ int wiener_dmma(Plan* p, int t, const double* Z64, double* Zhat, cudaStream_t st
   FEPLL_CUDA(cudaGetDevice(&dev));
   FEPLL_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const size_t cap = (size_t)optin;
-  const bool big = n_total >= (int64_t)1024 * std::max(1, p->n_leaf_nodes) && smem_for(128, 2) <= cap;
+  // 64-row tiles, two CTAs per SM (one CTA's loads, barriers and stores
+  // overlap the other's DMMAs) when two fit in shared memory; else 128-row
+  // tiles when the buckets are large, else 64-row tiles with deeper staging
+  int per_sm_cap = 0;
+  FEPLL_CUDA(cudaDeviceGetAttribute(&per_sm_cap, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+  const bool pair = g_wiener_pair && 2 * (smem_for(64, 2) + 1024) <= (size_t)per_sm_cap;
+  const bool big = !pair && n_total >= (int64_t)1024 * std::max(1, p->n_leaf_nodes) && smem_for(128, 2) <= cap;
   const int mt = big ? 128 : 64;
-  const int ns = big ? 2 : (smem_for(64, 4) <= cap ? 4 : 2);
+  const int ns = big || pair ? 2 : (smem_for(64, 4) <= cap ? 4 : 2);
   FEPLL_REQUIRE(smem_for(mt, ns) <= cap, "wiener: tile buffers exceed shared memory");
   const size_t smem = smem_for(mt, ns);
   const int nt2 = geo.Pn / 8;
@@ -428,6 +478,11 @@ bool wiener_dmma_supported(const Plan* p) {
 }
 
 }  // namespace fepll
+
+extern "C" int fepll_debug_wiener_pair(int32_t on) {
+  fepll::g_wiener_pair = on;
+  return 0;
+}
 
 extern "C" int fepll_debug_wiener_trace(void* device_buffer) {
   uint64_t* p = static_cast<uint64_t*>(device_buffer);
