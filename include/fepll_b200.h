@@ -129,13 +129,16 @@ int fepll_select_rescored(fepll_plan_t plan, int32_t* dst, void* stream);
 /* gmm.py:352-359 / solver.py:233-241: FP64 Wiener estimates of the patches
  * under their labels, grouped by label (the leaf buckets of the last select).
  * With Z64 (the FP64 patch rows of fepll_extract) it runs on the FP64 tensor
- * cores (DMMA); otherwise it re-extracts the patches from x. */
+ * cores (DMMA); otherwise it re-extracts the patches from x.  Zhat receives
+ * est + dc (patches.py:198-222's reprojection values), ready for
+ * fepll_aggregate* with dc == NULL. */
 int fepll_wiener(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32_t W,
                  const int32_t* anchors, int32_t n_img, const double* dc, const double* Z64,
                  int64_t n_total, double* Zhat, void* stream);
 
 /* patches.py:198-222 (+ operators.py:284-287 when kind==0):
- * per-pixel ordered gather of (Zhat + dc) over covering anchors.
+ * per-pixel ordered gather of (Zhat + dc) over covering anchors; dc may be
+ * NULL when Zhat already holds est + dc (fepll_wiener's output).
  * grid geometry: n_rows x n_cols nominal anchors, spacing, half, side.
  * kind 0: x = (aty + bs2*xt) / (diag + bs2)  (pixel-diagonal update fused)
  * kind 1: rhs = aty + bs2*xt (FFT/CG kinds).  Outputs may be NULL. */

@@ -1,7 +1,8 @@
 // Kernel (d) + fused pixel-diagonal kernel (e).
 //
 // Aggregation restates pkg/src/fepll/patches.py:198-222: x~(p) = sum over
-// covering patches of (zhat + dc) / count, with the lo == hi rule returning
+// covering patches of (zhat + dc) / count (dc == NULL: the Wiener kernels
+// already wrote zhat + dc, rounded exactly as here), with the lo == hi rule returning
 // the common value verbatim.  np.bincount accumulates each pixel's values in
 // increasing patch index; this kernel gathers, per pixel, the candidate
 // anchors of the nominal grid in the same (row-major) order, so the FP64
@@ -104,7 +105,8 @@ aggregate_kernel(const double* __restrict__ Zhat, const double* __restrict__ dc,
   int count = 0;
   for_each_cover(geo, geo.row0 + r_loc, c, [&](int i, int dr, int dcol) {
     const int64_t g = gbase + i;
-    const double v = __dadd_rn(Zhat[g * P + dr * geo.side + dcol], dc[g]);
+    const double z = Zhat[g * P + dr * geo.side + dcol];
+    const double v = dc ? __dadd_rn(z, dc[g]) : z;  // dc == NULL: Zhat holds est + dc
     sum += v;
     lo = fmin(lo, v);
     hi = fmax(hi, v);
@@ -193,84 +195,106 @@ __global__ void scan_apply_kernel(const int32_t* __restrict__ counts, int64_t n,
   if (i == n - 1) ptr[n] = bsum[blockIdx.x] + tmp[threadIdx.x];
 }
 
-// Gather over the cover list.  A block owns 256 pixels of one row for the
-// whole batch: their cover entries are staged in shared memory once (the
-// plan is the batch's), then every image's Zhat / dc loads issue straight
-// from them — one dependent global round trip per pixel and image, two
-// images in flight per thread.  Per image the operations are exactly
-// aggregate_kernel's.
+// Gather over the cover list.  A thread owns one pixel for a group of the
+// batch's images (blockIdx.z): the pixel's cover entries (the plan is the
+// batch's) are decoded once into element offsets held in registers, then
+// each image costs its Zhat loads, the ordered sum and the pixel update —
+// the gather is issue-bound, so the per-image instruction count is what is
+// minimised.  Per image the result is aggregate_kernel's:
+//  * the sum runs over the entries in ascending patch order from 0.0;
+//  * lo == hi (patches.py:221) is "every value equals the first" (NaN
+//    compares unequal, so a NaN still reaches the sum);
+//  * sum / count for a power-of-two count is the exact product with 1/count.
 constexpr int kCoverThreads = 256;
-constexpr int kCoverMaxEntries = 16;  // per pixel, staged (more: read from global)
+constexpr int kCoverRegEntries = 9;   // entries decoded into registers (more: generic loop)
+constexpr int kCoverImgPerBlock = 16; // images per block (blockIdx.z groups)
 
+__device__ __forceinline__ void pixel_update(double xt, int64_t pix, const double* aty,
+                                             const double* diag, double bs2, int kind,
+                                             double* x_out, double* xt_out, int32_t* status) {
+  if (xt_out) xt_out[pix] = xt;
+  const double at = aty ? aty[pix] : 0.0;
+  const double rhs = __dadd_rn(at, __dmul_rn(bs2, xt));
+  if (kind == 0) {
+    const double dg = diag ? diag[pix] : 1.0;
+    const double x = __ddiv_rn(rhs, __dadd_rn(dg, bs2));
+    if (!isfinite(x)) atomicOr(status, 2);
+    if (x_out) x_out[pix] = x;
+  } else if (x_out) {
+    x_out[pix] = rhs;
+  }
+}
+
+template <bool kDc>
 __global__ void __launch_bounds__(kCoverThreads)
 aggregate_cover_kernel(const double* __restrict__ Zhat, const double* __restrict__ dc,
                        const int32_t* __restrict__ ptr, const int32_t* __restrict__ entries, int P,
                        int n_local, int batch, int H, int W, int r_begin,
                        const double* __restrict__ aty, const double* __restrict__ diag, double bs2,
                        int kind, double* __restrict__ x_out, double* __restrict__ xt_out,
-                       int32_t* status) {
-  __shared__ int32_t s_ent[kCoverThreads * kCoverMaxEntries];
-  __shared__ int32_t s_ptr[kCoverThreads + 1];
-  const int c0 = blockIdx.x * kCoverThreads;
-  const int c = c0 + threadIdx.x;
-  const int r_loc = r_begin + blockIdx.y;
-  const int64_t p0 = (int64_t)blockIdx.y * W + c0;
-  const int npx = min(kCoverThreads, W - c0);
-  if (threadIdx.x < npx) s_ptr[threadIdx.x] = __ldg(ptr + p0 + threadIdx.x);
-  if (threadIdx.x == 0) s_ptr[npx] = __ldg(ptr + p0 + npx);
-  __syncthreads();
-  const int base = s_ptr[0];
-  const int span = s_ptr[npx] - base;
-  const bool staged = span <= kCoverThreads * kCoverMaxEntries;
-  if (staged)
-    for (int k = threadIdx.x; k < span; k += kCoverThreads) s_ent[k] = __ldg(entries + base + k);
-  __syncthreads();
+                       int32_t* status, int ipb) {
+  const int c = blockIdx.x * kCoverThreads + threadIdx.x;
   if (c >= W) return;
-  const int e0 = s_ptr[threadIdx.x] - base, e1 = s_ptr[threadIdx.x + 1] - base;
-  const int32_t* ent = entries + base;
-  auto entry = [&](int e) {
-    int v;
-    if (staged)
-      v = s_ent[e];
-    else
-      v = ent[e];  // (a plain load: a select between the two address spaces must stay generic)
-    return v;
-  };
-  const int64_t pix0 = (int64_t)r_loc * W + c;
+  const int64_t p = (int64_t)blockIdx.y * W + c;  // pixel within the cover rows
+  const int e0 = __ldg(ptr + p), cnt = __ldg(ptr + p + 1) - e0;
+  const int64_t pix0 = (int64_t)(r_begin + blockIdx.y) * W + c;
   const int64_t img = (int64_t)H * W;
-  for (int b = 0; b < batch; b += 2) {
-    const bool two = b + 1 < batch;
-    double sum[2] = {0.0, 0.0}, lo[2] = {INFINITY, INFINITY}, hi[2] = {-INFINITY, -INFINITY};
-    for (int e = e0; e < e1; e += 4) {
-      double z[2][4], d[2][4];
+  const int64_t zimg = (int64_t)n_local * P;  // Zhat elements per image
+  const int b_begin = blockIdx.z * ipb;
+  const int b_end = min(batch, b_begin + ipb);
+  if (cnt == 0) {
+    atomicOr(status, 1);
+    for (int b = b_begin; b < b_end; ++b)
+      pixel_update(0.0, b * img + pix0, aty, diag, bs2, kind, x_out, xt_out, status);
+    return;
+  }
+  const bool pow2 = (cnt & (cnt - 1)) == 0;
+  const double inv = 1.0 / (double)cnt;  // exact when pow2
+  if (cnt <= kCoverRegEntries) {
+    int off[kCoverRegEntries];
+    int dco[kCoverRegEntries];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (e + q < e1) {
-          const int v = entry(e + q);
-#pragma unroll
-          for (int bb = 0; bb < 2; ++bb)
-            if (bb == 0 || two) {
-              const int64_t g = (int64_t)(b + bb) * n_local + (v >> 8);
-              z[bb][q] = __ldg(Zhat + g * P + (v & 255));
-              d[bb][q] = __ldg(dc + g);
-            }
-        }
-#pragma unroll
-      for (int bb = 0; bb < 2; ++bb)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if ((bb == 0 || two) && e + q < e1) {
-            const double v = __dadd_rn(z[bb][q], d[bb][q]);
-            sum[bb] += v;
-            lo[bb] = fmin(lo[bb], v);
-            hi[bb] = fmax(hi[bb], v);
-          }
+    for (int q = 0; q < kCoverRegEntries; ++q) {
+      const int v = q < cnt ? __ldg(entries + e0 + q) : 0;
+      off[q] = (v >> 8) * P + (v & 255);
+      dco[q] = v >> 8;
     }
-    finish_pixel(sum[0], lo[0], hi[0], e1 - e0, b * img + pix0, aty, diag, bs2, kind, x_out, xt_out,
-                 status);
-    if (two)
-      finish_pixel(sum[1], lo[1], hi[1], e1 - e0, (b + 1) * img + pix0, aty, diag, bs2, kind, x_out,
-                   xt_out, status);
+    for (int b = b_begin; b < b_end; ++b) {
+      const double* zb = Zhat + b * zimg;
+      double v[kCoverRegEntries];
+#pragma unroll
+      for (int q = 0; q < kCoverRegEntries; ++q)
+        if (q < cnt) {
+          v[q] = __ldg(zb + off[q]);
+          if (kDc) v[q] = __dadd_rn(v[q], __ldg(dc + (int64_t)b * n_local + dco[q]));
+        }
+      double sum = 0.0 + v[0];
+      bool same = true;
+#pragma unroll
+      for (int q = 1; q < kCoverRegEntries; ++q)
+        if (q < cnt) {
+          sum += v[q];
+          same = same && v[q] == v[0];
+        }
+      const double xt = same ? v[0] : pow2 ? sum * inv : __ddiv_rn(sum, (double)cnt);
+      pixel_update(xt, b * img + pix0, aty, diag, bs2, kind, x_out, xt_out, status);
+    }
+  } else {
+    for (int b = b_begin; b < b_end; ++b) {
+      const double* zb = Zhat + b * zimg;
+      double sum = 0.0, v0 = 0.0;
+      bool same = true;
+      for (int q = 0; q < cnt; ++q) {
+        const int e = __ldg(entries + e0 + q);
+        double v = __ldg(zb + (int64_t)(e >> 8) * P + (e & 255));
+        if (kDc) v = __dadd_rn(v, __ldg(dc + (int64_t)b * n_local + (e >> 8)));
+        if (q == 0) v0 = v;
+        sum += v;
+        same = same && v == v0;
+      }
+      const double xt = same ? v0 : pow2 ? sum * inv : __ddiv_rn(sum, (double)cnt);
+      pixel_update(xt, b * img + pix0, aty, diag, bs2, kind, x_out, xt_out, status);
+    }
   }
 }
 
@@ -284,7 +308,7 @@ extern "C" int fepll_aggregate_strip(const double* Zhat, const double* dc, const
                                      const double* aty, const double* diag, double bs2, int32_t kind,
                                      double* x_out, double* xtilde_out, int32_t* status, void* stream) {
   using namespace fepll;
-  FEPLL_REQUIRE(Zhat && dc && anchors && status, "aggregate: bad arguments");
+  FEPLL_REQUIRE(Zhat && anchors && status, "aggregate: bad arguments");
   FEPLL_REQUIRE(n_rows >= 1 && n_cols >= 1 && spacing >= 1 && side >= 1 && half >= 0,
                 "aggregate: bad grid geometry");
   FEPLL_REQUIRE(H >= 1 && W >= side && batch >= 1 && H_glob >= side, "aggregate: bad image dims");
@@ -365,16 +389,20 @@ extern "C" int fepll_aggregate_cover(const double* Zhat, const double* dc, const
                                      double bs2, int32_t kind, double* x_out, double* xtilde_out,
                                      int32_t* status, void* stream) {
   using namespace fepll;
-  FEPLL_REQUIRE(Zhat && dc && ptr && entries && status, "aggregate_cover: bad arguments");
+  FEPLL_REQUIRE(Zhat && ptr && entries && status, "aggregate_cover: bad arguments");
   FEPLL_REQUIRE(kind == 0 || kind == 1, "aggregate_cover: unknown kind");
   FEPLL_REQUIRE(0 <= r_begin && r_begin <= r_end && r_end <= H && batch >= 1,
                 "aggregate_cover: bad rows");
   if (r_end == r_begin) return kOk;
   FEPLL_REQUIRE(r_end - r_begin <= 65535, "aggregate_cover: strip taller than the launch grid");
-  dim3 grid((unsigned)((W + kCoverThreads - 1) / kCoverThreads), r_end - r_begin);
-  aggregate_cover_kernel<<<grid, kCoverThreads, 0, (cudaStream_t)stream>>>(
+  const int ipb = kCoverImgPerBlock;
+  FEPLL_REQUIRE((int64_t)n_local * P < (int64_t(1) << 31), "aggregate_cover: image patch array above 2^31 elements");
+  dim3 grid((unsigned)((W + kCoverThreads - 1) / kCoverThreads), r_end - r_begin,
+            (unsigned)((batch + ipb - 1) / ipb));
+  auto kernel = dc ? aggregate_cover_kernel<true> : aggregate_cover_kernel<false>;
+  kernel<<<grid, kCoverThreads, 0, (cudaStream_t)stream>>>(
       Zhat, dc, ptr, entries, P, n_local, batch, H, W, r_begin, aty, diag, bs2, kind, x_out,
-      xtilde_out, status);
+      xtilde_out, status, ipb);
   FEPLL_LAUNCH();
   return kOk;
 }

@@ -231,7 +231,8 @@ rescore_fp64_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restr
 }
 
 // Wiener estimate per patch (fallback for large P / rank), iterating the leaf
-// buckets (gmm.py:352-359: U((gamma-gamma_tail) c) + gamma_tail z).
+// buckets (gmm.py:352-359: U((gamma-gamma_tail) c) + gamma_tail z).  Every
+// Wiener kernel writes est + dc, the values patches.py:198-222 reprojects.
 __global__ void __launch_bounds__(kWienerWarps * 32)
 wiener_fp64_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, int n_leaf_nodes,
                    const int32_t* __restrict__ cnt, const int64_t* __restrict__ off,
@@ -277,7 +278,8 @@ wiener_fp64_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       const double* row = U + (int64_t)p * r;
       double e = 0.0;
       for (int j = 0; j < r; ++j) e = fma(cs[j], __ldg(row + j), e);
-      out[p] = e + gt * zs[p];
+      const double est = e + gt * zs[p];
+      out[p] = __dadd_rn(est, ps.dc[patch]);  // reprojection input: est + dc
     }
     __syncwarp();
   }
@@ -413,7 +415,10 @@ wiener_tile_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const int p = pc0 + jg + 16 * c;
-          if (p < P) Zhat[(int64_t)row * P + p] = acc[a][c] + gt * Zs[i * zs_ld + p];
+          if (p < P) {
+            const double est = acc[a][c] + gt * Zs[i * zs_ld + p];
+            Zhat[(int64_t)row * P + p] = __dadd_rn(est, ps.dc[row]);  // + dc
+          }
         }
       }
     }
@@ -458,7 +463,7 @@ int rescore_queue_x(Plan* p, const LevelArgs& a, const double* x, const int32_t*
   return kOk;
 }
 
-int wiener_dmma(Plan* p, int t, const double* Z64, double* Zhat, cudaStream_t st);
+int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zhat, cudaStream_t st);
 bool wiener_dmma_supported(const Plan* p);
 
 LevelArgs make_level(Plan* p, int d, int t, int32_t* labels) {
@@ -581,7 +586,7 @@ extern "C" int fepll_wiener(fepll_plan_t plan, int32_t t, const double* x, int32
         n_total, p->rs.leafseg, p->rs.cnt, p->rs.off, p->rs.leaf_base, (int32_t*)nullptr, -1);
     FEPLL_LAUNCH();
   }
-  if (Z64 != nullptr && wiener_dmma_supported(p)) return wiener_dmma(p, t, Z64, Zhat, st);
+  if (Z64 != nullptr && wiener_dmma_supported(p)) return wiener_dmma(p, t, Z64, dc, Zhat, st);
   PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P)};
   const int P = p->v.P;
   const int rmax = p->max_model_rank;

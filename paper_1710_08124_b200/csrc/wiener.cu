@@ -4,6 +4,8 @@
 // (the grouping of pkg/src/fepll/solver.py:233-241):
 //     C    = (Z U_k) * (gamma - gamma_tail)        64 x r
 //     Zhat = C U_k^T + gamma_tail Z                64 x P
+// and writes Zhat + dc (the reprojection input of pkg/src/fepll/patches.py:
+// 198-222, `vals = est + dc`, rounded once here instead of in kernel (d)),
 // in FP64 — the estimates become the next iteration's image, whose tree
 // decisions must stay the FP64 reference's, so no reduced precision here.
 //
@@ -68,6 +70,12 @@ __device__ __forceinline__ void dmma16(double (&d)[4], const double (&a)[4], con
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
                    static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
                "l"(src)
                : "memory");
@@ -207,7 +215,7 @@ __global__ void __launch_bounds__(MT * 2)
 wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, int n_leaf_nodes,
                    const int32_t* __restrict__ cnt, const int64_t* __restrict__ off,
                    const int32_t* __restrict__ leafseg, const double* __restrict__ Z64,
-                   double* __restrict__ Zhat, Geo geo) {
+                   const double* __restrict__ dc, double* __restrict__ Zhat, Geo geo) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int kRows = MT;
   constexpr int kThreads = MT * 2;  // one warp per 16 rows
@@ -217,6 +225,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
   double* Zs0 = reinterpret_cast<double*>(smem + ((sizeof(Head) + 127) & ~size_t(127)));
   double* Us = Zs0 + NS * kRows * geo.zld;     // [Pn][uld]   (p, j)
   double* sh = Us + geo.Pn * geo.uld;          // [R8]
+  double* dcs = sh + geo.R8;                   // [NS][MT] dc of the buffered rows
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int P = geo.P;
   // K padding columns of the row buffers stay zero (cp.async fills [0, P))
@@ -268,12 +277,14 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
     if (j >= t_end) return;
     const int32_t* rows = h.rows[(j - t_begin) % kRing];
     double* Zs = Zs0 + ((j - t_begin) % NS) * kRows * geo.zld;
+    double* dcb = dcs + ((j - t_begin) % NS) * kRows;
     for (int e = tid + s0 * kThreads; e < min(s1 * kThreads, kRows * C); e += kThreads) {
       const int i = e / C, c = e - i * C;
       const int g = rows[i];
       double* d = Zs + i * geo.zld + 2 * c;
       if (g >= 0) {
         cp_async16(d, Z64 + (int64_t)g * P + 2 * c);
+        if (c == 0) cp_async8(dcb + i, dc + g);
       } else {
         d[0] = 0.0;
         d[1] = 0.0;
@@ -332,6 +343,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
     const bool inter = kInterleave && P == 64 && jn < t_end;
     int gsl[16];
     double* zn = Zs0 + ((jn - t_begin) % NS) * kRows * geo.zld + 2 * lane;
+    double* dcn = dcs + ((jn - t_begin) % NS) * kRows;
     if (inter) {
       const int32_t* rn = h.rows[(jn - t_begin) % kRing];
 #pragma unroll
@@ -346,6 +358,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
         double* d = zn + (warp + kWarps * q) * geo.zld;
         if (gsl[q] >= 0) {
           cp_async16(d, Z64 + (int64_t)gsl[q] * 64 + 2 * lane);
+          if (lane == 0) cp_async8(dcn + warp + kWarps * q, dc + gsl[q]);
         } else {
           d[0] = 0.0;
           d[1] = 0.0;
@@ -368,18 +381,22 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
     {
       wstamp(i, 4);
       const double gt = pv.model_gamma_tail[(int64_t)t * pv.K + comp];
-      // Zhat = acc + gamma_tail z, written over this warp's own rows of Zs
-      // (each element read and written by the same lane)...
+      // Zhat + dc = (acc + gamma_tail z) + dc, written over this warp's own
+      // rows of Zs (each element read and written by the same lane)...
       double* zw = const_cast<double*>(Zs);
+      const double* dct = dcs + (i % NS) * kRows;
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         double* zr = zw + (m0 + g4 + 8 * half) * geo.zld;
+        const double d = dct[m0 + g4 + 8 * half];
 #pragma unroll
         for (int n = 0; n < NT2; ++n) {
           const int col = n * 8 + 2 * t4;
           if (col < P) {
-            zr[col] = acc[n][2 * half] + gt * zr[col];
-            zr[col + 1] = acc[n][2 * half + 1] + gt * zr[col + 1];
+            const double e0 = acc[n][2 * half] + gt * zr[col];
+            const double e1 = acc[n][2 * half + 1] + gt * zr[col + 1];
+            zr[col] = __dadd_rn(e0, d);
+            zr[col + 1] = __dadd_rn(e1, d);
           }
         }
       }
@@ -404,7 +421,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
 
 int g_wiener_pair = 1;
 
-int wiener_dmma(Plan* p, int t, const double* Z64, double* Zhat, cudaStream_t st) {
+int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zhat, cudaStream_t st) {
   const int P = p->v.P;
   wn::Geo geo;
   geo.P = P;
@@ -416,7 +433,7 @@ int wiener_dmma(Plan* p, int t, const double* Z64, double* Zhat, cudaStream_t st
   auto smem_for = [&](int mt, int ns) {
     return ((sizeof(wn::Head) + 127) & ~size_t(127)) +
            sizeof(double) * (ns * (size_t)mt * geo.zld + (size_t)geo.Pn * geo.uld +
-                             geo.R8);
+                             geo.R8 + (size_t)ns * mt);
   };
   // 128-row tiles (16 warps) once the average leaf bucket is large enough
   // that the extra padding rows do not matter, and the tile fits in smem
@@ -442,8 +459,8 @@ int wiener_dmma(Plan* p, int t, const double* Z64, double* Zhat, cudaStream_t st
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, mt * 2, smem);
     kernel<<<kSMs * std::max(1, per_sm), mt * 2, smem, st>>>(
-        p->v, t, p->d_leaf_nodes, p->n_leaf_nodes, p->rs.cnt, p->rs.off, p->rs.leafseg, Z64, Zhat,
-        geo);
+        p->v, t, p->d_leaf_nodes, p->n_leaf_nodes, p->rs.cnt, p->rs.off, p->rs.leafseg, Z64, dc,
+        Zhat, geo);
     FEPLL_LAUNCH();
     return kOk;
   };

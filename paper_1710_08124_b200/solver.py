@@ -376,7 +376,8 @@ class Restorer:
                N.ptr(self.dc), N.ptr(self.Z64), nt, N.ptr(self.Zhat), st)
         self._mark(timer, "wiener")
         bs2 = float(self.betas[t]) * self.sigma * self.sigma
-        # reproject (patches.py:198-222); pixel-diagonal kinds fuse the image
+        # reproject (patches.py:198-222; Zhat already holds est + dc, so the
+        # gathers get no dc); pixel-diagonal kinds fuse the image
         # update (operators.py:281-287), the others get rhs = A^T y + bs2 x~ for
         # the FFT / CG solve.  Batches gather over the plan's cover lists
         # (shared by all images); a single image (strip mode included) has
@@ -390,11 +391,11 @@ class Restorer:
             sp = self.strip
             row0, H_glob, a_first, n_loc = ((sp.slab_lo, sp.H, sp.a_lo, sp.a_hi - sp.a_lo + 1)
                                             if sp is not None else (0, H, 0, nr))
-            N.call("fepll_aggregate_strip", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(anchors), nr, nc,
+            N.call("fepll_aggregate_strip", N.ptr(self.Zhat), None, N.ptr(anchors), nr, nc,
                    self.config.spacing, half, side, B, H, W, row0, H_glob, a_first, n_loc, r0, r1,
                    N.ptr(self.aty), N.ptr(diag), bs2, kind, N.ptr(out), N.ptr(xt), N.ptr(self.status), st)
         else:
-            N.call("fepll_aggregate_cover", N.ptr(self.Zhat), N.ptr(self.dc), N.ptr(ptr),
+            N.call("fepll_aggregate_cover", N.ptr(self.Zhat), None, N.ptr(ptr),
                    N.ptr(entries), P, n, B, H, W, r0, r1, N.ptr(self.aty), N.ptr(diag), bs2, kind,
                    N.ptr(out), N.ptr(xt), N.ptr(self.status), st)
         self._mark(timer, "aggregate")

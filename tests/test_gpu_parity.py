@@ -356,6 +356,44 @@ def test_aggregate_kernel_bitwise_vs_bincount():
         np.testing.assert_array_equal(xc.cpu().numpy()[0], ref)
 
 
+def test_aggregate_cover_batch_with_and_without_dc():
+    """Batched cover gather (images split over block groups, several images in
+    flight per thread) equals np.bincount per image, both when it adds dc and
+    when the estimates already hold est + dc (the Wiener kernels' output)."""
+    import torch
+    from paper_1710_08124_b200 import _native as N, jitter_rng, jittered_grid
+    from paper_1710_08124_b200.patches import axis_anchors
+
+    P, H, W, s, B = 64, 72, 300, 4, 19
+    side = 8
+    pos = jittered_grid(H, W, P, s, jitter_rng(7, 2)).positions.astype(np.int32)
+    n = pos.shape[0]
+    rng = np.random.default_rng(5)
+    est = rng.standard_normal((B, n, P)) * 30
+    dc = rng.standard_normal((B, n)) * 100
+    refs = [O.reproject(est[b], dc[b], pos.astype(np.int64), side, H, W) for b in range(B)]
+    nr, nc = axis_anchors(H, side, s).size, axis_anchors(W, side, s).size
+    st = torch.cuda.current_stream().cuda_stream
+    pd = _dev(pos)
+    ptr = torch.empty(H * W + 1, dtype=torch.int32, device="cuda")
+    ent = torch.empty(n * P, dtype=torch.int32, device="cuda")
+    scr = torch.empty(int(N.lib().fepll_cover_scratch_ints(H * W)), dtype=torch.int32, device="cuda")
+    N.call("fepll_cover_build", N.ptr(pd), nr, nc, s, (side - s) // 2, side, W, 0, H, 0, nr, 0, H,
+           N.ptr(ptr), N.ptr(ent), n * P, N.ptr(scr), st)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for pre_added in (False, True):
+        vals = est + dc[:, :, None] if pre_added else est
+        ed = _dev(np.ascontiguousarray(vals.reshape(B * n, P)))
+        dd = None if pre_added else _dev(dc.reshape(-1))
+        xc = torch.empty((B, H, W), dtype=torch.float64, device="cuda")
+        N.call("fepll_aggregate_cover", N.ptr(ed), N.ptr(dd), N.ptr(ptr), N.ptr(ent), P, n, B, H, W,
+               0, H, None, None, 1.0, 1, None, N.ptr(xc), N.ptr(status), st)
+        got = xc.cpu().numpy()
+        for b in range(B):
+            np.testing.assert_array_equal(got[b], refs[b])
+    assert int(status.item()) == 0
+
+
 def test_lo_eq_hi_rule_returns_common_value():
     """Identical overlapping contributions come back verbatim (patches.py:221)."""
     import torch
