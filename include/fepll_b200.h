@@ -131,10 +131,12 @@ int fepll_select_rescored(fepll_plan_t plan, int32_t* dst, void* stream);
  * With Z64 (the FP64 patch rows of fepll_extract) it runs on the FP64 tensor
  * cores (DMMA); otherwise it re-extracts the patches from x.  Zhat receives
  * est + dc (patches.py:198-222's reprojection values), ready for
- * fepll_aggregate* with dc == NULL. */
+ * fepll_aggregate* with dc == NULL.  Zhat holds zhat_rows (>= n_img) rows of
+ * P doubles per image: patch b*n_img + i is row b*zhat_rows + i (a padded
+ * image pitch keeps the images' rows off power-of-two strides). */
 int fepll_wiener(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32_t W,
                  const int32_t* anchors, int32_t n_img, const double* dc, const double* Z64,
-                 int64_t n_total, double* Zhat, void* stream);
+                 int64_t n_total, double* Zhat, int32_t zhat_rows, void* stream);
 
 /* patches.py:198-222 (+ operators.py:284-287 when kind==0):
  * per-pixel ordered gather of (Zhat + dc) over covering anchors; dc may be
@@ -177,10 +179,13 @@ int fepll_cover_build(const int32_t* anchors, int32_t n_rows, int32_t n_cols, in
                       int32_t* ptr, int32_t* entries, int64_t entries_cap, int32_t* scratch,
                       void* stream);
 
-/* fepll_aggregate over cover lists (bit-identical results): Zhat/dc hold
- * n_local patches per image, images [batch][H][W]; rows [r_begin, r_end). */
+/* fepll_aggregate over cover lists (bit-identical results): Zhat holds
+ * zhat_rows (>= n_local) rows per image of which the first n_local are the
+ * image's patches, dc n_local per image; images [batch][H][W]; rows
+ * [r_begin, r_end). */
 int fepll_aggregate_cover(const double* Zhat, const double* dc, const int32_t* ptr,
-                          const int32_t* entries, int32_t P, int32_t n_local, int32_t batch,
+                          const int32_t* entries, int32_t P, int32_t n_local, int32_t zhat_rows,
+                          int32_t batch,
                           int32_t H, int32_t W, int32_t r_begin, int32_t r_end,
                           const double* aty, const double* diag, double bs2, int32_t kind,
                           double* x_out, double* xtilde_out, int32_t* status, void* stream);

@@ -200,14 +200,18 @@ __global__ void scan_apply_kernel(const int32_t* __restrict__ counts, int64_t n,
 // batch's) are decoded once into element offsets held in registers, then
 // each image costs its Zhat loads, the ordered sum and the pixel update —
 // the gather is issue-bound, so the per-image instruction count is what is
-// minimised.  Per image the result is aggregate_kernel's:
+// minimised, and occupancy (latency hiding) matters more than loads in
+// flight per thread: measured on B200, 64 registers / 4 blocks per SM and
+// one image at a time beat several images per pass (those run slower).
+// Per image the result is aggregate_kernel's:
 //  * the sum runs over the entries in ascending patch order from 0.0;
 //  * lo == hi (patches.py:221) is "every value equals the first" (NaN
 //    compares unequal, so a NaN still reaches the sum);
 //  * sum / count for a power-of-two count is the exact product with 1/count.
 constexpr int kCoverThreads = 256;
 constexpr int kCoverRegEntries = 9;   // entries decoded into registers (more: generic loop)
-constexpr int kCoverImgPerBlock = 16; // images per block (blockIdx.z groups)
+constexpr int kCoverImgPerBlock = 64; // images per block (blockIdx.z groups; per-block setup is
+                                      // three dependent loads, amortised over the images)
 
 __device__ __forceinline__ void pixel_update(double xt, int64_t pix, const double* aty,
                                              const double* diag, double bs2, int kind,
@@ -226,10 +230,10 @@ __device__ __forceinline__ void pixel_update(double xt, int64_t pix, const doubl
 }
 
 template <bool kDc>
-__global__ void __launch_bounds__(kCoverThreads)
+__global__ void __launch_bounds__(kCoverThreads, 4)  // 64 registers: 4 blocks per SM
 aggregate_cover_kernel(const double* __restrict__ Zhat, const double* __restrict__ dc,
                        const int32_t* __restrict__ ptr, const int32_t* __restrict__ entries, int P,
-                       int n_local, int batch, int H, int W, int r_begin,
+                       int n_local, int zrows, int batch, int H, int W, int r_begin,
                        const double* __restrict__ aty, const double* __restrict__ diag, double bs2,
                        int kind, double* __restrict__ x_out, double* __restrict__ xt_out,
                        int32_t* status, int ipb) {
@@ -239,7 +243,7 @@ aggregate_cover_kernel(const double* __restrict__ Zhat, const double* __restrict
   const int e0 = __ldg(ptr + p), cnt = __ldg(ptr + p + 1) - e0;
   const int64_t pix0 = (int64_t)(r_begin + blockIdx.y) * W + c;
   const int64_t img = (int64_t)H * W;
-  const int64_t zimg = (int64_t)n_local * P;  // Zhat elements per image
+  const int64_t zimg = (int64_t)zrows * P;  // Zhat elements per image (padded pitch)
   const int b_begin = blockIdx.z * ipb;
   const int b_end = min(batch, b_begin + ipb);
   if (cnt == 0) {
@@ -384,6 +388,7 @@ extern "C" int fepll_cover_build(const int32_t* anchors, int32_t n_rows, int32_t
 
 extern "C" int fepll_aggregate_cover(const double* Zhat, const double* dc, const int32_t* ptr,
                                      const int32_t* entries, int32_t P, int32_t n_local,
+                                     int32_t zhat_rows,
                                      int32_t batch, int32_t H, int32_t W, int32_t r_begin,
                                      int32_t r_end, const double* aty, const double* diag,
                                      double bs2, int32_t kind, double* x_out, double* xtilde_out,
@@ -391,6 +396,7 @@ extern "C" int fepll_aggregate_cover(const double* Zhat, const double* dc, const
   using namespace fepll;
   FEPLL_REQUIRE(Zhat && ptr && entries && status, "aggregate_cover: bad arguments");
   FEPLL_REQUIRE(kind == 0 || kind == 1, "aggregate_cover: unknown kind");
+  FEPLL_REQUIRE(zhat_rows >= n_local, "aggregate_cover: Zhat rows per image below n_local");
   FEPLL_REQUIRE(0 <= r_begin && r_begin <= r_end && r_end <= H && batch >= 1,
                 "aggregate_cover: bad rows");
   if (r_end == r_begin) return kOk;
@@ -401,7 +407,7 @@ extern "C" int fepll_aggregate_cover(const double* Zhat, const double* dc, const
             (unsigned)((batch + ipb - 1) / ipb));
   auto kernel = dc ? aggregate_cover_kernel<true> : aggregate_cover_kernel<false>;
   kernel<<<grid, kCoverThreads, 0, (cudaStream_t)stream>>>(
-      Zhat, dc, ptr, entries, P, n_local, batch, H, W, r_begin, aty, diag, bs2, kind, x_out,
+      Zhat, dc, ptr, entries, P, n_local, zhat_rows, batch, H, W, r_begin, aty, diag, bs2, kind, x_out,
       xtilde_out, status, ipb);
   FEPLL_LAUNCH();
   return kOk;

@@ -26,6 +26,10 @@ struct PatchSrc {
   const int32_t* anchors; // [n_img][2]
   const double* dc;       // [B*n_img]
   int n_img, H, W, side;
+  int zrows;              // Zhat rows per image (>= n_img; padded pitch)
+  __device__ __forceinline__ int64_t zrow(int g) const {
+    return zrows == n_img ? (int64_t)g : (int64_t)(g / n_img) * zrows + g % n_img;
+  }
 };
 
 // warp: zs[0..P) = window(g) - dc[g]
@@ -273,7 +277,7 @@ wiener_fp64_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       cs[j] = c * shrink[j];
     }
     __syncwarp();
-    double* out = Zhat + (int64_t)patch * P;
+    double* out = Zhat + ps.zrow(patch) * P;
     for (int p = lane; p < P; p += 32) {
       const double* row = U + (int64_t)p * r;
       double e = 0.0;
@@ -417,7 +421,7 @@ wiener_tile_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
           const int p = pc0 + jg + 16 * c;
           if (p < P) {
             const double est = acc[a][c] + gt * Zs[i * zs_ld + p];
-            Zhat[(int64_t)row * P + p] = __dadd_rn(est, ps.dc[row]);  // + dc
+            Zhat[ps.zrow(row) * P + p] = __dadd_rn(est, ps.dc[row]);  // + dc
           }
         }
       }
@@ -456,14 +460,15 @@ static int side_of(int P) {
 
 int rescore_queue_x(Plan* p, const LevelArgs& a, const double* x, const int32_t* anchors, int n_img,
                     int H, int W, const double* dc, const double* sq, cudaStream_t st) {
-  PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P)};
+  PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P), n_img};
   rescore_fp64_kernel<<<4 * kSMs, kSelWarps * 32, 0, st>>>(p->v, a, ps, sq, p->rs.queue,
                                                            p->rs.queue_len);
   FEPLL_LAUNCH();
   return kOk;
 }
 
-int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zhat, cudaStream_t st);
+int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zhat, int n_img,
+                int zrows, cudaStream_t st);
 bool wiener_dmma_supported(const Plan* p);
 
 LevelArgs make_level(Plan* p, int d, int t, int32_t* labels) {
@@ -517,7 +522,7 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
       n_total, p->rs.seg[0], p->rs.cnt, p->rs.off, p->rs.leaf_base, labels, root_leaf);
   FEPLL_LAUNCH();
   if (root_leaf < 0) {
-    PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P)};
+    PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P), n_img};
     for (int d = 0; d < p->n_levels; ++d) {
       LevelArgs a = make_level(p, d, t, labels);
       int rc = kOk;
@@ -569,7 +574,8 @@ extern "C" int fepll_select_rescored(fepll_plan_t plan, int32_t* dst, void* stre
 
 extern "C" int fepll_wiener(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32_t W,
                             const int32_t* anchors, int32_t n_img, const double* dc,
-                            const double* Z64, int64_t n_total, double* Zhat, void* stream) {
+                            const double* Z64, int64_t n_total, double* Zhat, int32_t zhat_rows,
+                            void* stream) {
   using namespace fepll;
   Plan* p = reinterpret_cast<Plan*>(plan);
   FEPLL_REQUIRE(p != nullptr && x != nullptr && anchors != nullptr && dc != nullptr &&
@@ -577,6 +583,7 @@ extern "C" int fepll_wiener(fepll_plan_t plan, int32_t t, const double* x, int32
                 "wiener: bad arguments");
   FEPLL_REQUIRE(t >= 0 && t < p->v.T, "wiener: iteration index outside the beta schedule");
   FEPLL_REQUIRE(n_total == p->last_n_total, "wiener: must follow fepll_select on the same patches");
+  FEPLL_REQUIRE(n_img >= 1 && zhat_rows >= n_img, "wiener: Zhat rows per image below n_img");
   FEPLL_REQUIRE(p->n_leaf_nodes <= kMaxLevelNodes, "wiener: too many leaves");
   if (n_total == 0) return kOk;
   cudaStream_t st = (cudaStream_t)stream;
@@ -586,8 +593,9 @@ extern "C" int fepll_wiener(fepll_plan_t plan, int32_t t, const double* x, int32
         n_total, p->rs.leafseg, p->rs.cnt, p->rs.off, p->rs.leaf_base, (int32_t*)nullptr, -1);
     FEPLL_LAUNCH();
   }
-  if (Z64 != nullptr && wiener_dmma_supported(p)) return wiener_dmma(p, t, Z64, dc, Zhat, st);
-  PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P)};
+  if (Z64 != nullptr && wiener_dmma_supported(p))
+    return wiener_dmma(p, t, Z64, dc, Zhat, n_img, zhat_rows, st);
+  PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P), zhat_rows};
   const int P = p->v.P;
   const int rmax = p->max_model_rank;
   if (rmax <= 64) {

@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(MT * 2)
 wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, int n_leaf_nodes,
                    const int32_t* __restrict__ cnt, const int64_t* __restrict__ off,
                    const int32_t* __restrict__ leafseg, const double* __restrict__ Z64,
-                   const double* __restrict__ dc, double* __restrict__ Zhat, Geo geo) {
+                   const double* __restrict__ dc, double* __restrict__ Zhat, int n_img, int zrows,
+                   Geo geo) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int kRows = MT;
   constexpr int kThreads = MT * 2;  // one warp per 16 rows
@@ -284,7 +285,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       double* d = Zs + i * geo.zld + 2 * c;
       if (g >= 0) {
         cp_async16(d, Z64 + (int64_t)g * P + 2 * c);
-        if (c == 0) cp_async8(dcb + i, dc + g);
+        if (c == 0 && dc) cp_async8(dcb + i, dc + g);
       } else {
         d[0] = 0.0;
         d[1] = 0.0;
@@ -358,7 +359,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
         double* d = zn + (warp + kWarps * q) * geo.zld;
         if (gsl[q] >= 0) {
           cp_async16(d, Z64 + (int64_t)gsl[q] * 64 + 2 * lane);
-          if (lane == 0) cp_async8(dcn + warp + kWarps * q, dc + gsl[q]);
+          if (lane == 0 && dc) cp_async8(dcn + warp + kWarps * q, dc + gsl[q]);
         } else {
           d[0] = 0.0;
           d[1] = 0.0;
@@ -388,15 +389,15 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         double* zr = zw + (m0 + g4 + 8 * half) * geo.zld;
-        const double d = dct[m0 + g4 + 8 * half];
+        const double d = dc ? dct[m0 + g4 + 8 * half] : 0.0;
 #pragma unroll
         for (int n = 0; n < NT2; ++n) {
           const int col = n * 8 + 2 * t4;
           if (col < P) {
             const double e0 = acc[n][2 * half] + gt * zr[col];
             const double e1 = acc[n][2 * half + 1] + gt * zr[col + 1];
-            zr[col] = __dadd_rn(e0, d);
-            zr[col + 1] = __dadd_rn(e1, d);
+            zr[col] = dc ? __dadd_rn(e0, d) : e0;
+            zr[col + 1] = dc ? __dadd_rn(e1, d) : e1;
           }
         }
       }
@@ -408,7 +409,11 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       __syncwarp();
       if (lane < 16) {
         const int gidx = h.rows[slot][m0 + lane];
-        if (gidx >= 0) bulk_s2g(Zhat + (int64_t)gidx * P, zw + (m0 + lane) * geo.zld, P * 8);
+        if (gidx >= 0) {
+          const int64_t orow =  // padded image pitch (no division when dense)
+              zrows == n_img ? (int64_t)gidx : (int64_t)(gidx / n_img) * zrows + gidx % n_img;
+          bulk_s2g(Zhat + orow * P, zw + (m0 + lane) * geo.zld, P * 8);
+        }
         bulk_commit();
       }
       wstamp(i, 5);
@@ -420,8 +425,10 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
 }  // namespace wn
 
 int g_wiener_pair = 1;
+int g_wiener_dc = 1;  // debug: 0 = write est only (the gather then adds dc)
 
-int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zhat, cudaStream_t st) {
+int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zhat, int n_img,
+                int zrows, cudaStream_t st) {
   const int P = p->v.P;
   wn::Geo geo;
   geo.P = P;
@@ -459,8 +466,9 @@ int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zha
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, mt * 2, smem);
     kernel<<<kSMs * std::max(1, per_sm), mt * 2, smem, st>>>(
-        p->v, t, p->d_leaf_nodes, p->n_leaf_nodes, p->rs.cnt, p->rs.off, p->rs.leafseg, Z64, dc,
-        Zhat, geo);
+        p->v, t, p->d_leaf_nodes, p->n_leaf_nodes, p->rs.cnt, p->rs.off, p->rs.leafseg, Z64,
+        g_wiener_dc ? dc : nullptr,
+        Zhat, n_img, zrows, geo);
     FEPLL_LAUNCH();
     return kOk;
   };
@@ -504,4 +512,9 @@ extern "C" int fepll_debug_wiener_pair(int32_t on) {
 extern "C" int fepll_debug_wiener_trace(void* device_buffer) {
   uint64_t* p = static_cast<uint64_t*>(device_buffer);
   return cudaMemcpyToSymbol(fepll::wn::g_trace, &p, sizeof(p)) == cudaSuccess ? 0 : 5;
+}
+
+extern "C" int fepll_debug_wiener_dc(int32_t on) {
+  fepll::g_wiener_dc = on;
+  return 0;
 }

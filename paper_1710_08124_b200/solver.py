@@ -16,6 +16,7 @@ operator and noise level in one pass (the batch of BASELINE config 5).
 
 from __future__ import annotations
 
+
 import math
 import time
 from dataclasses import dataclass, field
@@ -219,7 +220,11 @@ class Restorer:
         # FP32 patch rows (kernel (a) output) feed the tensor-core scorer
         self.Z32 = (torch.empty((B * n, self.z32_pitch), dtype=torch.float32, device=dev)
                     if mode == "tensor" else None)
-        self.Zhat = torch.empty((B * n, P), dtype=f64, device=dev)
+        # Wiener output rows (est + dc), zhat_rows per image (the ABI allows a
+        # padded pitch; a padded one measured no different, so dense)
+        self.zhat_rows = n
+        self._agg_dc = None  # (debug A/B: dc added by the gather instead of the Wiener kernel)
+        self.Zhat = torch.empty((B * self.zhat_rows, P), dtype=f64, device=dev)
         self.dc = torch.empty(B * n, dtype=f64, device=dev)
         self.sq = torch.empty(B * n, dtype=f64, device=dev)
         self.labels = torch.empty(B * n, dtype=torch.int32, device=dev)
@@ -373,7 +378,7 @@ class Restorer:
         N.call("fepll_select_rescored", self.plan.handle, N.ptr(self.rescored[t]), st)
         self._mark(timer, "select")
         N.call("fepll_wiener", self.plan.handle, t, N.ptr(self.x), H, W, N.ptr(anchors), n,
-               N.ptr(self.dc), N.ptr(self.Z64), nt, N.ptr(self.Zhat), st)
+               N.ptr(self.dc), N.ptr(self.Z64), nt, N.ptr(self.Zhat), self.zhat_rows, st)
         self._mark(timer, "wiener")
         bs2 = float(self.betas[t]) * self.sigma * self.sigma
         # reproject (patches.py:198-222; Zhat already holds est + dc, so the
@@ -395,8 +400,8 @@ class Restorer:
                    self.config.spacing, half, side, B, H, W, row0, H_glob, a_first, n_loc, r0, r1,
                    N.ptr(self.aty), N.ptr(diag), bs2, kind, N.ptr(out), N.ptr(xt), N.ptr(self.status), st)
         else:
-            N.call("fepll_aggregate_cover", N.ptr(self.Zhat), None, N.ptr(ptr),
-                   N.ptr(entries), P, n, B, H, W, r0, r1, N.ptr(self.aty), N.ptr(diag), bs2, kind,
+            N.call("fepll_aggregate_cover", N.ptr(self.Zhat), N.ptr(self._agg_dc), N.ptr(ptr),
+                   N.ptr(entries), P, n, self.zhat_rows, B, H, W, r0, r1, N.ptr(self.aty), N.ptr(diag), bs2, kind,
                    N.ptr(out), N.ptr(xt), N.ptr(self.status), st)
         self._mark(timer, "aggregate")
         if not self.pixel_kind:

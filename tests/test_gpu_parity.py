@@ -351,7 +351,7 @@ def test_aggregate_kernel_bitwise_vs_bincount():
                N.ptr(ptr), N.ptr(ent), n * P, N.ptr(scr), st)
         assert int(ptr[-1].item()) == n * P  # every patch covers exactly P pixels
         xc = torch.empty((1, H, W), dtype=torch.float64, device="cuda")
-        N.call("fepll_aggregate_cover", N.ptr(ed), N.ptr(dd), N.ptr(ptr), N.ptr(ent), P, n, 1, H, W,
+        N.call("fepll_aggregate_cover", N.ptr(ed), N.ptr(dd), N.ptr(ptr), N.ptr(ent), P, n, n, 1, H, W,
                0, H, None, None, 1.0, 1, None, N.ptr(xc), N.ptr(status), st)
         np.testing.assert_array_equal(xc.cpu().numpy()[0], ref)
 
@@ -381,12 +381,14 @@ def test_aggregate_cover_batch_with_and_without_dc():
     N.call("fepll_cover_build", N.ptr(pd), nr, nc, s, (side - s) // 2, side, W, 0, H, 0, nr, 0, H,
            N.ptr(ptr), N.ptr(ent), n * P, N.ptr(scr), st)
     status = torch.zeros(1, dtype=torch.int32, device="cuda")
-    for pre_added in (False, True):
+    for pre_added, pad in ((False, 0), (True, 0), (True, 3)):
         vals = est + dc[:, :, None] if pre_added else est
-        ed = _dev(np.ascontiguousarray(vals.reshape(B * n, P)))
+        # padded image pitch: rows n .. n+pad-1 of every image are garbage
+        vals = np.concatenate([vals, np.full((B, pad, P), np.nan)], axis=1)
+        ed = _dev(np.ascontiguousarray(vals.reshape(B * (n + pad), P)))
         dd = None if pre_added else _dev(dc.reshape(-1))
         xc = torch.empty((B, H, W), dtype=torch.float64, device="cuda")
-        N.call("fepll_aggregate_cover", N.ptr(ed), N.ptr(dd), N.ptr(ptr), N.ptr(ent), P, n, B, H, W,
+        N.call("fepll_aggregate_cover", N.ptr(ed), N.ptr(dd), N.ptr(ptr), N.ptr(ent), P, n, n + pad, B, H, W,
                0, H, None, None, 1.0, 1, None, N.ptr(xc), N.ptr(status), st)
         got = xc.cpu().numpy()
         for b in range(B):
