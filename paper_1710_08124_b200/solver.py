@@ -457,21 +457,24 @@ class Restorer:
 
 class HostPipeline:
     """Batch restoration from and to pinned host buffers with the copies
-    overlapped: the batch is cut into ``chunks`` equal parts that alternate
-    between two restorers on two CUDA streams, so the upload of chunk c+1 and
-    the download of chunk c-1 run on the copy engines while chunk c computes.
+    overlapped: the batch is cut into ``chunks`` equal parts that rotate over
+    ``streams`` restorers, one CUDA stream each, so the upload of chunk c+1
+    and the download of chunk c-1 run on the copy engines while chunk c
+    computes — across consecutive :meth:`submit` calls too (a stream of
+    batches; with chunks=1 every batch keeps the full-batch kernel
+    efficiency and its copies hide behind its neighbours' compute).
     Results are identical to :class:`Restorer` on the whole batch (every
     image is restored independently)."""
 
-    def __init__(self, A, model, tree, config, batch: int, chunks: int = 4, lam: float | None = None,
-                 mode: str = "tensor", device=None):
+    def __init__(self, A, model, tree, config, batch: int, chunks: int = 1, lam: float | None = None,
+                 mode: str = "tensor", device=None, streams: int = 2):
         torch = _torch()
         if batch % chunks:
             raise DataError(f"batch {batch} does not split into {chunks} chunks")
         self.torch = torch
         self.batch, self.chunks = int(batch), int(chunks)
         self.per = self.batch // self.chunks
-        k = min(2, self.chunks)
+        k = max(1, int(streams))  # restorers / streams the chunks rotate over
         self.restorers = [Restorer(A, model, tree, config, batch=self.per, lam=lam, mode=mode,
                                    device=device) for _ in range(k)]
         dev = self.restorers[0].device
@@ -483,32 +486,60 @@ class HostPipeline:
         self.y64 = [torch.empty((self.per, Ho, Wo), dtype=torch.float64, device=dev) for _ in range(k)]
         self.x32 = [torch.empty((self.per, H, W), dtype=torch.float32, device=dev) for _ in range(k)]
         self.status = [torch.zeros(1, dtype=torch.int32, device=dev) for _ in range(k)]
+        self._next = 0  # chunk counter: chunk j runs on restorer / stream j % k
+        self._computed = None  # event: the last queued chunk's compute is done
 
-    def run(self, y_host, x_host) -> None:
-        """y_host: pinned (batch, Ho, Wo) float32 observations; x_host: pinned
-        (batch, H, W) float32 output.  Returns after both are complete."""
+    def submit(self, y_host, x_host) -> None:
+        """Queue one batch without waiting: y_host pinned (batch, Ho, Wo)
+        float32 observations, x_host pinned (batch, H, W) float32 output.
+        Chunks keep rotating over the streams across calls, so the copies of
+        one batch overlap the compute of its neighbours (with chunks=1, batch
+        s+1 uploads while batch s computes); neither buffer may be touched
+        until :meth:`wait` returns."""
         torch = self.torch
         main = torch.cuda.current_stream(self.device)
-        for s, st in zip(self.streams, self.status):
+        for s in self.streams:
             s.wait_stream(main)
-            st.zero_()
         for c in range(self.chunks):
-            k = c % len(self.restorers)
+            k = self._next % len(self.restorers)
+            self._next += 1
             r, s = self.restorers[k], self.streams[k]
             lo, hi = c * self.per, (c + 1) * self.per
             with torch.cuda.stream(s):
                 self.y32[k].copy_(y_host[lo:hi], non_blocking=True)
                 self.y64[k].copy_(self.y32[k])
+                # computes run one after another (two restorations sharing
+                # the SMs measured slower than back to back); only the copies
+                # overlap them
+                if self._computed is not None:
+                    s.wait_event(self._computed)
                 x, _ = r.run(self.y64[k])
+                self._computed = torch.cuda.Event()
+                self._computed.record(s)
                 self.x32[k].copy_(x)
                 x_host[lo:hi].copy_(self.x32[k], non_blocking=True)
                 self.status[k].bitwise_or_(r.status)  # run() clears it per chunk
+
+    def join(self) -> None:
+        """Make the current stream wait for every queued batch (no host sync)."""
+        main = self.torch.cuda.current_stream(self.device)
         for s in self.streams:
             main.wait_stream(s)
-        main.synchronize()
+
+    def wait(self) -> None:
+        """Block until every queued batch is in its host buffer; raise on a
+        numerical / coverage error of any of them."""
+        self.join()
+        self.torch.cuda.current_stream(self.device).synchronize()
         for r, st in zip(self.restorers, self.status):
             r.status.copy_(st)
+            st.zero_()
             r.check_status()
+
+    def run(self, y_host, x_host) -> None:
+        """submit() + wait(): returns after the batch is restored into x_host."""
+        self.submit(y_host, x_host)
+        self.wait()
 
 
 def restore(y, A, model, tree=None, config=None, *, mode: str = "tensor", lam=None):

@@ -134,6 +134,16 @@ def test_host_pipeline_equals_batch_restore(models):
     hp.run(pin_in, pin_out)
     xb, _ = restore_batch(ys.astype(np.float64), cases[0].A, model, tree, cfg)
     np.testing.assert_array_equal(pin_out.numpy(), xb.astype(np.float32))
+    # a stream of batches: three submits (one chunk each, rotating over the
+    # two restorers / streams) before one wait, each into its own buffer
+    hs = HostPipeline(cases[0].A, model, tree, cfg, batch=2, chunks=1)
+    ins = [torch.from_numpy(ys[i:i + 2]).pin_memory() for i in (0, 2, 1)]
+    outs = [torch.empty((2,) + ys.shape[1:], dtype=torch.float32).pin_memory() for _ in ins]
+    for a, b in zip(ins, outs):
+        hs.submit(a, b)
+    hs.wait()
+    for (i, b) in zip((0, 2, 1), outs):
+        np.testing.assert_array_equal(b.numpy(), xb[i:i + 2].astype(np.float32))
 
 
 def test_same_seed_bit_identical_and_batch_equals_single(models):
