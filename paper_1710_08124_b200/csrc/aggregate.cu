@@ -302,6 +302,62 @@ aggregate_cover_kernel(const double* __restrict__ Zhat, const double* __restrict
   }
 }
 
+// Single-image form (row strips, large single images): one pixel per thread
+// and nothing to amortise the entry decode over, so the kernel is the
+// ptr -> entries -> Zhat chain of dependent loads; kept to 32 registers for
+// full occupancy (twice the chains in flight of the batched kernel).
+template <bool kDc>
+__global__ void __launch_bounds__(kCoverThreads, 8)
+aggregate_cover1_kernel(const double* __restrict__ Zhat, const double* __restrict__ dc,
+                        const int32_t* __restrict__ ptr, const int32_t* __restrict__ entries,
+                        int P, int W, int r_begin, const double* __restrict__ aty,
+                        const double* __restrict__ diag, double bs2, int kind,
+                        double* __restrict__ x_out, double* __restrict__ xt_out, int32_t* status) {
+  const int c = blockIdx.x * kCoverThreads + threadIdx.x;
+  if (c >= W) return;
+  const int64_t p = (int64_t)blockIdx.y * W + c;
+  const int e0 = __ldg(ptr + p), cnt = __ldg(ptr + p + 1) - e0;
+  const int64_t pix = (int64_t)(r_begin + blockIdx.y) * W + c;
+  if (cnt == 0) {
+    atomicOr(status, 1);
+    pixel_update(0.0, pix, aty, diag, bs2, kind, x_out, xt_out, status);
+    return;
+  }
+  double sum = 0.0, v0 = 0.0;
+  bool same = true;
+  if (cnt <= 4) {
+    int e[4];
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) e[q] = q < cnt ? __ldg(entries + e0 + q) : 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q < cnt) {
+        v[q] = __ldg(Zhat + (int64_t)(e[q] >> 8) * P + (e[q] & 255));
+        if (kDc) v[q] = __dadd_rn(v[q], __ldg(dc + (e[q] >> 8)));
+      }
+    v0 = v[0];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q < cnt) {
+        sum += v[q];
+        same = same && v[q] == v0;
+      }
+  } else {
+    for (int q = 0; q < cnt; ++q) {
+      const int e = __ldg(entries + e0 + q);
+      double v = __ldg(Zhat + (int64_t)(e >> 8) * P + (e & 255));
+      if (kDc) v = __dadd_rn(v, __ldg(dc + (e >> 8)));
+      if (q == 0) v0 = v;
+      sum += v;
+      same = same && v == v0;
+    }
+  }
+  const bool pow2 = (cnt & (cnt - 1)) == 0;
+  const double xt = same ? v0 : pow2 ? sum * (1.0 / (double)cnt) : __ddiv_rn(sum, (double)cnt);
+  pixel_update(xt, pix, aty, diag, bs2, kind, x_out, xt_out, status);
+}
+
 }  // namespace fepll
 
 extern "C" int fepll_aggregate_strip(const double* Zhat, const double* dc, const int32_t* anchors,
@@ -405,6 +461,14 @@ extern "C" int fepll_aggregate_cover(const double* Zhat, const double* dc, const
   FEPLL_REQUIRE((int64_t)n_local * P < (int64_t(1) << 31), "aggregate_cover: image patch array above 2^31 elements");
   dim3 grid((unsigned)((W + kCoverThreads - 1) / kCoverThreads), r_end - r_begin,
             (unsigned)((batch + ipb - 1) / ipb));
+  if (batch == 1) {
+    dim3 g1((unsigned)((W + kCoverThreads - 1) / kCoverThreads), r_end - r_begin);
+    auto k1 = dc ? aggregate_cover1_kernel<true> : aggregate_cover1_kernel<false>;
+    k1<<<g1, kCoverThreads, 0, (cudaStream_t)stream>>>(Zhat, dc, ptr, entries, P, W, r_begin, aty,
+                                                       diag, bs2, kind, x_out, xtilde_out, status);
+    FEPLL_LAUNCH();
+    return kOk;
+  }
   auto kernel = dc ? aggregate_cover_kernel<true> : aggregate_cover_kernel<false>;
   kernel<<<grid, kCoverThreads, 0, (cudaStream_t)stream>>>(
       Zhat, dc, ptr, entries, P, n_local, zhat_rows, batch, H, W, r_begin, aty, diag, bs2, kind, x_out,
