@@ -42,12 +42,17 @@ namespace fepll {
 
 namespace ws2 {
 constexpr int kRows = 128;
-constexpr int kLoaderWarps = 2;         // warp w: rows 64w .. 64w+63, both K atoms
+#ifndef FEPLL_WS2_LOADERS
+#define FEPLL_WS2_LOADERS 4
+#endif
+constexpr int kLoaderWarps = FEPLL_WS2_LOADERS;  // warp w: rows kLoaderRows w .., both K atoms
+constexpr int kLoaderRows = kRows / kLoaderWarps;
+constexpr int kLoaderQ = kLoaderRows / 4;         // rows per lane (4 rows per instruction)
 constexpr int kLoaderThreads = 32 * kLoaderWarps;
-constexpr int kConvWarp0 = 2;           // warps 2..9: K atom (w-2)/4, TMEM lane quarter w%4
+constexpr int kConvWarp0 = kLoaderWarps;          // 8 warps: K atom, TMEM lane quarter w%4
 constexpr int kConvWarps = 8;
-constexpr int kMmaWarp = 10;
-constexpr int kEpiWarp0 = 11;
+constexpr int kMmaWarp = kConvWarp0 + kConvWarps;
+constexpr int kEpiWarp0 = kMmaWarp + 1;
 // epilogue groups (== TMEM accumulators) and accumulator width are template
 // parameters: <3, 128> for levels with nodes up to 128 padded columns,
 // <4, 96> where every node fits 96 (four groups keep up with the MMAs)
@@ -208,14 +213,14 @@ select_level_ws2_kernel(PlanView pv, Args args) {
     // commit group per tile); each lane then issues 32 cp.async of 16 bytes
     // (the warp's 64 rows x 2 K atoms, four whole row atoms per instruction)
     // and arrives on raw_full once they land.
-    const int r0 = 64 * warp;
+    const int r0 = kLoaderRows * warp;
     TileCursor cur_idx;
     auto issue_idx = [&](int j) {
       if (j < ntile) {
         const TileInfo ti = cur_idx.at(a, s.lv, t_begin + j);
         int32_t* ring = s.idx_ring[j % kIdxRing];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < kLoaderRows / 32; ++h) {
           const int row = r0 + 32 * h + lane;
           if (row < ti.m) tc::cp_async4(ring + row, a.seg_in + s.nd_off[ti.k] + ti.first + row);
           else ring[row] = -1;
@@ -235,17 +240,17 @@ select_level_ws2_kernel(PlanView pv, Args args) {
       tc::cp_async_wait<kIdxAhead - 1>();  // idx(i) landed (one group per tile)
       __syncwarp();                         // ... including the other lanes' entries
       const int32_t* rg = s.idx_ring[i % kIdxRing] + r0;
-      int g[16];
+      int g[kLoaderQ];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) g[q] = rg[4 * q + (lane >> 3)];
+      for (int q = 0; q < kLoaderQ; ++q) g[q] = rg[4 * q + (lane >> 3)];
       uint8_t* stg = stageA + st * kStageBytes + (r0 >> 3) * 1024;
 #pragma unroll
       for (int ka = 0; ka < kMaxKAtoms; ++ka) {
         if (ka < args.katoms) {
           const float* zb = args.Z32 + ka * 32 + 4 * c16;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int r = 4 * q + (lane >> 3);  // row inside the warp's 64
+          for (int q = 0; q < kLoaderQ; ++q) {
+            const int r = 4 * q + (lane >> 3);  // row inside the warp's rows
             uint8_t* dst = stg + ka * kAtomA + (r >> 3) * 1024 + (r & 7) * 128 + ((c16 ^ (r & 7)) << 4);
             // rows past the tile's end land as zeros (no bytes read)
             tc::cp_async16_zfill(dst, g[q] >= 0 ? zb + g[q] * pitch : args.Z32, g[q] >= 0 ? 16u : 0u);
