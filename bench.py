@@ -384,7 +384,7 @@ def main():
         flops_launch = sel_flops / max(1, lvl_n.value // args.steps)
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic_per_launch(n_step),
-                "kernel": "select_level_ws_kernel (tcgen05 3xTF32 tree level)",
+                "kernel": "select_level_ws2_kernel (tcgen05 tree level: tf32 main + bf16 cross pass)",
                 "launch_ms": launch_ms, "launches_timed": int(lvl_n.value),
                 "bytes_per_launch": n_step * per_patch,
                 "work": f"{per_patch} B per patch-level: FP32 row gather + index in/out",
@@ -406,6 +406,28 @@ def main():
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": None, "kernel": dominant}
     roof["phase_ms_per_step"] = {k: round(v, 3) for k, v in phases.items()}
+    # the other kernels against their own bounds (phase times from CUDA events
+    # around each phase; algorithmic bytes / flops per step)
+    iters = len(r.betas)
+    px = int(np.prod(ys.shape)) * iters      # pixels processed per step (all iterations)
+    dmma_peak = 37.2                         # FP64 mma.sync TFLOP/s, tools/dmma_bench.cu (B200)
+    kb = {"extract": (n_patch * (PB + 4 * ppad + 16) + 8 * px,
+                      "writes Z64 (8P) + Z32 (4P_pad) + dc, sq per patch; reads x once"),
+          "aggregate": (n_patch * PB + 16 * px,
+                        "reads Zhat (est + dc, 8P per patch), A^T y; writes x")}
+    kern = {}
+    for name, (nbytes, what) in kb.items():
+        if phases.get(name):
+            gbs = nbytes / (phases[name] / 1e3) / 1e9
+            kern[name] = {"bound": "hbm", "achieved_gbs": round(gbs, 1), "frac": round(gbs / hbm, 3),
+                          "work": what}
+    if phases.get("wiener"):
+        tf = est_flops / (phases["wiener"] / 1e3) / 1e12
+        kern["wiener"] = {"bound": "fp64 tensor (DMMA)", "achieved_tflops": round(tf, 2),
+                          "peak_tflops": dmma_peak, "frac": round(tf / dmma_peak, 3),
+                          "work": "2 x reference estimation_multiplies (gmm.py:254-263); the DMMA "
+                                  "tiles pad the rank to a multiple of 8"}
+    roof["kernels"] = kern
     roof["selection_tflops"] = sel_flops / (phases.get("select", 1e-9) / 1e3) / 1e12
     roof["rescored_fraction"] = float(r.rescored.sum().item()) / max(1, n_patch * 7)
 

@@ -7,7 +7,7 @@
 //
 //   * tcgen05 kind::tf32 reads only the top 19 bits of an FP32 operand
 //     (truncation, tools/tf32_trunc_test.cu), so the raw FP32 patch row is
-//     the hi operand as is.  Two loader warps pull the rows by cp.async
+//     the hi operand as is.  Four loader warps pull the rows by cp.async
 //     (every instruction moves four whole 128-byte row atoms) into one of
 //     four 32 KB raw stages and signal the stage's mbarrier when the copies
 //     land (cp.async.mbarrier.arrive) — three tiles of loads in flight, no
@@ -42,21 +42,27 @@ namespace fepll {
 
 namespace ws2 {
 constexpr int kRows = 128;
-#ifndef FEPLL_WS2_LOADERS
-#define FEPLL_WS2_LOADERS 4
-#endif
-constexpr int kLoaderWarps = FEPLL_WS2_LOADERS;  // warp w: rows kLoaderRows w .., both K atoms
-constexpr int kLoaderRows = kRows / kLoaderWarps;
-constexpr int kLoaderQ = kLoaderRows / 4;         // rows per lane (4 rows per instruction)
-constexpr int kLoaderThreads = 32 * kLoaderWarps;
-constexpr int kConvWarp0 = kLoaderWarps;          // 8 warps: K atom, TMEM lane quarter w%4
-constexpr int kConvWarps = 8;
-constexpr int kMmaWarp = kConvWarp0 + kConvWarps;
-constexpr int kEpiWarp0 = kMmaWarp + 1;
+// warp roles for LW loader warps: warps 0..LW-1 load (warp w: rows
+// 128/LW * w .., both K atoms), the next 8 convert (K atom, TMEM lane quarter
+// w % 4), then the MMA issuer, then 4 NG epilogue warps.  Four loader warps
+// issue a tile's 2048 cp.async 10-15 % faster than two (levels 320 -> 288 us
+// at 64 x 1024^2); eight measured no faster (the LSU, not the issuing warps,
+// is then the limit: tools/ldgsts_rate.cu, 0.98 vs 0.90 us per tile alone)
+template <int LW>
+struct Roles {
+  static constexpr int kLoaderWarps = LW;
+  static constexpr int kLoaderRows = kRows / LW;
+  static constexpr int kLoaderQ = kLoaderRows / 4;  // rows per lane (4 rows per instruction)
+  static constexpr int kLoaderThreads = 32 * LW;
+  static constexpr int kConvWarp0 = LW;
+  static constexpr int kConvWarps = 8;
+  static constexpr int kMmaWarp = kConvWarp0 + kConvWarps;
+  static constexpr int kEpiWarp0 = kMmaWarp + 1;
+};
 // epilogue groups (== TMEM accumulators) and accumulator width are template
 // parameters: <3, 128> for levels with nodes up to 128 padded columns,
 // <4, 96> where every node fits 96 (four groups keep up with the MMAs)
-constexpr int threads_for(int ng) { return (kEpiWarp0 + 4 * ng) * 32; }
+constexpr int threads_for(int ng, int lw) { return (Roles<1>::kEpiWarp0 - 1 + lw + 4 * ng) * 32; }
 constexpr int kStages = 4;              // raw row stages (hi operand)
 constexpr int kLoBufs = 2;              // TMEM lo buffers
 constexpr int kAtomA = kRows * 128;     // bytes of one K atom of A
@@ -151,9 +157,13 @@ struct TileCursor {
   }
 };
 
-template <int NG, int ACC>
-__global__ void __launch_bounds__(threads_for(NG), 1)
+template <int NG, int ACC, int LW>
+__global__ void __launch_bounds__(threads_for(NG, LW), 1)
 select_level_ws2_kernel(PlanView pv, Args args) {
+  using R = Roles<LW>;
+  constexpr int kLoaderWarps = R::kLoaderWarps, kLoaderRows = R::kLoaderRows, kLoaderQ = R::kLoaderQ;
+  constexpr int kLoaderThreads = R::kLoaderThreads, kConvWarp0 = R::kConvWarp0;
+  constexpr int kConvWarps = R::kConvWarps, kMmaWarp = R::kMmaWarp, kEpiWarp0 = R::kEpiWarp0;
   constexpr int kGroups = NG;
   constexpr int kAcc = ACC;                          // accumulator columns (>= node width)
   constexpr uint32_t kXCol0 = NG * ACC;              // TMEM column of A' buffer 0
@@ -220,7 +230,8 @@ select_level_ws2_kernel(PlanView pv, Args args) {
         const TileInfo ti = cur_idx.at(a, s.lv, t_begin + j);
         int32_t* ring = s.idx_ring[j % kIdxRing];
 #pragma unroll
-        for (int h = 0; h < kLoaderRows / 32; ++h) {
+        for (int h = 0; h < (kLoaderRows + 31) / 32; ++h) {
+          if (32 * h + lane >= kLoaderRows) break;
           const int row = r0 + 32 * h + lane;
           if (row < ti.m) tc::cp_async4(ring + row, a.seg_in + s.nd_off[ti.k] + ti.first + row);
           else ring[row] = -1;
@@ -513,12 +524,11 @@ int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double
     return kOk;
   };
   if (p->level_tc_npad[a.depth] <= 96)
-    launch(ws2::select_level_ws2_kernel<4, 96>, sizeof(ws2::Smem<4>), ws2::threads_for(4));
+    launch(ws2::select_level_ws2_kernel<4, 96, 4>, sizeof(ws2::Smem<4>), ws2::threads_for(4, 4));
   else
-    launch(ws2::select_level_ws2_kernel<3, 128>, sizeof(ws2::Smem<3>), ws2::threads_for(3));
+    launch(ws2::select_level_ws2_kernel<3, 128, 4>, sizeof(ws2::Smem<3>), ws2::threads_for(3, 4));
   FEPLL_LAUNCH();
   return kOk;
 }
 
 }  // namespace fepll
-
