@@ -425,8 +425,12 @@ def main():
         tf = est_flops / (phases["wiener"] / 1e3) / 1e12
         kern["wiener"] = {"bound": "fp64 tensor (DMMA)", "achieved_tflops": round(tf, 2),
                           "peak_tflops": dmma_peak, "frac": round(tf / dmma_peak, 3),
-                          "work": "2 x reference estimation_multiplies (gmm.py:254-263); the DMMA "
-                                  "tiles pad the rank to a multiple of 8"}
+                          "executed_tflops": round(2 * tf, 2),
+                          "executed_frac": round(2 * tf / dmma_peak, 3),
+                          "work": "achieved = 2 x reference estimation_multiplies (gmm.py:260-263, "
+                                  "which reuse the selection's projection); executed ~ twice that: "
+                                  "the projection is recomputed in FP64 (selection ran on tf32/bf16 "
+                                  "tensor cores), and the DMMA tiles pad the rank to a multiple of 8"}
     roof["kernels"] = kern
     roof["selection_tflops"] = sel_flops / (phases.get("select", 1e-9) / 1e3) / 1e12
     roof["rescored_fraction"] = float(r.rescored.sum().item()) / max(1, n_patch * 7)

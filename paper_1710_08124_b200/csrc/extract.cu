@@ -170,7 +170,7 @@ extract_pow2_kernel(const double* __restrict__ x, int batch, int H, int W,
 // one SIDE-lane store (64 B / 32 B segments per patch row at SIDE = 8).  No
 // shared memory, no barriers: a few dozen instructions per patch, where the
 // staged tile kernel spends several hundred on its staging loops.
-template <int SIDE>
+template <int SIDE, int U>
 __global__ void __launch_bounds__(256)
 extract_cols_kernel(const double* __restrict__ x, int batch, int H, int W,
                     const int32_t* __restrict__ anchors, int n, double* __restrict__ Z64,
@@ -182,60 +182,69 @@ extract_cols_kernel(const double* __restrict__ x, int batch, int H, int W,
   const int c = lane % SIDE;
   const int64_t total = (int64_t)batch * n;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w * PER_WARP < total;
-       w += warps) {
-    const int64_t g = w * PER_WARP + lane / SIDE;
-    const bool valid = g < total;
-    double v[SIDE];
-    if (valid) {
-      const int b = (int)(g / n);
-      const int i = (int)(g - (int64_t)b * n);
-      const int2 a = __ldg(reinterpret_cast<const int2*>(anchors) + i);
-      const double* src = x + ((int64_t)b * H + a.x) * W + a.y + c;
+  // U consecutive lane groups per warp iteration: all U x SIDE window loads
+  // are issued before the first fold (the kernel is load-latency bound)
+  for (int64_t w0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * U;
+       w0 * PER_WARP < total; w0 += warps * U) {
+    double v[U][SIDE];
+    int64_t g[U];
 #pragma unroll
-      for (int r = 0; r < SIDE; ++r) v[r] = __ldg(src + (int64_t)r * W);
-    } else {
+    for (int u = 0; u < U; ++u) {
+      g[u] = (w0 + u) * PER_WARP + lane / SIDE;
+      if (g[u] < total) {
+        const int b = (int)(g[u] / n);
+        const int i = (int)(g[u] - (int64_t)b * n);
+        const int2 a = __ldg(reinterpret_cast<const int2*>(anchors) + i);
+        const double* src = x + ((int64_t)b * H + a.x) * W + a.y + c;
 #pragma unroll
-      for (int r = 0; r < SIDE; ++r) v[r] = 0.0;
-    }
-    double acc[SIDE];
+        for (int r = 0; r < SIDE; ++r) v[u][r] = __ldg(src + (int64_t)r * W);
+      } else {
 #pragma unroll
-    for (int r = 0; r < SIDE; ++r) acc[r] = v[r];
-#pragma unroll
-    for (int h = SIDE / 2; h >= 1; h >>= 1)
-#pragma unroll
-      for (int r = 0; r < h; ++r) acc[r] = acc[r] + acc[r + h];
-    double col = acc[0];
-#pragma unroll
-    for (int h = SIDE / 2; h >= 1; h >>= 1) {
-      const double o = __shfl_down_sync(0xffffffffu, col, h, SIDE);
-      if (c < h) col = col + o;
-    }
-    const double dc = __shfl_sync(0xffffffffu, col, 0, SIDE) / (double)P;
-    double sq = 0.0;
-    if (valid) {
-      double* zcol = Z64 ? Z64 + g * P + c : nullptr;
-      float* fcol = Z32 ? Z32 + g * z32_pitch + c : nullptr;
-#pragma unroll
-      for (int r = 0; r < SIDE; ++r) {
-        const double z = v[r] - dc;
-        sq = fma(z, z, sq);
-        if (zcol) zcol[r * SIDE] = z;
-        if (fcol) fcol[r * SIDE] = (float)z;
+        for (int r = 0; r < SIDE; ++r) v[u][r] = 0.0;
       }
-      if (fcol)
-        for (int p = P + c; p < z32_pitch; p += SIDE) Z32[g * z32_pitch + p] = 0.0f;
     }
 #pragma unroll
-    for (int h = SIDE / 2; h >= 1; h >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, h, SIDE);
-    if (valid && c == 0) {
-      if (dc_out) dc_out[g] = dc;
-      if (sq_out) sq_out[g] = sq;
+    for (int u = 0; u < U; ++u) {
+      const bool valid = g[u] < total;
+      double acc[SIDE];
+#pragma unroll
+      for (int r = 0; r < SIDE; ++r) acc[r] = v[u][r];
+#pragma unroll
+      for (int h = SIDE / 2; h >= 1; h >>= 1)
+#pragma unroll
+        for (int r = 0; r < h; ++r) acc[r] = acc[r] + acc[r + h];
+      double col = acc[0];
+#pragma unroll
+      for (int h = SIDE / 2; h >= 1; h >>= 1) {
+        const double o = __shfl_down_sync(0xffffffffu, col, h, SIDE);
+        if (c < h) col = col + o;
+      }
+      const double dc = __shfl_sync(0xffffffffu, col, 0, SIDE) / (double)P;
+      double sq = 0.0;
+      if (valid) {
+        double* zcol = Z64 ? Z64 + g[u] * P + c : nullptr;
+        float* fcol = Z32 ? Z32 + g[u] * z32_pitch + c : nullptr;
+#pragma unroll
+        for (int r = 0; r < SIDE; ++r) {
+          const double z = v[u][r] - dc;
+          sq = fma(z, z, sq);
+          if (zcol) zcol[r * SIDE] = z;
+          if (fcol) fcol[r * SIDE] = (float)z;
+        }
+        if (fcol)
+          for (int p = P + c; p < z32_pitch; p += SIDE) Z32[g[u] * z32_pitch + p] = 0.0f;
+      }
+#pragma unroll
+      for (int h = SIDE / 2; h >= 1; h >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, h, SIDE);
+      if (valid && c == 0) {
+        if (dc_out) dc_out[g[u]] = dc;
+        if (sq_out) sq_out[g[u]] = sq;
+      }
     }
   }
 }
 
-int g_extract_variant = 0;  // debug: 1 = staged tile kernel
+int g_extract_variant = 0;  // debug: 1 = staged tile kernel, 2 = U=1, 4 = U=4
 
 // Tiled variant for power-of-two sides on a row-major anchor grid: a block
 // takes PB consecutive anchors of one nominal row (grid_cols anchors per
@@ -412,16 +421,20 @@ extern "C" int fepll_extract(const double* x, int32_t batch, int32_t H, int32_t 
   if (n == 0) return kOk;
   const int64_t total = (int64_t)batch * n;
   cudaStream_t st = (cudaStream_t)stream;
-  if (g_extract_variant == 0 && (side == 8 || side == 4 || side == 16)) {
+  if (g_extract_variant != 1 && (side == 8 || side == 4 || side == 16)) {
     const int per_warp = 32 / side;
     const int64_t warps = (total + per_warp - 1) / per_warp;
-    const int grid = grid_for(warps, 8, 148 * 8);
-    if (side == 8)
-      extract_cols_kernel<8><<<grid, 256, 0, st>>>(x, batch, H, W, anchors, n, Z64, Z32, z32_pitch, dc, sq);
-    else if (side == 4)
-      extract_cols_kernel<4><<<grid, 256, 0, st>>>(x, batch, H, W, anchors, n, Z64, Z32, z32_pitch, dc, sq);
-    else
-      extract_cols_kernel<16><<<grid, 256, 0, st>>>(x, batch, H, W, anchors, n, Z64, Z32, z32_pitch, dc, sq);
+    const int u = g_extract_variant == 0 ? 2 : g_extract_variant == 2 ? 1 : 4;  // debug 2: U=1, 4: U=4
+    const int grid = grid_for((warps + u - 1) / u, 8, 148 * 8);
+#define FEPLL_EXT(S, U) extract_cols_kernel<S, U><<<grid, 256, 0, st>>>(x, batch, H, W, anchors, n, Z64, Z32, z32_pitch, dc, sq)
+    if (side == 8) {
+      if (u == 1) FEPLL_EXT(8, 1); else if (u == 2) FEPLL_EXT(8, 2); else FEPLL_EXT(8, 4);
+    } else if (side == 4) {
+      FEPLL_EXT(4, 2);
+    } else {
+      FEPLL_EXT(16, 1);
+    }
+#undef FEPLL_EXT
   } else if (grid_cols > 0 && n % grid_cols == 0 && (side == 8 || side == 4 || side == 16) &&
       (Z32 == nullptr || z32_pitch % 4 == 0)) {
     if (side == 8)
