@@ -41,8 +41,9 @@ constexpr int kMaxRows = 128;
 struct Head {
   int32_t tpre[kMaxLevelNodes + 1];
   uint64_t scan_tmp[256];
-  int32_t leaf_v[kMaxLevelNodes];   // leaf BFS id, bucket count and offset
-  int32_t leaf_cnt[kMaxLevelNodes];
+  int32_t leaf_cr[kMaxLevelNodes];  // component | rank << 16, bucket count and offset,
+  int32_t leaf_cnt[kMaxLevelNodes]; // gamma_tail at this iteration: every per-tile
+  double leaf_gt[kMaxLevelNodes];   // constant from smem (no global round trip per tile)
   int64_t leaf_off[kMaxLevelNodes];
   int32_t rows[8][kMaxRows];        // patch-index ring (2 x stages slots)
   int32_t t_begin, t_end;
@@ -128,7 +129,9 @@ struct Geo {
 // NT2-1, runs before phase-1 k-step s: the caller issues the next tile's row
 // copies there, so their issue shares the SM with the DMMAs instead of
 // preceding them.
-template <int NT2, int NT1, class Step>
+// RW = 16: the warp's rows g and g + 8 (two DMMAs per B fragment); RW = 8:
+// row g only (half the accumulators and registers, twice the warps per SM)
+template <int NT2, int NT1, int RW, class Step>
 __device__ __forceinline__ void wiener_rows(const double* za, const double* zb, const double* Us, int uld,
                                             const double* sh, int t4, int g4, Step&& step,
                                             double (&acc2)[NT2][4]) {
@@ -138,7 +141,8 @@ __device__ __forceinline__ void wiener_rows(const double* za, const double* zb, 
 #pragma unroll
   for (int k0 = 0; k0 < NT2 * 8; k0 += 8) {  // NT2 * 8 == Pn
     step(k0 / 8);
-    const double a0 = za[k0], a1 = zb[k0], a2 = za[k0 + 4], a3 = zb[k0 + 4];
+    const double a0 = za[k0], a2 = za[k0 + 4];
+    const double a1 = RW == 16 ? zb[k0] : 0.0, a3 = RW == 16 ? zb[k0 + 4] : 0.0;
     const double* u0 = Us + (k0 + t4) * uld + g4;
     const double* u1 = u0 + 4 * uld;
     double b0[NT1], b1[NT1];
@@ -152,12 +156,12 @@ __device__ __forceinline__ void wiener_rows(const double* za, const double* zb, 
 #pragma unroll
     for (int n = 0; n < NT1; ++n) {
       dmma8(acc[n][0], acc[n][1], a0, b0[n]);
-      dmma8(acc[n][2], acc[n][3], a1, b0[n]);
+      if (RW == 16) dmma8(acc[n][2], acc[n][3], a1, b0[n]);
     }
 #pragma unroll
     for (int n = 0; n < NT1; ++n) {
       dmma8(acc[n][0], acc[n][1], a2, b1[n]);
-      dmma8(acc[n][2], acc[n][3], a3, b1[n]);
+      if (RW == 16) dmma8(acc[n][2], acc[n][3], a3, b1[n]);
     }
   }
   // C = acc * shrink: lane (g, t) holds C[g][8n + 2t + e] (acc[n][e]) and
@@ -167,8 +171,10 @@ __device__ __forceinline__ void wiener_rows(const double* za, const double* zb, 
     const int col = n * 8 + 2 * t4;
     acc[n][0] *= sh[col];
     acc[n][1] *= sh[col + 1];
-    acc[n][2] *= sh[col];
-    acc[n][3] *= sh[col + 1];
+    if (RW == 16) {
+      acc[n][2] *= sh[col];
+      acc[n][3] *= sh[col + 1];
+    }
   }
 #pragma unroll
   for (int n = 0; n < NT2; ++n) acc2[n][0] = acc2[n][1] = acc2[n][2] = acc2[n][3] = 0.0;
@@ -181,14 +187,19 @@ __device__ __forceinline__ void wiener_rows(const double* za, const double* zb, 
   for (int kb = 0; kb < NT1; ++kb) {
     double a[4];
     {
+      // the source lane sends the element the receiver's parity needs
       const double e0 = __shfl_sync(0xffffffffu, acc[kb][0], q0), e1 = __shfl_sync(0xffffffffu, acc[kb][1], q0);
-      const double f0 = __shfl_sync(0xffffffffu, acc[kb][2], q0), f1 = __shfl_sync(0xffffffffu, acc[kb][3], q0);
       const double h0 = __shfl_sync(0xffffffffu, acc[kb][0], q1), h1 = __shfl_sync(0xffffffffu, acc[kb][1], q1);
-      const double j0 = __shfl_sync(0xffffffffu, acc[kb][2], q1), j1 = __shfl_sync(0xffffffffu, acc[kb][3], q1);
       a[0] = odd ? e1 : e0;
-      a[1] = odd ? f1 : f0;
       a[2] = odd ? h1 : h0;
-      a[3] = odd ? j1 : j0;
+      if (RW == 16) {
+        const double f0 = __shfl_sync(0xffffffffu, acc[kb][2], q0), f1 = __shfl_sync(0xffffffffu, acc[kb][3], q0);
+        const double j0 = __shfl_sync(0xffffffffu, acc[kb][2], q1), j1 = __shfl_sync(0xffffffffu, acc[kb][3], q1);
+        a[1] = odd ? f1 : f0;
+        a[3] = odd ? j1 : j0;
+      } else {
+        a[1] = a[3] = 0.0;
+      }
     }
     const double* u0 = Us + g4 * uld + 8 * kb + t4;  // U[8n + g][k + t] = U^T[k][n]
     double b0[NT2], b1[NT2];
@@ -200,18 +211,18 @@ __device__ __forceinline__ void wiener_rows(const double* za, const double* zb, 
 #pragma unroll
     for (int n = 0; n < NT2; ++n) {
       dmma8(acc2[n][0], acc2[n][1], a[0], b0[n]);
-      dmma8(acc2[n][2], acc2[n][3], a[1], b0[n]);
+      if (RW == 16) dmma8(acc2[n][2], acc2[n][3], a[1], b0[n]);
     }
 #pragma unroll
     for (int n = 0; n < NT2; ++n) {
       dmma8(acc2[n][0], acc2[n][1], a[2], b1[n]);
-      dmma8(acc2[n][2], acc2[n][3], a[3], b1[n]);
+      if (RW == 16) dmma8(acc2[n][2], acc2[n][3], a[3], b1[n]);
     }
   }
 }
 
-template <int NT2, int MT, int NS>
-__global__ void __launch_bounds__(MT * 2)
+template <int NT2, int MT, int NS, int RW>
+__global__ void __launch_bounds__(MT / RW * 32, RW == 8 ? 2 : 1)
 wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, int n_leaf_nodes,
                    const int32_t* __restrict__ cnt, const int64_t* __restrict__ off,
                    const int32_t* __restrict__ leafseg, const double* __restrict__ Z64,
@@ -219,7 +230,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
                    Geo geo) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int kRows = MT;
-  constexpr int kThreads = MT * 2;  // one warp per 16 rows
+  constexpr int kThreads = MT / RW * 32;  // one warp per RW rows
   Head& h = *reinterpret_cast<Head*>(smem);
   constexpr int kRing = 2 * NS;      // index ring slots
   constexpr int kLead = 2 * NS - 2;  // tiles of indices fetched ahead of their rows' issue
@@ -236,7 +247,9 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
   }
   for (int k = tid; k < n_leaf_nodes; k += kThreads) {
     const int v = leaf_nodes[k];
-    h.leaf_v[k] = v;
+    const int comp = pv.leaf_index[v];
+    h.leaf_cr[k] = comp | (pv.model_rank[comp] << 16);
+    h.leaf_gt[k] = pv.model_gamma_tail[(int64_t)t * pv.K + comp];
     h.leaf_cnt[k] = cnt[v];
     h.leaf_off[k] = off[v];
     h.tpre[k] = (cnt[v] + kRows - 1) / kRows;
@@ -256,9 +269,12 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
   // issued NS - 1 tiles ahead of its compute; its patch indices land in ring
   // slot j % kRing another NS - 1 tiles earlier — no global round trip on
   // the compute path, NS - 1 tiles of random 8P-byte row reads in flight.
+  int fli = prefix_find(h.tpre, n_leaf_nodes, t_begin);  // leaf of the next index fetch
+  int cli = fli;                                         // leaf of the computed tile
   auto fetch_rows = [&](int j) {
     if (j < t_end && tid < kRows) {
-      const int li = prefix_find(h.tpre, n_leaf_nodes, j);
+      while (fli + 1 < n_leaf_nodes && h.tpre[fli + 1] <= j) ++fli;  // tiles ascend
+      const int li = fli;
       const int first = (j - h.tpre[li]) * kRows;
       int32_t* dst = &h.rows[(j - t_begin) % kRing][tid];
       if (tid < h.leaf_cnt[li] - first)
@@ -305,9 +321,10 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
   for (int tile = t_begin; tile < t_end; ++tile) {
     const int i = tile - t_begin;
     const int slot = i % kRing;
-    const int li = prefix_find(h.tpre, n_leaf_nodes, tile);
-    const int comp = pv.leaf_index[h.leaf_v[li]];
-    const int r = pv.model_rank[comp];
+    while (cli + 1 < n_leaf_nodes && h.tpre[cli + 1] <= tile) ++cli;  // tiles ascend
+    const int li = cli;
+    const int comp = h.leaf_cr[li] & 0xFFFF;
+    const int r = h.leaf_cr[li] >> 16;
     wstamp(i, 0);
     bulk_wait_read();  // the previous tile's row stores have left its buffer
     cp_async_wait_group<NS - 2>();
@@ -329,8 +346,8 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
     wstamp(i, 2);
     const double* Zs = Zs0 + (i % NS) * kRows * geo.zld;
     const int g4 = lane >> 2, t4 = lane & 3;
-    const int m0 = warp * 16;
-    const double* za = Zs + (m0 + g4) * geo.zld + t4;       // rows g, g+8 of the warp
+    const int m0 = warp * RW;
+    const double* za = Zs + (m0 + g4) * geo.zld + t4;       // rows g (, g+8) of the warp
     const double* zb = za + 8 * geo.zld;
     // ---- phase 1: C[m0..m0+15][0..R8) = (Z . U) * shrink, with the
     // leaf's n-tile count as a compile-time constant (predicated-off DMMAs
@@ -342,20 +359,21 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
     // the whole copy here.
     const int jn = tile + NS - 1;
     const bool inter = kInterleave && P == 64 && jn < t_end;
-    int gsl[16];
+    constexpr int kRowsPerThread = kRows / kWarps;  // == RW: RW / 8 rows per k-step
+    int gsl[kRowsPerThread];
     double* zn = Zs0 + ((jn - t_begin) % NS) * kRows * geo.zld + 2 * lane;
     double* dcn = dcs + ((jn - t_begin) % NS) * kRows;
     if (inter) {
       const int32_t* rn = h.rows[(jn - t_begin) % kRing];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) gsl[q] = rn[warp + kWarps * q];
+      for (int q = 0; q < kRowsPerThread; ++q) gsl[q] = rn[warp + kWarps * q];
     } else {
       fetch_z_slices(jn, 0, n_slices);
     }
     auto zstep = [&](int st) {
       if (!inter) return;
 #pragma unroll
-      for (int q = 2 * st; q < 2 * st + 2; ++q) {
+      for (int q = st * (kRowsPerThread / 8); q < (st + 1) * (kRowsPerThread / 8); ++q) {
         double* d = zn + (warp + kWarps * q) * geo.zld;
         if (gsl[q] >= 0) {
           cp_async16(d, Z64 + (int64_t)gsl[q] * 64 + 2 * lane);
@@ -368,26 +386,26 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
     };
     double acc[NT2][4];
     switch ((r + 7) / 8) {
-      case 1: wiener_rows<NT2, 1>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
-      case 2: wiener_rows<NT2, 2>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
-      case 3: wiener_rows<NT2, 3>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
-      case 4: wiener_rows<NT2, 4>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
-      case 5: wiener_rows<NT2, 5>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
-      case 6: wiener_rows<NT2, 6>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
-      case 7: wiener_rows<NT2, 7>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
-      default: wiener_rows<NT2, 8>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 1: wiener_rows<NT2, 1, RW>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 2: wiener_rows<NT2, 2, RW>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 3: wiener_rows<NT2, 3, RW>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 4: wiener_rows<NT2, 4, RW>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 5: wiener_rows<NT2, 5, RW>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 6: wiener_rows<NT2, 6, RW>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 7: wiener_rows<NT2, 7, RW>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      default: wiener_rows<NT2, 8, RW>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
     }
     cp_async_commit();
     wstamp(i, 3);
     {
       wstamp(i, 4);
-      const double gt = pv.model_gamma_tail[(int64_t)t * pv.K + comp];
+      const double gt = h.leaf_gt[li];
       // Zhat + dc = (acc + gamma_tail z) + dc, written over this warp's own
       // rows of Zs (each element read and written by the same lane)...
       double* zw = const_cast<double*>(Zs);
       const double* dct = dcs + (i % NS) * kRows;
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
+      for (int half = 0; half < RW / 8; ++half) {
         double* zr = zw + (m0 + g4 + 8 * half) * geo.zld;
         const double d = dc ? dct[m0 + g4 + 8 * half] : 0.0;
 #pragma unroll
@@ -407,7 +425,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       // coalesced 16-byte stores from the same rows measured slower)
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane < 16) {
+      if (lane < RW) {
         const int gidx = h.rows[slot][m0 + lane];
         if (gidx >= 0) {
           const int64_t orow =  // padded image pitch (no division when dense)
@@ -425,6 +443,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
 }  // namespace wn
 
 int g_wiener_pair = 1;
+int g_wiener_rw = 8;  // rows per warp in the two-CTAs-per-SM configuration (debug: 16)
 int g_wiener_dc = 1;  // debug: 0 = write est only (the gather then adds dc)
 
 int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zhat, int n_img,
@@ -461,11 +480,13 @@ int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zha
   FEPLL_REQUIRE(smem_for(mt, ns) <= cap, "wiener: tile buffers exceed shared memory");
   const size_t smem = smem_for(mt, ns);
   const int nt2 = geo.Pn / 8;
+  const int rw = pair && g_wiener_rw == 8 ? 8 : 16;
+  const int threads = mt / rw * 32;
   auto launch = [&](auto kernel) -> int {
     FEPLL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, mt * 2, smem);
-    kernel<<<kSMs * std::max(1, per_sm), mt * 2, smem, st>>>(
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    kernel<<<kSMs * std::max(1, per_sm), threads, smem, st>>>(
         p->v, t, p->d_leaf_nodes, p->n_leaf_nodes, p->rs.cnt, p->rs.off, p->rs.leafseg, Z64,
         g_wiener_dc ? dc : nullptr,
         Zhat, n_img, zrows, geo);
@@ -474,9 +495,10 @@ int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zha
   };
 #define FEPLL_WN_CASE(N)                                                   \
   case N:                                                                  \
-    return big ? launch(wn::wiener_dmma_kernel<N, 128, 2>)                 \
-               : ns == 4 ? launch(wn::wiener_dmma_kernel<N, 64, 4>)        \
-                         : launch(wn::wiener_dmma_kernel<N, 64, 2>);
+    return big ? launch(wn::wiener_dmma_kernel<N, 128, 2, 16>)             \
+               : ns == 4 ? launch(wn::wiener_dmma_kernel<N, 64, 4, 16>)    \
+               : rw == 8 ? launch(wn::wiener_dmma_kernel<N, 64, 2, 8>)     \
+                         : launch(wn::wiener_dmma_kernel<N, 64, 2, 16>);
   switch (nt2) {
     FEPLL_WN_CASE(1)
     FEPLL_WN_CASE(2)
@@ -516,5 +538,10 @@ extern "C" int fepll_debug_wiener_trace(void* device_buffer) {
 
 extern "C" int fepll_debug_wiener_dc(int32_t on) {
   fepll::g_wiener_dc = on;
+  return 0;
+}
+
+extern "C" int fepll_debug_wiener_rw(int32_t rw) {
+  fepll::g_wiener_rw = rw;
   return 0;
 }
