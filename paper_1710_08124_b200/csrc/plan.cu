@@ -175,6 +175,9 @@ static void free_scratch(Plan* p) {
   RouteScratch& r = p->rs;
   cudaFree(r.seg[0]);
   cudaFree(r.seg[1]);
+  cudaFree(r.segsq[0]);
+  cudaFree(r.segsq[1]);
+  r.segsq[0] = r.segsq[1] = nullptr;
   cudaFree(r.leafseg);
   cudaFree(r.queue);
   r.seg[0] = r.seg[1] = r.leafseg = r.queue = nullptr;
@@ -191,6 +194,8 @@ static int reserve(Plan* p, int64_t max_patches) {
   const int64_t lseg = np * std::max(1, p->max_leaf_children);
   FEPLL_CUDA(cudaMalloc(&r.seg[0], sizeof(int32_t) * std::max(seg, np)));  // level 0 = all patches
   FEPLL_CUDA(cudaMalloc(&r.seg[1], sizeof(int32_t) * seg));
+  FEPLL_CUDA(cudaMalloc(&r.segsq[0], sizeof(double) * std::max(seg, np)));
+  FEPLL_CUDA(cudaMalloc(&r.segsq[1], sizeof(double) * seg));
   FEPLL_CUDA(cudaMalloc(&r.leafseg, sizeof(int32_t) * lseg));
   r.queue_cap = std::max<int64_t>(1024, max_patches);
   FEPLL_CUDA(cudaMalloc(&r.queue, sizeof(int32_t) * 2 * r.queue_cap));

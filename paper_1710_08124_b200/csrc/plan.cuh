@@ -51,6 +51,7 @@ struct RouteScratch {
   int64_t cap = 0;          // patches
   int64_t seg_cap = 0;      // entries per segment buffer
   int32_t* seg[2] = {nullptr, nullptr};
+  double* segsq[2] = {nullptr, nullptr};  // ||z||^2 alongside seg[] (ws2 levels read it coalesced)
   int32_t* leafseg = nullptr;
   int32_t* cnt = nullptr;     // [n_nodes] patches routed into the node this call
   int64_t* off = nullptr;     // [n_nodes] segment offset (internal: seg buf, leaf: leafseg)

@@ -28,6 +28,11 @@ struct LevelArgs {
   int64_t* leaf_base;
   int32_t* labels;
   int t;
+  // ||z||^2 in segment order (ws2 levels): read at the rows' segment
+  // positions instead of a random 8-byte gather sq[patch], written next to
+  // the routed index for the next level; nullptr = not kept
+  const double* sq_in = nullptr;
+  double* sq_out = nullptr;
 };
 
 template <int NMAX>

@@ -225,6 +225,7 @@ rescore_fp64_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restr
       const int slot = atomicAdd(&a.cnt[v], 1);
       if (pv.child_count[v] > 0) {
         a.seg_out[a.off[v] + slot] = patch;
+        if (a.sq_out) a.sq_out[a.off[v] + slot] = sq[patch];
       } else {
         a.leafseg[a.off[v] + slot] = patch;
         a.labels[patch] = pv.leaf_index[v];
@@ -449,6 +450,7 @@ int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double
 // loader / converter warps; measured faster on every level of the cfg5
 // tree), 2: ws2 on levels of <= 16 nodes, ws on the wider ones
 int g_select_variant = 1;
+int g_seg_sq = 1;  // debug: 0 = ws2 levels gather sq[patch] as before
 int select_level_ws(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                     cudaStream_t st);
 
@@ -523,8 +525,21 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
   FEPLL_LAUNCH();
   if (root_leaf < 0) {
     PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P), n_img};
+    // which levels run the ws2 kernel (the dispatch below): consecutive ws2
+    // levels hand ||z||^2 over in segment order
+    auto is_ws2 = [&](int d) {
+      if (d < 0 || d >= p->n_levels || mode != 1 || p->v.P > 128) return false;
+      const bool wide = p->level_wide[d] || p->level_tc_npad[d] > 256;
+      return !wide && select_ws_supported(p, d) && p->v.tc_x != nullptr &&
+             (g_select_variant == 1 ||
+              (g_select_variant == 2 && p->level_start[d + 1] - p->level_start[d] <= 16));
+    };
     for (int d = 0; d < p->n_levels; ++d) {
       LevelArgs a = make_level(p, d, t, labels);
+      if (g_seg_sq && is_ws2(d)) {
+        a.sq_in = d == 0 ? sq : is_ws2(d - 1) ? p->rs.segsq[d & 1] : nullptr;
+        a.sq_out = is_ws2(d + 1) ? p->rs.segsq[(d + 1) & 1] : nullptr;
+      }
       int rc = kOk;
       const bool prof = p->prof_used < (int)p->prof_ev.size() / 2;
       if (prof) FEPLL_CUDA(cudaEventRecord(p->prof_ev[2 * p->prof_used], st));
@@ -557,6 +572,11 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
     FEPLL_LAUNCH();
   }
   return kOk;
+}
+
+extern "C" int fepll_debug_seg_sq(int32_t v) {
+  fepll::g_seg_sq = v;
+  return 0;
 }
 
 extern "C" int fepll_debug_select_variant(int32_t v) {

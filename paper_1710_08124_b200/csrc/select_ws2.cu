@@ -405,6 +405,7 @@ select_level_ws2_kernel(PlanView pv, Args args) {
     // pending (previous tile's) route of this thread's row
     bool p_valid = false;
     int p_kind = 0, p_key = 0, p_lrank = 0, p_g = 0, p_u = 0, p_leaf = 0;
+    double p_sq = 0.0;
     int64_t p_b0 = 0;
     int res = 0, res_key = -1;  // this thread's in-flight global atomic (count reservation)
     int it = 0;
@@ -418,6 +419,7 @@ select_level_ws2_kernel(PlanView pv, Args args) {
         args.queue[2 * slot + 1] = p_u;
       } else if (p_kind == 1) {
         a.seg_out[p_b0 + slot] = p_g;
+        if (a.sq_out) a.sq_out[p_b0 + slot] = p_sq;
       } else {
         a.leafseg[p_b0 + slot] = p_g;
         a.labels[p_g] = p_leaf;
@@ -430,8 +432,9 @@ select_level_ws2_kernel(PlanView pv, Args args) {
       const int u = ti.u;
       const int nk = s.nd_nk[ti.k];
       const bool valid = row < ti.m;
-      const int g = valid ? a.seg_in[s.nd_off[ti.k] + ti.first + row] : -1;
-      const double sqv = valid ? args.sq[g] : 0.0;
+      const int64_t spos = s.nd_off[ti.k] + ti.first + row;  // segment position
+      const int g = valid ? a.seg_in[spos] : -1;
+      const double sqv = valid ? (a.sq_in ? a.sq_in[spos] : args.sq[g]) : 0.0;
       if (u != E.node) {
         named_bar(bar_id, 128);  // everyone done with the previous tables
         epi_load_node(pv, t, u, E.ch, etid, 128);
@@ -476,6 +479,7 @@ select_level_ws2_kernel(PlanView pv, Args args) {
         p_key = key;
         p_lrank = lrank;
         p_g = g;
+        p_sq = sqv;
         p_u = u;
         if (key == kMaxChildren) {
           p_kind = 0;
