@@ -114,12 +114,14 @@ int fepll_extract(const double* x, int32_t batch, int32_t H, int32_t W, int32_t 
  * ([batch][H][W]) at anchors ([n_img][2]) minus dc (patches.py:178).
  * mode 0: exact FP64 scoring; mode 1: tcgen05 3xTF32 scoring with
  * margin-guarded FP64 re-scoring (needs Z32, the FP32 patch rows written by
- * fepll_extract).  guard <= 0 selects the default bound 2^-16 (tc_epi.cuh).
+ * fepll_extract).  Z64 (optional, the FP64 rows of fepll_extract, bitwise
+ * the re-extracted values) saves the exact / re-scoring paths the window
+ * reads.  guard <= 0 selects the default bound 2^-16 (tc_epi.cuh).
  * labels: [n_total] int32 leaf indices.  leaf_counts (optional, device
  * int64 [K]) receives the label histogram. */
 int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32_t W,
                  const int32_t* anchors, int32_t n_img, const double* dc, const double* sq,
-                 const float* Z32, int64_t n_total, int32_t mode, double guard,
+                 const float* Z32, const double* Z64, int64_t n_total, int32_t mode, double guard,
                  int32_t* labels, int64_t* leaf_counts, void* stream);
 
 /* diagnostics: per-level count of decisions the last tensor-mode select sent

@@ -27,6 +27,7 @@ struct PatchSrc {
   const double* dc;       // [B*n_img]
   int n_img, H, W, side;
   int zrows;              // Zhat rows per image (>= n_img; padded pitch)
+  const double* z64 = nullptr;  // FP64 patch rows of fepll_extract (bitwise window - dc), or NULL
   __device__ __forceinline__ int64_t zrow(int g) const {
     return zrows == n_img ? (int64_t)g : (int64_t)(g / n_img) * zrows + g % n_img;
   }
@@ -34,6 +35,11 @@ struct PatchSrc {
 
 // warp: zs[0..P) = window(g) - dc[g]
 __device__ __forceinline__ void load_patch(const PatchSrc& ps, int g, int P, double* zs) {
+  if (ps.z64) {  // the extracted row: one round trip instead of anchors -> image -> dc
+    for (int p = lane_id(); p < P; p += 32) zs[p] = ps.z64[(int64_t)g * P + p];
+    __syncwarp();
+    return;
+  }
   const int b = g / ps.n_img;
   const int ia = g - b * ps.n_img;
   const int pr = ps.anchors[2 * ia], pc = ps.anchors[2 * ia + 1];
@@ -461,8 +467,9 @@ static int side_of(int P) {
 }
 
 int rescore_queue_x(Plan* p, const LevelArgs& a, const double* x, const int32_t* anchors, int n_img,
-                    int H, int W, const double* dc, const double* sq, cudaStream_t st) {
-  PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P), n_img};
+                    int H, int W, const double* dc, const double* sq, const double* Z64,
+                    cudaStream_t st) {
+  PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P), n_img, Z64};
   rescore_fp64_kernel<<<4 * kSMs, kSelWarps * 32, 0, st>>>(p->v, a, ps, sq, p->rs.queue,
                                                            p->rs.queue_len);
   FEPLL_LAUNCH();
@@ -497,7 +504,8 @@ using namespace fepll;
 
 extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32_t W,
                             const int32_t* anchors, int32_t n_img, const double* dc,
-                            const double* sq, const float* Z32, int64_t n_total, int32_t mode,
+                            const double* sq, const float* Z32, const double* Z64,
+                            int64_t n_total, int32_t mode,
                             double guard, int32_t* labels, int64_t* leaf_counts, void* stream) {
   Plan* p = reinterpret_cast<Plan*>(plan);
   FEPLL_REQUIRE(p != nullptr && labels != nullptr && sq != nullptr && x != nullptr &&
@@ -524,7 +532,7 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
       n_total, p->rs.seg[0], p->rs.cnt, p->rs.off, p->rs.leaf_base, labels, root_leaf);
   FEPLL_LAUNCH();
   if (root_leaf < 0) {
-    PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P), n_img};
+    PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P), n_img, Z64};
     // which levels run the ws2 kernel (the dispatch below): consecutive ws2
     // levels hand ||z||^2 over in segment order
     auto is_ws2 = [&](int d) {
@@ -555,7 +563,7 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
                         : select_level_ws(p, a, Z32, sq, guard, st))
                  : select_level_tc(p, a, Z32, sq, guard, st);
         if (prof) FEPLL_CUDA(cudaEventRecord(p->prof_ev[2 * p->prof_used++ + 1], st));
-        if (!rc) rc = rescore_queue_x(p, a, x, anchors, n_img, H, W, dc, sq, st);
+        if (!rc) rc = rescore_queue_x(p, a, x, anchors, n_img, H, W, dc, sq, Z64, st);
       } else {  // exact mode, or P > 128 (beyond the tcgen05 kernels' K atoms):
                 // FP64 scoring (wide nodes: block-wise scan) — the same labels
         select_level_fp64_kernel<<<grid_for(n_total, kSelWarps, 148 * 8), kSelWarps * 32, 0, st>>>(

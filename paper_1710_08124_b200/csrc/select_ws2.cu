@@ -214,6 +214,11 @@ select_level_ws2_kernel(PlanView pv, Args args) {
   tc::fence_after_sync();
   const uint32_t tmem = s.tmem_base;
   const int t_begin = s.t_begin, t_end = s.t_end;
+  if (args.trace && tid == 0) {  // CTA span on the global clock (load-balance check)
+    uint64_t g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    args.trace[((size_t)blockIdx.x * 64 + 63) * 16 + 14] = g;
+  }
   const int ntile = t_end - t_begin;
   const int t = a.t;
 
@@ -499,6 +504,11 @@ select_level_ws2_kernel(PlanView pv, Args args) {
   }
   tc::fence_before_sync();
   __syncthreads();
+  if (args.trace && tid == 0) {
+    uint64_t g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    args.trace[((size_t)blockIdx.x * 64 + 63) * 16 + 15] = g;
+  }
   if (warp == kMmaWarp) tc::tmem_dealloc(tmem, kTmemCols);
 }
 

@@ -377,7 +377,8 @@ class Restorer:
                N.ptr(self.Z64), N.ptr(self.Z32), self.z32_pitch, N.ptr(self.dc), N.ptr(self.sq), st)
         self._mark(timer, "extract")
         N.call("fepll_select", self.plan.handle, t, N.ptr(self.x), H, W, N.ptr(anchors), n,
-               N.ptr(self.dc), N.ptr(self.sq), N.ptr(self.Z32), nt, mode, float(self.guard),
+               N.ptr(self.dc), N.ptr(self.sq), N.ptr(self.Z32), N.ptr(self.Z64), nt, mode,
+               float(self.guard),
                N.ptr(self.labels), N.ptr(self.leaf_counts[t]), st)
         N.call("fepll_select_rescored", self.plan.handle, N.ptr(self.rescored[t]), st)
         self._mark(timer, "select")

@@ -36,3 +36,11 @@ m = lambda a, b: np.median((tr[:, 3:39, b] - tr[:, 3:39, a])[tr[:, 3:39, b] > 0]
 print("MMA loop: prev issued -> top", np.median((tr[:, 3:39, 10] - tr[:, 2:38, 3])[tr[:, 3:39, 10] > 0]),
       "acc_empty wait", m(10, 9), "lo_full wait", m(9, 2))
 print("converter: raw_full passed (p0) - loader issued (slot 7)", m(7, 0))
+
+g0 = tr[:, 63, 14] * 1.965; g1 = tr[:, 63, 15] * 1.965  # globaltimer ns (undo the cycle scaling)
+ok = (g0 > 0) & (g1 > 0)
+if ok.any():
+    span = g1[ok] - g0[ok]
+    print(f"CTA spans (globaltimer): mean {span.mean()/1e3:.1f} us, max {span.max()/1e3:.1f} us; "
+          f"kernel start->last CTA end {(g1[ok].max() - g0[ok].min())/1e3:.1f} us; "
+          f"first CTA end {(g1[ok].min() - g0[ok].min())/1e3:.1f} us")
