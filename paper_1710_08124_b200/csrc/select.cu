@@ -158,11 +158,19 @@ __device__ __forceinline__ int score_children_fp64(const PlanView& pv, int t, in
   const int32_t* kids = pv.child_list + pv.child_start[u];
   double best = INFINITY;
   int bestk = 0;
+  // one block of all children when they fit (width = sum of the child ranks,
+  // plan.py): the block split below walks the children with two dependent
+  // loads each, the longest chain of the re-scoring kernel
+  const bool one_block = nk <= 32 && width <= kMaxGroupCols;
   for (int k0 = 0; k0 < nk;) {
-    const int col0 = pv.child_col_off[kids[k0]];
-    int k1 = k0, cols = 0;
-    while (k1 < nk && k1 - k0 < 32 && cols + pv.node_rank[kids[k1]] <= kMaxGroupCols)
-      cols += pv.node_rank[kids[k1++]];
+    int col0 = 0, k1 = nk, cols = width;
+    if (!one_block) {
+      col0 = pv.child_col_off[kids[k0]];
+      k1 = k0;
+      cols = 0;
+      while (k1 < nk && k1 - k0 < 32 && cols + pv.node_rank[kids[k1]] <= kMaxGroupCols)
+        cols += pv.node_rank[kids[k1++]];
+    }
     block_terms(G + col0, w + col0, width, cols, P, zs, lane, tv);
     double b;
     int bk;
