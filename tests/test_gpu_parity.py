@@ -463,3 +463,38 @@ def test_operator_adjoint_identity_and_normal(name):
         nx = torch.empty(A.input_dims, dtype=torch.float64, device="cuda")
         op.normal(xd, 0.5, nx, st)
         np.testing.assert_allclose(nx.cpu().numpy(), o.normal(x) + 0.5 * x, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("knob,values", [
+    ("fepll_debug_wiener_rw", (8, 16)),          # Wiener: 8 vs 16 rows per warp
+    ("fepll_debug_seg_sq", (1, 0)),              # ws2: segment-order ||z||^2 vs gather
+    ("fepll_debug_extract_variant", (0, 1, 2)),  # extraction: 2 / staged tile / 1 group per pass
+    ("fepll_debug_select_variant", (1, 0)),      # tree level: ws2 vs ws kernel
+])
+def test_kernel_variants_bitwise_equal(knob, values, models):
+    """Every performance variant kept behind a debug switch computes the same
+    images and labels bit for bit (same FP64 operation order per element),
+    on a batch that exercises the cover gather and the DMMA Wiener kernel."""
+    import ctypes
+    import torch
+    from paper_1710_08124_b200 import Restorer, RestorationConfig, synthetic, _native as N
+
+    model, tree = models[64]
+    cases = [synthetic.baseline_case("cfg1", 144, image_seed=i, noise_seed=70 + i) for i in range(3)]
+    y = torch.from_numpy(np.stack([c.y for c in cases])).cuda()
+    fn = getattr(N.lib(), knob)
+    fn.argtypes = [ctypes.c_int32]
+    r = Restorer(cases[0].A, model, tree, RestorationConfig(sigma=20.0, spacing=4, seed=9), batch=3)
+    outs = []
+    try:
+        for v in values:
+            fn(v)
+            x, rec = r.run(y, trace=True)
+            outs.append((x.cpu().numpy().copy(), [t["labels"] for t in rec]))
+    finally:
+        fn(values[0])
+    x0, l0 = outs[0]
+    for x1, l1 in outs[1:]:
+        assert np.array_equal(x0, x1)
+        for a, b in zip(l0, l1):
+            np.testing.assert_array_equal(a, b)
