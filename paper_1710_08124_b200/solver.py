@@ -237,6 +237,7 @@ class Restorer:
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.rescored = torch.zeros((config.iterations, 64), dtype=torch.int32, device=dev)
         self.x = torch.empty((B, H, W), dtype=f64, device=dev)
+        self._y_in = None  # identity restores: the observation, read in place
         self.xt = torch.empty((B, H, W), dtype=f64, device=dev)
         kind = A.kind
         self.diag = None
@@ -330,10 +331,17 @@ class Restorer:
         A = self.A
         self.status.zero_()
         self._mark(timer, "start")
+        self._y_in = None
         if A.kind == "identity":
-            # solver.py:195-196: x0 = y; A^T y = y
-            self.aty.copy_(y_dev)
-            self.x.copy_(y_dev)
+            # solver.py:195-196: x0 = y; A^T y = y.  The observation buffer
+            # itself serves as A^T y and as iteration 0's image (no copies);
+            # strips keep copies (their halo rows are refreshed in place)
+            if (self.strip is None and y_dev.dtype == torch.float64 and y_dev.is_contiguous()
+                    and tuple(y_dev.shape) == tuple(self.x.shape) and y_dev.device == self.x.device):
+                self._y_in = y_dev
+            else:
+                self.aty.copy_(y_dev)
+                self.x.copy_(y_dev)
         else:
             cg = self.config.cg
             for b in range(self.batch):
@@ -373,16 +381,19 @@ class Restorer:
         nt = B * n
         mode = self._select_mode
         self._mark(timer, "start")
-        N.call("fepll_extract", N.ptr(self.x), B, H, W, side, N.ptr(anchors), n, nc,
+        # iteration 0 of an identity restore reads the observation in place
+        xin = self._y_in if (t == 0 and self._y_in is not None) else self.x
+        aty = self._y_in if self._y_in is not None else self.aty
+        N.call("fepll_extract", N.ptr(xin), B, H, W, side, N.ptr(anchors), n, nc,
                N.ptr(self.Z64), N.ptr(self.Z32), self.z32_pitch, N.ptr(self.dc), N.ptr(self.sq), st)
         self._mark(timer, "extract")
-        N.call("fepll_select", self.plan.handle, t, N.ptr(self.x), H, W, N.ptr(anchors), n,
+        N.call("fepll_select", self.plan.handle, t, N.ptr(xin), H, W, N.ptr(anchors), n,
                N.ptr(self.dc), N.ptr(self.sq), N.ptr(self.Z32), N.ptr(self.Z64), nt, mode,
                float(self.guard),
                N.ptr(self.labels), N.ptr(self.leaf_counts[t]), st)
         N.call("fepll_select_rescored", self.plan.handle, N.ptr(self.rescored[t]), st)
         self._mark(timer, "select")
-        N.call("fepll_wiener", self.plan.handle, t, N.ptr(self.x), H, W, N.ptr(anchors), n,
+        N.call("fepll_wiener", self.plan.handle, t, N.ptr(xin), H, W, N.ptr(anchors), n,
                N.ptr(self.dc), N.ptr(self.Z64), nt, N.ptr(self.Zhat), self.zhat_rows, st)
         self._mark(timer, "wiener")
         bs2 = float(self.betas[t]) * self.sigma * self.sigma
@@ -403,10 +414,10 @@ class Restorer:
                                             if sp is not None else (0, H, 0, nr))
             N.call("fepll_aggregate_strip", N.ptr(self.Zhat), None, N.ptr(anchors), nr, nc,
                    self.config.spacing, half, side, B, H, W, row0, H_glob, a_first, n_loc, r0, r1,
-                   N.ptr(self.aty), N.ptr(diag), bs2, kind, N.ptr(out), N.ptr(xt), N.ptr(self.status), st)
+                   N.ptr(aty), N.ptr(diag), bs2, kind, N.ptr(out), N.ptr(xt), N.ptr(self.status), st)
         else:
             N.call("fepll_aggregate_cover", N.ptr(self.Zhat), N.ptr(self._agg_dc), N.ptr(ptr),
-                   N.ptr(entries), P, n, self.zhat_rows, B, H, W, r0, r1, N.ptr(self.aty), N.ptr(diag), bs2, kind,
+                   N.ptr(entries), P, n, self.zhat_rows, B, H, W, r0, r1, N.ptr(aty), N.ptr(diag), bs2, kind,
                    N.ptr(out), N.ptr(xt), N.ptr(self.status), st)
         self._mark(timer, "aggregate")
         if not self.pixel_kind:
