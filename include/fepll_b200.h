@@ -131,11 +131,17 @@ int fepll_select_rescored(fepll_plan_t plan, int32_t* dst, void* stream);
 /* gmm.py:352-359 / solver.py:233-241: FP64 Wiener estimates of the patches
  * under their labels, grouped by label (the leaf buckets of the last select).
  * With Z64 (the FP64 patch rows of fepll_extract) it runs on the FP64 tensor
- * cores (DMMA); otherwise it re-extracts the patches from x.  Zhat receives
+ * cores (DMMA); without, on the DMMA kernel reading the windows of x when
+ * fepll_wiener_reads_image(plan), else on CUDA cores re-extracting from x.  Zhat receives
  * est + dc (patches.py:198-222's reprojection values), ready for
  * fepll_aggregate* with dc == NULL.  Zhat holds zhat_rows (>= n_img) rows of
  * P doubles per image: patch b*n_img + i is row b*zhat_rows + i (a padded
  * image pitch keeps the images' rows off power-of-two strides). */
+/* 1 when fepll_wiener, given Z64 == NULL, runs the DMMA kernel on 8 x 8
+ * windows of x (minus dc) itself — P = 64 — so fepll_extract need not write
+ * the FP64 rows; 0 when it needs Z64 for the DMMA path. */
+int fepll_wiener_reads_image(fepll_plan_t plan);
+
 int fepll_wiener(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32_t W,
                  const int32_t* anchors, int32_t n_img, const double* dc, const double* Z64,
                  int64_t n_total, double* Zhat, int32_t zhat_rows, void* stream);

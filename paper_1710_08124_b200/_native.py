@@ -53,6 +53,7 @@ _SIGS = {
     "fepll_sample_grid": (i32, [C.c_uint64, C.c_uint64, i32, i32, i32, i32, i32, C.c_uint32, vp, vp, vp, vp]),
     "fepll_extract": (i32, [vp, i32, i32, i32, i32, vp, i32, i32, vp, vp, i32, vp, vp, vp]),
     "fepll_select": (i32, [vp, i32, vp, i32, i32, vp, i32, vp, vp, vp, vp, i64, i32, f64, vp, vp, vp]),
+    "fepll_wiener_reads_image": (i32, [vp]),
     "fepll_wiener": (i32, [vp, i32, vp, i32, i32, vp, i32, vp, vp, i64, vp, i32, vp]),
     "fepll_select_rescored": (i32, [vp, vp, vp]),
     "fepll_aggregate": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, vp, vp, f64,

@@ -485,7 +485,8 @@ int rescore_queue_x(Plan* p, const LevelArgs& a, const double* x, const int32_t*
 }
 
 int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zhat, int n_img,
-                int zrows, cudaStream_t st);
+                int zrows, const double* x, const int32_t* anchors, int H, int W, cudaStream_t st);
+bool wiener_xw_supported(const Plan* p);
 bool wiener_dmma_supported(const Plan* p);
 
 LevelArgs make_level(Plan* p, int d, int t, int32_t* labels) {
@@ -590,6 +591,10 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
   return kOk;
 }
 
+extern "C" int fepll_wiener_reads_image(fepll_plan_t plan) {
+  return fepll::wiener_xw_supported(reinterpret_cast<fepll::Plan*>(plan)) ? 1 : 0;
+}
+
 extern "C" int fepll_debug_seg_sq(int32_t v) {
   fepll::g_seg_sq = v;
   return 0;
@@ -629,8 +634,8 @@ extern "C" int fepll_wiener(fepll_plan_t plan, int32_t t, const double* x, int32
         n_total, p->rs.leafseg, p->rs.cnt, p->rs.off, p->rs.leaf_base, (int32_t*)nullptr, -1);
     FEPLL_LAUNCH();
   }
-  if (Z64 != nullptr && wiener_dmma_supported(p))
-    return wiener_dmma(p, t, Z64, dc, Zhat, n_img, zhat_rows, st);
+  if (wiener_dmma_supported(p) && (Z64 != nullptr || wiener_xw_supported(p)))
+    return wiener_dmma(p, t, Z64, dc, Zhat, n_img, zhat_rows, x, anchors, H, W, st);
   PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P), zhat_rows};
   const int P = p->v.P;
   const int rmax = p->max_model_rank;

@@ -132,17 +132,19 @@ struct Geo {
 // RW = 16: the warp's rows g and g + 8 (two DMMAs per B fragment); RW = 8:
 // row g only (half the accumulators and registers, twice the warps per SM)
 template <int NT2, int NT1, int RW, class Step>
-__device__ __forceinline__ void wiener_rows(const double* za, const double* zb, const double* Us, int uld,
-                                            const double* sh, int t4, int g4, Step&& step,
-                                            double (&acc2)[NT2][4]) {
+__device__ __forceinline__ void wiener_rows(const double* za, const double* zb, double da, double db,
+                                            const double* Us, int uld, const double* sh, int t4,
+                                            int g4, Step&& step, double (&acc2)[NT2][4]) {
   double acc[NT1][4];
 #pragma unroll
   for (int n = 0; n < NT1; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0;
 #pragma unroll
   for (int k0 = 0; k0 < NT2 * 8; k0 += 8) {  // NT2 * 8 == Pn
     step(k0 / 8);
-    const double a0 = za[k0], a2 = za[k0 + 4];
-    const double a1 = RW == 16 ? zb[k0] : 0.0, a3 = RW == 16 ? zb[k0 + 4] : 0.0;
+    // z = window - dc, the extraction's FP64 subtraction (da = db = 0 when
+    // the rows are already z: x - 0 is x for every x, signed zeros included)
+    const double a0 = za[k0] - da, a2 = za[k0 + 4] - da;
+    const double a1 = RW == 16 ? zb[k0] - db : 0.0, a3 = RW == 16 ? zb[k0 + 4] - db : 0.0;
     const double* u0 = Us + (k0 + t4) * uld + g4;
     const double* u1 = u0 + 4 * uld;
     double b0[NT1], b1[NT1];
@@ -221,23 +223,32 @@ __device__ __forceinline__ void wiener_rows(const double* za, const double* zb, 
   }
 }
 
-template <int NT2, int MT, int NS, int RW>
+// XW: the rows are 8 x 8 windows of the image x (P = 64 only) instead of the
+// extracted Z64 rows; z = window - dc is formed at the fragment loads, so the
+// extraction need not write (and this kernel not read) the 512-byte Z64 rows
+// (off by default: slower, see g_wiener_xw).
+template <int NT2, int MT, int NS, int RW, bool XW>
 __global__ void __launch_bounds__(MT / RW * 32, RW == 8 ? 2 : 1)
 wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, int n_leaf_nodes,
                    const int32_t* __restrict__ cnt, const int64_t* __restrict__ off,
                    const int32_t* __restrict__ leafseg, const double* __restrict__ Z64,
                    const double* __restrict__ dc, double* __restrict__ Zhat, int n_img, int zrows,
+                   const double* __restrict__ x, const int32_t* __restrict__ anchors, int H, int W,
                    Geo geo) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int kRows = MT;
   constexpr int kThreads = MT / RW * 32;  // one warp per RW rows
   Head& h = *reinterpret_cast<Head*>(smem);
   constexpr int kRing = 2 * NS;      // index ring slots
-  constexpr int kLead = 2 * NS - 2;  // tiles of indices fetched ahead of their rows' issue
+  // tiles of indices fetched ahead of their rows' issue (XW: one more, for
+  // the anchors fetched between the index and the window copies)
+  constexpr int kLead = XW ? 2 * NS - 1 : 2 * NS - 2;
+  static_assert(!XW || (NS == 2 && NT2 == 8), "XW: the P = 64 two-stage pipeline");
   double* Zs0 = reinterpret_cast<double*>(smem + ((sizeof(Head) + 127) & ~size_t(127)));
   double* Us = Zs0 + NS * kRows * geo.zld;     // [Pn][uld]   (p, j)
   double* sh = Us + geo.Pn * geo.uld;          // [R8]
   double* dcs = sh + geo.R8;                   // [NS][MT] dc of the buffered rows
+  int2* anc = reinterpret_cast<int2*>(dcs + NS * kRows);  // XW: [4][MT] anchors of the rows
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int P = geo.P;
   // K padding columns of the row buffers stay zero (cp.async fills [0, P))
@@ -290,6 +301,25 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
   const int n_slices = (kRows * C + kThreads - 1) / kThreads;
   constexpr int kWarps = kThreads / 32;
   constexpr bool kInterleave = NT2 == 8;  // P = 64 layout below: 16 slices, 8 k-steps
+  auto fetch_anc = [&](int j) {  // XW: anchors of tile j's rows (indices landed)
+    if (XW && j < t_end && tid < kRows) {
+      const int g = h.rows[(j - t_begin) % kRing][tid];
+      if (g >= 0) cp_async8(&anc[((j - t_begin) & 3) * kRows + tid], anchors + 2 * (g % n_img));
+    }
+  };
+  // XW: thread chunk c (16 bytes = window columns 2(c%4), +1 of window row
+  // c/4) of row i of tile j; odd anchor columns are 8-byte aligned only
+  auto copy_window_chunk = [&](int j, int i, int c, int g, double* d) {
+    const int2 a = anc[((j - t_begin) & 3) * kRows + i];
+    const int b = g / n_img;
+    const double* src = x + ((int64_t)b * H + a.x + (c >> 2)) * W + a.y + 2 * (c & 3);
+    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+      cp_async16(d, src);
+    } else {
+      cp_async8(d, src);
+      cp_async8(d + 1, src + 1);
+    }
+  };
   auto fetch_z_slices = [&](int j, int s0, int s1) {
     if (j >= t_end) return;
     const int32_t* rows = h.rows[(j - t_begin) % kRing];
@@ -300,8 +330,11 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       const int g = rows[i];
       double* d = Zs + i * geo.zld + 2 * c;
       if (g >= 0) {
-        cp_async16(d, Z64 + (int64_t)g * P + 2 * c);
-        if (c == 0 && dc) cp_async8(dcb + i, dc + g);
+        if (XW)
+          copy_window_chunk(j, i, c, g, d);
+        else
+          cp_async16(d, Z64 + (int64_t)g * P + 2 * c);
+        if (c == 0) cp_async8(dcb + i, dc + g);
       } else {
         d[0] = 0.0;
         d[1] = 0.0;
@@ -314,6 +347,13 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
   cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
+  if (XW) {
+    fetch_anc(t_begin);
+    fetch_anc(t_begin + 1);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+  }
   for (int j = 0; j < NS - 1; ++j) {
     fetch_z_slices(t_begin + j, 0, n_slices);
     cp_async_commit();
@@ -331,6 +371,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
     __syncthreads();  // this tile's rows landed; the buffer refilled next is free
     wstamp(i, 1);
     fetch_rows(tile + kLead);  // committed with the row copies below (one group per tile)
+    fetch_anc(tile + 2);       // XW: its indices landed with the last group
     if (comp != cur_leaf) {
       const double* U = pv.model_basis + pv.model_off64[comp];
       for (int e = tid; e < geo.Pn * geo.R8; e += kThreads) {
@@ -361,12 +402,18 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
     const bool inter = kInterleave && P == 64 && jn < t_end;
     constexpr int kRowsPerThread = kRows / kWarps;  // == RW: RW / 8 rows per k-step
     int gsl[kRowsPerThread];
+    int2 asl[XW ? kRowsPerThread : 1];
     double* zn = Zs0 + ((jn - t_begin) % NS) * kRows * geo.zld + 2 * lane;
     double* dcn = dcs + ((jn - t_begin) % NS) * kRows;
     if (inter) {
       const int32_t* rn = h.rows[(jn - t_begin) % kRing];
 #pragma unroll
       for (int q = 0; q < kRowsPerThread; ++q) gsl[q] = rn[warp + kWarps * q];
+      if (XW) {
+        const int2* an = anc + ((jn - t_begin) & 3) * kRows;
+#pragma unroll
+        for (int q = 0; q < kRowsPerThread; ++q) asl[XW ? q : 0] = an[warp + kWarps * q];
+      }
     } else {
       fetch_z_slices(jn, 0, n_slices);
     }
@@ -376,8 +423,20 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       for (int q = st * (kRowsPerThread / 8); q < (st + 1) * (kRowsPerThread / 8); ++q) {
         double* d = zn + (warp + kWarps * q) * geo.zld;
         if (gsl[q] >= 0) {
-          cp_async16(d, Z64 + (int64_t)gsl[q] * 64 + 2 * lane);
-          if (lane == 0 && dc) cp_async8(dcn + warp + kWarps * q, dc + gsl[q]);
+          if (XW) {
+            const int2 a = asl[XW ? q : 0];
+            const int b = gsl[q] / n_img;
+            const double* src = x + ((int64_t)b * H + a.x + (lane >> 2)) * W + a.y + 2 * (lane & 3);
+            if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+              cp_async16(d, src);
+            } else {
+              cp_async8(d, src);
+              cp_async8(d + 1, src + 1);
+            }
+          } else {
+            cp_async16(d, Z64 + (int64_t)gsl[q] * 64 + 2 * lane);
+          }
+          if (lane == 0) cp_async8(dcn + warp + kWarps * q, dc + gsl[q]);
         } else {
           d[0] = 0.0;
           d[1] = 0.0;
@@ -385,15 +444,18 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       }
     };
     double acc[NT2][4];
+    const double* dcc = dcs + (i % NS) * kRows;  // dc of this tile's rows
+    const double da = XW ? dcc[m0 + g4] : 0.0;
+    const double db = XW && RW == 16 ? dcc[m0 + g4 + 8] : 0.0;
     switch ((r + 7) / 8) {
-      case 1: wiener_rows<NT2, 1, RW>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
-      case 2: wiener_rows<NT2, 2, RW>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
-      case 3: wiener_rows<NT2, 3, RW>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
-      case 4: wiener_rows<NT2, 4, RW>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
-      case 5: wiener_rows<NT2, 5, RW>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
-      case 6: wiener_rows<NT2, 6, RW>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
-      case 7: wiener_rows<NT2, 7, RW>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
-      default: wiener_rows<NT2, 8, RW>(za, zb, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 1: wiener_rows<NT2, 1, RW>(za, zb, da, db, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 2: wiener_rows<NT2, 2, RW>(za, zb, da, db, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 3: wiener_rows<NT2, 3, RW>(za, zb, da, db, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 4: wiener_rows<NT2, 4, RW>(za, zb, da, db, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 5: wiener_rows<NT2, 5, RW>(za, zb, da, db, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 6: wiener_rows<NT2, 6, RW>(za, zb, da, db, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      case 7: wiener_rows<NT2, 7, RW>(za, zb, da, db, Us, geo.uld, sh, t4, g4, zstep, acc); break;
+      default: wiener_rows<NT2, 8, RW>(za, zb, da, db, Us, geo.uld, sh, t4, g4, zstep, acc); break;
     }
     cp_async_commit();
     wstamp(i, 3);
@@ -407,15 +469,16 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
 #pragma unroll
       for (int half = 0; half < RW / 8; ++half) {
         double* zr = zw + (m0 + g4 + 8 * half) * geo.zld;
-        const double d = dc ? dct[m0 + g4 + 8 * half] : 0.0;
+        const double d = dct[m0 + g4 + 8 * half];
+        const double dz = XW ? d : 0.0;  // XW rows hold the window: z = w - dc
 #pragma unroll
         for (int n = 0; n < NT2; ++n) {
           const int col = n * 8 + 2 * t4;
           if (col < P) {
-            const double e0 = acc[n][2 * half] + gt * zr[col];
-            const double e1 = acc[n][2 * half + 1] + gt * zr[col + 1];
-            zr[col] = dc ? __dadd_rn(e0, d) : e0;
-            zr[col + 1] = dc ? __dadd_rn(e1, d) : e1;
+            const double e0 = acc[n][2 * half] + gt * (zr[col] - dz);
+            const double e1 = acc[n][2 * half + 1] + gt * (zr[col + 1] - dz);
+            zr[col] = __dadd_rn(e0, d);
+            zr[col + 1] = __dadd_rn(e1, d);
           }
         }
       }
@@ -442,12 +505,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
 
 }  // namespace wn
 
-int g_wiener_pair = 1;
-int g_wiener_rw = 8;  // rows per warp in the two-CTAs-per-SM configuration (debug: 16)
-int g_wiener_dc = 1;  // debug: 0 = write est only (the gather then adds dc)
-
-int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zhat, int n_img,
-                int zrows, cudaStream_t st) {
+static wn::Geo wiener_geo(const Plan* p) {
   const int P = p->v.P;
   wn::Geo geo;
   geo.P = P;
@@ -456,11 +514,49 @@ int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zha
   geo.zld = ld(geo.Pn, 4);
   geo.R8 = (p->max_model_rank + 7) / 8 * 8;
   geo.uld = ld(geo.R8, 4);
-  auto smem_for = [&](int mt, int ns) {
-    return ((sizeof(wn::Head) + 127) & ~size_t(127)) +
-           sizeof(double) * (ns * (size_t)mt * geo.zld + (size_t)geo.Pn * geo.uld +
-                             geo.R8 + (size_t)ns * mt);
-  };
+  return geo;
+}
+
+// dynamic shared memory of an (mt rows, ns stages) configuration: head,
+// row stages, basis, shrink, dc ring, XW anchors ring
+static size_t wiener_smem(const wn::Geo& geo, int mt, int ns) {
+  return ((sizeof(wn::Head) + 127) & ~size_t(127)) +
+         sizeof(double) * (ns * (size_t)mt * geo.zld + (size_t)geo.Pn * geo.uld + geo.R8 +
+                           (size_t)ns * mt) +
+         sizeof(int2) * 4 * (size_t)mt;
+}
+
+static bool wiener_pair_fits(const wn::Geo& geo) {
+  int dev = 0, per_sm_cap = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  if (cudaDeviceGetAttribute(&per_sm_cap, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) != cudaSuccess)
+    return false;
+  return 2 * (wiener_smem(geo, 64, 2) + 1024) <= (size_t)per_sm_cap;
+}
+
+int g_wiener_pair = 1;
+int g_wiener_rw = 8;  // rows per warp in the two-CTAs-per-SM configuration (debug: 16)
+// Window-source mode: measured slower on B200 (64 x 1024^2: extraction
+// 3.48 -> 2.06 ms/step without the Z64 writes, but the Wiener kernel 6.8 ->
+// 9.3 ms/step gathering 8 x 64-byte window rows per patch instead of one
+// 512-byte row), so off by default; it saves the 8P-byte-per-patch Z64
+// buffer where HBM capacity matters more.
+int g_wiener_xw = 0;
+
+// the window-source (XW) kernel: P = 64 in the two-CTAs-per-SM, 8-rows-per-
+// warp configuration
+bool wiener_xw_supported(const Plan* p) {
+  return g_wiener_xw && p->v.P == 64 && g_wiener_pair && g_wiener_rw == 8 &&
+         p->max_model_rank <= wn::kMaxR && wiener_pair_fits(wiener_geo(p));
+}
+
+int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zhat, int n_img,
+                int zrows, const double* x, const int32_t* anchors, int H, int W, cudaStream_t st) {
+  const wn::Geo geo = wiener_geo(p);
+  auto smem_for = [&](int mt, int ns) { return wiener_smem(geo, mt, ns); };
+  const bool xw = Z64 == nullptr;
+  FEPLL_REQUIRE(!xw || wiener_xw_supported(p),
+                "wiener: the window-source kernel needs P = 64 and two CTAs per SM");
   // 128-row tiles (16 warps) once the average leaf bucket is large enough
   // that the extra padding rows do not matter, and the tile fits in smem
   const int64_t n_total = p->last_n_total;
@@ -488,17 +584,17 @@ int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zha
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
     kernel<<<kSMs * std::max(1, per_sm), threads, smem, st>>>(
         p->v, t, p->d_leaf_nodes, p->n_leaf_nodes, p->rs.cnt, p->rs.off, p->rs.leafseg, Z64,
-        g_wiener_dc ? dc : nullptr,
-        Zhat, n_img, zrows, geo);
+        dc, Zhat, n_img, zrows, x, anchors, H, W, geo);
     FEPLL_LAUNCH();
     return kOk;
   };
 #define FEPLL_WN_CASE(N)                                                   \
   case N:                                                                  \
-    return big ? launch(wn::wiener_dmma_kernel<N, 128, 2, 16>)             \
-               : ns == 4 ? launch(wn::wiener_dmma_kernel<N, 64, 4, 16>)    \
-               : rw == 8 ? launch(wn::wiener_dmma_kernel<N, 64, 2, 8>)     \
-                         : launch(wn::wiener_dmma_kernel<N, 64, 2, 16>);
+    return big ? launch(wn::wiener_dmma_kernel<N, 128, 2, 16, false>)      \
+               : ns == 4 ? launch(wn::wiener_dmma_kernel<N, 64, 4, 16, false>) \
+               : rw == 8 ? launch(wn::wiener_dmma_kernel<N, 64, 2, 8, false>)  \
+                         : launch(wn::wiener_dmma_kernel<N, 64, 2, 16, false>);
+  if (xw) return launch(wn::wiener_dmma_kernel<8, 64, 2, 8, true>);
   switch (nt2) {
     FEPLL_WN_CASE(1)
     FEPLL_WN_CASE(2)
@@ -536,12 +632,13 @@ extern "C" int fepll_debug_wiener_trace(void* device_buffer) {
   return cudaMemcpyToSymbol(fepll::wn::g_trace, &p, sizeof(p)) == cudaSuccess ? 0 : 5;
 }
 
-extern "C" int fepll_debug_wiener_dc(int32_t on) {
-  fepll::g_wiener_dc = on;
-  return 0;
-}
 
 extern "C" int fepll_debug_wiener_rw(int32_t rw) {
   fepll::g_wiener_rw = rw;
+  return 0;
+}
+
+extern "C" int fepll_debug_wiener_xw(int32_t on) {
+  fepll::g_wiener_xw = on;
   return 0;
 }

@@ -219,8 +219,10 @@ class Restorer:
         B, H, W = self.batch, self.H, self.W
         f64 = torch.float64
         self.z32_pitch = ((P + 31) // 32) * 32
-        # FP64 patch rows (kernel (a) output) feed the DMMA Wiener kernel
-        self.Z64 = torch.empty((B * n, P), dtype=f64, device=dev)
+        # FP64 patch rows (kernel (a) output) feed the DMMA Wiener kernel —
+        # unless it reads the image windows itself (P = 64): allocated on
+        # first need (_z64)
+        self.Z64 = None
         # FP32 patch rows (kernel (a) output) feed the tensor-core scorer
         self.Z32 = (torch.empty((B * n, self.z32_pitch), dtype=torch.float32, device=dev)
                     if mode == "tensor" else None)
@@ -384,17 +386,18 @@ class Restorer:
         # iteration 0 of an identity restore reads the observation in place
         xin = self._y_in if (t == 0 and self._y_in is not None) else self.x
         aty = self._y_in if self._y_in is not None else self.aty
+        z64 = self._z64()
         N.call("fepll_extract", N.ptr(xin), B, H, W, side, N.ptr(anchors), n, nc,
-               N.ptr(self.Z64), N.ptr(self.Z32), self.z32_pitch, N.ptr(self.dc), N.ptr(self.sq), st)
+               N.ptr(z64), N.ptr(self.Z32), self.z32_pitch, N.ptr(self.dc), N.ptr(self.sq), st)
         self._mark(timer, "extract")
         N.call("fepll_select", self.plan.handle, t, N.ptr(xin), H, W, N.ptr(anchors), n,
-               N.ptr(self.dc), N.ptr(self.sq), N.ptr(self.Z32), N.ptr(self.Z64), nt, mode,
+               N.ptr(self.dc), N.ptr(self.sq), N.ptr(self.Z32), N.ptr(z64), nt, mode,
                float(self.guard),
                N.ptr(self.labels), N.ptr(self.leaf_counts[t]), st)
         N.call("fepll_select_rescored", self.plan.handle, N.ptr(self.rescored[t]), st)
         self._mark(timer, "select")
         N.call("fepll_wiener", self.plan.handle, t, N.ptr(xin), H, W, N.ptr(anchors), n,
-               N.ptr(self.dc), N.ptr(self.Z64), nt, N.ptr(self.Zhat), self.zhat_rows, st)
+               N.ptr(self.dc), N.ptr(z64), nt, N.ptr(self.Zhat), self.zhat_rows, st)
         self._mark(timer, "wiener")
         bs2 = float(self.betas[t]) * self.sigma * self.sigma
         # reproject (patches.py:198-222; Zhat already holds est + dc, so the
@@ -426,6 +429,16 @@ class Restorer:
                 self.op.solve(self.rhs[b], self.xt[b], bs2, cg.tolerance, cg.max_iterations,
                               self.x[b], self.solve_info[t, b], self.status, st)
             self._mark(timer, "image_solve")
+
+    def _z64(self):
+        """The FP64 patch rows, or None when the Wiener kernel reads the
+        image windows itself (fepll_wiener_reads_image)."""
+        if N.lib().fepll_wiener_reads_image(self.plan.handle):
+            return None
+        if self.Z64 is None:
+            self.Z64 = self.torch.empty((self.batch * self.n, self.P), dtype=self.torch.float64,
+                                        device=self.device)
+        return self.Z64
 
     @staticmethod
     def phase_times(timer: dict) -> dict:
