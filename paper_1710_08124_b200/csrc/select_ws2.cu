@@ -59,10 +59,20 @@ struct Roles {
   static constexpr int kMmaWarp = kConvWarp0 + kConvWarps;
   static constexpr int kEpiWarp0 = kMmaWarp + 1;
 };
+// + (SCHED) one scheduler warp after the epilogue warps: it walks the tiles
+// ahead of the MMA issuer, waits on every tile's barriers (raw stage landed,
+// lo written, accumulator free) and publishes the tile's node and width with
+// one mbarrier, so the issuer's loop between two tiles' MMAs is one wait.
+// Measured: levels on the four-group <4, 96> kernel 286 -> 268 us and
+// 348 -> 322 us; the three-group <3, 128> kernel, whose epilogue groups are
+// the limit, got slower (292 -> 310 us), so it keeps the issuer-side waits.
 // epilogue groups (== TMEM accumulators) and accumulator width are template
 // parameters: <3, 128> for levels with nodes up to 128 padded columns,
 // <4, 96> where every node fits 96 (four groups keep up with the MMAs)
-constexpr int threads_for(int ng, int lw) { return (Roles<1>::kEpiWarp0 - 1 + lw + 4 * ng) * 32; }
+constexpr int threads_for(int ng, int lw, bool sched) {
+  return (Roles<1>::kEpiWarp0 - 1 + lw + 4 * ng + (sched ? 1 : 0)) * 32;
+}
+constexpr int kReady = 4;  // scheduler -> issuer ring
 constexpr int kStages = 4;              // raw row stages (hi operand)
 constexpr int kLoBufs = 2;              // TMEM lo buffers
 constexpr int kAtomA = kRows * 128;     // bytes of one K atom of A
@@ -102,6 +112,8 @@ struct Smem {
   uint64_t raw_full[kStages], mma_done[kStages], lo_full[kLoBufs];
   uint64_t acc_full[NG], acc_empty[NG];
   uint64_t b_full, drain;
+  uint64_t ready[kReady];       // scheduler: tile i's barriers passed, tinfo[i % kReady] valid
+  int32_t tinfo_u[kReady], tinfo_npad[kReady];
   uint32_t tmem_base;
   int32_t t_begin, t_end;
 };
@@ -157,8 +169,8 @@ struct TileCursor {
   }
 };
 
-template <int NG, int ACC, int LW>
-__global__ void __launch_bounds__(threads_for(NG, LW), 1)
+template <int NG, int ACC, int LW, bool SCHED>
+__global__ void __launch_bounds__(threads_for(NG, LW, SCHED), 1)
 select_level_ws2_kernel(PlanView pv, Args args) {
   using R = Roles<LW>;
   constexpr int kLoaderWarps = R::kLoaderWarps, kLoaderRows = R::kLoaderRows, kLoaderQ = R::kLoaderQ;
@@ -193,6 +205,7 @@ select_level_ws2_kernel(PlanView pv, Args args) {
       tc::mbar_init(&s.acc_empty[i], 4);
     }
     tc::mbar_init(&s.b_full, 1);
+    for (int i = 0; i < kReady; ++i) tc::mbar_init(&s.ready[i], 1);
     tc::mbar_init(&s.drain, 1);
     tc::fence_mbar_init();
   }
@@ -326,7 +339,7 @@ select_level_ws2_kernel(PlanView pv, Args args) {
       if (lane == 0) mbar_arrive(&s.lo_full[lb]);
       if (cw == 0 && lane == 0) stamp(args, i, 1);
     }
-  } else if (warp == kMmaWarp) {
+  } else if (!SCHED && warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     // The whole warp runs this loop (uniform values); one elected lane
     // issues each tcgen05 instruction (tc.cuh *_warp).
@@ -396,6 +409,98 @@ select_level_ws2_kernel(PlanView pv, Args args) {
       tc::mma_commit_warp(&s.mma_done[st]);
       tc::mma_commit_warp(&s.acc_full[ac]);
       if (lane == 0) stamp(args, i, 3);
+    }
+  } else if (SCHED && warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer
+    // The whole warp runs this loop (uniform values); one elected lane
+    // issues each tcgen05 instruction (tc.cuh *_warp).  Per tile: one wait
+    // (the scheduler's ready), the node's B image when it changes, 16 MMAs.
+    int cur = -1;
+    uint32_t b_loads = 0, drains = 0;
+    const uint64_t a_base = tc::desc_sw128(tc::smem_u32(stageA));
+    const uint64_t b_base = tc::desc_sw128(tc::smem_u32(bbuf));
+    for (int i = 0; i < ntile; ++i) {
+      const int st = i % kStages;
+      const int ac = i % kGroups;
+      tc::mbar_wait(&s.ready[i % kReady], (i / kReady) & 1);
+      const int u = s.tinfo_u[i % kReady];
+      const int npad = s.tinfo_npad[i % kReady];
+      const uint32_t bhalf = (uint32_t)args.katoms * npad * 128u;
+      if (u != cur) {
+        if (i > 0) {  // every MMA reading the old B must be done
+          tc::mma_commit_warp(&s.drain);
+          tc::mbar_wait(&s.drain, drains & 1);
+          ++drains;
+        }
+        if (lane == 0) {
+          tc::mbar_arrive_expect_tx(&s.b_full, 2 * bhalf);
+          const int64_t boff = (int64_t)t * pv.tc_tstride + pv.tc_off[u];
+          tc::bulk_g2s(bbuf, pv.tc_hi + boff, bhalf, &s.b_full);
+          tc::bulk_g2s(bbuf + bhalf, pv.tc_x + boff, bhalf, &s.b_full);
+        }
+        __syncwarp();
+        tc::mbar_wait(&s.b_full, b_loads & 1);
+        ++b_loads;
+        cur = u;
+      }
+      const uint32_t d = tmem + ac * kAcc;
+      // raw stage (cp.async writes; the converters fenced the async proxy
+      // after observing it land) and lo buffer observed through ready
+      tc::fence_after_sync();
+      tc::fence_proxy_async_smem();
+      if (lane == 0) stamp(args, i, 2);
+      const uint32_t idesc = tc::idesc_tf32(kRows, npad);
+      // descriptor start-address field counts 16-byte units
+      const uint64_t A0 = a_base + (uint64_t)((st * kStageBytes) >> 4);
+      for (int kq = 0; kq < args.katoms; ++kq) {
+        const uint64_t a_hi = A0 + (uint64_t)((kq * kAtomA) >> 4);
+        const uint64_t b_hi = b_base + (uint64_t)((kq * npad * 128) >> 4);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t ko = 2 * kk;  // 8 tf32 = 32 bytes inside the swizzle atom
+          tc::mma_tf32_warp(d, a_hi + ko, b_hi + ko, idesc, (kq > 0 || kk > 0) ? 1u : 0u);
+        }
+      }
+      // cross terms: A' (TMEM, bf16 pairs) . B' (bf16, K = 2 Ppad)
+      const int lb = i % kLoBufs;
+      const uint32_t idesc16 = tc::idesc_bf16(kRows, npad);
+      const uint32_t a_x = tmem + kXCol0 + lb * 64;
+      const uint64_t b_x = b_base + (uint64_t)(bhalf >> 4);
+      for (int kq = 0; kq < args.katoms; ++kq) {  // B' atom kq: 64 bf16 of K
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)             // K = 16 = 32 bytes per MMA
+          tc::mma_bf16_tmemA_warp(d, a_x + 32 * kq + 8 * kk,
+                                  b_x + (uint64_t)((kq * npad * 128 + 32 * kk) >> 4), idesc16, 1u);
+      }
+      tc::mma_commit_warp(&s.mma_done[st]);
+      tc::mma_commit_warp(&s.acc_full[ac]);
+      if (lane == 0) stamp(args, i, 3);
+    }
+  } else if (SCHED && warp == kEpiWarp0 + 4 * kGroups) {
+    // ------------------------------------------------------------ scheduler
+    // tile i: its raw stage landed (raw_full), its lo buffer is written
+    // (lo_full), its accumulator drained by the epilogue (acc_empty) and its
+    // ready slot consumed (the issuer committed tile i - kReady: mma_done);
+    // then node + width go to the issuer through ready[i % kReady]
+    TileCursor tcur;
+    for (int i = 0; i < ntile; ++i) {
+      const int st = i % kStages, ac = i % kGroups, lb = i % kLoBufs;
+      const TileInfo ti = tcur.at(a, s.lv, t_begin + i);
+      if (i >= kReady) {
+        const int j = i - kReady;
+        tc::mbar_wait(&s.mma_done[j % kStages], (j / kStages) & 1);
+      }
+      if (lane == 0) stamp(args, i, 10);
+      if (i >= kGroups) tc::mbar_wait(&s.acc_empty[ac], ((i / kGroups) - 1) & 1);
+      if (lane == 0) stamp(args, i, 9);
+      tc::mbar_wait(&s.raw_full[st], (i / kStages) & 1);
+      tc::mbar_wait(&s.lo_full[lb], (i / kLoBufs) & 1);
+      if (lane == 0) {
+        s.tinfo_u[i % kReady] = ti.u;
+        s.tinfo_npad[i % kReady] = s.nd_npad[ti.k];
+        mbar_arrive(&s.ready[i % kReady]);  // release: the slot's writes above
+      }
+      __syncwarp();
     }
   } else {
     // ------------------------------------------------------------ epilogue
@@ -538,9 +643,9 @@ int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double
     return kOk;
   };
   if (p->level_tc_npad[a.depth] <= 96)
-    launch(ws2::select_level_ws2_kernel<4, 96, 4>, sizeof(ws2::Smem<4>), ws2::threads_for(4, 4));
+    launch(ws2::select_level_ws2_kernel<4, 96, 4, true>, sizeof(ws2::Smem<4>), ws2::threads_for(4, 4, true));
   else
-    launch(ws2::select_level_ws2_kernel<3, 128, 4>, sizeof(ws2::Smem<3>), ws2::threads_for(3, 4));
+    launch(ws2::select_level_ws2_kernel<3, 128, 4, false>, sizeof(ws2::Smem<3>), ws2::threads_for(3, 4, false));
   FEPLL_LAUNCH();
   return kOk;
 }
