@@ -310,7 +310,9 @@ def main():
     pin_out = torch.empty(clean.shape, dtype=torch.float32).pin_memory()
     chunks = args.e2e_chunks if (not strip and len(mine) % args.e2e_chunks == 0
                                  and len(mine) >= args.e2e_chunks) else 1
-    if not strip:
+    # one rank's strip is the whole image: the same streaming API applies
+    pipelined = not strip or world == 1
+    if pipelined:
         from paper_1710_08124_b200 import HostPipeline
         hp = HostPipeline(A, model, tree, cfg, batch=len(mine), chunks=chunks, lam=r.lam,
                           mode=args.mode, device=dev)
@@ -476,7 +478,7 @@ def main():
                     "api": ("HostPipeline.submit per step (pinned f32 in/out, "
                             f"{chunks} chunk(s) per step rotating over 2 streams; a step's copies "
                             "overlap its neighbours' compute, every step's H2D and D2H inside the "
-                            "timed region)" if not strip else "Restorer.run with per-step H2D/D2H")},
+                            "timed region)" if pipelined else "StripRestorer.run with per-step H2D/D2H")},
             "gpu_launches": int(launches),
             "clocks": clocks,
             "quality": {"psnr_in_db": float(np.mean(psnr_in)), "psnr_out_db": float(np.mean(psnr_out))},
