@@ -499,3 +499,49 @@ def test_kernel_variants_bitwise_equal(knob, values, models):
         assert np.array_equal(x0, x1)
         for a, b in zip(l0, l1):
             np.testing.assert_array_equal(a, b)
+
+
+def test_cover_gather_lo_eq_hi_verbatim_and_pipeline_errors(models):
+    """Identical contributions come back verbatim through both cover-list
+    gathers (batched and single-image kernels; patches.py:221 — a sum / count
+    would round differently for counts 3, 5, 6, 7, 9 of the jittered grid),
+    and HostPipeline.wait() raises the reference's NumericalError for a
+    non-finite observation."""
+    import torch
+    from paper_1710_08124_b200 import (HostPipeline, NumericalError, RestorationConfig, synthetic,
+                                       _native as N, jitter_rng, jittered_grid)
+    from paper_1710_08124_b200.patches import axis_anchors
+
+    P, H, W, s, side = 64, 40, 56, 4, 8
+    pos = jittered_grid(H, W, P, s, jitter_rng(3, 0)).positions.astype(np.int32)
+    n = pos.shape[0]
+    nr, nc = axis_anchors(H, side, s).size, axis_anchors(W, side, s).size
+    st = torch.cuda.current_stream().cuda_stream
+    pd = _dev(pos)
+    ptr = torch.empty(H * W + 1, dtype=torch.int32, device="cuda")
+    ent = torch.empty(n * P, dtype=torch.int32, device="cuda")
+    scr = torch.empty(int(N.lib().fepll_cover_scratch_ints(H * W)), dtype=torch.int32, device="cuda")
+    N.call("fepll_cover_build", N.ptr(pd), nr, nc, s, (side - s) // 2, side, W, 0, H, 0, nr, 0, H,
+           N.ptr(ptr), N.ptr(ent), n * P, N.ptr(scr), st)
+    counts = np.diff(ptr.cpu().numpy())
+    assert len(set(counts.tolist()) - {1, 2, 4, 8}) > 0  # non-power-of-two counts present
+    c = 0.1 + 0.2
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for B in (1, 3):
+        vals = _dev(np.full((B * n, P), c))
+        xc = torch.empty((B, H, W), dtype=torch.float64, device="cuda")
+        N.call("fepll_aggregate_cover", N.ptr(vals), None, N.ptr(ptr), N.ptr(ent), P, n, n, B, H, W,
+               0, H, None, None, 1.0, 1, None, N.ptr(xc), N.ptr(status), st)
+        assert np.all(xc.cpu().numpy() == c)
+    assert int(status.item()) == 0
+
+    model, tree = models[64]
+    case = synthetic.baseline_case("cfg1", 64)
+    ys = np.stack([case.y, case.y]).astype(np.float32)
+    ys[1, 10, 10] = np.nan
+    hp = HostPipeline(case.A, model, tree, RestorationConfig(sigma=20.0, spacing=4), batch=2)
+    pin_in = torch.from_numpy(ys).pin_memory()
+    pin_out = torch.empty(ys.shape, dtype=torch.float32).pin_memory()
+    hp.submit(pin_in, pin_out)
+    with pytest.raises(NumericalError):
+        hp.wait()
