@@ -221,19 +221,28 @@ extract_cols_kernel(const double* __restrict__ x, int batch, int H, int W,
       }
       const double dc = __shfl_sync(0xffffffffu, col, 0, SIDE) / (double)P;
       double sq = 0.0;
-      if (valid) {
-        double* zcol = Z64 ? Z64 + g[u] * P + c : nullptr;
-        float* fcol = Z32 ? Z32 + g[u] * z32_pitch + c : nullptr;
+      double zz[SIDE];
 #pragma unroll
-        for (int r = 0; r < SIDE; ++r) {
-          const double z = v[u][r] - dc;
-          sq = fma(z, z, sq);
-          if (zcol) zcol[r * SIDE] = z;
-          if (fcol) fcol[r * SIDE] = (float)z;
-        }
-        if (fcol)
-          for (int p = P + c; p < z32_pitch; p += SIDE) Z32[g[u] * z32_pitch + p] = 0.0f;
+      for (int r = 0; r < SIDE; ++r) {
+        zz[r] = v[u][r] - dc;
+        sq = fma(zz[r], zz[r], sq);
       }
+      // rows r, r + 1 leave as 16-byte (Z64) / 8-byte (Z32) pairs: the even
+      // lane of a column pair writes row r's two columns, the odd lane row
+      // r + 1's, after one exchange of the element the other needs
+      const bool odd = c & 1;
+#pragma unroll
+      for (int r = 0; r < SIDE; r += 2) {
+        const double got = __shfl_xor_sync(0xffffffffu, odd ? zz[r] : zz[r + 1], 1);
+        if (valid) {
+          const int e = odd ? (r + 1) * SIDE + c - 1 : r * SIDE + c;
+          const double a0 = odd ? got : zz[r], a1 = odd ? zz[r + 1] : got;
+          if (Z64) *reinterpret_cast<double2*>(Z64 + g[u] * P + e) = make_double2(a0, a1);
+          if (Z32) *reinterpret_cast<float2*>(Z32 + g[u] * z32_pitch + e) = make_float2((float)a0, (float)a1);
+        }
+      }
+      if (valid && Z32)
+        for (int p = P + c; p < z32_pitch; p += SIDE) Z32[g[u] * z32_pitch + p] = 0.0f;
 #pragma unroll
       for (int h = SIDE / 2; h >= 1; h >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, h, SIDE);
       if (valid && c == 0) {
@@ -244,7 +253,7 @@ extract_cols_kernel(const double* __restrict__ x, int batch, int H, int W,
   }
 }
 
-int g_extract_variant = 0;  // debug: 1 = staged tile kernel, 2 = U=1, 4 = U=4
+int g_extract_variant = 0;  // debug: 1 = staged tile kernel, 2 = U=2, 4 = U=4
 
 // Tiled variant for power-of-two sides on a row-major anchor grid: a block
 // takes PB consecutive anchors of one nominal row (grid_cols anchors per
@@ -424,7 +433,9 @@ extern "C" int fepll_extract(const double* x, int32_t batch, int32_t H, int32_t 
   if (g_extract_variant != 1 && (side == 8 || side == 4 || side == 16)) {
     const int per_warp = 32 / side;
     const int64_t warps = (total + per_warp - 1) / per_warp;
-    const int u = g_extract_variant == 0 ? 2 : g_extract_variant == 2 ? 1 : 4;  // debug 2: U=1, 4: U=4
+    // one lane group per warp pass: with the paired row stores it measured
+    // 2-4 % faster than two (fewer registers); debug 2: U=2, 4: U=4
+    const int u = g_extract_variant == 0 ? 1 : g_extract_variant == 2 ? 2 : 4;
     const int grid = grid_for((warps + u - 1) / u, 8, 148 * 8);
 #define FEPLL_EXT(S, U) extract_cols_kernel<S, U><<<grid, 256, 0, st>>>(x, batch, H, W, anchors, n, Z64, Z32, z32_pitch, dc, sq)
     if (side == 8) {

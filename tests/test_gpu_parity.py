@@ -469,7 +469,7 @@ def test_operator_adjoint_identity_and_normal(name):
     ("fepll_debug_wiener_rw", (8, 16)),          # Wiener: 8 vs 16 rows per warp
     ("fepll_debug_wiener_xw", (0, 1)),           # Wiener: extracted Z64 rows vs image windows
     ("fepll_debug_seg_sq", (1, 0)),              # ws2: segment-order ||z||^2 vs gather
-    ("fepll_debug_extract_variant", (0, 1, 2)),  # extraction: 2 / staged tile / 1 group per pass
+    ("fepll_debug_extract_variant", (0, 1, 2)),  # extraction: 1 / staged tile / 2 groups per pass
     ("fepll_debug_select_variant", (1, 0)),      # tree level: ws2 vs ws kernel
 ])
 def test_kernel_variants_bitwise_equal(knob, values, models):
