@@ -78,6 +78,22 @@ int fepll_plan_create(const fepll_plan_desc* desc, fepll_plan_t* out);
 /* scratch for up to max_patches patches per select call */
 int fepll_plan_reserve(fepll_plan_t plan, int64_t max_patches);
 int fepll_plan_destroy(fepll_plan_t plan);
+/* Per-plan kernel choices (no process-global state): A/B switches between
+ * kernel variants that produce bitwise-identical results, plus the Wiener
+ * output form.  Names and values:
+ *   select_variant 0 | 1 | 2  tree-level kernel: select_ws.cu (3xTF32),
+ *                             select_ws2.cu (tf32 + bf16 cross pass, default 1),
+ *                             ws2 on levels of <= 16 nodes and ws elsewhere;
+ *   seg_sq 0 | 1              ws2 levels pass ||z||^2 in segment order (default 1);
+ *   wiener_pair 0 | 1         two 64-row Wiener CTAs per SM when they fit (1);
+ *   wiener_rw 8 | 16          rows per warp in that configuration (8);
+ *   wiener_xw 0 | 1           Wiener reads 8x8 windows of x instead of Z64 (0);
+ *   wiener_add_dc 0 | 1       fepll_wiener writes est + dc (1) or the bare
+ *                             estimates (0: the trace's `estimates`; pass dc
+ *                             to the aggregation then).
+ * Unknown names or out-of-range values: data error. */
+int fepll_plan_set_option(fepll_plan_t plan, const char* name, int64_t value);
+int fepll_plan_get_option(fepll_plan_t plan, const char* name, int64_t* value);
 /* Timing of the tree-level kernels (kernel (b)): with capacity > 0 the next
  * `capacity` level launches of fepll_select are bracketed by CUDA events on
  * the caller's stream; _read returns their summed duration and count and
@@ -101,10 +117,12 @@ int fepll_sample_grid(uint64_t key0, uint64_t key1, int32_t H, int32_t W, int32_
 
 /* patches.py:167-183 (extract + _row_mean pairwise fold):
  * x: [batch][H][W] fp64; anchors: [n][2] int32 (row, col);
- * grid_cols: anchors per nominal grid row when anchors is a row-major grid
- * (enables the shared-memory tiled kernel), else 0;
+ * grid_cols: unused (kept for ABI stability), pass 0;
  * outputs (any may be NULL): Z64 [batch*n][P], Z32 [batch*n][z32_pitch]
- * (zero-padded past P; the tcgen05 scorer reads 128-byte K atoms), dc, sq. */
+ * (zero-padded past P; the tcgen05 scorer reads 128-byte K atoms), dc, sq.
+ * Any pitch >= P and any element alignment are accepted; the fast kernel
+ * (paired 16-/8-byte row stores) runs when Z64 is 16-byte aligned, Z32
+ * 8-byte aligned and z32_pitch even, a per-row-store kernel otherwise. */
 int fepll_extract(const double* x, int32_t batch, int32_t H, int32_t W, int32_t side,
                   const int32_t* anchors, int32_t n, int32_t grid_cols, double* Z64, float* Z32,
                   int32_t z32_pitch, double* dc, double* sq, void* stream);
@@ -112,8 +130,10 @@ int fepll_extract(const double* x, int32_t batch, int32_t H, int32_t W, int32_t 
 /* tree.py:387-434 (greedy descent, first-min tie break) over n_total =
  * batch * n_img patches whose values are re-extracted from the FP64 images x
  * ([batch][H][W]) at anchors ([n_img][2]) minus dc (patches.py:178).
- * mode 0: exact FP64 scoring; mode 1: tcgen05 3xTF32 scoring with
- * margin-guarded FP64 re-scoring (needs Z32, the FP32 patch rows written by
+ * mode 0: exact FP64 scoring; mode 1: tcgen05 tensor-core scoring (P <= 64:
+ * one kind::tf32 pass + one bf16 cross pass, select_ws2.cu; P <= 128:
+ * 3xTF32) with a certified argmin and FP64 re-scoring of every decision the
+ * certificate does not cover (needs Z32, the FP32 patch rows written by
  * fepll_extract).  Z64 (optional, the FP64 rows of fepll_extract, bitwise
  * the re-extracted values) saves the exact / re-scoring paths the window
  * reads.  guard <= 0 selects the default bound 2^-16 (tc_epi.cuh).

@@ -47,6 +47,8 @@ _SIGS = {
     "fepll_plan_create": (i32, [C.POINTER(PlanDesc), C.POINTER(vp)]),
     "fepll_plan_reserve": (i32, [vp, i64]),
     "fepll_plan_destroy": (i32, [vp]),
+    "fepll_plan_set_option": (i32, [vp, C.c_char_p, i64]),
+    "fepll_plan_get_option": (i32, [vp, C.c_char_p, C.POINTER(i64)]),
     "fepll_plan_profile": (i32, [vp, i32]),
     "fepll_plan_profile_read": (i32, [vp, C.POINTER(f64), C.POINTER(i32)]),
     "fepll_grid_scratch_ints": (i32, []),

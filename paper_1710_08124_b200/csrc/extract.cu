@@ -164,12 +164,13 @@ extract_pow2_kernel(const double* __restrict__ x, int batch, int H, int W,
 // Direct column variant for power-of-two sides: a group of SIDE lanes owns
 // one patch, lane c holds window column c (SIDE rows) in registers, loaded
 // straight from the image (the groups of a warp read overlapping spans of the
-// same image rows, so the loads mostly hit L1).  The fold is the tile
-// kernel's (row halvings in registers, column halvings by shuffles: the same
-// FP64 additions as patches.py:153-164), and every row of Z64 / Z32 leaves as
-// one SIDE-lane store (64 B / 32 B segments per patch row at SIDE = 8).  No
-// shared memory, no barriers: a few dozen instructions per patch, where the
-// staged tile kernel spends several hundred on its staging loops.
+// same image rows, so the loads mostly hit L1).  The fold: row halvings in
+// registers, then column halvings by shuffles (the same FP64 additions as patches.py:153-164).  Rows r, r + 1 of a column pair
+// leave together after one lane-pair shuffle: the even lane stores row r's
+// two columns, the odd lane row r + 1's, as one 16-byte (Z64) / 8-byte (Z32)
+// store each — hence the alignment rule of paired_stores_ok().  No
+// shared memory, no barriers: a few dozen instructions per patch (a staged
+// shared-memory tile kernel measured several hundred, round 1).
 template <int SIDE, int U>
 __global__ void __launch_bounds__(256)
 extract_cols_kernel(const double* __restrict__ x, int batch, int H, int W,
@@ -253,171 +254,15 @@ extract_cols_kernel(const double* __restrict__ x, int batch, int H, int W,
   }
 }
 
-int g_extract_variant = 0;  // debug: 1 = staged tile kernel, 2 = U=2, 4 = U=4
-
-// Tiled variant for power-of-two sides on a row-major anchor grid: a block
-// takes PB consecutive anchors of one nominal row (grid_cols anchors per
-// row), stages the image window they touch in shared memory with coalesced
-// loads, runs the same shuffle fold per patch (bitwise-equal dc), stages the
-// patch rows, and writes the block's contiguous Z64 / Z32 span with 16-byte
-// stores — the per-lane 8-byte global accesses of extract_pow2_kernel were
-// LSU-issue bound.  Blocks whose window exceeds the staging area (irregular
-// anchors) read the image directly.
-template <int SIDE>
-__global__ void __launch_bounds__(256)
-extract_tile_kernel(const double* __restrict__ x, int batch, int H, int W,
-                    const int32_t* __restrict__ anchors, int n, int grid_cols, int win_cap,
-                    double* __restrict__ Z64, float* __restrict__ Z32, int z32_pitch,
-                    double* __restrict__ dc_out, double* __restrict__ sq_out) {
-  constexpr int P = SIDE * SIDE;
-  constexpr int PER_WARP = 32 / SIDE;
-  constexpr int PB = 8 * PER_WARP;  // patches per block
-  extern __shared__ __align__(16) double sm[];
-  double* zs = sm;                       // [PB][P] staged FP64 rows
-  double* win = sm + PB * P;             // [rows][cols] image window (win_cap doubles)
-  __shared__ int s_pr[PB], s_pc[PB];
-  __shared__ int s_lo[2], s_hi[2];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int col_blocks = (grid_cols + PB - 1) / PB;
-  const int rows_total = n / grid_cols;
-  for (int64_t blk = blockIdx.x; blk < (int64_t)batch * rows_total * col_blocks; blk += gridDim.x) {
-    const int b = (int)(blk / ((int64_t)rows_total * col_blocks));
-    const int rem = (int)(blk - (int64_t)b * rows_total * col_blocks);
-    const int a = rem / col_blocks, cb = rem - a * col_blocks;
-    const int i0 = a * grid_cols + cb * PB;
-    const int m = min(PB, grid_cols - cb * PB);
-    const int64_t g0 = (int64_t)b * n + i0;
-    if (tid < 2) {
-      s_lo[tid] = INT_MAX;
-      s_hi[tid] = INT_MIN;
-    }
-    __syncthreads();
-    if (tid < m) {
-      const int pr = anchors[2 * (i0 + tid)], pc = anchors[2 * (i0 + tid) + 1];
-      s_pr[tid] = pr;
-      s_pc[tid] = pc;
-      atomicMin(&s_lo[0], pr);
-      atomicMax(&s_hi[0], pr);
-      atomicMin(&s_lo[1], pc);
-      atomicMax(&s_hi[1], pc);
-    }
-    __syncthreads();
-    const int r_lo = s_lo[0], c_lo = s_lo[1];
-    const int wr = s_hi[0] - r_lo + SIDE, wc = s_hi[1] - c_lo + SIDE;
-    const bool staged = wr * wc <= win_cap;
-    const double* img = x + (int64_t)b * H * W;
-    if (staged) {
-      for (int r = warp; r < wr; r += 8) {
-        const double* src = img + (int64_t)(r_lo + r) * W + c_lo;
-        for (int c = lane; c < wc; c += 32) win[r * wc + c] = __ldg(src + c);
-      }
-    }
-    __syncthreads();
-    // one lane group per patch, lane c = window COLUMN c: the reference's
-    // halvings of the flattened row (patches.py:156-163) first add row r + h
-    // to row r elementwise — in-register adds down this lane's column — and
-    // then halve the surviving row across the group's lanes: the same FP64
-    // additions in the same order as extract_pow2_kernel, a fraction of its
-    // shuffles
-    const int p = warp * PER_WARP + lane / SIDE;
-    const int c = lane % SIDE;
-    const bool valid = p < m;
-    double v[SIDE];  // v[r] = window(r, c)
-    if (valid) {
-      const int pr = s_pr[p], pc = s_pc[p];
-      if (staged) {
-        const double* src = win + (pr - r_lo) * wc + (pc - c_lo + c);
-#pragma unroll
-        for (int r = 0; r < SIDE; ++r) v[r] = src[r * wc];
-      } else {
-        const double* src = img + (int64_t)pr * W + pc + c;
-#pragma unroll
-        for (int r = 0; r < SIDE; ++r) v[r] = __ldg(src + (int64_t)r * W);
-      }
-    } else {
-#pragma unroll
-      for (int r = 0; r < SIDE; ++r) v[r] = 0.0;
-    }
-    double acc[SIDE];
-#pragma unroll
-    for (int r = 0; r < SIDE; ++r) acc[r] = v[r];
-#pragma unroll
-    for (int h = SIDE / 2; h >= 1; h >>= 1)
-#pragma unroll
-      for (int r = 0; r < h; ++r) acc[r] = acc[r] + acc[r + h];
-    double col = acc[0];  // row 0 of the halved rows, column c
-#pragma unroll
-    for (int h = SIDE / 2; h >= 1; h >>= 1) {
-      const double o = __shfl_down_sync(0xffffffffu, col, h, SIDE);
-      if (c < h) col = col + o;
-    }
-    const double dc = __shfl_sync(0xffffffffu, col, 0, SIDE) / (double)P;
-    double sq = 0.0;
-    if (valid) {
-      double* zcol = zs + p * P + c;
-#pragma unroll
-      for (int r = 0; r < SIDE; ++r) {
-        const double z = v[r] - dc;
-        sq = fma(z, z, sq);
-        zcol[r * SIDE] = z;
-      }
-    }
-#pragma unroll
-    for (int h = SIDE / 2; h >= 1; h >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, h, SIDE);
-    if (valid && c == 0) {
-      if (dc_out) dc_out[g0 + p] = dc;
-      if (sq_out) sq_out[g0 + p] = sq;
-    }
-    __syncthreads();
-    // contiguous spans: m rows of Z64 (P doubles), m rows of Z32 (z32_pitch floats)
-    if (Z64) {
-      const double2* src = reinterpret_cast<const double2*>(zs);
-      double2* dst = reinterpret_cast<double2*>(Z64 + g0 * P);
-      for (int k = tid; k < m * P / 2; k += 256) dst[k] = src[k];
-    }
-    if (Z32 && z32_pitch == P) {  // no padding: a flat conversion
-      const double2* src = reinterpret_cast<const double2*>(zs);
-      float4* dst = reinterpret_cast<float4*>(Z32 + g0 * P);
-      for (int k = tid; k < m * P / 4; k += 256) {
-        const double2 a0 = src[2 * k], a1 = src[2 * k + 1];
-        dst[k] = make_float4((float)a0.x, (float)a0.y, (float)a1.x, (float)a1.y);
-      }
-    } else if (Z32) {
-      const int q4 = z32_pitch / 4;
-      float4* dst = reinterpret_cast<float4*>(Z32 + g0 * z32_pitch);
-      for (int k = tid; k < m * q4; k += 256) {
-        const int row = k / q4, col = (k - row * q4) * 4;
-        float4 f;
-        f.x = col + 0 < P ? (float)zs[row * P + col + 0] : 0.0f;
-        f.y = col + 1 < P ? (float)zs[row * P + col + 1] : 0.0f;
-        f.z = col + 2 < P ? (float)zs[row * P + col + 2] : 0.0f;
-        f.w = col + 3 < P ? (float)zs[row * P + col + 3] : 0.0f;
-        dst[k] = f;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-template <int SIDE>
-static void launch_tile(const double* x, int batch, int H, int W, const int32_t* anchors, int n,
-                        int grid_cols, double* Z64, float* Z32, int z32_pitch, double* dc, double* sq,
-                        cudaStream_t st) {
-  constexpr int P = SIDE * SIDE;
-  constexpr int PB = 8 * (32 / SIDE);
-  const int win_cap = SIDE == 16 ? 8192 : 2048;  // staged window (doubles)
-  const size_t smem = sizeof(double) * ((size_t)PB * P + win_cap);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(extract_tile_kernel<SIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  const int64_t blocks = (int64_t)batch * (n / grid_cols) * ((grid_cols + PB - 1) / PB);
-  extract_tile_kernel<SIDE><<<grid_for(blocks, 1, kSMs * 8), 256, smem, st>>>(
-      x, batch, H, W, anchors, n, grid_cols, win_cap, Z64, Z32, z32_pitch, dc, sq);
-}
-
 }  // namespace fepll
+
+// The column kernel stores rows in 16-byte (Z64) and 8-byte (Z32) pairs:
+// it needs 16-byte aligned Z64, 8-byte aligned Z32 and an even z32_pitch.
+// Other layouts (valid under the ABI) take the per-row-store kernel.
+static bool paired_stores_ok(const double* Z64, const float* Z32, int z32_pitch) {
+  return (reinterpret_cast<uintptr_t>(Z64) % 16 == 0) &&
+         (Z32 == nullptr || (reinterpret_cast<uintptr_t>(Z32) % 8 == 0 && z32_pitch % 2 == 0));
+}
 
 extern "C" int fepll_extract(const double* x, int32_t batch, int32_t H, int32_t W, int32_t side,
                              const int32_t* anchors, int32_t n, int32_t grid_cols, double* Z64,
@@ -427,34 +272,25 @@ extern "C" int fepll_extract(const double* x, int32_t batch, int32_t H, int32_t 
   FEPLL_REQUIRE(side >= 1 && side * side <= kMaxP, "extract: patch side out of range");
   FEPLL_REQUIRE(H >= side && W >= side, "extract: image smaller than the patch");
   FEPLL_REQUIRE(Z32 == nullptr || z32_pitch >= side * side, "extract: Z32 pitch below P");
+  (void)grid_cols;
   if (n == 0) return kOk;
   const int64_t total = (int64_t)batch * n;
   cudaStream_t st = (cudaStream_t)stream;
-  if (g_extract_variant != 1 && (side == 8 || side == 4 || side == 16)) {
+  const bool pow2 = side == 8 || side == 4 || side == 16;
+  if (pow2 && paired_stores_ok(Z64, Z32, z32_pitch)) {
     const int per_warp = 32 / side;
     const int64_t warps = (total + per_warp - 1) / per_warp;
-    // one lane group per warp pass: with the paired row stores it measured
-    // 2-4 % faster than two (fewer registers); debug 2: U=2, 4: U=4
-    const int u = g_extract_variant == 0 ? 1 : g_extract_variant == 2 ? 2 : 4;
+    // one lane group per warp pass (side 4: two): with the paired row stores
+    // it measured 2-4 % faster than two or four (fewer registers)
+    const int u = side == 4 ? 2 : 1;
     const int grid = grid_for((warps + u - 1) / u, 8, 148 * 8);
-#define FEPLL_EXT(S, U) extract_cols_kernel<S, U><<<grid, 256, 0, st>>>(x, batch, H, W, anchors, n, Z64, Z32, z32_pitch, dc, sq)
-    if (side == 8) {
-      if (u == 1) FEPLL_EXT(8, 1); else if (u == 2) FEPLL_EXT(8, 2); else FEPLL_EXT(8, 4);
-    } else if (side == 4) {
-      FEPLL_EXT(4, 2);
-    } else {
-      FEPLL_EXT(16, 1);
-    }
-#undef FEPLL_EXT
-  } else if (grid_cols > 0 && n % grid_cols == 0 && (side == 8 || side == 4 || side == 16) &&
-      (Z32 == nullptr || z32_pitch % 4 == 0)) {
     if (side == 8)
-      launch_tile<8>(x, batch, H, W, anchors, n, grid_cols, Z64, Z32, z32_pitch, dc, sq, st);
+      extract_cols_kernel<8, 1><<<grid, 256, 0, st>>>(x, batch, H, W, anchors, n, Z64, Z32, z32_pitch, dc, sq);
     else if (side == 4)
-      launch_tile<4>(x, batch, H, W, anchors, n, grid_cols, Z64, Z32, z32_pitch, dc, sq, st);
+      extract_cols_kernel<4, 2><<<grid, 256, 0, st>>>(x, batch, H, W, anchors, n, Z64, Z32, z32_pitch, dc, sq);
     else
-      launch_tile<16>(x, batch, H, W, anchors, n, grid_cols, Z64, Z32, z32_pitch, dc, sq, st);
-  } else if (side == 8 || side == 4 || side == 16) {
+      extract_cols_kernel<16, 1><<<grid, 256, 0, st>>>(x, batch, H, W, anchors, n, Z64, Z32, z32_pitch, dc, sq);
+  } else if (pow2) {
     const int per_warp = 32 / side;
     const int64_t warps = (total + per_warp - 1) / per_warp;
     const int grid = grid_for(warps, 8, 148 * 32);
@@ -470,9 +306,4 @@ extern "C" int fepll_extract(const double* x, int32_t batch, int32_t H, int32_t 
   }
   FEPLL_LAUNCH();
   return kOk;
-}
-
-extern "C" int fepll_debug_extract_variant(int32_t v) {
-  fepll::g_extract_variant = v;
-  return 0;
 }

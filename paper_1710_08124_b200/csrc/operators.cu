@@ -226,6 +226,7 @@ struct CgArgs {
   double* low;
   double* partial;
   double* out;       // [0] iterations, [1] residual, [2] converged, [3] finite
+  int32_t* status;   // optional: bit 2 set when the solution is non-finite
   double tol;
   int maxit;
 };
@@ -320,6 +321,8 @@ __global__ void __launch_bounds__(256) cg_kernel(CgArgs a) {
     a.out[1] = res;
     a.out[2] = res <= a.tol ? 1.0 : 0.0;
     a.out[3] = t2[1] == 0.0 ? 1.0 : 0.0;
+    // sticky across the calls sharing one status word (out[] is per call)
+    if (a.status && t2[1] != 0.0) atomicOr(a.status, 2);
   }
 }
 
@@ -732,6 +735,7 @@ int fepll_op_init(void* op, const double* y, const double* aty, double sigma, do
   a.low = p->low;
   a.partial = p->partial;
   a.out = info ? info : p->scal;
+  a.status = nullptr;
   a.tol = tol;
   a.maxit = maxit;
   return coop_launch((const void*)cg_kernel, &a, p, st);
@@ -765,6 +769,7 @@ int fepll_op_solve(void* op, const double* rhs, const double* xtilde, double bs2
   a.low = p->low;
   a.partial = p->partial;
   a.out = info;
+  a.status = status;
   a.tol = tol;
   a.maxit = maxit;
   return coop_launch((const void*)cg_kernel, &a, p, st);

@@ -254,6 +254,40 @@ int fepll_plan_profile_read(fepll_plan_t plan, double* total_ms, int32_t* launch
   return fepll::kOk;
 }
 
+static int* plan_option(Plan* p, const char* name) {
+  const std::string n(name ? name : "");
+  if (n == "select_variant") return &p->opt.select_variant;
+  if (n == "seg_sq") return &p->opt.seg_sq;
+  if (n == "wiener_pair") return &p->opt.wiener_pair;
+  if (n == "wiener_rw") return &p->opt.wiener_rw;
+  if (n == "wiener_xw") return &p->opt.wiener_xw;
+  if (n == "wiener_add_dc") return &p->opt.wiener_add_dc;
+  return nullptr;
+}
+
+int fepll_plan_set_option(fepll_plan_t plan, const char* name, int64_t value) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  FEPLL_REQUIRE(p != nullptr, "plan_set_option: bad arguments");
+  int* slot = plan_option(p, name);
+  FEPLL_REQUIRE(slot != nullptr, std::string("plan_set_option: unknown option ") + (name ? name : "(null)"));
+  const std::string n(name);
+  const bool ok = (n == "select_variant") ? (value >= 0 && value <= 2)
+                  : (n == "wiener_rw")    ? (value == 8 || value == 16)
+                                          : (value == 0 || value == 1);
+  FEPLL_REQUIRE(ok, "plan_set_option: value out of range for " + n);
+  *slot = (int)value;
+  return fepll::kOk;
+}
+
+int fepll_plan_get_option(fepll_plan_t plan, const char* name, int64_t* value) {
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  FEPLL_REQUIRE(p != nullptr && value != nullptr, "plan_get_option: bad arguments");
+  int* slot = plan_option(p, name);
+  FEPLL_REQUIRE(slot != nullptr, std::string("plan_get_option: unknown option ") + (name ? name : "(null)"));
+  *value = *slot;
+  return fepll::kOk;
+}
+
 int fepll_plan_destroy(fepll_plan_t plan) {
   Plan* p = reinterpret_cast<Plan*>(plan);
   if (!p) return fepll::kOk;

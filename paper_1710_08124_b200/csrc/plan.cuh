@@ -62,7 +62,20 @@ struct RouteScratch {
   int32_t* node_tmp = nullptr;
 };
 
+// Per-plan kernel choices (fepll_plan_set_option): A/B switches between
+// bitwise-equivalent kernel variants, owned by the plan so concurrent plans
+// and streams never share them.
+struct PlanOptions {
+  int select_variant = 1;  // 0: select_ws.cu on every level, 1: select_ws2.cu, 2: ws2 on levels of <= 16 nodes
+  int seg_sq = 1;          // 1: consecutive ws2 levels hand ||z||^2 over in segment order
+  int wiener_pair = 1;     // 1: two 64-row CTAs per SM when they fit
+  int wiener_rw = 8;       // rows per warp in the pair configuration (8 or 16)
+  int wiener_xw = 0;       // 1: the Wiener kernel reads 8x8 windows of x (no Z64 rows)
+  int wiener_add_dc = 1;   // 1: fepll_wiener writes est + dc; 0: the bare estimates (traces)
+};
+
 struct Plan {
+  PlanOptions opt;
   fepll_plan_desc h{};  // sizes only (pointers are host temporaries)
   PlanView v{};
   std::vector<void*> owned;

@@ -28,6 +28,7 @@ struct PatchSrc {
   int n_img, H, W, side;
   int zrows;              // Zhat rows per image (>= n_img; padded pitch)
   const double* z64 = nullptr;  // FP64 patch rows of fepll_extract (bitwise window - dc), or NULL
+  int add_dc = 1;               // Wiener output: est + dc (1) or the bare estimates (0)
   __device__ __forceinline__ int64_t zrow(int g) const {
     return zrows == n_img ? (int64_t)g : (int64_t)(g / n_img) * zrows + g % n_img;
   }
@@ -298,7 +299,7 @@ wiener_fp64_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       double e = 0.0;
       for (int j = 0; j < r; ++j) e = fma(cs[j], __ldg(row + j), e);
       const double est = e + gt * zs[p];
-      out[p] = __dadd_rn(est, ps.dc[patch]);  // reprojection input: est + dc
+      out[p] = ps.add_dc ? __dadd_rn(est, ps.dc[patch]) : est;  // reprojection input: est + dc
     }
     __syncwarp();
   }
@@ -436,7 +437,7 @@ wiener_tile_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
           const int p = pc0 + jg + 16 * c;
           if (p < P) {
             const double est = acc[a][c] + gt * Zs[i * zs_ld + p];
-            Zhat[ps.zrow(row) * P + p] = __dadd_rn(est, ps.dc[row]);  // + dc
+            Zhat[ps.zrow(row) * P + p] = ps.add_dc ? __dadd_rn(est, ps.dc[row]) : est;  // + dc
           }
         }
       }
@@ -460,11 +461,10 @@ int select_level_wide(Plan* p, const LevelArgs& a, const float* Z32, const doubl
                       cudaStream_t st);
 int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                      cudaStream_t st);
-// 0: select_ws.cu (3xTF32), 1: select_ws2.cu (tf32 + bf16 cross pass, split
-// loader / converter warps; measured faster on every level of the cfg5
-// tree), 2: ws2 on levels of <= 16 nodes, ws on the wider ones
-int g_select_variant = 1;
-int g_seg_sq = 1;  // debug: 0 = ws2 levels gather sq[patch] as before
+// Plan option select_variant: 0 select_ws.cu (3xTF32), 1 (default)
+// select_ws2.cu (tf32 + bf16 cross pass, split loader / converter warps;
+// measured faster on every level of the cfg5 tree), 2 ws2 on levels of
+// <= 16 nodes, ws on the wider ones
 int select_level_ws(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                     cudaStream_t st);
 
@@ -548,12 +548,12 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
       if (d < 0 || d >= p->n_levels || mode != 1 || p->v.P > 128) return false;
       const bool wide = p->level_wide[d] || p->level_tc_npad[d] > 256;
       return !wide && select_ws_supported(p, d) && p->v.tc_x != nullptr &&
-             (g_select_variant == 1 ||
-              (g_select_variant == 2 && p->level_start[d + 1] - p->level_start[d] <= 16));
+             (p->opt.select_variant == 1 ||
+              (p->opt.select_variant == 2 && p->level_start[d + 1] - p->level_start[d] <= 16));
     };
     for (int d = 0; d < p->n_levels; ++d) {
       LevelArgs a = make_level(p, d, t, labels);
-      if (g_seg_sq && is_ws2(d)) {
+      if (p->opt.seg_sq && is_ws2(d)) {
         a.sq_in = d == 0 ? sq : is_ws2(d - 1) ? p->rs.segsq[d & 1] : nullptr;
         a.sq_out = is_ws2(d + 1) ? p->rs.segsq[(d + 1) & 1] : nullptr;
       }
@@ -566,8 +566,8 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
         rc = wide ? select_level_wide(p, a, Z32, sq, guard, st)
              : select_ws_supported(p, d)
                  ? ((p->v.tc_x != nullptr &&
-                     (g_select_variant == 1 ||
-                      (g_select_variant == 2 && p->level_start[d + 1] - p->level_start[d] <= 16)))
+                     (p->opt.select_variant == 1 ||
+                      (p->opt.select_variant == 2 && p->level_start[d + 1] - p->level_start[d] <= 16)))
                         ? select_level_ws2(p, a, Z32, sq, guard, st)
                         : select_level_ws(p, a, Z32, sq, guard, st))
                  : select_level_tc(p, a, Z32, sq, guard, st);
@@ -593,16 +593,6 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
 
 extern "C" int fepll_wiener_reads_image(fepll_plan_t plan) {
   return fepll::wiener_xw_supported(reinterpret_cast<fepll::Plan*>(plan)) ? 1 : 0;
-}
-
-extern "C" int fepll_debug_seg_sq(int32_t v) {
-  fepll::g_seg_sq = v;
-  return 0;
-}
-
-extern "C" int fepll_debug_select_variant(int32_t v) {
-  fepll::g_select_variant = v;
-  return 0;
 }
 
 extern "C" int fepll_select_rescored(fepll_plan_t plan, int32_t* dst, void* stream) {
@@ -637,6 +627,7 @@ extern "C" int fepll_wiener(fepll_plan_t plan, int32_t t, const double* x, int32
   if (wiener_dmma_supported(p) && (Z64 != nullptr || wiener_xw_supported(p)))
     return wiener_dmma(p, t, Z64, dc, Zhat, n_img, zhat_rows, x, anchors, H, W, st);
   PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P), zhat_rows};
+  ps.add_dc = p->opt.wiener_add_dc;
   const int P = p->v.P;
   const int rmax = p->max_model_rank;
   if (rmax <= 64) {

@@ -116,6 +116,7 @@ struct Geo {
   int zld;       // Zs [MT][zld], columns P..Pn-1 zero
   int R8;        // rank rounded up to 8
   int uld;       // Us [Pn][uld]  (phase-1 B: k = p, n = j; phase-2 B: k = j, n = p)
+  int add_dc;    // 1: write est + dc (default), 0: the bare estimates (plan option wiener_add_dc)
 };
 
 // NT2: phase-2 n-tiles (P/8 rounded up): 8 for P=64, 13 for P=100.
@@ -226,7 +227,7 @@ __device__ __forceinline__ void wiener_rows(const double* za, const double* zb, 
 // XW: the rows are 8 x 8 windows of the image x (P = 64 only) instead of the
 // extracted Z64 rows; z = window - dc is formed at the fragment loads, so the
 // extraction need not write (and this kernel not read) the 512-byte Z64 rows
-// (off by default: slower, see g_wiener_xw).
+// (off by default: slower, see plan option wiener_xw).
 template <int NT2, int MT, int NS, int RW, bool XW>
 __global__ void __launch_bounds__(MT / RW * 32, RW == 8 ? 2 : 1)
 wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, int n_leaf_nodes,
@@ -477,8 +478,8 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
           if (col < P) {
             const double e0 = acc[n][2 * half] + gt * (zr[col] - dz);
             const double e1 = acc[n][2 * half + 1] + gt * (zr[col + 1] - dz);
-            zr[col] = __dadd_rn(e0, d);
-            zr[col + 1] = __dadd_rn(e1, d);
+            zr[col] = geo.add_dc ? __dadd_rn(e0, d) : e0;
+            zr[col + 1] = geo.add_dc ? __dadd_rn(e1, d) : e1;
           }
         }
       }
@@ -514,6 +515,7 @@ static wn::Geo wiener_geo(const Plan* p) {
   geo.zld = ld(geo.Pn, 4);
   geo.R8 = (p->max_model_rank + 7) / 8 * 8;
   geo.uld = ld(geo.R8, 4);
+  geo.add_dc = p->opt.wiener_add_dc;
   return geo;
 }
 
@@ -534,19 +536,17 @@ static bool wiener_pair_fits(const wn::Geo& geo) {
   return 2 * (wiener_smem(geo, 64, 2) + 1024) <= (size_t)per_sm_cap;
 }
 
-int g_wiener_pair = 1;
-int g_wiener_rw = 8;  // rows per warp in the two-CTAs-per-SM configuration (debug: 16)
-// Window-source mode: measured slower on B200 (64 x 1024^2: extraction
+// Plan options wiener_pair / wiener_rw: two 64-row CTAs per SM, 8 rows
+// per warp (defaults).  Window-source mode (option wiener_xw): measured slower on B200 (64 x 1024^2: extraction
 // 3.48 -> 2.06 ms/step without the Z64 writes, but the Wiener kernel 6.8 ->
 // 9.3 ms/step gathering 8 x 64-byte window rows per patch instead of one
 // 512-byte row), so off by default; it saves the 8P-byte-per-patch Z64
 // buffer where HBM capacity matters more.
-int g_wiener_xw = 0;
 
 // the window-source (XW) kernel: P = 64 in the two-CTAs-per-SM, 8-rows-per-
 // warp configuration
 bool wiener_xw_supported(const Plan* p) {
-  return g_wiener_xw && p->v.P == 64 && g_wiener_pair && g_wiener_rw == 8 &&
+  return p->opt.wiener_xw && p->v.P == 64 && p->opt.wiener_pair && p->opt.wiener_rw == 8 &&
          p->max_model_rank <= wn::kMaxR && wiener_pair_fits(wiener_geo(p));
 }
 
@@ -569,14 +569,14 @@ int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zha
   // tiles when the buckets are large, else 64-row tiles with deeper staging
   int per_sm_cap = 0;
   FEPLL_CUDA(cudaDeviceGetAttribute(&per_sm_cap, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
-  const bool pair = g_wiener_pair && 2 * (smem_for(64, 2) + 1024) <= (size_t)per_sm_cap;
+  const bool pair = p->opt.wiener_pair && 2 * (smem_for(64, 2) + 1024) <= (size_t)per_sm_cap;
   const bool big = !pair && n_total >= (int64_t)1024 * std::max(1, p->n_leaf_nodes) && smem_for(128, 2) <= cap;
   const int mt = big ? 128 : 64;
   const int ns = big || pair ? 2 : (smem_for(64, 4) <= cap ? 4 : 2);
   FEPLL_REQUIRE(smem_for(mt, ns) <= cap, "wiener: tile buffers exceed shared memory");
   const size_t smem = smem_for(mt, ns);
   const int nt2 = geo.Pn / 8;
-  const int rw = pair && g_wiener_rw == 8 ? 8 : 16;
+  const int rw = pair && p->opt.wiener_rw == 8 ? 8 : 16;
   const int threads = mt / rw * 32;
   auto launch = [&](auto kernel) -> int {
     FEPLL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -622,23 +622,9 @@ bool wiener_dmma_supported(const Plan* p) {
 
 }  // namespace fepll
 
-extern "C" int fepll_debug_wiener_pair(int32_t on) {
-  fepll::g_wiener_pair = on;
-  return 0;
-}
-
 extern "C" int fepll_debug_wiener_trace(void* device_buffer) {
   uint64_t* p = static_cast<uint64_t*>(device_buffer);
   return cudaMemcpyToSymbol(fepll::wn::g_trace, &p, sizeof(p)) == cudaSuccess ? 0 : 5;
 }
 
 
-extern "C" int fepll_debug_wiener_rw(int32_t rw) {
-  fepll::g_wiener_rw = rw;
-  return 0;
-}
-
-extern "C" int fepll_debug_wiener_xw(int32_t on) {
-  fepll::g_wiener_xw = on;
-  return 0;
-}

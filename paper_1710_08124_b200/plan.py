@@ -324,6 +324,17 @@ class DevicePlan:
         self.path_mults = h["path_mults"]
         self.reserved = 0
 
+    OPTIONS = ("select_variant", "seg_sq", "wiener_pair", "wiener_rw", "wiener_xw", "wiener_add_dc")
+
+    def set_option(self, name: str, value: int) -> None:
+        """Per-plan kernel choice (include/fepll_b200.h fepll_plan_set_option)."""
+        N.call("fepll_plan_set_option", self.handle, name.encode(), int(value))
+
+    def get_option(self, name: str) -> int:
+        v = C.c_int64()
+        N.call("fepll_plan_get_option", self.handle, name.encode(), C.byref(v))
+        return int(v.value)
+
     def reserve(self, n_patches: int) -> None:
         if n_patches > self.reserved:
             N.call("fepll_plan_reserve", self.handle, int(n_patches))

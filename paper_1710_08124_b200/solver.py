@@ -16,8 +16,10 @@ operator and noise level in one pass (the batch of BASELINE config 5).
 
 from __future__ import annotations
 
+import hashlib
 import math
 import time
+from collections import OrderedDict
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -27,13 +29,14 @@ from . import _native as N
 from .errors import DataError, NumericalError
 from .gmm import score_flat_cost, wiener_flat_cost
 from .operators import CgConfig
-from .patches import axis_anchors, philox_key
+from .patches import SampleGrid, axis_anchors, jitter_rng, jittered_grid, philox_key, regular_grid
 from .device_ops import DeviceOperator
 from .plan import DevicePlan
 from .tree import star_tree
 
 __all__ = ["RestorationConfig", "IterationStats", "SolverStats", "beta_schedule",
-           "restore", "restore_batch", "Restorer", "SIGMA_FLOOR_8BIT"]
+           "restore", "restore_batch", "Restorer", "HostPipeline", "cached_restorer",
+           "clear_plan_cache", "SIGMA_FLOOR_8BIT"]
 
 SIGMA_FLOOR_8BIT = 0.5
 
@@ -145,7 +148,8 @@ class Restorer:
     MODES = {"exact": 0, "tensor": 1}
 
     def __init__(self, A, model, tree, config, batch: int = 1, lam: float | None = None,
-                 mode: str = "tensor", device=None, guard: float = 0.0, strip=None):
+                 mode: str = "tensor", device=None, guard: float = 0.0, strip=None,
+                 options: dict | None = None):
         _validate_config(config)
         # strip mode (strips.StripSpec): A covers the strip's slab of a larger
         # image; only the owned rows are aggregated (denoise, batch 1)
@@ -197,6 +201,10 @@ class Restorer:
             self.lam = float(lam)
         self.betas = beta_schedule(self.sigma, self.lam, config.beta_multipliers)
         self.plan = DevicePlan(model, tree, self.betas, with_tc=(mode == "tensor"))
+        # per-plan kernel choices (bitwise-equivalent variants; fepll_plan_set_option)
+        self.options = dict(options or {})
+        for k, v in self.options.items():
+            self.plan.set_option(k, v)
         # a model with a positive score weight has no pre-scaled tcgen05 images:
         # its tree walk runs on the exact FP64 scorer (the same labels)
         self._select_mode = self.MODES[mode] if (mode == "exact" or self.plan.has_tc) else 0
@@ -211,8 +219,14 @@ class Restorer:
         # (batches share them; a row strip or a large single image reuses them
         # across restores of the same plan — the gather over them is ~2x the
         # speed of the candidate search; small single images search directly)
-        self._use_cover = (self.batch > 1 or self.strip is not None
-                           or self.H * self.W >= (4 << 20))
+        # Cover-list entries pack (patch << 8 | offset) in 31 bits: planes of
+        # 2^23 or more patches (8192^2 at spacing 2, 3000^2 at spacing 1)
+        # gather by candidate search instead, which has no such limit.
+        n_loc_rows = (self.strip.a_hi - self.strip.a_lo + 1) if self.strip is not None else \
+            self._grids[0][1]
+        self._use_cover = ((self.batch > 1 or self.strip is not None
+                            or self.H * self.W >= (4 << 20))
+                           and n_loc_rows * self._grids[0][2] < (1 << 23))
         self._covers = [self._cover(t) if self._use_cover else self._cover_rows()
                         for t in range(config.iterations)]
         self.plan.reserve(n * self.batch)
@@ -229,7 +243,7 @@ class Restorer:
         # Wiener output rows (est + dc), zhat_rows per image (the ABI allows a
         # padded pitch; a padded one measured no different, so dense)
         self.zhat_rows = n
-        self._agg_dc = None  # (debug A/B: dc added by the gather instead of the Wiener kernel)
+        self._agg_dc = None  # traces: dc added by the gather (the Wiener kernel writes bare estimates)
         self.Zhat = torch.empty((B * self.zhat_rows, P), dtype=f64, device=dev)
         self.dc = torch.empty(B * n, dtype=f64, device=dev)
         self.sq = torch.empty(B * n, dtype=f64, device=dev)
@@ -240,6 +254,9 @@ class Restorer:
         self.rescored = torch.zeros((config.iterations, 64), dtype=torch.int32, device=dev)
         self.x = torch.empty((B, H, W), dtype=f64, device=dev)
         self._y_in = None  # identity restores: the observation, read in place
+        self._force_z64 = False
+        self._want_xt = False
+        self.graph = None
         self.xt = torch.empty((B, H, W), dtype=f64, device=dev)
         kind = A.kind
         self.diag = None
@@ -355,19 +372,54 @@ class Restorer:
 
     def iterate(self, t: int, trace: bool = False, timer: dict | None = None) -> list:
         """One HQS iteration (solver.py:200-262); returns its trace record
-        (empty unless ``trace``)."""
+        (empty unless ``trace``) with the reference's keys
+        (`pkg/src/fepll/solver.py:258-266`): beta, grid (a SampleGrid),
+        patches, dc, selected, estimates (the bare Wiener estimates, without
+        dc), x_tilde — each with a leading batch axis — plus x."""
         st = self.torch.cuda.current_stream(self.device).cuda_stream
         self._want_xt = trace
-        self._iteration(t, st, timer)
         if not trace:
+            self._iteration(t, st, timer)
             return []
-        B, n = self.batch, self.n
+        # trace: the Wiener kernel writes the bare estimates and the gather
+        # adds dc (the same single FP64 rounding of patches.py:209, so x is
+        # bitwise the untraced result); the FP64 patch rows are kept
+        self.plan.set_option("wiener_add_dc", 0)
+        self._agg_dc = self.dc
+        self._force_z64 = True
+        try:
+            self._iteration(t, st, timer)
+        finally:
+            self.plan.set_option("wiener_add_dc", self.options.get("wiener_add_dc", 1))
+            self._agg_dc = None
+            self._force_z64 = False
+        B, n, P = self.batch, self.n, self.P
         return [{"beta": float(self.betas[t]),
-                 "positions": self.anchors[t].cpu().numpy().astype(np.int64),
-                 "labels": self.labels.view(B, n).cpu().numpy().copy(),
+                 "grid": self.sample_grid(t),
+                 "patches": self.Z64.view(B, n, P).cpu().numpy().copy(),
                  "dc": self.dc.view(B, n).cpu().numpy().copy(),
+                 "selected": self.labels.view(B, n).cpu().numpy().astype(np.int64),
+                 "estimates": self.Zhat.view(B, self.zhat_rows, P)[:, :n].cpu().numpy().copy(),
                  "x_tilde": self.xt.cpu().numpy().copy(),
                  "x": self.x.cpu().numpy().copy()}]
+
+    def sample_grid(self, t: int) -> SampleGrid:
+        """Iteration t's sampling plan as the reference's SampleGrid
+        (`pkg/src/fepll/patches.py:40-69`): positions from the device
+        generator; the host generator supplies offsets and global_shift."""
+        c = self.config
+        H, W = self.H, self.W
+        if self.strip is not None:
+            H = self.strip.H
+        if c.sampling == "jittered":
+            g = jittered_grid(H, W, self.P, c.spacing, jitter_rng(c.seed, t))
+        else:
+            g = regular_grid(H, W, self.P, c.spacing)
+        pos = self.anchors[t].cpu().numpy().astype(np.int64)
+        if self.strip is None and not np.array_equal(pos, g.positions):
+            raise N.DeviceError("device sampling plan differs from the reference generator")
+        return SampleGrid(pos, (self.H, self.W), g.patch_side, g.spacing, g.mode,
+                          offsets=g.offsets, global_shift=g.global_shift)
 
     def _mark(self, timer, name):
         if timer is None:
@@ -415,7 +467,7 @@ class Restorer:
             sp = self.strip
             row0, H_glob, a_first, n_loc = ((sp.slab_lo, sp.H, sp.a_lo, sp.a_hi - sp.a_lo + 1)
                                             if sp is not None else (0, H, 0, nr))
-            N.call("fepll_aggregate_strip", N.ptr(self.Zhat), None, N.ptr(anchors), nr, nc,
+            N.call("fepll_aggregate_strip", N.ptr(self.Zhat), N.ptr(self._agg_dc), N.ptr(anchors), nr, nc,
                    self.config.spacing, half, side, B, H, W, row0, H_glob, a_first, n_loc, r0, r1,
                    N.ptr(aty), N.ptr(diag), bs2, kind, N.ptr(out), N.ptr(xt), N.ptr(self.status), st)
         else:
@@ -432,24 +484,75 @@ class Restorer:
 
     def _z64(self):
         """The FP64 patch rows, or None when the Wiener kernel reads the
-        image windows itself (fepll_wiener_reads_image)."""
-        if N.lib().fepll_wiener_reads_image(self.plan.handle):
+        image windows itself (plan option wiener_xw) and no trace wants them."""
+        if N.lib().fepll_wiener_reads_image(self.plan.handle) and not self._force_z64:
             return None
         if self.Z64 is None:
             self.Z64 = self.torch.empty((self.batch * self.n, self.P), dtype=self.torch.float64,
                                         device=self.device)
         return self.Z64
 
+    # reference names of the phases (pkg/src/fepll/solver.py:206-254)
+    PHASE_NAMES = {"extract": "extract", "select": "select", "wiener": "estimate",
+                   "aggregate": "reproject", "image_solve": "image_solve"}
+
     @staticmethod
     def phase_times(timer: dict) -> dict:
-        """Sum of milliseconds per phase from the marks recorded by run()."""
+        """Milliseconds per phase from the marks recorded by run().  Every
+        interval between consecutive marks is attributed: the stretch before
+        an iteration's first mark (host launch gaps between iterations)
+        counts as "gap", so the phases add up to the run's span."""
         out: dict = {}
         marks = timer.get("_marks", [])
         for (n0, e0), (n1, e1) in zip(marks, marks[1:]):
+            key = "gap" if n1 == "start" else n1
+            out[key] = out.get(key, 0.0) + e0.elapsed_time(e1)
+        return out
+
+    @classmethod
+    def iteration_times(cls, timer: dict) -> list:
+        """Seconds per phase of each HQS iteration, under the reference's
+        ``IterationStats.times`` keys (grid, extract, select, estimate,
+        reproject, image_solve).  The sampling plans are part of the cached
+        device plan (generated once, csrc/grid.cu), so "grid" is 0.  For the
+        pixel-diagonal kinds the image update is fused into the gather and
+        its time is inside "reproject"."""
+        out = []
+        marks = timer.get("_marks", [])
+        cur = None
+        for (n0, e0), (n1, e1) in zip(marks, marks[1:]):
             if n1 == "start":
                 continue
-            out[n1] = out.get(n1, 0.0) + e0.elapsed_time(e1)
+            if n1 == "extract":
+                cur = {"grid": 0.0}
+                out.append(cur)
+            if cur is None or n1 not in cls.PHASE_NAMES:
+                continue
+            cur[cls.PHASE_NAMES[n1]] = e0.elapsed_time(e1) / 1e3
         return out
+
+    # ---------------------------------------------------------------- graphs
+    def capture(self, y_dev):
+        """Record one whole restore (x0 + every iteration) of the device
+        observation buffer ``y_dev`` as a CUDA graph; :meth:`replay` re-runs
+        it (refill ``y_dev`` in place between replays).  The C ABI is
+        stream-ordered with no host synchronisation, so the captured launch
+        sequence is exactly :meth:`run`'s.  Returns the output tensor."""
+        torch = self.torch
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):  # warm-up off the capture (lazy allocations)
+            self.run(y_dev)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            x, _ = self.run(y_dev)
+        self._graph_y = y_dev
+        return x
+
+    def replay(self):
+        self.graph.replay()
+        return self.x
 
     def counters(self):
         """(patches, evals, selection mults, estimation mults) per iteration
@@ -571,27 +674,82 @@ class HostPipeline:
         self.wait()
 
 
-def restore(y, A, model, tree=None, config=None, *, mode: str = "tensor", lam=None):
-    """GPU drop-in for `pkg/src/fepll/solver.py:161-274`."""
+# ------------------------------------------------------------------ plan cache
+_CACHE_SIZE = 4
+_restorer_cache: "OrderedDict[tuple, tuple]" = None  # key -> (Restorer, pinned key objects)
+
+
+def _array_digest(a) -> str:
+    if a is None:
+        return ""
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    return hashlib.sha1(a.tobytes()).hexdigest() + str(a.shape)
+
+
+def _plan_key(A, model, tree, config, batch, lam, mode, options):
+    """Cache key of a Restorer: model and tree by identity (immutable and
+    shareable; the cache pins them so an id is never
+    reused while cached), the operator by value (kind, dims, factor, kernel
+    and pixel-map bytes), every config field that shapes the plan."""
+    cg = config.cg
+    op = (A.kind, tuple(A.input_dims), tuple(A.output_dims), getattr(A, "factor", None),
+          _array_digest(getattr(A, "kernel", None)), _array_digest(getattr(A, "pixel_map", None)))
+    cfg = (float(config.sigma), int(config.iterations), tuple(float(v) for v in config.beta_multipliers),
+           int(config.spacing), config.sampling, bool(config.use_tree), bool(config.use_flat_tail),
+           int(config.seed), float(cg.tolerance), int(cg.max_iterations))
+    return (id(model), id(tree), op, cfg, int(batch), None if lam is None else float(lam), mode,
+            tuple(sorted((options or {}).items())))
+
+
+def cached_restorer(A, model, tree, config, batch: int = 1, lam=None, mode: str = "tensor",
+                    options: dict | None = None) -> "Restorer":
+    """The Restorer for these arguments, built once and reused by later
+    :func:`restore` / :func:`restore_batch` calls (plan packing, lambda,
+    sampling plans, cover lists and scratch are the per-call setup the
+    reference redoes every call).  Least-recently-used, 4 entries."""
+    global _restorer_cache
+    if _restorer_cache is None:
+        _restorer_cache = OrderedDict()
+    key = _plan_key(A, model, tree, config, batch, lam, mode, options)
+    hit = _restorer_cache.get(key)
+    if hit is not None:
+        _restorer_cache.move_to_end(key)
+        return hit[0]
+    r = Restorer(A, model, tree, config, batch=batch, lam=lam, mode=mode, options=options)
+    _restorer_cache[key] = (r, (model, tree))
+    while len(_restorer_cache) > _CACHE_SIZE:
+        _restorer_cache.popitem(last=False)
+    return r
+
+
+def clear_plan_cache() -> None:
+    global _restorer_cache
+    _restorer_cache = None
+
+
+def restore(y, A, model, tree=None, config=None, *, mode: str = "tensor", lam=None,
+            options: dict | None = None):
+    """GPU drop-in for `pkg/src/fepll/solver.py:161-274`: same signature,
+    validations, errors, counters, ``IterationStats.times`` and trace
+    records (one image, no batch axis)."""
     if config is None:
         config = RestorationConfig(sigma=20.0)
     _validate_config(config)
     y = np.asarray(y, dtype=np.float64)
     if tuple(y.shape) != tuple(A.output_dims):
         raise DataError(f"observation shape {y.shape} != operator output {tuple(A.output_dims)}")
-    x, stats = restore_batch(y[None], A, model, tree, config, mode=mode, lam=lam)
+    x, stats = restore_batch(y[None], A, model, tree, config, mode=mode, lam=lam, options=options)
     if config.trace:
         for rec in stats.trace:
-            rec["selected"] = rec.pop("labels")[0]
-            rec["x_tilde"] = rec["x_tilde"][0]
-            rec["dc"] = rec["dc"][0]
-            rec["x"] = rec["x"][0]
+            for k in ("patches", "dc", "selected", "estimates", "x_tilde", "x"):
+                rec[k] = rec[k][0]
     return x[0], stats
 
 
 def restore_batch(ys, A, model, tree=None, config=None, *, mode: str = "tensor", lam=None,
-                  restorer: Restorer | None = None):
-    """Restore a (B, H, W) stack sharing operator, sigma and seed."""
+                  restorer: Restorer | None = None, options: dict | None = None):
+    """Restore a (B, H, W) stack sharing operator, sigma and seed.  The
+    device plan comes from the plan cache unless ``restorer`` is given."""
     if config is None:
         config = RestorationConfig(sigma=20.0)
     t0 = time.perf_counter()
@@ -600,21 +758,28 @@ def restore_batch(ys, A, model, tree=None, config=None, *, mode: str = "tensor",
         raise DataError("restore_batch expects a (B, H, W) stack")
     if tuple(ys.shape[1:]) != tuple(A.output_dims):
         raise DataError(f"observation shape {ys.shape[1:]} != operator output {tuple(A.output_dims)}")
-    r = restorer or Restorer(A, model, tree, config, batch=ys.shape[0], lam=lam, mode=mode)
+    r = restorer or cached_restorer(A, model, tree, config, batch=ys.shape[0], lam=lam, mode=mode,
+                                    options=options)
+    if r.batch != ys.shape[0]:
+        raise DataError(f"restorer batch {r.batch} != {ys.shape[0]} observations")
     torch = r.torch
     y_dev = torch.from_numpy(np.ascontiguousarray(ys)).to(r.device)
     t1 = time.perf_counter()
-    x_dev, recs = r.run(y_dev, trace=config.trace)
+    timer: dict = {}
+    x_dev, recs = r.run(y_dev, trace=config.trace, timer=timer)
     x = x_dev.cpu().numpy()
     r.check_status()
     stats = SolverStats(lam=r.lam)
-    stats.init_seconds = t1 - t0
+    phases = Restorer.phase_times(timer)
+    stats.init_seconds = (t1 - t0) + phases.get("init", 0.0) / 1e3
     infos = r.solve_infos()
+    times = Restorer.iteration_times(timer)
     for t, (npatch, ev, sm, em) in enumerate(r.counters()):
         it = IterationStats(beta=float(r.betas[t]), patches=npatch // max(r.batch, 1),
                             image_solve_converged=infos[t][0], image_solve_residual=infos[t][1],
                             score_evaluations=ev, selection_multiplies=sm,
-                            estimation_multiplies=em)
+                            estimation_multiplies=em,
+                            times=times[t] if t < len(times) else {})
         stats.iterations.append(it)
     stats.trace = recs
     stats.rescored = [int(v) for v in r.rescored.sum(dim=1).cpu()]

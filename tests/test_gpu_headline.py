@@ -1,0 +1,256 @@
+"""Parity where the headline number is quoted, and adversarial ties.
+
+* cfg5 batch: 4 of the 64 BASELINE config-5 images (1024^2, sigma 25,
+  stride 4), restored inside the full 64-image batch exactly as bench.py
+  runs it, against the CPU oracle: labels identical every iteration, RMSE
+  <= 1e-3 on [0, 255], |dPSNR| <= 0.01 dB (BASELINE north_star); the
+  HostPipeline (bench e2e path) returns the float32 of the same images.
+* cfg5 strip: a 2048^2 image in 4 row strips vs the oracle.
+* ties: models whose tree nodes have duplicated children — exact ties and
+  scores a few ulps apart — through every tensor-core kernel (ws2, ws, the
+  P = 100 streaming-K kernel, the no-tree chunked scan) and the FP64 path.
+  The labels must be the FP64 first minimum (`pkg/src/fepll/tree.py:425`,
+  np.argmin), i.e. the oracle's.
+"""
+
+import copy
+import math
+
+import numpy as np
+import pytest
+
+import fepll_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+RMSE_TOL = 1e-3
+PSNR_TOL = 0.01
+
+
+def rmse255(a, b):
+    return 255.0 * float(np.sqrt(np.mean((np.asarray(a) - np.asarray(b)) ** 2)))
+
+
+def psnr(x, ref):
+    return 10 * np.log10(1.0 / float(np.mean((np.clip(x, 0, 1) - ref) ** 2)))
+
+
+# ---------------------------------------------------------------- cfg5 batch
+def test_cfg5_batch_headline_vs_oracle(models):
+    import torch
+    from paper_1710_08124_b200 import HostPipeline, RestorationConfig, Restorer, synthetic
+
+    B, size = 64, 1024
+    spec = synthetic.CONFIGS["cfg5"]
+    cases = [synthetic.baseline_case("cfg5", size, image_seed=i, noise_seed=1000 + i) for i in range(B)]
+    ys = np.stack([c.y for c in cases])
+    A = cases[0].A
+    model, tree = models[64]
+    cfg = RestorationConfig(sigma=spec["sigma"], spacing=spec["spacing"], seed=0)
+    r = Restorer(A, model, tree, cfg, batch=B)
+    y_dev = torch.from_numpy(ys).cuda()
+    pick = [0, 21, 42, 63]
+    labels = []
+    r.start(y_dev)
+    for t in range(len(r.betas)):
+        r.iterate(t)
+        labels.append(r.labels.view(B, r.n)[pick].cpu().numpy())
+    x = r.x.cpu().numpy()
+    r.check_status()
+    # the bench's end-to-end path: pinned float32 through HostPipeline
+    hp = HostPipeline(A, model, tree, cfg, batch=B, lam=r.lam)
+    pin_in = torch.from_numpy(ys.astype(np.float32)).pin_memory()
+    pin_out = torch.empty(ys.shape, dtype=torch.float32).pin_memory()
+    hp.run(pin_in, pin_out)
+    ref32 = Restorer(A, model, tree, cfg, batch=B, lam=r.lam)
+    x32, _ = ref32.run(torch.from_numpy(ys.astype(np.float32).astype(np.float64)).cuda())
+    np.testing.assert_array_equal(pin_out.numpy()[pick], x32.cpu().numpy()[pick].astype(np.float32))
+    del ref32, hp, y_dev
+    for j, i in enumerate(pick):
+        xo, so = O.restore(ys[i], A, model, tree, sigma=spec["sigma"], spacing=spec["spacing"], seed=0,
+                           trace=True)
+        for t, rec in enumerate(so.trace):
+            np.testing.assert_array_equal(labels[t][j], rec["selected"], err_msg=f"image {i} iteration {t}")
+        assert rmse255(x[i], xo) <= RMSE_TOL
+        assert abs(psnr(x[i], cases[i].clean) - psnr(xo, cases[i].clean)) <= PSNR_TOL
+
+
+# ---------------------------------------------------------------- cfg5 strip
+def test_cfg5_strip_2048_vs_oracle(models):
+    from paper_1710_08124_b200 import RestorationConfig, synthetic
+    from paper_1710_08124_b200.strips import restore_strips_single_process
+
+    spec = synthetic.CONFIGS["cfg5"]
+    c = synthetic.baseline_case("cfg5", 2048, image_seed=5, noise_seed=77)
+    model, tree = models[64]
+    cfg = RestorationConfig(sigma=spec["sigma"], spacing=spec["spacing"], seed=0)
+    x = restore_strips_single_process(c.y, model, tree, cfg, 4)
+    xo, so = O.restore(c.y, c.A, model, tree, sigma=spec["sigma"], spacing=spec["spacing"], seed=0)
+    assert rmse255(x, xo) <= RMSE_TOL
+    assert abs(psnr(x, c.clean) - psnr(xo, c.clean)) <= PSNR_TOL
+
+
+# ---------------------------------------------------------------- ties
+# const offsets of the duplicated child (FP64 score units): 0 = exact tie
+# (identical components: the first child must win); +D = the duplicate is
+# worse; -D = the duplicate is better by far more than the scores' rounding
+# (D = 2^-24 is >= 4 ulps of any score below 2^26; here |score| < 3e5) but
+# below the tensor-core error bound of all but the flattest patches (so the
+# certificate rarely decides and the FP64 re-score must); +d = worse by a
+# sub-ulp amount at typical magnitudes (rounds to a tie or to child 0).  A
+# duplicate better by under ~2 ulps is left out: its winner depends on the
+# rounding of the shared score terms, which no two FP64 summation orders
+# share.
+OFFSETS = (0.0, 2.0 ** -24, -(2.0 ** -24), 2.0 ** -46)
+
+
+def _clone(comp, weight):
+    c = copy.copy(comp)
+    c.weight = float(weight)
+    c.kept_basis = np.array(comp.kept_basis, copy=True)
+    c.kept_eigenvalues = np.array(comp.kept_eigenvalues, copy=True)
+    return c
+
+
+def _dup_model(model, groups):
+    """Copy of ``model`` where, in every group (a list of component indices
+    sharing a parent), the second member becomes a clone of the first with
+    iota = -2 log w shifted by OFFSETS[g % 4]; weights renormalised."""
+    from paper_1710_08124_b200 import GmmModel
+
+    comps = [_clone(c, c.weight) for c in model.components]
+    for g, members in enumerate(groups):
+        if len(members) < 2:
+            continue
+        a, b = members[0], members[1]
+        off = OFFSETS[g % len(OFFSETS)]
+        comps[b] = _clone(comps[a], comps[a].weight * math.exp(-off / 2.0))
+    s = float(sum(c.weight for c in comps))
+    for c in comps:
+        c.weight = c.weight / s
+    return GmmModel(model.patch_dim, comps, model.rho)
+
+
+def _dup_root_tree(model, tree):
+    """A tree whose root has two identical children: the baseline tree's
+    first root subtree and a deep copy of it (every patch ties at the root;
+    the first child must win at every level below too).  Returns the new
+    model (the subtree's leaves, then their copies) and tree."""
+    from paper_1710_08124_b200 import GmmModel, GmmTree, TreeNode
+
+    sub = tree.root.children[0]
+    scale = 0.5 / sub.component.weight
+    leaves = []
+
+    def rebuild(node):
+        comp = _clone(node.component, node.component.weight * scale)
+        if node.is_leaf:
+            nd = TreeNode(comp, leaf_index=len(leaves))
+            leaves.append(comp)
+            return nd
+        return TreeNode(comp, children=[rebuild(c) for c in node.children])
+
+    a = rebuild(sub)
+    b = rebuild(sub)
+    root = TreeNode(_clone(tree.root.component, 1.0), children=[a, b])
+    levels = [1]
+    frontier = [root]
+    while frontier[0].children:
+        frontier = [c for n in frontier for c in n.children]
+        levels.append(len(frontier))
+    t = GmmTree(root, tuple(levels), model.patch_dim)
+    return GmmModel(model.patch_dim, leaves, model.rho), t, len(leaves) // 2
+
+
+def _leaf_groups(tree):
+    from paper_1710_08124_b200.tree import tree_topology
+
+    topo = tree_topology(tree)
+    out = []
+    for u in range(topo.n_nodes):
+        kids = topo.child_list[topo.child_start[u]:topo.child_start[u] + topo.child_count[u]]
+        if len(kids) and all(topo.leaf_index[k] >= 0 for k in kids):
+            out.append([int(topo.leaf_index[k]) for k in kids])
+    return out
+
+
+def _run_all(y, A, model, tree, s, use_tree=True, runs=None):
+    from paper_1710_08124_b200 import RestorationConfig, restore
+
+    cfg = RestorationConfig(sigma=20.0, spacing=s, seed=4, trace=True, use_tree=use_tree)
+    xo, so = O.restore(y, A, model, tree if use_tree else None, sigma=20.0, spacing=s, seed=4,
+                       use_tree=use_tree, trace=True)
+    for mode, opts in runs:
+        x, st = restore(y, A, model, tree if use_tree else None, cfg, mode=mode, options=opts)
+        for t, (a, b) in enumerate(zip(st.trace, so.trace)):
+            np.testing.assert_array_equal(a["selected"], b["selected"],
+                                          err_msg=f"{mode} {opts} iteration {t}")
+        assert rmse255(x, xo) <= RMSE_TOL
+    return so
+
+
+def _image(H, seed):
+    from paper_1710_08124_b200 import identity_operator, synthetic
+
+    img = synthetic.synthetic_image(H, H, seed) / 255.0
+    y = img + (20.0 / 255.0) * np.random.default_rng(seed + 1).standard_normal((H, H))
+    return y, identity_operator((H, H))
+
+
+TENSOR_P64 = [("exact", {}), ("tensor", {"select_variant": 1}), ("tensor", {"select_variant": 0}),
+              ("tensor", {"select_variant": 2})]
+
+
+def test_ties_duplicated_leaves_p64(models):
+    """Every leaf parent of the cfg5 tree gets a duplicated child."""
+    from paper_1710_08124_b200.tree import tree_from_partitions, tree_partitions
+
+    model, tree = models[64]
+    parts = tree_partitions(tree)
+    dm = _dup_model(model, parts[0])
+    dt = tree_from_partitions(dm, parts)
+    y, A = _image(128, 3)
+    so = _run_all(y, A, dm, dt, 4, runs=TENSOR_P64)
+    # ties were hit: patches chose the first member of an exact-tie pair
+    exact_pairs = [g for i, g in enumerate(parts[0]) if len(g) > 1 and OFFSETS[i % 4] == 0.0]
+    firsts = {g[0] for g in exact_pairs}
+    seconds = {g[1] for g in exact_pairs}
+    sel = np.concatenate([r["selected"] for r in so.trace])
+    assert np.isin(sel, list(firsts)).sum() > 100
+    assert not np.isin(sel, list(seconds)).any()
+
+
+def test_ties_duplicated_root_subtree_p64(models):
+    """The root's two children are identical subtrees: every patch ties at
+    every level of the copy; the first child wins everywhere."""
+    model, tree = models[64]
+    dm, dt, half = _dup_root_tree(model, tree)
+    y, A = _image(96, 5)
+    so = _run_all(y, A, dm, dt, 4, runs=TENSOR_P64)
+    sel = np.concatenate([r["selected"] for r in so.trace])
+    assert sel.max() < half
+
+
+def test_ties_duplicated_leaves_p100(models):
+    """P = 100: the streaming-K tcgen05 kernel (select_tc.cu) + re-scoring."""
+    from paper_1710_08124_b200.tree import tree_from_partitions, tree_partitions
+
+    model, tree = models[100]
+    parts = tree_partitions(tree)
+    dm = _dup_model(model, parts[0])
+    dt = tree_from_partitions(dm, parts)
+    y, A = _image(120, 7)
+    _run_all(y, A, dm, dt, 6, runs=[("exact", {}), ("tensor", {})])
+
+
+def test_ties_duplicated_components_no_tree(models):
+    """No-tree profile (np.argmin over all components, gmm.py:383-391):
+    components 2j+1 clone 2j, through the chunked tcgen05 scan."""
+    model, _ = models[64]
+    groups = [[2 * j, 2 * j + 1] for j in range(len(model.components) // 2)]
+    dm = _dup_model(model, groups)
+    y, A = _image(64, 9)
+    so = _run_all(y, A, dm, None, 4, use_tree=False, runs=[("exact", {}), ("tensor", {})])
+    sel = np.concatenate([r["selected"] for r in so.trace])
+    exact_seconds = [g[1] for i, g in enumerate(groups) if OFFSETS[i % 4] == 0.0]
+    assert not np.isin(sel, exact_seconds).any()

@@ -163,28 +163,20 @@ def test_same_seed_bit_identical_and_batch_equals_single(models):
 def test_select_kernel_variants_agree(models):
     """Both tensor-core level kernels (select_ws.cu, select_ws2.cu) and the
     per-level hybrid route every patch identically, and equal the FP64 path."""
-    import ctypes
-    from paper_1710_08124_b200 import RestorationConfig, _native as N, restore_batch, synthetic
+    from paper_1710_08124_b200 import RestorationConfig, restore_batch, synthetic
 
     model, tree = models[64]
     cases = [synthetic.baseline_case("cfg5", 192, image_seed=i, noise_seed=40 + i) for i in range(3)]
     ys = np.stack([c.y for c in cases])
     cfg = RestorationConfig(sigma=25.0, spacing=4, seed=9, trace=True)
-    f = N.lib().fepll_debug_select_variant
-    f.argtypes = [ctypes.c_int32]
-    outs = []
-    try:
-        for v in (0, 1, 2):
-            f(v)
-            outs.append(restore_batch(ys, cases[0].A, model, tree, cfg, mode="tensor"))
-    finally:
-        f(1)
+    outs = [restore_batch(ys, cases[0].A, model, tree, cfg, mode="tensor",
+                          options={"select_variant": v}) for v in (0, 1, 2)]
     xe, se = restore_batch(ys, cases[0].A, model, tree, cfg, mode="exact")
     for x, st in outs:
         np.testing.assert_array_equal(x, outs[0][0])
         assert len(st.trace) == len(se.trace) == 5
         for a, b in zip(st.trace, se.trace):
-            np.testing.assert_array_equal(a["labels"], b["labels"])
+            np.testing.assert_array_equal(a["selected"], b["selected"])
         assert rmse255(x, xe) <= 1e-9
 
 
@@ -238,28 +230,35 @@ def _dev(a, dtype=None):
 
 
 def test_extract_kernel_bitwise():
+    """Kernel (a) vs the oracle's extract (patches.py:153-183), bitwise, over
+    patch sides and spacings — and over output layouts the ABI allows: the
+    padded 128-byte pitch (paired-store kernel), an odd Z32 pitch and Z64/Z32
+    pointers offset by one element (per-row-store kernel)."""
     import torch
     from paper_1710_08124_b200 import _native as N, jitter_rng, jittered_grid
 
-    from paper_1710_08124_b200 import axis_anchors
-
-    for P, H, W, s, tiled in [(64, 70, 61, 3, 1), (64, 70, 61, 3, 0), (100, 64, 64, 6, 1),
-                              (36, 30, 40, 2, 1), (16, 50, 47, 1, 1), (256, 64, 80, 16, 1),
-                              (64, 300, 280, 1, 1), (64, 300, 280, 8, 1), (256, 90, 70, 3, 1)]:
+    for P, H, W, s, layout in [(64, 70, 61, 3, "padded"), (64, 70, 61, 3, "odd"),
+                               (64, 70, 61, 3, "offset"), (100, 64, 64, 6, "padded"),
+                               (36, 30, 40, 2, "padded"), (16, 50, 47, 1, "padded"),
+                               (16, 50, 47, 1, "odd"), (256, 64, 80, 16, "padded"),
+                               (64, 300, 280, 1, "padded"), (64, 300, 280, 8, "padded"),
+                               (256, 90, 70, 3, "offset")]:
         side = int(np.sqrt(P))
         x = np.random.default_rng(P).random((H, W))
         pos = jittered_grid(H, W, P, s, jitter_rng(1, 2)).positions.astype(np.int32)
         n = pos.shape[0]
-        grid_cols = axis_anchors(W, side, s).size if tiled else 0
         Zo, dco = O.extract(x, pos.astype(np.int64), side)
-        pitch = (P + 31) // 32 * 32
-        Z64 = torch.empty((n, P), dtype=torch.float64, device="cuda")
-        Z32 = torch.empty((n, pitch), dtype=torch.float32, device="cuda")
+        pitch = {"padded": (P + 31) // 32 * 32, "odd": P + 1, "offset": P}[layout]
+        off = 1 if layout == "offset" else 0
+        Z64b = torch.empty(n * P + off, dtype=torch.float64, device="cuda")
+        Z32b = torch.empty(n * pitch + off, dtype=torch.float32, device="cuda")
+        Z64, Z32 = Z64b[off:].view(n, P), Z32b[off:].view(n, pitch)
         dc = torch.empty(n, dtype=torch.float64, device="cuda")
         sq = torch.empty(n, dtype=torch.float64, device="cuda")
         xd, pd = _dev(x), _dev(pos)  # keep the device inputs alive across the async launch
-        N.call("fepll_extract", N.ptr(xd), 1, H, W, side, N.ptr(pd), n, grid_cols, N.ptr(Z64),
+        N.call("fepll_extract", N.ptr(xd), 1, H, W, side, N.ptr(pd), n, 0, N.ptr(Z64),
                N.ptr(Z32), pitch, N.ptr(dc), N.ptr(sq), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
         np.testing.assert_array_equal(dc.cpu().numpy(), dco)           # pairwise fold, bitwise
         np.testing.assert_array_equal(Z64.cpu().numpy(), Zo)
         np.testing.assert_array_equal(Z32.cpu().numpy()[:, :P], Zo.astype(np.float32))
@@ -466,34 +465,34 @@ def test_operator_adjoint_identity_and_normal(name):
 
 
 @pytest.mark.parametrize("knob,values", [
-    ("fepll_debug_wiener_rw", (8, 16)),          # Wiener: 8 vs 16 rows per warp
-    ("fepll_debug_wiener_xw", (0, 1)),           # Wiener: extracted Z64 rows vs image windows
-    ("fepll_debug_seg_sq", (1, 0)),              # ws2: segment-order ||z||^2 vs gather
-    ("fepll_debug_extract_variant", (0, 1, 2)),  # extraction: 1 / staged tile / 2 groups per pass
-    ("fepll_debug_select_variant", (1, 0)),      # tree level: ws2 vs ws kernel
+    ("wiener_rw", (8, 16)),          # Wiener: 8 vs 16 rows per warp
+    ("wiener_xw", (0, 1)),           # Wiener: extracted Z64 rows vs image windows
+    ("wiener_pair", (1, 0)),         # Wiener: two 64-row CTAs per SM vs deeper staging
+    ("seg_sq", (1, 0)),              # ws2: segment-order ||z||^2 vs gather
+    ("select_variant", (1, 0, 2)),   # tree level: ws2 vs ws kernel vs per-level hybrid
+    ("wiener_add_dc", (1, 0)),       # est + dc from the Wiener kernel vs dc added by the gather
 ])
 def test_kernel_variants_bitwise_equal(knob, values, models):
-    """Every performance variant kept behind a debug switch computes the same
+    """Every performance variant kept behind a plan option computes the same
     images and labels bit for bit (same FP64 operation order per element),
-    on a batch that exercises the cover gather and the DMMA Wiener kernel."""
-    import ctypes
+    on a batch that exercises the cover gather and the DMMA Wiener kernel.
+    The options live on the plan: a second restorer in the same process
+    keeps its defaults."""
     import torch
-    from paper_1710_08124_b200 import Restorer, RestorationConfig, synthetic, _native as N
+    from paper_1710_08124_b200 import Restorer, RestorationConfig, synthetic
 
     model, tree = models[64]
     cases = [synthetic.baseline_case("cfg1", 144, image_seed=i, noise_seed=70 + i) for i in range(3)]
     y = torch.from_numpy(np.stack([c.y for c in cases])).cuda()
-    fn = getattr(N.lib(), knob)
-    fn.argtypes = [ctypes.c_int32]
-    r = Restorer(cases[0].A, model, tree, RestorationConfig(sigma=20.0, spacing=4, seed=9), batch=3)
+    cfg = RestorationConfig(sigma=20.0, spacing=4, seed=9)
     outs = []
-    try:
-        for v in values:
-            fn(v)
-            x, rec = r.run(y, trace=True)
-            outs.append((x.cpu().numpy().copy(), [t["labels"] for t in rec]))
-    finally:
-        fn(values[0])
+    for v in values:
+        r = Restorer(cases[0].A, model, tree, cfg, batch=3, options={knob: v})
+        assert r.plan.get_option(knob) == v
+        x, rec = r.run(y, trace=True)
+        outs.append((x.cpu().numpy().copy(), [t["selected"] for t in rec]))
+    other = Restorer(cases[0].A, model, tree, cfg, batch=3)
+    assert other.plan.get_option(knob) == values[0]
     x0, l0 = outs[0]
     for x1, l1 in outs[1:]:
         assert np.array_equal(x0, x1)

@@ -3,6 +3,7 @@
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1710_08124_b200/csrc tools/mma_bench.cu -o /tmp/mma_bench
 #include <cstdio>
 #include <cstdint>
+#include <string>
 #include "tc.cuh"
 
 using namespace fepll;
@@ -74,10 +75,32 @@ __global__ void bench(int kind, int N, int iters, unsigned long long* out, int n
   if (threadIdx.x < 32) tc::tmem_dealloc(tmem, 512);
 }
 
-int main() {
+int main(int argc, char** argv) {
   unsigned long long* d;
   cudaMalloc(&d, 148 * 8);
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  if (argc > 1 && std::string(argv[1]) == "--peak") {
+    // dense TF32 / BF16 peak on all 148 SMs, CUDA-event timed: a short burst
+    // and a ~2 s sustained run (power-capped clocks), M128 x N256 MMAs
+    for (int kind : {2, 1}) {
+      for (int iters : {4000, 400000}) {
+        bench<<<148, 128, 80 * 1024>>>(kind, 256, 100, d, 1);  // warm-up
+        cudaEventRecord(e0);
+        bench<<<148, 128, 80 * 1024>>>(kind, 256, iters, d, 1);
+        cudaEventRecord(e1);
+        cudaError_t e = cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double flops = 148.0 * iters * 4 * 2.0 * 128 * 256 * (kind == 1 ? 16 : 8);
+        printf("{\"kind\": \"%s\", \"iters\": %d, \"ms\": %.3f, \"tflops\": %.1f, \"status\": \"%s\"}\n",
+               kind == 1 ? "f16" : "tf32", iters, ms, flops / (ms * 1e-3) / 1e12, cudaGetErrorString(e));
+      }
+    }
+    return 0;
+  }
   for (int nacc : {1, 2, 4})
   for (int kind = 0; kind < 3; ++kind)
     for (int N : {64, 128, 256}) {
