@@ -10,9 +10,13 @@ Outputs (all small):
   lambda, betas, per-iteration selected labels, counters, CG flags, and the
   final image;
 * ``grids.npz`` — reference ``jittered_grid`` anchors for a sweep of
-  (H, W, P, s, seed, t), including spacing 1 and half == 0 cases.
+  (H, W, P, s, seed, t), including spacing 1 and half == 0 cases;
+* ``solver_<scenario>.npz`` — the scenarios of the reference's own restore
+  tests (``pkg/tests/test_solver.py``): model and tree files written by the
+  reference (FEPLLGM1 / FEPLLTR1 bytes), its phantom image, observations,
+  restored images, per-iteration labels and counters.
 
-Run:  PYTHONDONTWRITEBYTECODE=1 python oracle/make_golden.py
+Run:  PYTHONDONTWRITEBYTECODE=1 python oracle/make_golden.py [--solver-only]
 """
 
 from __future__ import annotations
@@ -74,8 +78,106 @@ def case_inputs(spec):
     return RA, c.y, c.sigma8, c.spacing, c.patch_dim
 
 
+def _noisy(img, sigma8, seed):
+    """pkg/tests/test_solver.py:23-25"""
+    rng = np.random.default_rng(seed)
+    return img + (sigma8 / 255.0) * rng.standard_normal(img.shape)
+
+
+# The scenarios of the reference's own restore tests (pkg/tests/
+# test_solver.py), with the models, trees and phantom images built by the
+# reference (its conftest builders, build_tree, phantom_image).  Each run
+# stores the reference's outputs so the GPU drop-in replays them exactly.
+SOLVER_SCENARIOS = {
+    # TestRestoreBasics (:44-84): 5-component P=64 model flattened at 0.95 + tree
+    "basics": dict(model=(5, 64, 0), flatten=0.95, tree=dict(seed=0), image=(48, 1), runs={
+        "noiseless": dict(noise=None, cfg=dict(sigma=0.0, spacing=4, seed=0)),
+        "seeded": dict(noise=(20, 2), cfg=dict(sigma=20.0, seed=3)),
+        "unclamped": dict(noise="plus_half", cfg=dict(sigma=0.0, spacing=4, seed=0))}),
+    # TestAccelerationSoundness.test_exact_profile_selections (:87-102)
+    "exact16": dict(model=(6, 16, 6), flatten=None, tree=None, image=(24, 7), runs={
+        "exact": dict(noise=(20, 8), cfg=dict(sigma=20.0, use_tree=False, use_flat_tail=False,
+                                              spacing=1, sampling="regular", trace=True))}),
+    # test_patch_estimates_minimize_surrogate (:104-119)
+    "estimates16": dict(model=(4, 16, 9), flatten=0.9, tree=dict(levels=(2, 1), seed=0), image=(24, 10),
+                        runs={"run": dict(noise=(20, 11), cfg=dict(sigma=20.0, spacing=3, trace=True, seed=1))}),
+    # test_image_update_optimality (:121-134)
+    "update16": dict(model=(4, 16, 13), flatten=None, tree=None, image=(24, 14), runs={
+        "run": dict(noise=(20, 15), cfg=dict(sigma=20.0, use_tree=False, use_flat_tail=False,
+                                            spacing=1, sampling="regular", trace=True))}),
+    # TestWorkers (:137-148)
+    "workers64": dict(model=(6, 64, 16), flatten=0.9, tree=dict(seed=0), image=(96, 17), runs={
+        "w1": dict(noise=(20, 18), cfg=dict(sigma=20.0, spacing=1, sampling="regular", seed=5)),
+        "w8": dict(noise=(20, 18), cfg=dict(sigma=20.0, spacing=1, sampling="regular", seed=5,
+                                            workers=8))}),
+    # TestCompareProfiles.test_counter_ratio_and_quality_rows (:152-170)
+    "profiles64": dict(model=(5, 64, 19), flatten=None, tree=None, image=(128, 20), runs={
+        "none": dict(noise=(20, 21), cfg=dict(sigma=20.0, seed=0, use_flat_tail=False, use_tree=False,
+                                              spacing=1, sampling="regular")),
+        "subsample": dict(noise=(20, 21), cfg=dict(sigma=20.0, seed=0, use_flat_tail=False,
+                                                   use_tree=False))}),
+    # test_tree_profile_reduces_evaluations (:172-187): tree of the full-rank
+    # model at rho 1 (solver.py:292-311 _profile_assets)
+    "tree16": dict(model=(20, 16, 22), flatten=None, tree=dict(seed=0, rho=1.0), image=(64, 23), runs={
+        "tree": dict(noise=(20, 24), cfg=dict(sigma=20.0, spacing=2, seed=0, use_flat_tail=False)),
+        "no-tree": dict(noise=(20, 24), cfg=dict(sigma=20.0, spacing=2, seed=0, use_flat_tail=False,
+                                                 use_tree=False))}),
+}
+
+
+def solver_scenarios():
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from conftest import synthetic_model  # the reference's own builder
+    from fepll.model_io import model_write
+    from fepll.operators import identity_operator
+    from fepll.phantoms import phantom_image
+
+    for name, sc in SOLVER_SCENARIOS.items():
+        K, P, mseed = sc["model"]
+        model = synthetic_model(K, P, seed=mseed)
+        if sc["flatten"] is not None:
+            model = model.flatten(sc["flatten"])
+        tree = None
+        if sc["tree"] is not None:
+            tkw = dict(sc["tree"])
+            tree = build_tree(model, tkw.pop("levels", None), seed=tkw.pop("seed"), **tkw)
+        mpath, tpath = Path(f"/tmp/golden_{name}.gm"), Path(f"/tmp/golden_{name}.tr")
+        model_write(model, mpath)
+        out = {"model": np.frombuffer(mpath.read_bytes(), np.uint8)}
+        if tree is not None:
+            tree_write(tree, tpath)
+            out["tree"] = np.frombuffer(tpath.read_bytes(), np.uint8)
+        H, iseed = sc["image"]
+        img = phantom_image(H, H, iseed)
+        out["img"] = img
+        meta = {"runs": {}}
+        for run, spec in sc["runs"].items():
+            if spec["noise"] is None:
+                y = img.copy()
+            elif spec["noise"] == "plus_half":
+                y = img + 0.5
+            else:
+                y = _noisy(img, *spec["noise"])
+            cfg = RestorationConfig(**spec["cfg"])
+            x, st = restore(y, identity_operator(y.shape), model, tree if cfg.use_tree else None, cfg)
+            out[f"y_{run}"] = y
+            out[f"x_{run}"] = x
+            if cfg.trace:
+                out[f"selected_{run}"] = np.stack([r["selected"] for r in st.trace]).astype(np.int16)
+            out[f"counters_{run}"] = np.array([[it.patches, it.score_evaluations, it.selection_multiplies,
+                                                it.estimation_multiplies] for it in st.iterations],
+                                              dtype=np.int64)
+            meta["runs"][run] = spec["cfg"]
+        out["meta"] = json.dumps(meta)
+        np.savez_compressed(OUT / f"solver_{name}.npz", **out)
+        print("scenario", name, {k: v.shape for k, v in out.items() if hasattr(v, "shape")})
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
+    if "--solver-only" in sys.argv:
+        solver_scenarios()
+        return
     models, trees = {}, {}
     for P in (64, 100):
         m = synthetic.synthetic_gmm(200, P, 0, 0.95)
@@ -126,6 +228,7 @@ def main():
     shas = np.array([hashlib.sha256(p.astype("<i4").tobytes()).hexdigest() for _, p in sweep])
     np.savez_compressed(OUT / "grids.npz", keys=keys, sha=shas, **small)
     print("grids", len(sweep))
+    solver_scenarios()
 
 
 if __name__ == "__main__":

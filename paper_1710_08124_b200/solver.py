@@ -599,7 +599,7 @@ class HostPipeline:
     image is restored independently)."""
 
     def __init__(self, A, model, tree, config, batch: int, chunks: int = 1, lam: float | None = None,
-                 mode: str = "tensor", device=None, streams: int = 2):
+                 mode: str = "tensor", device=None, streams: int = 2, graphs: bool = False):
         torch = _torch()
         if batch % chunks:
             raise DataError(f"batch {batch} does not split into {chunks} chunks")
@@ -618,6 +618,14 @@ class HostPipeline:
         self.y64 = [torch.empty((self.per, Ho, Wo), dtype=torch.float64, device=dev) for _ in range(k)]
         self.x32 = [torch.empty((self.per, H, W), dtype=torch.float32, device=dev) for _ in range(k)]
         self.status = [torch.zeros(1, dtype=torch.int32, device=dev) for _ in range(k)]
+        # graphs: each restorer's whole restore of its y64 buffer is captured
+        # once and replayed per chunk (one launch instead of ~100)
+        self.graphs = bool(graphs)
+        if self.graphs:
+            for yb, r in zip(self.y64, self.restorers):
+                yb.zero_()
+                r.capture(yb)
+            torch.cuda.synchronize(dev)
         self._next = 0  # chunk counter: chunk j runs on restorer / stream j % k
         self._computed = None  # event: the last queued chunk's compute is done
 
@@ -645,7 +653,7 @@ class HostPipeline:
                 # overlap them
                 if self._computed is not None:
                     s.wait_event(self._computed)
-                x, _ = r.run(self.y64[k])
+                x = r.replay() if self.graphs else r.run(self.y64[k])[0]
                 self._computed = torch.cuda.Event()
                 self._computed.record(s)
                 self.x32[k].copy_(x)

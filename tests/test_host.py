@@ -224,3 +224,50 @@ def test_restore_validates_before_touching_the_device(models):
         restore(np.zeros((30, 32)), A, model, tree, RestorationConfig(sigma=20.0))
     with pytest.raises(DataError, match="full-rank"):
         restore(y, A, model, tree, RestorationConfig(sigma=20.0, use_flat_tail=False))
+
+
+# ---------------------------------------------------------------- reference-native objects
+REF_SRC = Path("/root/reference/pkg/src")
+
+
+@pytest.mark.skipif(not REF_SRC.exists(), reason="the reference package is only in the build container")
+def test_reference_objects_pack_like_native_ones():
+    """The reference's own GmmModel / GmmTree / DegradationOperator /
+    RestorationConfig objects go through the drop-in's host side (duck
+    typing): the packed device plan is byte-identical to the one built from
+    the package's own types, the closed-form ||A^T A||_F^2 equals the
+    reference's, the plan-cache key is computable, and validation raises the
+    same errors."""
+    import sys
+
+    sys.path.insert(0, str(REF_SRC))
+    from fepll import operators as rops
+    from fepll.gmm import FlatTailComponent as RComp, GmmModel as RModel
+    from fepll.solver import RestorationConfig as RConfig
+    from fepll.tree import build_tree as rbuild_tree
+
+    from paper_1710_08124_b200.solver import _plan_key
+
+    model = synthetic.synthetic_gmm(200, 64, 0, 0.95)
+    tree = synthetic.baseline_tree(model)
+    rmodel = RModel(64, [RComp(c.weight, c.kept_basis, c.kept_eigenvalues, c.tail_value)
+                         for c in model.components], model.rho)
+    rtree = rbuild_tree(rmodel, seed=0)
+    betas = beta_schedule(25.0 / 255.0, 1.0, (1, 4, 8, 16, 32))
+    a, b = pack_plan(model, tree, betas), pack_plan(rmodel, rtree, betas)
+    for k in ("grp_basis", "node_const", "node_nu_tail", "grp_sqw", "mbasis", "shrink", "gtail",
+              "tc_hi", "tc_lo", "tc_x", "tc_w", "path_evals", "path_mults"):
+        assert np.array_equal(a[k], b[k]), k
+    for A in (rops.identity_operator((64, 64)), rops.mask_operator(np.random.default_rng(0).random((64, 64)) < .5),
+              rops.convolution_operator(rops.gaussian_kernel(1.6, 4), (64, 64)),
+              rops.decimate_operator(3, (63, 63), rops.gaussian_kernel(1.2, 3))):
+        assert frobenius_norm_sq_ata(A) == pytest.approx(rops.frobenius_norm_sq_ata(A), rel=1e-12)
+        _plan_key(A, rmodel, rtree, RConfig(sigma=20.0), 1, None, "tensor", None)
+    y = np.zeros((64, 64))
+    A = rops.identity_operator((64, 64))
+    with pytest.raises(DataError, match="tree"):
+        restore(y, A, rmodel, None, RConfig(sigma=20.0))
+    with pytest.raises(DataError, match="spacing"):
+        restore(y, A, rmodel, rtree, RConfig(sigma=20.0, spacing=9))
+    with pytest.raises(DataError):
+        restore(y, A, rmodel, rtree, RConfig(sigma=20.0, iterations=2))
