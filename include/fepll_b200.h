@@ -90,7 +90,9 @@ int fepll_plan_destroy(fepll_plan_t plan);
  *   wiener_xw 0 | 1           Wiener reads 8x8 windows of x instead of Z64 (0);
  *   wiener_add_dc 0 | 1       fepll_wiener writes est + dc (1) or the bare
  *                             estimates (0: the trace's `estimates`; pass dc
- *                             to the aggregation then).
+ *                             to the aggregation then);
+ *   l2_prefetch 0 | 1         ws2 tree-level loaders prefetch each tile's rows
+ *                             into L2 three tiles before copying them (1).
  * Unknown names or out-of-range values: data error. */
 int fepll_plan_set_option(fepll_plan_t plan, const char* name, int64_t value);
 int fepll_plan_get_option(fepll_plan_t plan, const char* name, int64_t* value);
@@ -241,6 +243,22 @@ int fepll_op_solve(void* op, const double* rhs, const double* xtilde, double bs2
                    int32_t maxit, double* x, double* info, int32_t* status, void* stream);
 /* normal_apply (operators.py:233-235) + shift: y = A^T A x + shift x */
 int fepll_op_normal(void* op, const double* x, double shift, double* y, void* stream);
+
+/* ---- offline search-tree construction (tree.py:99-200, build_tree's
+ * device parts; csrc/tree_build.cu).
+ * fepll_tree_kl: inv, cov: device [K][P*P] FP64 (the dense inverses and
+ * covariances of tree.py:72-87); t_scratch: device [K][K]; kl: device
+ * [K][K] = 0.5 (t + t^T) - P, zero diagonal, t[a][b] = Tr(C_a^-1 C_b)
+ * (pairwise_symmetric_kl, tree.py:99-107). */
+int fepll_tree_kl(const double* inv, const double* cov, int32_t K, int32_t P, double* t_scratch,
+                  double* kl, void* stream);
+/* fepll_cluster_swap: the pairwise-swap local search of balanced_cluster
+ * (tree.py:169-198), sequentially exact: D device [n][n] divergences, cid
+ * device int64 [n] cluster ids (in/out), rowsum device [n][L] row sums of D
+ * over each cluster (in/out), at most `sweeps` passes; sweeps_done
+ * (optional, device int32) receives the passes run. */
+int fepll_cluster_swap(const double* D, int32_t n, int32_t L, int64_t* cid, double* rowsum,
+                       int32_t sweeps, int32_t* sweeps_done, void* stream);
 
 /* debugging: record per-tile pipeline timestamps of one tree level of the
  * warp-specialized scorer into a device buffer (148 x 64 x 8 uint64). */

@@ -14,5 +14,6 @@ from .operators import (CgConfig, DegradationOperator, SolveInfo, convolution_op
                         mask_operator, radial_gain_map)
 from .patches import SampleGrid, axis_anchors, jitter_rng, jittered_grid, regular_grid
 from .solver import (HostPipeline, IterationStats, RestorationConfig, Restorer, SolverStats,
-                     beta_schedule, restore, restore_batch)
+                     beta_schedule, cached_restorer, clear_plan_cache, restore, restore_batch)
 from .tree import GmmTree, TreeNode
+from .tree_build import auto_level_sizes, balanced_cluster, build_tree, pairwise_symmetric_kl

@@ -74,6 +74,8 @@ _SIGS = {
     "fepll_op_init": (i32, [vp, vp, vp, f64, f64, f64, i32, vp, vp, vp]),
     "fepll_op_solve": (i32, [vp, vp, vp, f64, f64, i32, vp, vp, vp, vp]),
     "fepll_op_normal": (i32, [vp, vp, f64, vp, vp]),
+    "fepll_tree_kl": (i32, [vp, vp, i32, i32, vp, vp, vp]),
+    "fepll_cluster_swap": (i32, [vp, i32, i32, vp, vp, i32, vp, vp]),
 }
 
 _lib = None

@@ -262,6 +262,7 @@ static int* plan_option(Plan* p, const char* name) {
   if (n == "wiener_rw") return &p->opt.wiener_rw;
   if (n == "wiener_xw") return &p->opt.wiener_xw;
   if (n == "wiener_add_dc") return &p->opt.wiener_add_dc;
+  if (n == "l2_prefetch") return &p->opt.l2_prefetch;
   return nullptr;
 }
 

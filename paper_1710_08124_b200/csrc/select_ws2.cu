@@ -96,7 +96,10 @@ struct EpiGroup {
 constexpr int kMaxNodes = 128;  // internal nodes per level handled by this kernel
 using WsLevelTables = LevelTablesN<256>;  // next level <= 256 nodes
 
-constexpr int kIdxAhead = 6;   // tiles of row indices in flight ahead of their rows
+constexpr int kPrefetch = 3;   // tiles ahead of its cp.async a row is prefetched into L2
+// tiles of row indices in flight ahead of their rows: the prefetch of tile
+// i + kPrefetch waits for its indices without waiting for recent row copies
+constexpr int kIdxAhead = 6 + kPrefetch;
 constexpr int kIdxRing = kIdxAhead + 1;
 
 template <int NG>
@@ -118,6 +121,10 @@ struct Smem {
   int32_t t_begin, t_end;
 };
 
+static_assert(1024 + kStages * kStageBytes + kBBytes + sizeof(Smem<4>) <= 232448 &&
+                  1024 + kStages * kStageBytes + kBBytes + sizeof(Smem<3>) <= 232448,
+              "ws2 shared memory exceeds 227 KB");
+
 struct Args {
   LevelArgs a;
   const float* Z32;      // [n_total][z32_pitch] FP32 patch rows (fepll_extract)
@@ -127,6 +134,7 @@ struct Args {
   int32_t* queue;
   int32_t* queue_len;
   int katoms;
+  int prefetch;          // tiles ahead whose rows the loaders prefetch into L2 (0: off)
   uint64_t* trace;       // debug timeline: [CTA][64 tiles][16] clock64 stamps (or NULL)
 };
 
@@ -266,7 +274,20 @@ select_level_ws2_kernel(PlanView pv, Args args) {
       const int st = i % kStages;
       if (i >= kStages) tc::mbar_wait(&s.mma_done[st], ((i / kStages) - 1) & 1);
       if (tid == 0) stamp(args, i, 8);
-      tc::cp_async_wait<kIdxAhead - 1>();  // idx(i) landed (one group per tile)
+      if (args.prefetch > 0) {
+        // idx(i + kPrefetch) landed (and with it idx(i)); each lane sends its
+        // row of that tile to L2 now, so the stage's cp.async later hits L2:
+        // DRAM requests stay in flight beyond the smem stages' capacity
+        tc::cp_async_wait<kIdxAhead - 1 - kPrefetch>();
+        const int jp = i + kPrefetch;
+        if (jp < ntile) {
+          const int gp = s.idx_ring[jp % kIdxRing][r0 + lane];
+          if (lane < kLoaderRows && gp >= 0)
+            tc::prefetch_l2_bulk(args.Z32 + (int64_t)gp * pitch, (uint32_t)(args.katoms * 128));
+        }
+      } else {
+        tc::cp_async_wait<kIdxAhead - 1>();  // idx(i) landed (one group per tile)
+      }
       __syncwarp();                         // ... including the other lanes' entries
       const int32_t* rg = s.idx_ring[i % kIdxRing] + r0;
       int g[kLoaderQ];
@@ -635,6 +656,7 @@ int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double
   args.queue = p->rs.queue;
   args.queue_len = p->rs.queue_len;
   args.katoms = (p->v.P + 31) / 32;
+  args.prefetch = p->opt.l2_prefetch;
   args.trace = (a.depth == g_ws_trace_level) ? g_ws_trace : nullptr;
   auto launch = [&](auto kernel, size_t tables, int threads) -> int {
     const size_t smem = 1024 + ws2::kStages * ws2::kStageBytes + ws2::kBBytes + tables;

@@ -324,7 +324,8 @@ class DevicePlan:
         self.path_mults = h["path_mults"]
         self.reserved = 0
 
-    OPTIONS = ("select_variant", "seg_sq", "wiener_pair", "wiener_rw", "wiener_xw", "wiener_add_dc")
+    OPTIONS = ("select_variant", "seg_sq", "wiener_pair", "wiener_rw", "wiener_xw", "wiener_add_dc",
+               "l2_prefetch")
 
     def set_option(self, name: str, value: int) -> None:
         """Per-plan kernel choice (include/fepll_b200.h fepll_plan_set_option)."""
