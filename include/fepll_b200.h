@@ -91,8 +91,12 @@ int fepll_plan_destroy(fepll_plan_t plan);
  *   wiener_add_dc 0 | 1       fepll_wiener writes est + dc (1) or the bare
  *                             estimates (0: the trace's `estimates`; pass dc
  *                             to the aggregation then);
- *   l2_prefetch 0 | 1         ws2 tree-level loaders prefetch each tile's rows
- *                             into L2 three tiles before copying them (1).
+ *   l2_prefetch 0 | 1 | 2     ws2 tree-level loaders prefetch each tile's rows
+ *                             into L2 three tiles before copying them, per
+ *                             line (1) or one bulk prefetch per row (2);
+ *                             measured slower, default 0;
+ *   rescore_by_node 0 | 1     FP64 re-scoring grouped by tree node, the node's
+ *                             group matrix staged in shared memory (1).
  * Unknown names or out-of-range values: data error. */
 int fepll_plan_set_option(fepll_plan_t plan, const char* name, int64_t value);
 int fepll_plan_get_option(fepll_plan_t plan, const char* name, int64_t* value);

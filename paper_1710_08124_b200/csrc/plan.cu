@@ -99,7 +99,9 @@ static int create(const fepll_plan_desc* d, Plan** out) {
   // they are scored in sub-groups / column chunks
   p->level_wide.assign(maxd + 1, 0);
   p->level_tc_npad.assign(maxd + 1, 0);
+  p->max_group_cols_at_depth.assign(maxd + 1, 0);
   for (int i = 0; i < n; ++i) {
+    p->max_group_cols_at_depth[d->depth[i]] = std::max(p->max_group_cols_at_depth[d->depth[i]], d->grp_width[i]);
     if (d->child_count[i] > kMaxChildren || d->grp_width[i] > kMaxGroupCols) p->level_wide[d->depth[i]] = 1;
     if (d->grp_tc_npad)
       p->level_tc_npad[d->depth[i]] = std::max(p->level_tc_npad[d->depth[i]], d->grp_tc_npad[i]);
@@ -263,6 +265,7 @@ static int* plan_option(Plan* p, const char* name) {
   if (n == "wiener_xw") return &p->opt.wiener_xw;
   if (n == "wiener_add_dc") return &p->opt.wiener_add_dc;
   if (n == "l2_prefetch") return &p->opt.l2_prefetch;
+  if (n == "rescore_by_node") return &p->opt.rescore_by_node;
   return nullptr;
 }
 
@@ -272,7 +275,7 @@ int fepll_plan_set_option(fepll_plan_t plan, const char* name, int64_t value) {
   int* slot = plan_option(p, name);
   FEPLL_REQUIRE(slot != nullptr, std::string("plan_set_option: unknown option ") + (name ? name : "(null)"));
   const std::string n(name);
-  const bool ok = (n == "select_variant") ? (value >= 0 && value <= 2)
+  const bool ok = (n == "select_variant" || n == "l2_prefetch") ? (value >= 0 && value <= 2)
                   : (n == "wiener_rw")    ? (value == 8 || value == 16)
                                           : (value == 0 || value == 1);
   FEPLL_REQUIRE(ok, "plan_set_option: value out of range for " + n);

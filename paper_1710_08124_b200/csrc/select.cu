@@ -58,7 +58,7 @@ __device__ __forceinline__ void load_patch(const PatchSrc& ps, int g, int P, dou
 // chain each, the same order for every width); CH rows of G are loaded
 // before they are consumed so a warp keeps CH*NC loads in flight instead of
 // one L2 round trip per row.
-template <int NC, int CH>
+template <int NC, int CH, bool kShared = false>
 __device__ __forceinline__ void project_cols(const double* G, int stride, int ncols, int P,
                                              const double* zs, int lane, double (&acc)[NC]) {
   const int ncol = (ncols - lane + 31) >> 5;
@@ -71,7 +71,9 @@ __device__ __forceinline__ void project_cols(const double* G, int stride, int nc
     for (int j = 0; j < CH; ++j)
 #pragma unroll
       for (int k = 0; k < NC; ++k)
-        g[j][k] = k < ncol ? __ldg(G + (int64_t)(p + j) * stride + lane + 32 * k) : 0.0;
+        g[j][k] = k < ncol ? (kShared ? G[(int64_t)(p + j) * stride + lane + 32 * k]
+                                      : __ldg(G + (int64_t)(p + j) * stride + lane + 32 * k))
+                           : 0.0;
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
       const double zp = zs[p + j];
@@ -83,16 +85,18 @@ __device__ __forceinline__ void project_cols(const double* G, int stride, int nc
     const double zp = zs[p];
 #pragma unroll
     for (int k = 0; k < NC; ++k)
-      if (k < ncol) acc[k] = fma(zp, __ldg(G + (int64_t)p * stride + lane + 32 * k), acc[k]);
+      if (k < ncol)
+        acc[k] = fma(zp, kShared ? G[(int64_t)p * stride + lane + 32 * k]
+                                 : __ldg(G + (int64_t)p * stride + lane + 32 * k), acc[k]);
   }
 }
 
 // tv[j] = c_j^2 w_j for the ncols columns of the block (c = z . G)
-template <int NC, int CH>
+template <int NC, int CH, bool kShared = false>
 __device__ __forceinline__ void child_terms(const double* G, const double* w, int stride, int ncols,
                                             int P, const double* zs, int lane, double* tv) {
   double acc[NC];
-  project_cols<NC, CH>(G, stride, ncols, P, zs, lane, acc);
+  project_cols<NC, CH, kShared>(G, stride, ncols, P, zs, lane, acc);
 #pragma unroll
   for (int k = 0; k < NC; ++k) {
     const int j = lane + 32 * k;
@@ -247,6 +251,115 @@ rescore_fp64_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restr
       }
     }
     __syncwarp();
+  }
+}
+
+// Node-grouped form of rescore_fp64_kernel: CTA (k, j) takes the queued
+// decisions of node u = lvl_begin + k (share j of gridDim.y), stages u's
+// group matrix (P x width FP64, the children's bases side by side) in
+// shared memory once, then scores each queued patch against it — the same
+// FP64 operations in the same order as score_children_fp64 (bitwise the
+// same scores), but one L2 read of the group per CTA instead of one per
+// decision, and no dependent L2 round trips per row.  Used when the widest
+// group of the level fits (kRescoreSmem).
+constexpr int kRescoreWarps = 8;
+constexpr int kRescoreChunk = 1024;  // queue entries compacted per pass
+constexpr size_t kRescoreSmem = 160 * 1024;  // group matrix bytes (+ 48 KB of per-warp rows)
+constexpr size_t kRescoreWarpSmem = sizeof(double) * kRescoreWarps * (kMaxP + kMaxGroupCols);
+
+__global__ void __launch_bounds__(kRescoreWarps * 32, 1)
+rescore_node_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restrict__ sq,
+                    const int32_t* __restrict__ queue, const int32_t* __restrict__ queue_len) {
+  // dynamic: per-warp patch rows and score terms, then the [P][width] group
+  // matrix of node u
+  extern __shared__ __align__(16) double dyn[];
+  double (*zbuf)[kMaxP] = reinterpret_cast<double (*)[kMaxP]>(dyn);
+  double (*tbuf)[kMaxGroupCols] = reinterpret_cast<double (*)[kMaxGroupCols]>(dyn + kRescoreWarps * kMaxP);
+  double* gs = dyn + kRescoreWarps * (kMaxP + kMaxGroupCols);
+  __shared__ int32_t list[kRescoreChunk];
+  __shared__ int32_t wcnt[kRescoreWarps];
+  const int lane = lane_id(), warp = warp_id();
+  const int total = queue_len[a.depth];
+  const int u = a.lvl_begin + blockIdx.x;
+  const int P = pv.P;
+  const int width = pv.grp_width[u];
+  const int nk = pv.child_count[u];
+  if (total == 0 || nk == 0) return;
+  const double* w = pv.grp_sqw + (int64_t)a.t * pv.grp_cols_total + pv.grp_col_off[u];
+  const int32_t* kids = pv.child_list + pv.child_start[u];
+  bool staged = false;
+  int seen = 0;  // matches of node u in earlier chunks (share j takes match m with m % gridDim.y == j)
+  for (int c0 = 0; c0 < total; c0 += kRescoreChunk) {
+    const int c1 = min(total, c0 + kRescoreChunk);
+    __syncthreads();  // the previous chunk's list is consumed
+    // compaction of node u's entries in queue order: every thread tests
+    // kPer entries (loads issued together), then per pass a warp ballot and
+    // a prefix over the warps' counts
+    constexpr int kPer = kRescoreChunk / (kRescoreWarps * 32);
+    int2 ent[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int i = c0 + k * kRescoreWarps * 32 + threadIdx.x;
+      ent[k] = i < c1 ? __ldg(reinterpret_cast<const int2*>(queue) + i) : make_int2(-1, -1);
+    }
+    int running = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const bool hit = ent[k].y == u;
+      const unsigned m = __ballot_sync(0xffffffffu, hit);
+      if (lane == 0) wcnt[warp] = __popc(m);
+      __syncthreads();
+      int before = running, pass = 0;
+      for (int w2 = 0; w2 < kRescoreWarps; ++w2) {
+        const int c = wcnt[w2];
+        if (w2 < warp) before += c;
+        pass += c;
+      }
+      if (hit) list[before + __popc(m & ((1u << lane) - 1u))] = ent[k].x;
+      running += pass;
+      __syncthreads();  // wcnt reused by the next pass
+    }
+    const int nl = running;
+    // this share's items: global match index (seen + q) % gridDim.y == blockIdx.y
+    const int first = (int)((blockIdx.y + gridDim.y - (unsigned)(seen % gridDim.y)) % gridDim.y);
+    seen += nl;
+    if (first >= nl) continue;
+    if (!staged) {
+      const int64_t nel = (int64_t)P * width;
+      const double* G = pv.grp_basis + pv.grp_off64[u];
+      for (int64_t e = threadIdx.x; e < nel; e += blockDim.x) gs[e] = __ldg(G + e);
+      __syncthreads();
+      staged = true;
+    }
+    double* zs = zbuf[warp];
+    double* tv = tbuf[warp];
+    for (int q = first + warp * gridDim.y; q < nl; q += kRescoreWarps * gridDim.y) {
+      const int patch = list[q];
+      load_patch(ps, patch, P, zs);
+      if (width <= 128)
+        child_terms<4, 8, true>(gs, w, width, width, P, zs, lane, tv);
+      else if (width <= 256)
+        child_terms<8, 4, true>(gs, w, width, width, P, zs, lane, tv);
+      else
+        child_terms<kColsPerLane, 2, true>(gs, w, width, width, P, zs, lane, tv);
+      __syncwarp();
+      double b;
+      int bk;
+      block_argmin(pv, a.t, u, 0, nk, 0, tv, sq[patch], b, bk);
+      const int v = kids[bk];
+      if (lane == 0) {
+        const int slot = atomicAdd(&a.cnt[v], 1);
+        if (pv.child_count[v] > 0) {
+          a.seg_out[a.off[v] + slot] = patch;
+          if (a.sq_out) a.sq_out[a.off[v] + slot] = sq[patch];
+        } else {
+          a.leafseg[a.off[v] + slot] = patch;
+          a.labels[patch] = pv.leaf_index[v];
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
   }
 }
 
@@ -478,8 +591,19 @@ int rescore_queue_x(Plan* p, const LevelArgs& a, const double* x, const int32_t*
                     int H, int W, const double* dc, const double* sq, const double* Z64,
                     cudaStream_t st) {
   PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P), n_img, Z64};
-  rescore_fp64_kernel<<<4 * kSMs, kSelWarps * 32, 0, st>>>(p->v, a, ps, sq, p->rs.queue,
-                                                           p->rs.queue_len);
+  const int nd = a.lvl_end - a.lvl_begin;
+  const size_t gbytes = sizeof(double) * (size_t)p->v.P * p->max_group_cols_at_depth[a.depth];
+  if (p->opt.rescore_by_node && gbytes <= kRescoreSmem && !p->level_wide[a.depth]) {
+    // node-grouped: the level's internal nodes x shares, ~two CTAs per SM
+    const int shares = std::max(1, (2 * kSMs + nd - 1) / nd);
+    FEPLL_CUDA(cudaFuncSetAttribute(rescore_node_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(kRescoreSmem + kRescoreWarpSmem)));
+    rescore_node_kernel<<<dim3(nd, shares), kRescoreWarps * 32, kRescoreWarpSmem + gbytes, st>>>(
+        p->v, a, ps, sq, p->rs.queue, p->rs.queue_len);
+  } else {
+    rescore_fp64_kernel<<<4 * kSMs, kSelWarps * 32, 0, st>>>(p->v, a, ps, sq, p->rs.queue,
+                                                             p->rs.queue_len);
+  }
   FEPLL_LAUNCH();
   return kOk;
 }

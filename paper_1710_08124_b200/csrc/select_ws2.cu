@@ -282,8 +282,14 @@ select_level_ws2_kernel(PlanView pv, Args args) {
         const int jp = i + kPrefetch;
         if (jp < ntile) {
           const int gp = s.idx_ring[jp % kIdxRing][r0 + lane];
-          if (lane < kLoaderRows && gp >= 0)
-            tc::prefetch_l2_bulk(args.Z32 + (int64_t)gp * pitch, (uint32_t)(args.katoms * 128));
+          if (lane < kLoaderRows && gp >= 0) {
+            const float* rowp = args.Z32 + (int64_t)gp * pitch;
+            if (args.prefetch == 2) {
+              tc::prefetch_l2_bulk(rowp, (uint32_t)(args.katoms * 128));
+            } else {
+              for (int ka = 0; ka < args.katoms; ++ka) tc::prefetch_l2(rowp + 32 * ka);
+            }
+          }
         }
       } else {
         tc::cp_async_wait<kIdxAhead - 1>();  // idx(i) landed (one group per tile)

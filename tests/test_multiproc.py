@@ -91,3 +91,55 @@ def test_batch_shard_rejects_uneven_split():
     with pytest.raises(DataError):
         batch_shard(63, 2, 0)
     assert strip_rows(10, 3, 2) == (6, 10)
+
+
+# ---------------------------------------------------------------- NCCL, >= 2 GPUs
+def _n_gpus():
+    try:
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+def _nccl_worker(rank, world, port, out):
+    """One rank per GPU over NCCL: (1) a strip-mode restore of one image with
+    the halo exchange between HQS iterations, (2) this rank's batch shard.
+    Each is compared with the single-process result on the same device."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    try:
+        from paper_1710_08124_b200 import RestorationConfig, restore_batch, synthetic
+        from paper_1710_08124_b200.strips import StripRestorer, restore_strips_single_process
+
+        model = synthetic.synthetic_gmm(200, 64, 0, 0.95)
+        tree = synthetic.baseline_tree(model)
+        cfg = RestorationConfig(sigma=25.0, spacing=4, seed=0)
+        c = synthetic.baseline_case("cfg5", 160, image_seed=2, noise_seed=9)
+        sr = StripRestorer(160, 160, model, tree, cfg, rank, world, device=dev)
+        sp = sr.spec
+        y = torch.from_numpy(np.ascontiguousarray(c.y[None, sp.slab_lo:sp.slab_hi])).to(dev)
+        mine = sr.run(y).cpu().numpy()
+        ref = restore_strips_single_process(c.y, model, tree, cfg, world)
+        ok = np.array_equal(mine, ref[sp.r0:sp.r1])
+        cases = [synthetic.baseline_case("cfg1", 64, image_seed=i, noise_seed=50 + i) for i in range(2 * world)]
+        ys = np.stack([x.y for x in cases])
+        shard = batch_shard(len(cases), world, rank)
+        xb, _ = restore_batch(ys[shard], cases[0].A, model, tree, RestorationConfig(sigma=20.0, spacing=4))
+        xa, _ = restore_batch(ys, cases[0].A, model, tree, RestorationConfig(sigma=20.0, spacing=4))
+        ok = ok and np.array_equal(xb, xa[shard])
+        out[rank] = int(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(_n_gpus() < 2, reason="needs >= 2 GPUs (NCCL over NVLink)")
+def test_nccl_world2_strips_and_batch_shard():
+    world = 2
+    out = torch.multiprocessing.get_context("spawn").Array("i", [0] * world)
+    mp.start_processes(_nccl_worker, args=(world, _free_port(), out), nprocs=world, join=True,
+                       start_method="spawn")
+    assert list(out) == [1] * world
