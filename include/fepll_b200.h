@@ -96,7 +96,8 @@ int fepll_plan_destroy(fepll_plan_t plan);
  *                             line (1) or one bulk prefetch per row (2);
  *                             measured slower, default 0;
  *   rescore_by_node 0 | 1     FP64 re-scoring grouped by tree node, the node's
- *                             group matrix staged in shared memory (1).
+ *                             group matrix staged in shared memory (measured
+ *                             slower, default 0).
  * Unknown names or out-of-range values: data error. */
 int fepll_plan_set_option(fepll_plan_t plan, const char* name, int64_t value);
 int fepll_plan_get_option(fepll_plan_t plan, const char* name, int64_t* value);

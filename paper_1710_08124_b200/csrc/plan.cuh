@@ -72,7 +72,10 @@ struct PlanOptions {
   int wiener_rw = 8;       // rows per warp in the pair configuration (8 or 16)
   int wiener_xw = 0;       // 1: the Wiener kernel reads 8x8 windows of x (no Z64 rows)
   int wiener_add_dc = 1;   // 1: fepll_wiener writes est + dc; 0: the bare estimates (traces)
-  int rescore_by_node = 1; // 1: re-scoring CTAs group the queued decisions by node (group matrix staged in smem once)
+  int rescore_by_node = 0; // 1: re-scoring CTAs group the queued decisions by node (group matrix staged in
+                           // smem once per CTA) — measured slower (select 11.3 -> 13.1 ms/step at 64 x 1024^2:
+                           // one 208 KB CTA per SM leaves 8 warps for latency-bound chains), off
+
   int l2_prefetch = 0;     // ws2 loaders prefetch rows into L2 three tiles ahead of their cp.async: 1 per 128-B line, 2 one bulk prefetch per row (both measured slower: level 0.295 -> 0.324 / 0.486 ms)
 };
 

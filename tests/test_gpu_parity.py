@@ -472,7 +472,7 @@ def test_operator_adjoint_identity_and_normal(name):
     ("select_variant", (1, 0, 2)),   # tree level: ws2 vs ws kernel vs per-level hybrid
     ("wiener_add_dc", (1, 0)),       # est + dc from the Wiener kernel vs dc added by the gather
     ("l2_prefetch", (0, 1)),         # ws2 loaders: L2 prefetch three tiles ahead vs none
-    ("rescore_by_node", (1, 0)),     # FP64 re-scoring grouped by node (smem group) vs per decision
+    ("rescore_by_node", (0, 1)),     # FP64 re-scoring per decision vs grouped by node (smem group)
 ])
 def test_kernel_variants_bitwise_equal(knob, values, models):
     """Every performance variant kept behind a plan option computes the same

@@ -22,6 +22,18 @@ __device__ __forceinline__ void mma_tf32_elect(uint32_t d, uint64_t a, uint64_t 
                "r"(idesc), "r"(acc) : "memory");
 }
 
+__device__ __forceinline__ void mma_i8_elect(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "elect.sync _|e, 0xffffffff;\n\t"
+               "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(d), "l"(a), "l"(b),
+               "r"(idesc), "r"(acc) : "memory");
+}
+
+// kind::i8: S32 accumulate (c_format 2), signed A and B (formats 1), K-major, K = 32
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
 __global__ void bench(int kind, int N, int iters, unsigned long long* out, int nacc) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~uintptr_t(1023));
@@ -34,7 +46,23 @@ __global__ void bench(int kind, int N, int iters, unsigned long long* out, int n
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
-  if (kind == 2 && threadIdx.x < 32) {
+  if (kind == 3 && threadIdx.x < 32) {
+    const uint32_t A = tc::smem_u32(base), B = tc::smem_u32(base + 32768);
+    const uint32_t idi = idesc_i8(128, N);
+    const uint64_t da = tc::desc_sw128(A), db = tc::desc_sw128(B);
+    unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t d = tmem + ((kk % nacc) * 128);
+        mma_i8_elect(d, da + 2 * kk, db + 2 * kk, idi, it | kk);
+      }
+    }
+    if (threadIdx.x == 0) { tc::mma_commit(&bar); tc::mbar_wait(&bar, 0); }
+    __syncwarp();
+    unsigned long long t1 = clock64();
+    if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  } else if (kind == 2 && threadIdx.x < 32) {
     const uint32_t A = tc::smem_u32(base), B = tc::smem_u32(base + 32768);
     const uint32_t idt = tc::idesc_tf32(128, N);
     const uint64_t da = tc::desc_sw128(A), db = tc::desc_sw128(B);
@@ -85,7 +113,7 @@ int main(int argc, char** argv) {
   if (argc > 1 && std::string(argv[1]) == "--peak") {
     // dense TF32 / BF16 peak on all 148 SMs, CUDA-event timed: a short burst
     // and a ~2 s sustained run (power-capped clocks), M128 x N256 MMAs
-    for (int kind : {2, 1}) {
+    for (int kind : {2, 1, 3}) {
       for (int iters : {4000, 400000}) {
         bench<<<148, 128, 80 * 1024>>>(kind, 256, 100, d, 1);  // warm-up
         cudaEventRecord(e0);
@@ -94,16 +122,16 @@ int main(int argc, char** argv) {
         cudaError_t e = cudaEventSynchronize(e1);
         float ms = 0.f;
         cudaEventElapsedTime(&ms, e0, e1);
-        const double flops = 148.0 * iters * 4 * 2.0 * 128 * 256 * (kind == 1 ? 16 : 8);
+        const double flops = 148.0 * iters * 4 * 2.0 * 128 * 256 * (kind == 1 ? 16 : kind == 3 ? 32 : 8);
         printf("{\"kind\": \"%s\", \"iters\": %d, \"ms\": %.3f, \"tflops\": %.1f, \"status\": \"%s\"}\n",
-               kind == 1 ? "f16" : "tf32", iters, ms, flops / (ms * 1e-3) / 1e12, cudaGetErrorString(e));
+               kind == 1 ? "f16" : kind == 3 ? "i8" : "tf32", iters, ms, flops / (ms * 1e-3) / 1e12, cudaGetErrorString(e));
       }
     }
     return 0;
   }
   for (int nacc : {1, 2, 4})
-  for (int kind = 0; kind < 3; ++kind)
-    for (int N : {64, 128, 256}) {
+  for (int kind = 0; kind < 4; ++kind)
+    for (int N : {32, 64, 128, 256}) {
       if (N == 256 && nacc > 2) continue;
       const int iters = 2000;
       bench<<<148, 128, 80 * 1024>>>(kind, N, iters, d, N == 256 ? 1 : nacc);
@@ -111,8 +139,8 @@ int main(int argc, char** argv) {
       unsigned long long h[148];
       cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
       double cyc = (double)h[0] / (iters * 4);
-      double macs = 128.0 * N * (kind == 1 ? 16 : 8);
-      printf("nacc=%d %s N=%3d: %.1f cycles/MMA  -> %.0f MAC/clk/SM (%s)\n", nacc, kind == 0 ? "tf32" : (kind == 1 ? "f16 " : "tf32E"),
+      double macs = 128.0 * N * (kind == 1 ? 16 : kind == 3 ? 32 : 8);
+      printf("nacc=%d %s N=%3d: %.1f cycles/MMA  -> %.0f MAC/clk/SM (%s)\n", nacc, kind == 0 ? "tf32" : (kind == 1 ? "f16 " : kind == 3 ? "i8  " : "tf32E"),
              N, cyc, macs / cyc, cudaGetErrorString(e));
     }
   return 0;
