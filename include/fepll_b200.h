@@ -173,6 +173,14 @@ int fepll_wiener(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32
                  const int32_t* anchors, int32_t n_img, const double* dc, const double* Z64,
                  int64_t n_total, double* Zhat, int32_t zhat_rows, void* stream);
 
+/* FP32-state mode (opt-in, Restorer(precision="fp32-state")): the Wiener
+ * kernel reads the FP32 patch rows of fepll_extract (z32_pitch floats per
+ * row, 16-byte aligned) and writes est + dc rounded once to FP32; the
+ * arithmetic in between is the FP64 DMMA of fepll_wiener. */
+int fepll_wiener_f32(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32_t W,
+                     const int32_t* anchors, int32_t n_img, const double* dc, const float* Z32,
+                     int32_t z32_pitch, int64_t n_total, float* Zhat, int32_t zhat_rows, void* stream);
+
 /* patches.py:198-222 (+ operators.py:284-287 when kind==0):
  * per-pixel ordered gather of (Zhat + dc) over covering anchors; dc may be
  * NULL when Zhat already holds est + dc (fepll_wiener's output).
@@ -199,6 +207,15 @@ int fepll_aggregate_strip(const double* Zhat, const double* dc, const int32_t* a
                           const double* aty, const double* diag, double bs2, int32_t kind,
                           double* x_out, double* xtilde_out, int32_t* status, void* stream);
 
+/* FP32-state form: Zhat holds FP32 est + dc; sums run in FP64 as above. */
+int fepll_aggregate_strip_f32(const float* Zhat, const double* dc, const int32_t* anchors,
+                              int32_t n_rows, int32_t n_cols, int32_t spacing, int32_t half,
+                              int32_t side, int32_t batch, int32_t H, int32_t W,
+                              int32_t row0, int32_t H_glob, int32_t a_first,
+                              int32_t n_local_rows, int32_t r_begin, int32_t r_end,
+                              const double* aty, const double* diag, double bs2, int32_t kind,
+                              double* x_out, double* xtilde_out, int32_t* status, void* stream);
+
 /* Cover lists (CSR) of a sampling plan: for local rows [r_begin, r_end) of a
  * (strip of an) image, the anchors covering each pixel in ascending patch
  * order (the np.bincount order of patches.py:213-220), entry = local patch
@@ -224,6 +241,13 @@ int fepll_aggregate_cover(const double* Zhat, const double* dc, const int32_t* p
                           int32_t H, int32_t W, int32_t r_begin, int32_t r_end,
                           const double* aty, const double* diag, double bs2, int32_t kind,
                           double* x_out, double* xtilde_out, int32_t* status, void* stream);
+
+/* FP32-state form of fepll_aggregate_cover (FP32 Zhat, FP64 sums). */
+int fepll_aggregate_cover_f32(const float* Zhat, const double* dc, const int32_t* ptr,
+                              const int32_t* entries, int32_t P, int32_t n_local, int32_t zhat_rows,
+                              int32_t batch, int32_t H, int32_t W, int32_t r_begin, int32_t r_end,
+                              const double* aty, const double* diag, double bs2, int32_t kind,
+                              double* x_out, double* xtilde_out, int32_t* status, void* stream);
 
 /* ---- degradation operators (operators.py:51-394); handle = opaque plan.
  * kind: 0 identity, 1 convolution, 2 mask, 3 gain, 4 decimate (factor).

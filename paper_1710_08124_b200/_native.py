@@ -58,6 +58,11 @@ _SIGS = {
     "fepll_wiener_reads_image": (i32, [vp]),
     "fepll_wiener": (i32, [vp, i32, vp, i32, i32, vp, i32, vp, vp, i64, vp, i32, vp]),
     "fepll_select_rescored": (i32, [vp, vp, vp]),
+    "fepll_wiener_f32": (i32, [vp, i32, vp, i32, i32, vp, i32, vp, vp, i32, i64, vp, i32, vp]),
+    "fepll_aggregate_strip_f32": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32,
+                                        i32, i32, i32, i32, i32, i32, vp, vp, f64, i32, vp, vp, vp, vp]),
+    "fepll_aggregate_cover_f32": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, vp, vp,
+                                        f64, i32, vp, vp, vp, vp]),
     "fepll_aggregate": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, vp, vp, f64,
                               i32, vp, vp, vp, vp]),
     "fepll_aggregate_strip": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32,

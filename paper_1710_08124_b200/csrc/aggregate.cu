@@ -88,8 +88,9 @@ __device__ __forceinline__ void finish_pixel(double sum, double lo, double hi, i
   }
 }
 
+template <typename ZT>
 __global__ void __launch_bounds__(256)
-aggregate_kernel(const double* __restrict__ Zhat, const double* __restrict__ dc, GridGeo geo,
+aggregate_kernel(const ZT* __restrict__ Zhat, const double* __restrict__ dc, GridGeo geo,
                  int batch, int H, const double* __restrict__ aty,
                  const double* __restrict__ diag, double bs2, int kind,
                  double* __restrict__ x_out, double* __restrict__ xt_out, int32_t* status,
@@ -105,7 +106,7 @@ aggregate_kernel(const double* __restrict__ Zhat, const double* __restrict__ dc,
   int count = 0;
   for_each_cover(geo, geo.row0 + r_loc, c, [&](int i, int dr, int dcol) {
     const int64_t g = gbase + i;
-    const double z = Zhat[g * P + dr * geo.side + dcol];
+    const double z = (double)Zhat[g * P + dr * geo.side + dcol];
     const double v = dc ? __dadd_rn(z, dc[g]) : z;  // dc == NULL: Zhat holds est + dc
     sum += v;
     lo = fmin(lo, v);
@@ -229,9 +230,9 @@ __device__ __forceinline__ void pixel_update(double xt, int64_t pix, const doubl
   }
 }
 
-template <bool kDc, int NB, bool CG>
+template <bool kDc, int NB, bool CG, typename ZT>
 __global__ void __launch_bounds__(kCoverThreads, 4)  // 64 registers: 4 blocks per SM
-aggregate_cover_kernel(const double* __restrict__ Zhat, const double* __restrict__ dc,
+aggregate_cover_kernel(const ZT* __restrict__ Zhat, const double* __restrict__ dc,
                        const int32_t* __restrict__ ptr, const int32_t* __restrict__ entries, int P,
                        int n_local, int zrows, int batch, int H, int W, int r_begin,
                        const double* __restrict__ aty, const double* __restrict__ diag, double bs2,
@@ -269,11 +270,11 @@ aggregate_cover_kernel(const double* __restrict__ Zhat, const double* __restrict
       double v[NB][kCoverRegEntries];
 #pragma unroll
       for (int k = 0; k < NB; ++k) {
-        const double* zb = Zhat + (b + k) * zimg;
+        const ZT* zb = Zhat + (b + k) * zimg;
 #pragma unroll
         for (int q = 0; q < kCoverRegEntries; ++q)
           if (q < cnt && (k == 0 || b + k < b_end)) {
-            v[k][q] = CG ? __ldcg(zb + off[q]) : __ldg(zb + off[q]);
+            v[k][q] = CG ? (double)__ldcg(zb + off[q]) : (double)__ldg(zb + off[q]);
             if (kDc) v[k][q] = __dadd_rn(v[k][q], __ldg(dc + (int64_t)(b + k) * n_local + dco[q]));
           }
       }
@@ -294,12 +295,12 @@ aggregate_cover_kernel(const double* __restrict__ Zhat, const double* __restrict
     }
   } else {
     for (int b = b_begin; b < b_end; ++b) {
-      const double* zb = Zhat + b * zimg;
+      const ZT* zb = Zhat + b * zimg;
       double sum = 0.0, v0 = 0.0;
       bool same = true;
       for (int q = 0; q < cnt; ++q) {
         const int e = __ldg(entries + e0 + q);
-        double v = __ldg(zb + (int64_t)(e >> 8) * P + (e & 255));
+        double v = (double)__ldg(zb + (int64_t)(e >> 8) * P + (e & 255));
         if (kDc) v = __dadd_rn(v, __ldg(dc + (int64_t)b * n_local + (e >> 8)));
         if (q == 0) v0 = v;
         sum += v;
@@ -315,9 +316,9 @@ aggregate_cover_kernel(const double* __restrict__ Zhat, const double* __restrict
 // and nothing to amortise the entry decode over, so the kernel is the
 // ptr -> entries -> Zhat chain of dependent loads; kept to 32 registers for
 // full occupancy (twice the chains in flight of the batched kernel).
-template <bool kDc>
+template <bool kDc, typename ZT>
 __global__ void __launch_bounds__(kCoverThreads, 8)
-aggregate_cover1_kernel(const double* __restrict__ Zhat, const double* __restrict__ dc,
+aggregate_cover1_kernel(const ZT* __restrict__ Zhat, const double* __restrict__ dc,
                         const int32_t* __restrict__ ptr, const int32_t* __restrict__ entries,
                         int P, int W, int r_begin, const double* __restrict__ aty,
                         const double* __restrict__ diag, double bs2, int kind,
@@ -342,7 +343,7 @@ aggregate_cover1_kernel(const double* __restrict__ Zhat, const double* __restric
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       if (q < cnt) {
-        v[q] = __ldg(Zhat + (int64_t)(e[q] >> 8) * P + (e[q] & 255));
+        v[q] = (double)__ldg(Zhat + (int64_t)(e[q] >> 8) * P + (e[q] & 255));
         if (kDc) v[q] = __dadd_rn(v[q], __ldg(dc + (e[q] >> 8)));
       }
     v0 = v[0];
@@ -355,7 +356,7 @@ aggregate_cover1_kernel(const double* __restrict__ Zhat, const double* __restric
   } else {
     for (int q = 0; q < cnt; ++q) {
       const int e = __ldg(entries + e0 + q);
-      double v = __ldg(Zhat + (int64_t)(e >> 8) * P + (e & 255));
+      double v = (double)__ldg(Zhat + (int64_t)(e >> 8) * P + (e & 255));
       if (kDc) v = __dadd_rn(v, __ldg(dc + (e >> 8)));
       if (q == 0) v0 = v;
       sum += v;
@@ -369,14 +370,15 @@ aggregate_cover1_kernel(const double* __restrict__ Zhat, const double* __restric
 
 }  // namespace fepll
 
-extern "C" int fepll_aggregate_strip(const double* Zhat, const double* dc, const int32_t* anchors,
+namespace fepll {
+template <typename ZT>
+static int aggregate_strip_impl(const ZT* Zhat, const double* dc, const int32_t* anchors,
                                      int32_t n_rows, int32_t n_cols, int32_t spacing, int32_t half,
                                      int32_t side, int32_t batch, int32_t H, int32_t W,
                                      int32_t row0, int32_t H_glob, int32_t a_first,
                                      int32_t n_local_rows, int32_t r_begin, int32_t r_end,
                                      const double* aty, const double* diag, double bs2, int32_t kind,
                                      double* x_out, double* xtilde_out, int32_t* status, void* stream) {
-  using namespace fepll;
   FEPLL_REQUIRE(Zhat && anchors && status, "aggregate: bad arguments");
   FEPLL_REQUIRE(n_rows >= 1 && n_cols >= 1 && spacing >= 1 && side >= 1 && half >= 0,
                 "aggregate: bad grid geometry");
@@ -390,11 +392,37 @@ extern "C" int fepll_aggregate_strip(const double* Zhat, const double* dc, const
   if (r_end == r_begin) return kOk;
   dim3 grid((W + 255) / 256, r_end - r_begin, batch);
   const GridGeo geo{anchors, n_rows, n_cols, spacing, half, side, W, row0, H_glob, a_first};
-  aggregate_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+  aggregate_kernel<ZT><<<grid, 256, 0, (cudaStream_t)stream>>>(
       Zhat, dc, geo, batch, H, aty, diag, bs2, kind, x_out, xtilde_out, status, n_local_rows,
       r_begin);
   FEPLL_LAUNCH();
   return kOk;
+}
+
+}  // namespace fepll
+
+extern "C" int fepll_aggregate_strip(const double* Zhat, const double* dc, const int32_t* anchors,
+                                     int32_t n_rows, int32_t n_cols, int32_t spacing, int32_t half,
+                                     int32_t side, int32_t batch, int32_t H, int32_t W,
+                                     int32_t row0, int32_t H_glob, int32_t a_first,
+                                     int32_t n_local_rows, int32_t r_begin, int32_t r_end,
+                                     const double* aty, const double* diag, double bs2, int32_t kind,
+                                     double* x_out, double* xtilde_out, int32_t* status, void* stream) {
+  return fepll::aggregate_strip_impl(Zhat, dc, anchors, n_rows, n_cols, spacing, half, side, batch, H, W,
+                                     row0, H_glob, a_first, n_local_rows, r_begin, r_end, aty, diag, bs2,
+                                     kind, x_out, xtilde_out, status, stream);
+}
+
+extern "C" int fepll_aggregate_strip_f32(const float* Zhat, const double* dc, const int32_t* anchors,
+                                         int32_t n_rows, int32_t n_cols, int32_t spacing, int32_t half,
+                                         int32_t side, int32_t batch, int32_t H, int32_t W,
+                                         int32_t row0, int32_t H_glob, int32_t a_first,
+                                         int32_t n_local_rows, int32_t r_begin, int32_t r_end,
+                                         const double* aty, const double* diag, double bs2, int32_t kind,
+                                         double* x_out, double* xtilde_out, int32_t* status, void* stream) {
+  return fepll::aggregate_strip_impl(Zhat, dc, anchors, n_rows, n_cols, spacing, half, side, batch, H, W,
+                                     row0, H_glob, a_first, n_local_rows, r_begin, r_end, aty, diag, bs2,
+                                     kind, x_out, xtilde_out, status, stream);
 }
 
 extern "C" int fepll_aggregate(const double* Zhat, const double* dc, const int32_t* anchors,
@@ -451,14 +479,15 @@ extern "C" int fepll_cover_build(const int32_t* anchors, int32_t n_rows, int32_t
   return kOk;
 }
 
-extern "C" int fepll_aggregate_cover(const double* Zhat, const double* dc, const int32_t* ptr,
+namespace fepll {
+template <typename ZT>
+static int aggregate_cover_impl(const ZT* Zhat, const double* dc, const int32_t* ptr,
                                      const int32_t* entries, int32_t P, int32_t n_local,
                                      int32_t zhat_rows,
                                      int32_t batch, int32_t H, int32_t W, int32_t r_begin,
                                      int32_t r_end, const double* aty, const double* diag,
                                      double bs2, int32_t kind, double* x_out, double* xtilde_out,
                                      int32_t* status, void* stream) {
-  using namespace fepll;
   FEPLL_REQUIRE(Zhat && ptr && entries && status, "aggregate_cover: bad arguments");
   FEPLL_REQUIRE(kind == 0 || kind == 1, "aggregate_cover: unknown kind");
   FEPLL_REQUIRE(zhat_rows >= n_local, "aggregate_cover: Zhat rows per image below n_local");
@@ -472,7 +501,7 @@ extern "C" int fepll_aggregate_cover(const double* Zhat, const double* dc, const
             (unsigned)((batch + ipb - 1) / ipb));
   if (batch == 1) {
     dim3 g1((unsigned)((W + kCoverThreads - 1) / kCoverThreads), r_end - r_begin);
-    auto k1 = dc ? aggregate_cover1_kernel<true> : aggregate_cover1_kernel<false>;
+    auto k1 = dc ? aggregate_cover1_kernel<true, ZT> : aggregate_cover1_kernel<false, ZT>;
     k1<<<g1, kCoverThreads, 0, (cudaStream_t)stream>>>(Zhat, dc, ptr, entries, P, W, r_begin, aty,
                                                        diag, bs2, kind, x_out, xtilde_out, status);
     FEPLL_LAUNCH();
@@ -480,10 +509,33 @@ extern "C" int fepll_aggregate_cover(const double* Zhat, const double* dc, const
   }
   // one image per pass, Zhat loads past L1 (measured: two images per pass
   // spill at 64 registers and run 15 % slower; L1-cached loads 2-3 % slower)
-  auto kernel = dc ? aggregate_cover_kernel<true, 1, true> : aggregate_cover_kernel<false, 1, true>;
+  auto kernel = dc ? aggregate_cover_kernel<true, 1, true, ZT> : aggregate_cover_kernel<false, 1, true, ZT>;
   kernel<<<grid, kCoverThreads, 0, (cudaStream_t)stream>>>(
       Zhat, dc, ptr, entries, P, n_local, zhat_rows, batch, H, W, r_begin, aty, diag, bs2, kind, x_out,
       xtilde_out, status, ipb);
   FEPLL_LAUNCH();
   return kOk;
+}
+}  // namespace fepll
+
+extern "C" int fepll_aggregate_cover(const double* Zhat, const double* dc, const int32_t* ptr,
+                                     const int32_t* entries, int32_t P, int32_t n_local,
+                                     int32_t zhat_rows,
+                                     int32_t batch, int32_t H, int32_t W, int32_t r_begin,
+                                     int32_t r_end, const double* aty, const double* diag,
+                                     double bs2, int32_t kind, double* x_out, double* xtilde_out,
+                                     int32_t* status, void* stream) {
+  return fepll::aggregate_cover_impl(Zhat, dc, ptr, entries, P, n_local, zhat_rows, batch, H, W, r_begin,
+                                     r_end, aty, diag, bs2, kind, x_out, xtilde_out, status, stream);
+}
+
+extern "C" int fepll_aggregate_cover_f32(const float* Zhat, const double* dc, const int32_t* ptr,
+                                         const int32_t* entries, int32_t P, int32_t n_local,
+                                         int32_t zhat_rows,
+                                         int32_t batch, int32_t H, int32_t W, int32_t r_begin,
+                                         int32_t r_end, const double* aty, const double* diag,
+                                         double bs2, int32_t kind, double* x_out, double* xtilde_out,
+                                         int32_t* status, void* stream) {
+  return fepll::aggregate_cover_impl(Zhat, dc, ptr, entries, P, n_local, zhat_rows, batch, H, W, r_begin,
+                                     r_end, aty, diag, bs2, kind, x_out, xtilde_out, status, stream);
 }

@@ -610,6 +610,9 @@ int rescore_queue_x(Plan* p, const LevelArgs& a, const double* x, const int32_t*
 
 int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zhat, int n_img,
                 int zrows, const double* x, const int32_t* anchors, int H, int W, cudaStream_t st);
+int wiener_dmma_f32(Plan* p, int t, const float* Z32, int z32_pitch, const double* dc, float* Zhat,
+                    int n_img, int zrows, const double* x, const int32_t* anchors, int H, int W,
+                    cudaStream_t st);
 bool wiener_xw_supported(const Plan* p);
 bool wiener_dmma_supported(const Plan* p);
 
@@ -769,4 +772,33 @@ extern "C" int fepll_wiener(fepll_plan_t plan, int32_t t, const double* x, int32
   }
   FEPLL_LAUNCH();
   return kOk;
+}
+
+// FP32-state form of fepll_wiener: the FP32 patch rows of fepll_extract in
+// (z32_pitch floats per row), est + dc rounded once to FP32 out; FP64
+// arithmetic in between (DMMA).
+extern "C" int fepll_wiener_f32(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32_t W,
+                                const int32_t* anchors, int32_t n_img, const double* dc,
+                                const float* Z32, int32_t z32_pitch, int64_t n_total, float* Zhat,
+                                int32_t zhat_rows, void* stream) {
+  using namespace fepll;
+  Plan* p = reinterpret_cast<Plan*>(plan);
+  FEPLL_REQUIRE(p != nullptr && dc != nullptr && Z32 != nullptr && Zhat != nullptr,
+                "wiener_f32: bad arguments");
+  FEPLL_REQUIRE(t >= 0 && t < p->v.T, "wiener_f32: iteration index outside the beta schedule");
+  FEPLL_REQUIRE(n_total == p->last_n_total, "wiener_f32: must follow fepll_select on the same patches");
+  FEPLL_REQUIRE(n_img >= 1 && zhat_rows >= n_img, "wiener_f32: Zhat rows per image below n_img");
+  FEPLL_REQUIRE(wiener_dmma_supported(p), "wiener_f32: patch size / rank outside the DMMA kernel");
+  FEPLL_REQUIRE(z32_pitch >= p->v.P && z32_pitch % 4 == 0 && p->v.P % 4 == 0 &&
+                    reinterpret_cast<uintptr_t>(Z32) % 16 == 0,
+                "wiener_f32: FP32 rows need a pitch >= P, a multiple of 4, and 16-byte alignment");
+  FEPLL_REQUIRE(p->opt.wiener_add_dc, "wiener_f32: writes est + dc only");
+  if (n_total == 0) return kOk;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (p->child_count[0] == 0) {
+    route_init_kernel<<<(unsigned)((n_total + 255) / 256), 256, 0, st>>>(
+        n_total, p->rs.leafseg, p->rs.cnt, p->rs.off, p->rs.leaf_base, (int32_t*)nullptr, -1);
+    FEPLL_LAUNCH();
+  }
+  return wiener_dmma_f32(p, t, Z32, z32_pitch, dc, Zhat, n_img, zhat_rows, x, anchors, H, W, st);
 }

@@ -117,6 +117,7 @@ struct Geo {
   int R8;        // rank rounded up to 8
   int uld;       // Us [Pn][uld]  (phase-1 B: k = p, n = j; phase-2 B: k = j, n = p)
   int add_dc;    // 1: write est + dc (default), 0: the bare estimates (plan option wiener_add_dc)
+  int zld32;     // row stride (floats) of the FP32-row variant: 4 mod 32, conflict-free fragment loads
 };
 
 // NT2: phase-2 n-tiles (P/8 rounded up): 8 for P=64, 13 for P=100.
@@ -132,8 +133,8 @@ struct Geo {
 // preceding them.
 // RW = 16: the warp's rows g and g + 8 (two DMMAs per B fragment); RW = 8:
 // row g only (half the accumulators and registers, twice the warps per SM)
-template <int NT2, int NT1, int RW, class Step>
-__device__ __forceinline__ void wiener_rows(const double* za, const double* zb, double da, double db,
+template <int NT2, int NT1, int RW, class ZT, class Step>
+__device__ __forceinline__ void wiener_rows(const ZT* za, const ZT* zb, double da, double db,
                                             const double* Us, int uld, const double* sh, int t4,
                                             int g4, Step&& step, double (&acc2)[NT2][4]) {
   double acc[NT1][4];
@@ -144,8 +145,8 @@ __device__ __forceinline__ void wiener_rows(const double* za, const double* zb, 
     step(k0 / 8);
     // z = window - dc, the extraction's FP64 subtraction (da = db = 0 when
     // the rows are already z: x - 0 is x for every x, signed zeros included)
-    const double a0 = za[k0] - da, a2 = za[k0 + 4] - da;
-    const double a1 = RW == 16 ? zb[k0] - db : 0.0, a3 = RW == 16 ? zb[k0 + 4] - db : 0.0;
+    const double a0 = (double)za[k0] - da, a2 = (double)za[k0 + 4] - da;
+    const double a1 = RW == 16 ? (double)zb[k0] - db : 0.0, a3 = RW == 16 ? (double)zb[k0 + 4] - db : 0.0;
     const double* u0 = Us + (k0 + t4) * uld + g4;
     const double* u1 = u0 + 4 * uld;
     double b0[NT1], b1[NT1];
@@ -228,12 +229,15 @@ __device__ __forceinline__ void wiener_rows(const double* za, const double* zb, 
 // extracted Z64 rows; z = window - dc is formed at the fragment loads, so the
 // extraction need not write (and this kernel not read) the 512-byte Z64 rows
 // (off by default: slower, see plan option wiener_xw).
-template <int NT2, int MT, int NS, int RW, bool XW>
+// ZT: element type of the patch rows in and the estimate rows out (double;
+// float for the FP32-state mode — rows converted exactly to FP64 at the
+// fragment loads, the FP64 result rounded once to FP32 at the store)
+template <int NT2, int MT, int NS, int RW, bool XW, class ZT = double>
 __global__ void __launch_bounds__(MT / RW * 32, RW == 8 ? 2 : 1)
 wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, int n_leaf_nodes,
                    const int32_t* __restrict__ cnt, const int64_t* __restrict__ off,
-                   const int32_t* __restrict__ leafseg, const double* __restrict__ Z64,
-                   const double* __restrict__ dc, double* __restrict__ Zhat, int n_img, int zrows,
+                   const int32_t* __restrict__ leafseg, const ZT* __restrict__ Z64, int zin_pitch,
+                   const double* __restrict__ dc, ZT* __restrict__ Zhat, int n_img, int zrows,
                    const double* __restrict__ x, const int32_t* __restrict__ anchors, int H, int W,
                    Geo geo) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -245,8 +249,12 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
   // the anchors fetched between the index and the window copies)
   constexpr int kLead = XW ? 2 * NS - 1 : 2 * NS - 2;
   static_assert(!XW || (NS == 2 && NT2 == 8), "XW: the P = 64 two-stage pipeline");
-  double* Zs0 = reinterpret_cast<double*>(smem + ((sizeof(Head) + 127) & ~size_t(127)));
-  double* Us = Zs0 + NS * kRows * geo.zld;     // [Pn][uld]   (p, j)
+  static_assert(!XW || sizeof(ZT) == 8, "XW reads FP64 windows");
+  constexpr int kEl = 16 / (int)sizeof(ZT);   // row elements per 16-byte copy
+  const int zld = sizeof(ZT) == 8 ? geo.zld : geo.zld32;
+  ZT* Zs0 = reinterpret_cast<ZT*>(smem + ((sizeof(Head) + 127) & ~size_t(127)));
+  double* Us = reinterpret_cast<double*>(
+      reinterpret_cast<uint8_t*>(Zs0) + ((NS * kRows * zld * sizeof(ZT) + 15) & ~size_t(15)));  // [Pn][uld] (p, j)
   double* sh = Us + geo.Pn * geo.uld;          // [R8]
   double* dcs = sh + geo.R8;                   // [NS][MT] dc of the buffered rows
   int2* anc = reinterpret_cast<int2*>(dcs + NS * kRows);  // XW: [4][MT] anchors of the rows
@@ -255,7 +263,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
   // K padding columns of the row buffers stay zero (cp.async fills [0, P))
   for (int e = tid; e < NS * kRows * (geo.Pn - P); e += kThreads) {
     const int w = geo.Pn - P, i = e / w;  // row i of the adjacent buffers
-    Zs0[i * geo.zld + P + (e - i * w)] = 0.0;
+    Zs0[i * zld + P + (e - i * w)] = (ZT)0;
   }
   for (int k = tid; k < n_leaf_nodes; k += kThreads) {
     const int v = leaf_nodes[k];
@@ -298,7 +306,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
   // consecutive threads take consecutive 16-byte chunks of a row (P even),
   // so each instruction reads whole lines of one or two rows; slice s of a
   // tile's copy is e in [s kThreads, (s + 1) kThreads)
-  const int C = P / 2;
+  const int C = P / kEl;
   const int n_slices = (kRows * C + kThreads - 1) / kThreads;
   constexpr int kWarps = kThreads / 32;
   constexpr bool kInterleave = NT2 == 8;  // P = 64 layout below: 16 slices, 8 k-steps
@@ -324,21 +332,21 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
   auto fetch_z_slices = [&](int j, int s0, int s1) {
     if (j >= t_end) return;
     const int32_t* rows = h.rows[(j - t_begin) % kRing];
-    double* Zs = Zs0 + ((j - t_begin) % NS) * kRows * geo.zld;
+    ZT* Zs = Zs0 + ((j - t_begin) % NS) * kRows * zld;
     double* dcb = dcs + ((j - t_begin) % NS) * kRows;
     for (int e = tid + s0 * kThreads; e < min(s1 * kThreads, kRows * C); e += kThreads) {
       const int i = e / C, c = e - i * C;
       const int g = rows[i];
-      double* d = Zs + i * geo.zld + 2 * c;
+      ZT* d = Zs + i * zld + kEl * c;
       if (g >= 0) {
-        if (XW)
+        if constexpr (XW)
           copy_window_chunk(j, i, c, g, d);
         else
-          cp_async16(d, Z64 + (int64_t)g * P + 2 * c);
+          cp_async16(d, Z64 + (int64_t)g * zin_pitch + kEl * c);
         if (c == 0) cp_async8(dcb + i, dc + g);
       } else {
-        d[0] = 0.0;
-        d[1] = 0.0;
+#pragma unroll
+        for (int q = 0; q < kEl; ++q) d[q] = (ZT)0;
       }
     }
   };
@@ -386,11 +394,11 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       __syncthreads();
     }
     wstamp(i, 2);
-    const double* Zs = Zs0 + (i % NS) * kRows * geo.zld;
+    const ZT* Zs = Zs0 + (i % NS) * kRows * zld;
     const int g4 = lane >> 2, t4 = lane & 3;
     const int m0 = warp * RW;
-    const double* za = Zs + (m0 + g4) * geo.zld + t4;       // rows g (, g+8) of the warp
-    const double* zb = za + 8 * geo.zld;
+    const ZT* za = Zs + (m0 + g4) * zld + t4;       // rows g (, g+8) of the warp
+    const ZT* zb = za + 8 * zld;
     // ---- phase 1: C[m0..m0+15][0..R8) = (Z . U) * shrink, with the
     // leaf's n-tile count as a compile-time constant (predicated-off DMMAs
     // would still occupy the pipe)
@@ -404,7 +412,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
     constexpr int kRowsPerThread = kRows / kWarps;  // == RW: RW / 8 rows per k-step
     int gsl[kRowsPerThread];
     int2 asl[XW ? kRowsPerThread : 1];
-    double* zn = Zs0 + ((jn - t_begin) % NS) * kRows * geo.zld + 2 * lane;
+    ZT* zn = Zs0 + ((jn - t_begin) % NS) * kRows * zld + kEl * lane;
     double* dcn = dcs + ((jn - t_begin) % NS) * kRows;
     if (inter) {
       const int32_t* rn = h.rows[(jn - t_begin) % kRing];
@@ -422,9 +430,10 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       if (!inter) return;
 #pragma unroll
       for (int q = st * (kRowsPerThread / 8); q < (st + 1) * (kRowsPerThread / 8); ++q) {
-        double* d = zn + (warp + kWarps * q) * geo.zld;
+        ZT* d = zn + (warp + kWarps * q) * zld;
+        if (kEl * lane >= 64) continue;  // FP32 rows: 16 lanes cover the 256-byte row
         if (gsl[q] >= 0) {
-          if (XW) {
+          if constexpr (XW) {
             const int2 a = asl[XW ? q : 0];
             const int b = gsl[q] / n_img;
             const double* src = x + ((int64_t)b * H + a.x + (lane >> 2)) * W + a.y + 2 * (lane & 3);
@@ -435,12 +444,12 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
               cp_async8(d + 1, src + 1);
             }
           } else {
-            cp_async16(d, Z64 + (int64_t)gsl[q] * 64 + 2 * lane);
+            cp_async16(d, Z64 + (int64_t)gsl[q] * zin_pitch + kEl * lane);
           }
           if (lane == 0) cp_async8(dcn + warp + kWarps * q, dc + gsl[q]);
         } else {
-          d[0] = 0.0;
-          d[1] = 0.0;
+#pragma unroll
+          for (int e2 = 0; e2 < kEl; ++e2) d[e2] = (ZT)0;
         }
       }
     };
@@ -465,21 +474,21 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       const double gt = h.leaf_gt[li];
       // Zhat + dc = (acc + gamma_tail z) + dc, written over this warp's own
       // rows of Zs (each element read and written by the same lane)...
-      double* zw = const_cast<double*>(Zs);
+      ZT* zw = const_cast<ZT*>(Zs);
       const double* dct = dcs + (i % NS) * kRows;
 #pragma unroll
       for (int half = 0; half < RW / 8; ++half) {
-        double* zr = zw + (m0 + g4 + 8 * half) * geo.zld;
+        ZT* zr = zw + (m0 + g4 + 8 * half) * zld;
         const double d = dct[m0 + g4 + 8 * half];
         const double dz = XW ? d : 0.0;  // XW rows hold the window: z = w - dc
 #pragma unroll
         for (int n = 0; n < NT2; ++n) {
           const int col = n * 8 + 2 * t4;
           if (col < P) {
-            const double e0 = acc[n][2 * half] + gt * (zr[col] - dz);
-            const double e1 = acc[n][2 * half + 1] + gt * (zr[col + 1] - dz);
-            zr[col] = geo.add_dc ? __dadd_rn(e0, d) : e0;
-            zr[col + 1] = geo.add_dc ? __dadd_rn(e1, d) : e1;
+            const double e0 = acc[n][2 * half] + gt * ((double)zr[col] - dz);
+            const double e1 = acc[n][2 * half + 1] + gt * ((double)zr[col + 1] - dz);
+            zr[col] = (ZT)(geo.add_dc ? __dadd_rn(e0, d) : e0);
+            zr[col + 1] = (ZT)(geo.add_dc ? __dadd_rn(e1, d) : e1);
           }
         }
       }
@@ -494,7 +503,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
         if (gidx >= 0) {
           const int64_t orow =  // padded image pitch (no division when dense)
               zrows == n_img ? (int64_t)gidx : (int64_t)(gidx / n_img) * zrows + gidx % n_img;
-          bulk_s2g(Zhat + orow * P, zw + (m0 + lane) * geo.zld, P * 8);
+          bulk_s2g(Zhat + orow * P, zw + (m0 + lane) * zld, P * (uint32_t)sizeof(ZT));
         }
         bulk_commit();
       }
@@ -513,6 +522,8 @@ static wn::Geo wiener_geo(const Plan* p) {
   geo.Pn = (P + 7) / 8 * 8;
   auto ld = [](int n, int rem) { int v = n; while (v % 16 != rem) ++v; return v; };
   geo.zld = ld(geo.Pn, 4);
+  geo.zld32 = geo.Pn;
+  while (geo.zld32 % 32 != 4) ++geo.zld32;
   geo.R8 = (p->max_model_rank + 7) / 8 * 8;
   geo.uld = ld(geo.R8, 4);
   geo.add_dc = p->opt.wiener_add_dc;
@@ -521,10 +532,10 @@ static wn::Geo wiener_geo(const Plan* p) {
 
 // dynamic shared memory of an (mt rows, ns stages) configuration: head,
 // row stages, basis, shrink, dc ring, XW anchors ring
-static size_t wiener_smem(const wn::Geo& geo, int mt, int ns) {
-  return ((sizeof(wn::Head) + 127) & ~size_t(127)) +
-         sizeof(double) * (ns * (size_t)mt * geo.zld + (size_t)geo.Pn * geo.uld + geo.R8 +
-                           (size_t)ns * mt) +
+static size_t wiener_smem(const wn::Geo& geo, int mt, int ns, size_t zt_bytes = 8) {
+  const size_t rows = zt_bytes == 8 ? ns * (size_t)mt * geo.zld * 8 : ns * (size_t)mt * geo.zld32 * zt_bytes;
+  return ((sizeof(wn::Head) + 127) & ~size_t(127)) + ((rows + 15) & ~size_t(15)) +
+         sizeof(double) * ((size_t)geo.Pn * geo.uld + geo.R8 + (size_t)ns * mt) +
          sizeof(int2) * 4 * (size_t)mt;
 }
 
@@ -550,10 +561,11 @@ bool wiener_xw_supported(const Plan* p) {
          p->max_model_rank <= wn::kMaxR && wiener_pair_fits(wiener_geo(p));
 }
 
-int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zhat, int n_img,
-                int zrows, const double* x, const int32_t* anchors, int H, int W, cudaStream_t st) {
+template <class ZT>
+static int wiener_dmma_t(Plan* p, int t, const ZT* Z64, int zin_pitch, const double* dc, ZT* Zhat, int n_img,
+                         int zrows, const double* x, const int32_t* anchors, int H, int W, cudaStream_t st) {
   const wn::Geo geo = wiener_geo(p);
-  auto smem_for = [&](int mt, int ns) { return wiener_smem(geo, mt, ns); };
+  auto smem_for = [&](int mt, int ns) { return wiener_smem(geo, mt, ns, sizeof(ZT)); };
   const bool xw = Z64 == nullptr;
   FEPLL_REQUIRE(!xw || wiener_xw_supported(p),
                 "wiener: the window-source kernel needs P = 64 and two CTAs per SM");
@@ -584,17 +596,19 @@ int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zha
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
     kernel<<<kSMs * std::max(1, per_sm), threads, smem, st>>>(
         p->v, t, p->d_leaf_nodes, p->n_leaf_nodes, p->rs.cnt, p->rs.off, p->rs.leafseg, Z64,
-        dc, Zhat, n_img, zrows, x, anchors, H, W, geo);
+        zin_pitch, dc, Zhat, n_img, zrows, x, anchors, H, W, geo);
     FEPLL_LAUNCH();
     return kOk;
   };
 #define FEPLL_WN_CASE(N)                                                   \
   case N:                                                                  \
-    return big ? launch(wn::wiener_dmma_kernel<N, 128, 2, 16, false>)      \
-               : ns == 4 ? launch(wn::wiener_dmma_kernel<N, 64, 4, 16, false>) \
-               : rw == 8 ? launch(wn::wiener_dmma_kernel<N, 64, 2, 8, false>)  \
-                         : launch(wn::wiener_dmma_kernel<N, 64, 2, 16, false>);
-  if (xw) return launch(wn::wiener_dmma_kernel<8, 64, 2, 8, true>);
+    return big ? launch(wn::wiener_dmma_kernel<N, 128, 2, 16, false, ZT>)      \
+               : ns == 4 ? launch(wn::wiener_dmma_kernel<N, 64, 4, 16, false, ZT>) \
+               : rw == 8 ? launch(wn::wiener_dmma_kernel<N, 64, 2, 8, false, ZT>)  \
+                         : launch(wn::wiener_dmma_kernel<N, 64, 2, 16, false, ZT>);
+  if constexpr (sizeof(ZT) == 8) {
+    if (xw) return launch(wn::wiener_dmma_kernel<8, 64, 2, 8, true>);
+  }
   switch (nt2) {
     FEPLL_WN_CASE(1)
     FEPLL_WN_CASE(2)
@@ -610,6 +624,18 @@ int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zha
 #undef FEPLL_WN_CASE
   set_error("wiener: unsupported patch size for the DMMA kernel");
   return kDataError;
+}
+
+int wiener_dmma(Plan* p, int t, const double* Z64, const double* dc, double* Zhat, int n_img,
+                int zrows, const double* x, const int32_t* anchors, int H, int W, cudaStream_t st) {
+  return wiener_dmma_t<double>(p, t, Z64, p->v.P, dc, Zhat, n_img, zrows, x, anchors, H, W, st);
+}
+
+// FP32-state mode: FP32 patch rows in (pitch z32_pitch), FP32 est + dc out
+int wiener_dmma_f32(Plan* p, int t, const float* Z32, int z32_pitch, const double* dc, float* Zhat,
+                    int n_img, int zrows, const double* x, const int32_t* anchors, int H, int W,
+                    cudaStream_t st) {
+  return wiener_dmma_t<float>(p, t, Z32, z32_pitch, dc, Zhat, n_img, zrows, x, anchors, H, W, st);
 }
 
 bool wiener_dmma_supported(const Plan* p) {

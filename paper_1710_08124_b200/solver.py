@@ -149,8 +149,18 @@ class Restorer:
 
     def __init__(self, A, model, tree, config, batch: int = 1, lam: float | None = None,
                  mode: str = "tensor", device=None, guard: float = 0.0, strip=None,
-                 options: dict | None = None):
+                 options: dict | None = None, precision: str = "fp64"):
         _validate_config(config)
+        # precision: "fp64" (default) keeps the patch rows and the Wiener
+        # estimates in FP64 (bitwise-reproducible, labels identical to the
+        # FP64 reference); "fp32-state" stores them in FP32 (no Z64 rows,
+        # FP32 est + dc) with FP64 arithmetic throughout and the exact FP64
+        # re-scoring from the FP64 image — about half the HBM bytes of
+        # extraction, Wiener and reprojection (FP32 state
+        # gave no label flips and RMSE ~4e-6 in emulation)
+        if precision not in ("fp64", "fp32-state"):
+            raise DataError(f"unknown precision {precision!r} (fp64 | fp32-state)")
+        self.precision = precision
         # strip mode (strips.StripSpec): A covers the strip's slab of a larger
         # image; only the owned rows are aggregated (denoise, batch 1)
         self.strip = strip
@@ -239,12 +249,13 @@ class Restorer:
         self.Z64 = None
         # FP32 patch rows (kernel (a) output) feed the tensor-core scorer
         self.Z32 = (torch.empty((B * n, self.z32_pitch), dtype=torch.float32, device=dev)
-                    if mode == "tensor" else None)
+                    if mode == "tensor" or precision == "fp32-state" else None)
         # Wiener output rows (est + dc), zhat_rows per image (the ABI allows a
         # padded pitch; a padded one measured no different, so dense)
         self.zhat_rows = n
         self._agg_dc = None  # traces: dc added by the gather (the Wiener kernel writes bare estimates)
-        self.Zhat = torch.empty((B * self.zhat_rows, P), dtype=f64, device=dev)
+        self.Zhat = torch.empty((B * self.zhat_rows, P), device=dev,
+                                dtype=torch.float32 if precision == "fp32-state" else f64)
         self.dc = torch.empty(B * n, dtype=f64, device=dev)
         self.sq = torch.empty(B * n, dtype=f64, device=dev)
         self.labels = torch.empty(B * n, dtype=torch.int32, device=dev)
@@ -384,22 +395,28 @@ class Restorer:
         # trace: the Wiener kernel writes the bare estimates and the gather
         # adds dc (the same single FP64 rounding of patches.py:209, so x is
         # bitwise the untraced result); the FP64 patch rows are kept
-        self.plan.set_option("wiener_add_dc", 0)
-        self._agg_dc = self.dc
+        fp32 = self.precision == "fp32-state"
+        if not fp32:
+            self.plan.set_option("wiener_add_dc", 0)
+            self._agg_dc = self.dc
         self._force_z64 = True
         try:
             self._iteration(t, st, timer)
         finally:
-            self.plan.set_option("wiener_add_dc", self.options.get("wiener_add_dc", 1))
+            if not fp32:
+                self.plan.set_option("wiener_add_dc", self.options.get("wiener_add_dc", 1))
             self._agg_dc = None
             self._force_z64 = False
         B, n, P = self.batch, self.n, self.P
+        est = self.Zhat.view(B, self.zhat_rows, P)[:, :n].double()
+        if fp32:  # FP32 est + dc: the estimates up to that rounding
+            est = est - self.dc.view(B, n, 1)
         return [{"beta": float(self.betas[t]),
                  "grid": self.sample_grid(t),
                  "patches": self.Z64.view(B, n, P).cpu().numpy().copy(),
                  "dc": self.dc.view(B, n).cpu().numpy().copy(),
                  "selected": self.labels.view(B, n).cpu().numpy().astype(np.int64),
-                 "estimates": self.Zhat.view(B, self.zhat_rows, P)[:, :n].cpu().numpy().copy(),
+                 "estimates": est.cpu().numpy().copy(),
                  "x_tilde": self.xt.cpu().numpy().copy(),
                  "x": self.x.cpu().numpy().copy()}]
 
@@ -448,8 +465,12 @@ class Restorer:
                N.ptr(self.labels), N.ptr(self.leaf_counts[t]), st)
         N.call("fepll_select_rescored", self.plan.handle, N.ptr(self.rescored[t]), st)
         self._mark(timer, "select")
-        N.call("fepll_wiener", self.plan.handle, t, N.ptr(xin), H, W, N.ptr(anchors), n,
-               N.ptr(self.dc), N.ptr(z64), nt, N.ptr(self.Zhat), self.zhat_rows, st)
+        if self.precision == "fp32-state":
+            N.call("fepll_wiener_f32", self.plan.handle, t, N.ptr(xin), H, W, N.ptr(anchors), n,
+                   N.ptr(self.dc), N.ptr(self.Z32), self.z32_pitch, nt, N.ptr(self.Zhat), self.zhat_rows, st)
+        else:
+            N.call("fepll_wiener", self.plan.handle, t, N.ptr(xin), H, W, N.ptr(anchors), n,
+                   N.ptr(self.dc), N.ptr(z64), nt, N.ptr(self.Zhat), self.zhat_rows, st)
         self._mark(timer, "wiener")
         bs2 = float(self.betas[t]) * self.sigma * self.sigma
         # reproject (patches.py:198-222; Zhat already holds est + dc, so the
@@ -459,6 +480,7 @@ class Restorer:
         # the plan's cover lists; small single images search their candidates
         # directly.
         ptr, entries, r0, r1 = self._covers[t]
+        sfx = "_f32" if self.precision == "fp32-state" else ""
         kind = 0 if self.pixel_kind else 1
         out = self.x if self.pixel_kind else self.rhs
         diag = self.diag if self.pixel_kind else None
@@ -467,11 +489,11 @@ class Restorer:
             sp = self.strip
             row0, H_glob, a_first, n_loc = ((sp.slab_lo, sp.H, sp.a_lo, sp.a_hi - sp.a_lo + 1)
                                             if sp is not None else (0, H, 0, nr))
-            N.call("fepll_aggregate_strip", N.ptr(self.Zhat), N.ptr(self._agg_dc), N.ptr(anchors), nr, nc,
+            N.call("fepll_aggregate_strip" + sfx, N.ptr(self.Zhat), N.ptr(self._agg_dc), N.ptr(anchors), nr, nc,
                    self.config.spacing, half, side, B, H, W, row0, H_glob, a_first, n_loc, r0, r1,
                    N.ptr(aty), N.ptr(diag), bs2, kind, N.ptr(out), N.ptr(xt), N.ptr(self.status), st)
         else:
-            N.call("fepll_aggregate_cover", N.ptr(self.Zhat), N.ptr(self._agg_dc), N.ptr(ptr),
+            N.call("fepll_aggregate_cover" + sfx, N.ptr(self.Zhat), N.ptr(self._agg_dc), N.ptr(ptr),
                    N.ptr(entries), P, n, self.zhat_rows, B, H, W, r0, r1, N.ptr(aty), N.ptr(diag), bs2, kind,
                    N.ptr(out), N.ptr(xt), N.ptr(self.status), st)
         self._mark(timer, "aggregate")
@@ -483,9 +505,12 @@ class Restorer:
             self._mark(timer, "image_solve")
 
     def _z64(self):
-        """The FP64 patch rows, or None when the Wiener kernel reads the
-        image windows itself (plan option wiener_xw) and no trace wants them."""
-        if N.lib().fepll_wiener_reads_image(self.plan.handle) and not self._force_z64:
+        """The FP64 patch rows, or None when nothing needs them: the Wiener
+        kernel reads the image windows (plan option wiener_xw) or the FP32
+        rows (fp32-state), and no trace wants them (the re-scoring then
+        re-extracts the FP64 patches from the image)."""
+        if ((self.precision == "fp32-state" or N.lib().fepll_wiener_reads_image(self.plan.handle))
+                and not self._force_z64):
             return None
         if self.Z64 is None:
             self.Z64 = self.torch.empty((self.batch * self.n, self.P), dtype=self.torch.float64,
@@ -599,7 +624,8 @@ class HostPipeline:
     image is restored independently)."""
 
     def __init__(self, A, model, tree, config, batch: int, chunks: int = 1, lam: float | None = None,
-                 mode: str = "tensor", device=None, streams: int = 2, graphs: bool = False):
+                 mode: str = "tensor", device=None, streams: int = 2, graphs: bool = False,
+                 precision: str = "fp64", options: dict | None = None):
         torch = _torch()
         if batch % chunks:
             raise DataError(f"batch {batch} does not split into {chunks} chunks")
@@ -608,7 +634,8 @@ class HostPipeline:
         self.per = self.batch // self.chunks
         k = max(1, int(streams))  # restorers / streams the chunks rotate over
         self.restorers = [Restorer(A, model, tree, config, batch=self.per, lam=lam, mode=mode,
-                                   device=device) for _ in range(k)]
+                                   device=device, precision=precision, options=options)
+                          for _ in range(k)]
         dev = self.restorers[0].device
         self.device = dev
         self.streams = [torch.cuda.Stream(dev) for _ in range(k)]
@@ -694,7 +721,7 @@ def _array_digest(a) -> str:
     return hashlib.sha1(a.tobytes()).hexdigest() + str(a.shape)
 
 
-def _plan_key(A, model, tree, config, batch, lam, mode, options):
+def _plan_key(A, model, tree, config, batch, lam, mode, options, precision="fp64"):
     """Cache key of a Restorer: model and tree by identity (immutable and
     shareable; the cache pins them so an id is never
     reused while cached), the operator by value (kind, dims, factor, kernel
@@ -706,11 +733,11 @@ def _plan_key(A, model, tree, config, batch, lam, mode, options):
            int(config.spacing), config.sampling, bool(config.use_tree), bool(config.use_flat_tail),
            int(config.seed), float(cg.tolerance), int(cg.max_iterations))
     return (id(model), id(tree), op, cfg, int(batch), None if lam is None else float(lam), mode,
-            tuple(sorted((options or {}).items())))
+            tuple(sorted((options or {}).items())), precision)
 
 
 def cached_restorer(A, model, tree, config, batch: int = 1, lam=None, mode: str = "tensor",
-                    options: dict | None = None) -> "Restorer":
+                    options: dict | None = None, precision: str = "fp64") -> "Restorer":
     """The Restorer for these arguments, built once and reused by later
     :func:`restore` / :func:`restore_batch` calls (plan packing, lambda,
     sampling plans, cover lists and scratch are the per-call setup the
@@ -718,12 +745,13 @@ def cached_restorer(A, model, tree, config, batch: int = 1, lam=None, mode: str 
     global _restorer_cache
     if _restorer_cache is None:
         _restorer_cache = OrderedDict()
-    key = _plan_key(A, model, tree, config, batch, lam, mode, options)
+    key = _plan_key(A, model, tree, config, batch, lam, mode, options, precision)
     hit = _restorer_cache.get(key)
     if hit is not None:
         _restorer_cache.move_to_end(key)
         return hit[0]
-    r = Restorer(A, model, tree, config, batch=batch, lam=lam, mode=mode, options=options)
+    r = Restorer(A, model, tree, config, batch=batch, lam=lam, mode=mode, options=options,
+                 precision=precision)
     _restorer_cache[key] = (r, (model, tree))
     while len(_restorer_cache) > _CACHE_SIZE:
         _restorer_cache.popitem(last=False)
@@ -736,7 +764,7 @@ def clear_plan_cache() -> None:
 
 
 def restore(y, A, model, tree=None, config=None, *, mode: str = "tensor", lam=None,
-            options: dict | None = None):
+            options: dict | None = None, precision: str = "fp64"):
     """GPU drop-in for `pkg/src/fepll/solver.py:161-274`: same signature,
     validations, errors, counters, ``IterationStats.times`` and trace
     records (one image, no batch axis)."""
@@ -746,7 +774,8 @@ def restore(y, A, model, tree=None, config=None, *, mode: str = "tensor", lam=No
     y = np.asarray(y, dtype=np.float64)
     if tuple(y.shape) != tuple(A.output_dims):
         raise DataError(f"observation shape {y.shape} != operator output {tuple(A.output_dims)}")
-    x, stats = restore_batch(y[None], A, model, tree, config, mode=mode, lam=lam, options=options)
+    x, stats = restore_batch(y[None], A, model, tree, config, mode=mode, lam=lam, options=options,
+                             precision=precision)
     if config.trace:
         for rec in stats.trace:
             for k in ("patches", "dc", "selected", "estimates", "x_tilde", "x"):
@@ -755,7 +784,8 @@ def restore(y, A, model, tree=None, config=None, *, mode: str = "tensor", lam=No
 
 
 def restore_batch(ys, A, model, tree=None, config=None, *, mode: str = "tensor", lam=None,
-                  restorer: Restorer | None = None, options: dict | None = None):
+                  restorer: Restorer | None = None, options: dict | None = None,
+                  precision: str = "fp64"):
     """Restore a (B, H, W) stack sharing operator, sigma and seed.  The
     device plan comes from the plan cache unless ``restorer`` is given."""
     if config is None:
@@ -767,7 +797,7 @@ def restore_batch(ys, A, model, tree=None, config=None, *, mode: str = "tensor",
     if tuple(ys.shape[1:]) != tuple(A.output_dims):
         raise DataError(f"observation shape {ys.shape[1:]} != operator output {tuple(A.output_dims)}")
     r = restorer or cached_restorer(A, model, tree, config, batch=ys.shape[0], lam=lam, mode=mode,
-                                    options=options)
+                                    options=options, precision=precision)
     if r.batch != ys.shape[0]:
         raise DataError(f"restorer batch {r.batch} != {ys.shape[0]} observations")
     torch = r.torch

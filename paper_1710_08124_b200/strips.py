@@ -150,7 +150,8 @@ class StripRestorer:
     """The restoration loop of one strip (wraps :class:`solver.Restorer`)."""
 
     def __init__(self, H: int, W: int, model, tree, config, rank: int, world: int,
-                 mode: str = "tensor", device=None, lam: float | None = None):
+                 mode: str = "tensor", device=None, lam: float | None = None,
+                 precision: str = "fp64", options: dict | None = None):
         from .operators import identity_operator
         from .solver import Restorer
 
@@ -168,7 +169,8 @@ class StripRestorer:
             lam, _ = DeviceOperator(identity_operator((H, W))).lambda_param(
                 max(config.sigma, SIGMA_FLOOR_8BIT) / 255.0)
         self.restorer = Restorer(identity_operator((sp.slab_rows, W)), model, tree, config, batch=1,
-                                 lam=lam, mode=mode, device=device, strip=sp)
+                                 lam=lam, mode=mode, device=device, strip=sp, precision=precision,
+                                 options=options)
 
     def run(self, y_slab_dev, group=None, timer=None):
         """y_slab_dev: (1, slab_rows, W) device tensor of the observation's
