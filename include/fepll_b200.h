@@ -95,6 +95,9 @@ int fepll_plan_destroy(fepll_plan_t plan);
  *                             into L2 three tiles before copying them, per
  *                             line (1) or one bulk prefetch per row (2);
  *                             measured slower, default 0;
+ *   aggregate_variant 0 | 1   batch reprojection kernel the host passes to
+ *                             fepll_aggregate_cover_ex (0: one thread per pixel
+ *                             over the images, 1: one per (pixel, image));
  *   rescore_by_node 0 | 1     FP64 re-scoring grouped by tree node, the node's
  *                             group matrix staged in shared memory (measured
  *                             slower, default 0).
@@ -241,6 +244,17 @@ int fepll_aggregate_cover(const double* Zhat, const double* dc, const int32_t* p
                           int32_t H, int32_t W, int32_t r_begin, int32_t r_end,
                           const double* aty, const double* diag, double bs2, int32_t kind,
                           double* x_out, double* xtilde_out, int32_t* status, void* stream);
+
+/* fepll_aggregate_cover with the Zhat element type and batch kernel
+ * explicit: exactly one of Zhat (FP64) / Zhat32 (FP32) non-NULL; variant 0:
+ * one thread per pixel looping over the images, 1: one thread per (pixel,
+ * image).  Bitwise-identical results. */
+int fepll_aggregate_cover_ex(const double* Zhat, const float* Zhat32, const double* dc,
+                             const int32_t* ptr, const int32_t* entries, int32_t P, int32_t n_local,
+                             int32_t zhat_rows, int32_t batch, int32_t H, int32_t W, int32_t r_begin,
+                             int32_t r_end, const double* aty, const double* diag, double bs2,
+                             int32_t kind, double* x_out, double* xtilde_out, int32_t* status,
+                             int32_t variant, void* stream);
 
 /* FP32-state form of fepll_aggregate_cover (FP32 Zhat, FP64 sums). */
 int fepll_aggregate_cover_f32(const float* Zhat, const double* dc, const int32_t* ptr,

@@ -61,6 +61,8 @@ _SIGS = {
     "fepll_wiener_f32": (i32, [vp, i32, vp, i32, i32, vp, i32, vp, vp, i32, i64, vp, i32, vp]),
     "fepll_aggregate_strip_f32": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32,
                                         i32, i32, i32, i32, i32, i32, vp, vp, f64, i32, vp, vp, vp, vp]),
+    "fepll_aggregate_cover_ex": (i32, [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, vp, vp,
+                                       f64, i32, vp, vp, vp, i32, vp]),
     "fepll_aggregate_cover_f32": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, vp, vp,
                                         f64, i32, vp, vp, vp, vp]),
     "fepll_aggregate": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, vp, vp, f64,

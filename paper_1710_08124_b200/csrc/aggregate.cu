@@ -322,12 +322,18 @@ aggregate_cover1_kernel(const ZT* __restrict__ Zhat, const double* __restrict__ 
                         const int32_t* __restrict__ ptr, const int32_t* __restrict__ entries,
                         int P, int W, int r_begin, const double* __restrict__ aty,
                         const double* __restrict__ diag, double bs2, int kind,
-                        double* __restrict__ x_out, double* __restrict__ xt_out, int32_t* status) {
+                        double* __restrict__ x_out, double* __restrict__ xt_out, int32_t* status,
+                        int64_t zimg = 0, int64_t img = 0, int n_local = 0) {
   const int c = blockIdx.x * kCoverThreads + threadIdx.x;
   if (c >= W) return;
+  // batches (blockIdx.z = image): one thread per (pixel, image) — every
+  // image re-reads the plan's ptr / entries (L2-resident) for 2x the
+  // resident threads of the per-pixel multi-image kernel
+  Zhat += (int64_t)blockIdx.z * zimg;
+  if (kDc) dc += (int64_t)blockIdx.z * n_local;
   const int64_t p = (int64_t)blockIdx.y * W + c;
   const int e0 = __ldg(ptr + p), cnt = __ldg(ptr + p + 1) - e0;
-  const int64_t pix = (int64_t)(r_begin + blockIdx.y) * W + c;
+  const int64_t pix = (int64_t)blockIdx.z * img + (int64_t)(r_begin + blockIdx.y) * W + c;
   if (cnt == 0) {
     atomicOr(status, 1);
     pixel_update(0.0, pix, aty, diag, bs2, kind, x_out, xt_out, status);
@@ -487,7 +493,7 @@ static int aggregate_cover_impl(const ZT* Zhat, const double* dc, const int32_t*
                                      int32_t batch, int32_t H, int32_t W, int32_t r_begin,
                                      int32_t r_end, const double* aty, const double* diag,
                                      double bs2, int32_t kind, double* x_out, double* xtilde_out,
-                                     int32_t* status, void* stream) {
+                                     int32_t* status, void* stream, int variant = 0) {
   FEPLL_REQUIRE(Zhat && ptr && entries && status, "aggregate_cover: bad arguments");
   FEPLL_REQUIRE(kind == 0 || kind == 1, "aggregate_cover: unknown kind");
   FEPLL_REQUIRE(zhat_rows >= n_local, "aggregate_cover: Zhat rows per image below n_local");
@@ -499,11 +505,13 @@ static int aggregate_cover_impl(const ZT* Zhat, const double* dc, const int32_t*
   FEPLL_REQUIRE((int64_t)n_local * P < (int64_t(1) << 31), "aggregate_cover: image patch array above 2^31 elements");
   dim3 grid((unsigned)((W + kCoverThreads - 1) / kCoverThreads), r_end - r_begin,
             (unsigned)((batch + ipb - 1) / ipb));
-  if (batch == 1) {
-    dim3 g1((unsigned)((W + kCoverThreads - 1) / kCoverThreads), r_end - r_begin);
+  if (batch == 1 || variant == 1) {
+    FEPLL_REQUIRE(batch <= 65535, "aggregate_cover: batch above the launch grid");
+    dim3 g1((unsigned)((W + kCoverThreads - 1) / kCoverThreads), r_end - r_begin, batch);
     auto k1 = dc ? aggregate_cover1_kernel<true, ZT> : aggregate_cover1_kernel<false, ZT>;
     k1<<<g1, kCoverThreads, 0, (cudaStream_t)stream>>>(Zhat, dc, ptr, entries, P, W, r_begin, aty,
-                                                       diag, bs2, kind, x_out, xtilde_out, status);
+                                                       diag, bs2, kind, x_out, xtilde_out, status,
+                                                       (int64_t)zhat_rows * P, (int64_t)H * W, n_local);
     FEPLL_LAUNCH();
     return kOk;
   }
@@ -538,4 +546,23 @@ extern "C" int fepll_aggregate_cover_f32(const float* Zhat, const double* dc, co
                                          int32_t* status, void* stream) {
   return fepll::aggregate_cover_impl(Zhat, dc, ptr, entries, P, n_local, zhat_rows, batch, H, W, r_begin,
                                      r_end, aty, diag, bs2, kind, x_out, xtilde_out, status, stream);
+}
+
+// fepll_aggregate_cover with an explicit batch kernel: variant 0 = one
+// thread per pixel looping over the images (entries decoded once),
+// 1 = one thread per (pixel, image).  Bitwise-identical results.
+extern "C" int fepll_aggregate_cover_ex(const double* Zhat, const float* Zhat32, const double* dc,
+                                        const int32_t* ptr, const int32_t* entries, int32_t P,
+                                        int32_t n_local, int32_t zhat_rows, int32_t batch, int32_t H,
+                                        int32_t W, int32_t r_begin, int32_t r_end, const double* aty,
+                                        const double* diag, double bs2, int32_t kind, double* x_out,
+                                        double* xtilde_out, int32_t* status, int32_t variant,
+                                        void* stream) {
+  FEPLL_REQUIRE((Zhat == nullptr) != (Zhat32 == nullptr), "aggregate_cover_ex: exactly one of Zhat / Zhat32");
+  FEPLL_REQUIRE(variant == 0 || variant == 1, "aggregate_cover_ex: unknown variant");
+  if (Zhat32)
+    return fepll::aggregate_cover_impl(Zhat32, dc, ptr, entries, P, n_local, zhat_rows, batch, H, W, r_begin,
+                                       r_end, aty, diag, bs2, kind, x_out, xtilde_out, status, stream, variant);
+  return fepll::aggregate_cover_impl(Zhat, dc, ptr, entries, P, n_local, zhat_rows, batch, H, W, r_begin,
+                                     r_end, aty, diag, bs2, kind, x_out, xtilde_out, status, stream, variant);
 }

@@ -266,6 +266,7 @@ static int* plan_option(Plan* p, const char* name) {
   if (n == "wiener_add_dc") return &p->opt.wiener_add_dc;
   if (n == "l2_prefetch") return &p->opt.l2_prefetch;
   if (n == "rescore_by_node") return &p->opt.rescore_by_node;
+  if (n == "aggregate_variant") return &p->opt.aggregate_variant;
   return nullptr;
 }
 

@@ -215,6 +215,7 @@ class Restorer:
         self.options = dict(options or {})
         for k, v in self.options.items():
             self.plan.set_option(k, v)
+        self._agg_variant = self.plan.get_option("aggregate_variant")
         # a model with a positive score weight has no pre-scaled tcgen05 images:
         # its tree walk runs on the exact FP64 scorer (the same labels)
         self._select_mode = self.MODES[mode] if (mode == "exact" or self.plan.has_tc) else 0
@@ -493,9 +494,10 @@ class Restorer:
                    self.config.spacing, half, side, B, H, W, row0, H_glob, a_first, n_loc, r0, r1,
                    N.ptr(aty), N.ptr(diag), bs2, kind, N.ptr(out), N.ptr(xt), N.ptr(self.status), st)
         else:
-            N.call("fepll_aggregate_cover" + sfx, N.ptr(self.Zhat), N.ptr(self._agg_dc), N.ptr(ptr),
+            z64, z32 = (None, self.Zhat) if sfx else (self.Zhat, None)
+            N.call("fepll_aggregate_cover_ex", N.ptr(z64), N.ptr(z32), N.ptr(self._agg_dc), N.ptr(ptr),
                    N.ptr(entries), P, n, self.zhat_rows, B, H, W, r0, r1, N.ptr(aty), N.ptr(diag), bs2, kind,
-                   N.ptr(out), N.ptr(xt), N.ptr(self.status), st)
+                   N.ptr(out), N.ptr(xt), N.ptr(self.status), self._agg_variant, st)
         self._mark(timer, "aggregate")
         if not self.pixel_kind:
             cg = self.config.cg

@@ -473,6 +473,7 @@ def test_operator_adjoint_identity_and_normal(name):
     ("wiener_add_dc", (1, 0)),       # est + dc from the Wiener kernel vs dc added by the gather
     ("l2_prefetch", (0, 1)),         # ws2 loaders: L2 prefetch three tiles ahead vs none
     ("rescore_by_node", (0, 1)),     # FP64 re-scoring per decision vs grouped by node (smem group)
+    ("aggregate_variant", (0, 1)),   # batch reprojection: thread per pixel vs per (pixel, image)
 ])
 def test_kernel_variants_bitwise_equal(knob, values, models):
     """Every performance variant kept behind a plan option computes the same
