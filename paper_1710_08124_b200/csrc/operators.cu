@@ -95,8 +95,9 @@ struct OpPlan {
   double* low = nullptr;      // Ho x Wo scratch (decimate)
   double* r = nullptr;        // CG vectors
   double* p = nullptr;
+  double* p2 = nullptr;       // CG direction ping-pong
   double* ap = nullptr;
-  double* partial = nullptr;  // per-block partial sums (2 per block)
+  double* partial = nullptr;  // per-block partial sums (4 per block: two buffers of up to 2)
   double* scal = nullptr;     // device scalars
   int coop_blocks = 0;
 };
@@ -107,15 +108,32 @@ __device__ __forceinline__ int wrap(int i, int n) {
   return i < 0 ? i + n : i;
 }
 
+// element sources for the stencils: a vector, or the CG direction formed
+// on the fly, p = r + beta p_old (the same FMA the update itself uses)
+struct VecSrc {
+  const double* x;
+  __device__ __forceinline__ double operator()(int64_t i) const { return x[i]; }
+};
+struct DirSrc {
+  const double* r;
+  const double* pold;
+  double beta;
+  __device__ __forceinline__ double operator()(int64_t i) const { return fma(beta, pold[i], r[i]); }
+};
+
 // (conv x)[p] = sum_ab k[a][b] x[p - (a - ch, b - cw)]   (operators.py:196-197 with kernel_ft)
-__device__ __forceinline__ double conv_at(const OpView& o, const double* x, int r, int c) {
+template <class Src>
+__device__ __forceinline__ double conv_at_src(const OpView& o, const Src& x, int r, int c) {
   const int ch = o.kh / 2, cw = o.kw / 2;
   double s = 0.0;
   for (int a = 0; a < o.kh; ++a) {
-    const double* row = x + (int64_t)wrap(r - a + ch, o.H) * o.W;
-    for (int b = 0; b < o.kw; ++b) s = fma(o.taps[a * o.kw + b], row[wrap(c - b + cw, o.W)], s);
+    const int64_t row = (int64_t)wrap(r - a + ch, o.H) * o.W;
+    for (int b = 0; b < o.kw; ++b) s = fma(o.taps[a * o.kw + b], x(row + wrap(c - b + cw, o.W)), s);
   }
   return s;
+}
+__device__ __forceinline__ double conv_at(const OpView& o, const double* x, int r, int c) {
+  return conv_at_src(o, VecSrc{x}, r, c);
 }
 
 // adjoint: correlation with the kernel (conj khat), over the zero-filled
@@ -136,10 +154,14 @@ __device__ __forceinline__ double corr_at(const OpView& o, const double* y, int 
   return s;
 }
 
+template <class Src>
+__device__ __forceinline__ double lap_at_src(const Src& x, int r, int c, int H, int W) {
+  const int64_t row = (int64_t)r * W;
+  return 4.0 * x(row + c) - x((int64_t)wrap(r - 1, H) * W + c) - x((int64_t)wrap(r + 1, H) * W + c) -
+         x(row + wrap(c - 1, W)) - x(row + wrap(c + 1, W));
+}
 __device__ __forceinline__ double lap_at(const double* x, int r, int c, int H, int W) {
-  const double* row = x + (int64_t)r * W;
-  return 4.0 * row[c] - x[(int64_t)wrap(r - 1, H) * W + c] - x[(int64_t)wrap(r + 1, H) * W + c] -
-         row[wrap(c - 1, W)] - row[wrap(c + 1, W)];
+  return lap_at_src(VecSrc{x}, r, c, H, W);
 }
 
 // ------------------------------------------------------------------ reductions
@@ -165,13 +187,18 @@ __device__ inline void block_reduce_store(double (&v)[NV], double* partial, doub
   __syncthreads();
 }
 
+// every block: the sum of the block partials, warp 0 in a fixed order (lane
+// l sums blocks l, l + 32, ... in turn, then a fixed shuffle tree) — one
+// round of independent loads instead of a serial walk over the blocks
 template <int NV>
 __device__ inline void grid_total(const double* partial, double (&out)[NV], double* red) {
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
     for (int i = 0; i < NV; ++i) {
       double s = 0.0;
-      for (int b = 0; b < (int)gridDim.x; ++b) s += partial[b * NV + i];
-      red[i] = s;
+      for (int b = lane; b < (int)gridDim.x; b += 32) s += partial[b * NV + i];
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) red[i] = s;
     }
   }
   __syncthreads();
@@ -188,31 +215,42 @@ struct NormalArgs {
   double shift, lapc;
 };
 
-__device__ inline void normal_phase_a(const NormalArgs& n, const double* x, double* low,
-                                      int64_t gtid, int64_t gstride) {
+template <class Src>
+__device__ inline void normal_phase_a_src(const NormalArgs& n, const Src& x, double* low,
+                                          int64_t gtid, int64_t gstride) {
   const OpView& o = n.o;
   if (o.kind != kConvolution && o.kind != kDecimate) return;
   const int64_t total = (int64_t)o.Ho * o.Wo;
   for (int64_t i = gtid; i < total; i += gstride) {
     const int r = (int)(i / o.Wo), c = (int)(i - (int64_t)r * o.Wo);
-    low[i] = conv_at(o, x, r * o.d, c * o.d);
+    low[i] = conv_at_src(o, x, r * o.d, c * o.d);
   }
 }
+__device__ inline void normal_phase_a(const NormalArgs& n, const double* x, double* low,
+                                      int64_t gtid, int64_t gstride) {
+  normal_phase_a_src(n, VecSrc{x}, low, gtid, gstride);
+}
 
-__device__ inline double normal_phase_b(const NormalArgs& n, const double* x, const double* low,
-                                        int r, int c) {
+// xi = the source's element i (the caller has it at hand)
+template <class Src>
+__device__ inline double normal_phase_b_src(const NormalArgs& n, const Src& x, double xi,
+                                            const double* low, int r, int c) {
   const OpView& o = n.o;
   const int64_t i = (int64_t)r * o.W + c;
   double y;
   switch (o.kind) {
-    case kIdentity: y = x[i]; break;
+    case kIdentity: y = xi; break;
     case kMask:
-    case kGain: y = o.diag[i] * x[i]; break;
+    case kGain: y = o.diag[i] * xi; break;
     default: y = corr_at(o, low, r, c); break;
   }
-  if (n.shift != 0.0) y += n.shift * x[i];
-  if (n.lapc != 0.0) y += n.lapc * lap_at(x, r, c, o.H, o.W);
+  if (n.shift != 0.0) y += n.shift * xi;
+  if (n.lapc != 0.0) y += n.lapc * lap_at_src(x, r, c, o.H, o.W);
   return y;
+}
+__device__ inline double normal_phase_b(const NormalArgs& n, const double* x, const double* low,
+                                        int r, int c) {
+  return normal_phase_b_src(n, VecSrc{x}, x[(int64_t)r * n.o.W + c], low, r, c);
 }
 
 // ------------------------------------------------------------------ CG kernel
@@ -221,7 +259,8 @@ struct CgArgs {
   const double* rhs;
   double* x;         // in: x0, out: solution
   double* r;
-  double* p;
+  double* p;         // direction, ping-pong with p2
+  double* p2;
   double* ap;
   double* low;
   double* partial;
@@ -231,6 +270,12 @@ struct CgArgs {
   int maxit;
 };
 
+// Standard CG (operators.py:242-266) with three grid barriers per
+// iteration: the direction p_k = r_k + beta p_{k-1} is not written before
+// the next operator application — the stencils form it on the fly from r
+// and p_{k-1} (DirSrc, the update's own FMA) while each thread stores its
+// own elements into the other p buffer — and the two dot products use
+// separate partial buffers.  Iterates: those of the reference recursion.
 __global__ void __launch_bounds__(256) cg_kernel(CgArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[64];
@@ -238,21 +283,22 @@ __global__ void __launch_bounds__(256) cg_kernel(CgArgs a) {
   const int64_t N = (int64_t)o.H * o.W;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+  double* partA = a.partial;                  // <p, Ap>, and the setup sums
+  double* partB = a.partial + 2 * gridDim.x;  // <r, r>
   double v1[1], t1[1];
   // rn = ||rhs||
   v1[0] = 0.0;
   for (int64_t i = gtid; i < N; i += gs) v1[0] = fma(a.rhs[i], a.rhs[i], v1[0]);
-  block_reduce_store(v1, a.partial, red);
+  block_reduce_store(v1, partA, red);
   grid.sync();
-  grid_total<1>(a.partial, t1, red);
+  grid_total<1>(partA, t1, red);
   const double rn = sqrt(t1[0]);
   if (rn == 0.0) {
     for (int64_t i = gtid; i < N; i += gs) a.x[i] = 0.0;
     if (gtid == 0) { a.out[0] = 0; a.out[1] = 0; a.out[2] = 1; a.out[3] = 1; }
     return;
   }
-  grid.sync();
-  // r = rhs - op(x); p = r; rs = <r,r>
+  // r = rhs - op(x); rs = <r,r>  (p_0 = r is formed on the fly)
   normal_phase_a(a.nrm, a.x, a.low, gtid, gs);
   grid.sync();
   v1[0] = 0.0;
@@ -260,45 +306,54 @@ __global__ void __launch_bounds__(256) cg_kernel(CgArgs a) {
     const int rr = (int)(i / o.W), cc = (int)(i - (int64_t)rr * o.W);
     const double ri = a.rhs[i] - normal_phase_b(a.nrm, a.x, a.low, rr, cc);
     a.r[i] = ri;
-    a.p[i] = ri;
     v1[0] = fma(ri, ri, v1[0]);
   }
-  block_reduce_store(v1, a.partial, red);
+  block_reduce_store(v1, partB, red);
   grid.sync();
-  grid_total<1>(a.partial, t1, red);
+  grid_total<1>(partB, t1, red);
   double rs = t1[0];
+  double beta = 0.0;
+  double* pold = a.p;   // p_{k-1} (unused while beta is 0 on the first pass)
+  double* pnew = a.p2;  // receives p_k
   int it = 0;
   for (it = 1; it <= a.maxit; ++it) {
     if (sqrt(rs) / rn <= a.tol) { --it; break; }
-    grid.sync();
-    normal_phase_a(a.nrm, a.p, a.low, gtid, gs);
+    // low = conv(p_k) with p_k = r + beta p_{k-1} on the fly
+    if (it == 1)
+      normal_phase_a(a.nrm, a.r, a.low, gtid, gs);
+    else
+      normal_phase_a_src(a.nrm, DirSrc{a.r, pold, beta}, a.low, gtid, gs);
     grid.sync();
     v1[0] = 0.0;
     for (int64_t i = gtid; i < N; i += gs) {
       const int rr = (int)(i / o.W), cc = (int)(i - (int64_t)rr * o.W);
-      const double api = normal_phase_b(a.nrm, a.p, a.low, rr, cc);
+      const double pi = it == 1 ? a.r[i] : fma(beta, pold[i], a.r[i]);
+      const double api = it == 1 ? normal_phase_b_src(a.nrm, VecSrc{a.r}, pi, a.low, rr, cc)
+                                 : normal_phase_b_src(a.nrm, DirSrc{a.r, pold, beta}, pi, a.low, rr, cc);
+      pnew[i] = pi;
       a.ap[i] = api;
-      v1[0] = fma(a.p[i], api, v1[0]);
+      v1[0] = fma(pi, api, v1[0]);
     }
-    block_reduce_store(v1, a.partial, red);
-    grid.sync();
-    grid_total<1>(a.partial, t1, red);
+    block_reduce_store(v1, partA, red);
+    grid.sync();  // partials ready; every stencil read of r and p_{k-1} is done
+    grid_total<1>(partA, t1, red);
     const double alpha = rs / t1[0];
-    grid.sync();
     v1[0] = 0.0;
     for (int64_t i = gtid; i < N; i += gs) {
-      a.x[i] += alpha * a.p[i];
+      a.x[i] += alpha * pnew[i];
       const double ri = a.r[i] - alpha * a.ap[i];
       a.r[i] = ri;
       v1[0] = fma(ri, ri, v1[0]);
     }
-    block_reduce_store(v1, a.partial, red);
-    grid.sync();
-    grid_total<1>(a.partial, t1, red);
+    block_reduce_store(v1, partB, red);
+    grid.sync();  // r_{k+1} and p_k complete for the next iteration's stencils
+    grid_total<1>(partB, t1, red);
     const double rs_new = t1[0];
-    const double beta = rs_new / rs;
-    for (int64_t i = gtid; i < N; i += gs) a.p[i] = a.r[i] + beta * a.p[i];
+    beta = rs_new / rs;
     rs = rs_new;
+    double* tp = pold;
+    pold = pnew;
+    pnew = tp;
   }
   if (it > a.maxit) it = a.maxit;
   // residual = ||rhs - op(x)|| / rn
@@ -312,9 +367,9 @@ __global__ void __launch_bounds__(256) cg_kernel(CgArgs a) {
     v2[0] = fma(d, d, v2[0]);
     if (!isfinite(a.x[i])) v2[1] += 1.0;
   }
-  block_reduce_store(v2, a.partial, red);
+  block_reduce_store(v2, partA, red);
   grid.sync();
-  grid_total<2>(a.partial, t2, red);
+  grid_total<2>(partA, t2, red);
   if (gtid == 0) {
     const double res = sqrt(t2[0]) / rn;
     a.out[0] = it;
@@ -630,6 +685,7 @@ int fepll_op_create(int32_t kind, int32_t H, int32_t W, int32_t factor, const do
   // CG / power-iteration scratch
   DALLOC(p->r, N);
   DALLOC(p->p, N);
+  DALLOC(p->p2, N);
   DALLOC(p->ap, N);
   DALLOC(p->low, (size_t)v.Ho * v.Wo);
   int per_sm = 1;
@@ -731,6 +787,7 @@ int fepll_op_init(void* op, const double* y, const double* aty, double sigma, do
   a.x = x;
   a.r = p->r;
   a.p = p->p;
+  a.p2 = p->p2;
   a.ap = p->ap;
   a.low = p->low;
   a.partial = p->partial;
@@ -765,6 +822,7 @@ int fepll_op_solve(void* op, const double* rhs, const double* xtilde, double bs2
   a.x = x;
   a.r = p->r;
   a.p = p->p;
+  a.p2 = p->p2;
   a.ap = p->ap;
   a.low = p->low;
   a.partial = p->partial;
