@@ -95,10 +95,6 @@ int fepll_plan_destroy(fepll_plan_t plan);
  *                             into L2 three tiles before copying them, per
  *                             line (1) or one bulk prefetch per row (2);
  *                             measured slower, default 0;
- *   local_rescore 1 | 0       ws2 tree-level kernels re-score the decisions their
- *                             epilogue could not certify in a tail after their
- *                             last tile (CTA-local queue of 1024; overflow and
- *                             the other level kernels use the re-scoring pass);
  *   aggregate_variant 0 | 1   batch reprojection kernel the host passes to
  *                             fepll_aggregate_cover_ex (0: one thread per pixel
  *                             over the images, 1: one per (pixel, image));

@@ -169,9 +169,6 @@ static int create(const fepll_plan_desc* d, Plan** out) {
   FEPLL_CUDA(cudaMalloc(&m, sizeof(int32_t) * kMaxDepth));
   p->owned.push_back(m);
   p->rs.queue_len = static_cast<int32_t*>(m);
-  FEPLL_CUDA(cudaMalloc(&m, sizeof(int32_t) * kMaxDepth));
-  p->owned.push_back(m);
-  p->rs.rescored_local = static_cast<int32_t*>(m);
   *out = p;
   return kOk;
 }
@@ -270,7 +267,6 @@ static int* plan_option(Plan* p, const char* name) {
   if (n == "l2_prefetch") return &p->opt.l2_prefetch;
   if (n == "rescore_by_node") return &p->opt.rescore_by_node;
   if (n == "aggregate_variant") return &p->opt.aggregate_variant;
-  if (n == "local_rescore") return &p->opt.local_rescore;
   return nullptr;
 }
 

@@ -58,7 +58,6 @@ struct RouteScratch {
   int64_t* leaf_base = nullptr;  // [levels+1]
   int32_t* queue = nullptr;   // rescore queue: (patch, node) pairs
   int32_t* queue_len = nullptr;
-  int32_t* rescored_local = nullptr;  // [kMaxDepth] decisions re-scored inside the ws2 level kernels
   int64_t queue_cap = 0;
   int32_t* node_tmp = nullptr;
 };
@@ -77,7 +76,6 @@ struct PlanOptions {
                            // smem once per CTA) — measured slower (select 11.3 -> 13.1 ms/step at 64 x 1024^2:
                            // one 208 KB CTA per SM leaves 8 warps for latency-bound chains), off
 
-  int local_rescore = 1;   // 1: ws2 level kernels re-score their uncertified rows in a tail (no extra pass)
   int aggregate_variant = 0; // batch reprojection kernel (read by the host for fepll_aggregate_cover_ex)
   int l2_prefetch = 0;     // ws2 loaders prefetch rows into L2 three tiles ahead of their cp.async: 1 per 128-B line, 2 one bulk prefetch per row (both measured slower: level 0.295 -> 0.324 / 0.486 ms)
 };

@@ -17,11 +17,6 @@
 
 namespace fepll {
 
-// per-level re-scored decisions: the global queue plus the ws2 tails
-__global__ void sum_counts_kernel(const int32_t* a, const int32_t* b, int32_t* out) {
-  out[threadIdx.x] = a[threadIdx.x] + b[threadIdx.x];
-}
-
 __global__ void route_init_kernel(int64_t n_total, int32_t* seg0, int32_t* cnt, int64_t* off,
                                   int64_t* leaf_base, int32_t* labels, int root_leaf) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -406,7 +401,7 @@ bool select_ws_supported(const Plan* p, int d);
 int select_level_wide(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                       cudaStream_t st);
 int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
-                     const PatchSrc& ps, cudaStream_t st);
+                     cudaStream_t st);
 // Plan option select_variant: 0 select_ws.cu (3xTF32), 1 (default)
 // select_ws2.cu (tf32 + bf16 cross pass, split loader / converter warps;
 // measured faster on every level of the cfg5 tree), 2 ws2 on levels of
@@ -492,7 +487,6 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
   p->last_n_total = (int)n_total;
   FEPLL_CUDA(cudaMemsetAsync(p->rs.cnt, 0, sizeof(int32_t) * p->v.n_nodes, st));
   FEPLL_CUDA(cudaMemsetAsync(p->rs.queue_len, 0, sizeof(int32_t) * kMaxDepth, st));
-  FEPLL_CUDA(cudaMemsetAsync(p->rs.rescored_local, 0, sizeof(int32_t) * kMaxDepth, st));
   if (n_total == 0) {
     if (leaf_counts) FEPLL_CUDA(cudaMemsetAsync(leaf_counts, 0, sizeof(int64_t) * p->v.K, st));
     return kOk;
@@ -529,7 +523,7 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
                  ? ((p->v.tc_x != nullptr &&
                      (p->opt.select_variant == 1 ||
                       (p->opt.select_variant == 2 && p->level_start[d + 1] - p->level_start[d] <= 16)))
-                        ? select_level_ws2(p, a, Z32, sq, guard, ps, st)
+                        ? select_level_ws2(p, a, Z32, sq, guard, st)
                         : select_level_ws(p, a, Z32, sq, guard, st))
                  : select_level_tc(p, a, Z32, sq, guard, st);
         if (prof) FEPLL_CUDA(cudaEventRecord(p->prof_ev[2 * p->prof_used++ + 1], st));
@@ -559,8 +553,8 @@ extern "C" int fepll_wiener_reads_image(fepll_plan_t plan) {
 extern "C" int fepll_select_rescored(fepll_plan_t plan, int32_t* dst, void* stream) {
   Plan* p = reinterpret_cast<Plan*>(plan);
   FEPLL_REQUIRE(p != nullptr && dst != nullptr, "select_rescored: bad arguments");
-  sum_counts_kernel<<<1, kMaxDepth, 0, (cudaStream_t)stream>>>(p->rs.queue_len, p->rs.rescored_local, dst);
-  FEPLL_LAUNCH();
+  FEPLL_CUDA(cudaMemcpyAsync(dst, p->rs.queue_len, sizeof(int32_t) * kMaxDepth,
+                             cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
   return kOk;
 }
 

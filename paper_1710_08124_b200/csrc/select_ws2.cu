@@ -34,7 +34,6 @@
 // kernel certifies with twice the guard (2^-15 by default).
 #include <algorithm>
 
-#include "fp64_score.cuh"
 #include "route.cuh"
 #include "tc.cuh"
 #include "tc_epi.cuh"
@@ -97,13 +96,10 @@ struct EpiGroup {
 constexpr int kMaxNodes = 128;  // internal nodes per level handled by this kernel
 using WsLevelTables = LevelTablesN<256>;  // next level <= 256 nodes
 
-constexpr int kPrefetch = 3;   // tiles ahead of its cp.async a row is prefetched into L2 (option)
-constexpr int kIdxAhead = 6;   // tiles of row indices in flight ahead of their rows
-// decisions the epilogue cannot certify are re-scored in FP64 by this CTA
-// after its last tile (a CTA-local queue; overflow goes to the global queue
-// and the separate re-scoring kernel)
-constexpr int kLocalQ = 1024;
-constexpr int kTailWarps = 16;  // warps of the re-scoring tail (smem rows in the free stages)
+constexpr int kPrefetch = 3;   // tiles ahead of its cp.async a row is prefetched into L2
+// tiles of row indices in flight ahead of their rows: the prefetch of tile
+// i + kPrefetch waits for its indices without waiting for recent row copies
+constexpr int kIdxAhead = 6 + kPrefetch;
 constexpr int kIdxRing = kIdxAhead + 1;
 
 template <int NG>
@@ -123,9 +119,6 @@ struct Smem {
   int32_t tinfo_u[kReady], tinfo_npad[kReady];
   uint32_t tmem_base;
   int32_t t_begin, t_end;
-  int32_t lq_count;
-  int32_t lq_g[kLocalQ];   // patch of a queued decision (-1: slot not written)
-  int16_t lq_k[kLocalQ];   // its node, level-local
 };
 
 static_assert(1024 + kStages * kStageBytes + kBBytes + sizeof(Smem<4>) <= 232448 &&
@@ -142,9 +135,6 @@ struct Args {
   int32_t* queue_len;
   int katoms;
   int prefetch;          // tiles ahead whose rows the loaders prefetch into L2 (0: off)
-  PatchSrc ps;           // FP64 patch source of the re-scoring tail (Z64 rows or the image)
-  int32_t* rescored_local;  // [depth] decisions re-scored in the tail (diagnostics)
-  int local_rescore;     // 1: the tail re-scores the CTA's decisions (else all go global)
   uint64_t* trace;       // debug timeline: [CTA][64 tiles][16] clock64 stamps (or NULL)
 };
 
@@ -228,8 +218,6 @@ select_level_ws2_kernel(PlanView pv, Args args) {
     tc::fence_mbar_init();
   }
   if (tid < kGroups) s.epi[tid].node = -1;
-  if (tid == 0) s.lq_count = 0;
-  for (int q = tid; q < kLocalQ; q += blockDim.x) s.lq_g[q] = -1;
   level_tables(pv, a, s.lv, kRows);  // contains __syncthreads
   for (int k = tid; k < a.lvl_end - a.lvl_begin; k += blockDim.x) {
     const int u = a.lvl_begin + k;
@@ -290,7 +278,7 @@ select_level_ws2_kernel(PlanView pv, Args args) {
         // idx(i + kPrefetch) landed (and with it idx(i)); each lane sends its
         // row of that tile to L2 now, so the stage's cp.async later hits L2:
         // DRAM requests stay in flight beyond the smem stages' capacity
-        tc::cp_async_wait<kIdxAhead - 1 - kPrefetch>();  // (also waits recent row copies)
+        tc::cp_async_wait<kIdxAhead - 1 - kPrefetch>();
         const int jp = i + kPrefetch;
         if (jp < ntile) {
           const int gp = s.idx_ring[jp % kIdxRing][r0 + lane];
@@ -562,17 +550,10 @@ select_level_ws2_kernel(PlanView pv, Args args) {
     named_bar(bar_id, 128);
     auto flush = [&](int buf) {  // write the pending row with bases bbase[buf]
       if (!p_valid) return;
-      const int base = E.bbase[buf][p_key];
-      const int slot = base + p_lrank;
+      const int slot = E.bbase[buf][p_key] + p_lrank;
       if (p_kind == 0) {
-        if (base >= 0) {  // CTA-local queue
-          s.lq_g[slot] = p_g;
-          s.lq_k[slot] = (int16_t)(p_u - a.lvl_begin);
-        } else {          // global queue, base encoded as -1 - b
-          const int gs = -1 - base + p_lrank;
-          args.queue[2 * gs] = p_g;
-          args.queue[2 * gs + 1] = p_u;
-        }
+        args.queue[2 * slot] = p_g;
+        args.queue[2 * slot + 1] = p_u;
       } else if (p_kind == 1) {
         a.seg_out[p_b0 + slot] = p_g;
         if (a.sq_out) a.sq_out[p_b0 + slot] = p_sq;
@@ -624,9 +605,7 @@ select_level_ws2_kernel(PlanView pv, Args args) {
         res = atomicAdd(&a.cnt[E.ch.bfs[etid]], E.bcnt[cb][etid]);
         res_key = etid;
       } else if (etid == 127 && E.bcnt[cb][kMaxChildren] > 0) {
-        const int cnt = E.bcnt[cb][kMaxChildren];
-        const int r0 = args.local_rescore ? atomicAdd(&s.lq_count, cnt) : kLocalQ;
-        res = r0 + cnt <= kLocalQ ? r0 : -1 - atomicAdd(&args.queue_len[a.depth], cnt);
+        res = atomicAdd(&args.queue_len[a.depth], E.bcnt[cb][kMaxChildren]);
         res_key = kMaxChildren;
       }
       // write the previous tile's rows
@@ -657,37 +636,12 @@ select_level_ws2_kernel(PlanView pv, Args args) {
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == kMmaWarp) tc::tmem_dealloc(tmem, kTmemCols);
-  // ---------------------------------------------------------- re-scoring tail
-  // every pipeline is drained: the raw stages hold the per-warp FP64 rows
-  // and score terms; exact FP64 scores (fp64_score.cuh, the exact path's
-  // arithmetic) decide the CTA's uncertified rows, routed like the
-  // separate re-scoring kernel would
-  const int nq = min(s.lq_count, kLocalQ);
-  if (nq > 0 && warp < kTailWarps) {
-    constexpr int kRowD = kMaxP + kMaxGroupCols;
-    static_assert(kTailWarps * kRowD * 8 <= kStages * kStageBytes, "tail rows exceed the stages");
-    double* zs = reinterpret_cast<double*>(stageA) + warp * kRowD;
-    double* tv = zs + kMaxP;
-    int done = 0;
-    for (int q = warp; q < nq; q += kTailWarps) {
-      const int g = s.lq_g[q];
-      if (g < 0) continue;
-      const int u = a.lvl_begin + s.lq_k[q];
-      load_patch(args.ps, g, pv.P, zs);
-      const double sqv = args.sq[g];
-      const int v = score_children_fp64_w128(pv, t, u, zs, sqv, tv);  // ws2 nodes: <= 128 columns
-      if (lane == 0) route_fp64_decision(pv, a, v, g, sqv);
-      __syncwarp();
-      ++done;
-    }
-    if (lane == 0 && done) atomicAdd(&args.rescored_local[a.depth], done);
-  }
   if (args.trace && tid == 0) {
     uint64_t g;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
     args.trace[((size_t)blockIdx.x * 64 + 63) * 16 + 15] = g;
   }
+  if (warp == kMmaWarp) tc::tmem_dealloc(tmem, kTmemCols);
 }
 
 }  // namespace ws2
@@ -697,11 +651,8 @@ extern uint64_t* g_ws_trace;
 extern int g_ws_trace_level;
 
 int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
-                     const PatchSrc& ps, cudaStream_t st) {
+                     cudaStream_t st) {
   ws2::Args args;
-  args.ps = ps;
-  args.rescored_local = p->rs.rescored_local;
-  args.local_rescore = p->opt.local_rescore;
   args.a = a;
   args.Z32 = Z32;
   args.z32_pitch = (p->v.P + 31) / 32 * 32;

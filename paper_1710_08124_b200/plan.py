@@ -325,7 +325,7 @@ class DevicePlan:
         self.reserved = 0
 
     OPTIONS = ("select_variant", "seg_sq", "wiener_pair", "wiener_rw", "wiener_xw", "wiener_add_dc",
-               "l2_prefetch", "rescore_by_node", "aggregate_variant", "local_rescore")
+               "l2_prefetch", "rescore_by_node", "aggregate_variant")
 
     def set_option(self, name: str, value: int) -> None:
         """Per-plan kernel choice (include/fepll_b200.h fepll_plan_set_option)."""

@@ -198,8 +198,7 @@ def _image(H, seed):
 
 
 TENSOR_P64 = [("exact", {}), ("tensor", {"select_variant": 1}), ("tensor", {"select_variant": 0}),
-              ("tensor", {"select_variant": 2}), ("tensor", {"rescore_by_node": 1}),
-              ("tensor", {"local_rescore": 0})]
+              ("tensor", {"select_variant": 2}), ("tensor", {"rescore_by_node": 1})]
 
 
 def test_ties_duplicated_leaves_p64(models):

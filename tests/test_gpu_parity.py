@@ -474,7 +474,6 @@ def test_operator_adjoint_identity_and_normal(name):
     ("l2_prefetch", (0, 1)),         # ws2 loaders: L2 prefetch three tiles ahead vs none
     ("rescore_by_node", (0, 1)),     # FP64 re-scoring per decision vs grouped by node (smem group)
     ("aggregate_variant", (0, 1)),   # batch reprojection: thread per pixel vs per (pixel, image)
-    ("local_rescore", (1, 0)),       # FP64 re-scoring in the ws2 tail vs the separate pass
 ])
 def test_kernel_variants_bitwise_equal(knob, values, models):
     """Every performance variant kept behind a plan option computes the same
