@@ -95,9 +95,11 @@ int fepll_plan_destroy(fepll_plan_t plan);
  *                             into L2 three tiles before copying them, per
  *                             line (1) or one bulk prefetch per row (2);
  *                             measured slower, default 0;
- *   aggregate_variant 0 | 1   batch reprojection kernel the host passes to
+ *   aggregate_variant 0|1|2   batch reprojection kernel the host uses:
  *                             fepll_aggregate_cover_ex (0: one thread per pixel
- *                             over the images, 1: one per (pixel, image));
+ *                             over the images, 1: one per (pixel, image)) or
+ *                             fepll_aggregate_tiles (2: staged in shared memory,
+ *                             default; batches only);
  *   rescore_by_node 0 | 1     FP64 re-scoring grouped by tree node, the node's
  *                             group matrix staged in shared memory (measured
  *                             slower, default 0).
@@ -255,6 +257,37 @@ int fepll_aggregate_cover_ex(const double* Zhat, const float* Zhat32, const doub
                              int32_t r_end, const double* aty, const double* diag, double bs2,
                              int32_t kind, double* x_out, double* xtilde_out, int32_t* status,
                              int32_t variant, void* stream);
+
+/* Staged reprojection of a batch (kernel (d), csrc/aggregate_tiles.cu):
+ * the same results as fepll_aggregate_cover_ex, read through shared memory.
+ * A tile is one pixel row x fepll_tiles_width() columns; fepll_tiles_build
+ * turns a plan's cover lists (ptr, entries over `rows` = r_end - r_begin
+ * rows) into per-tile segment tables — seg_off [n_tiles][seg_cap] (element
+ * offset patch*P + dr*side of a window row inside an image's Zhat rows),
+ * seg_cnt [n_tiles], cover16 [entries] (the entry re-addressed into the
+ * tile's stage) — and writes the largest count to *max_cnt (device int).
+ * seg_cap >= fepll_tiles_seg_cap(side, spacing, half); status bit 8: a tile
+ * does not fit the tables (use fepll_aggregate_cover_ex for that plan).
+ * n_tiles = rows * ceil(W / fepll_tiles_width()).  fepll_aggregate_tiles
+ * needs 16-byte aligned window rows (side * sizeof(element) % 16 == 0);
+ * exactly one of Zhat / Zhat32; dc (n_local per image) or NULL as in
+ * fepll_aggregate_cover. */
+int32_t fepll_tiles_width(void);
+int32_t fepll_tiles_seg_cap(int32_t side, int32_t spacing, int32_t half);
+/* dynamic shared memory fepll_aggregate_tiles needs for a plan (must stay
+ * <= 227 KB; larger plans keep fepll_aggregate_cover_ex) */
+int64_t fepll_tiles_smem_bytes(int32_t max_seg, int32_t side, int32_t elem_bytes, int32_t with_dc,
+                               int32_t with_diag);
+int fepll_tiles_build(const int32_t* ptr, const int32_t* entries, int32_t P, int32_t side, int32_t W,
+                      int32_t rows, int32_t seg_cap, int32_t* seg_off, int32_t* seg_cnt,
+                      uint16_t* cover16, int32_t* max_cnt, int32_t* status, void* stream);
+int fepll_aggregate_tiles(const double* Zhat, const float* Zhat32, const double* dc, int32_t n_local,
+                          const int32_t* ptr, const uint16_t* cover16, const int32_t* seg_off,
+                          const int32_t* seg_cnt, int32_t seg_cap, int32_t max_seg, int32_t P,
+                          int32_t zhat_rows, int32_t batch, int32_t H, int32_t W, int32_t r_begin,
+                          int32_t r_end, const double* aty, const double* diag, double bs2,
+                          int32_t kind, double* x_out, double* xtilde_out, int32_t* status,
+                          void* stream);
 
 /* FP32-state form of fepll_aggregate_cover (FP32 Zhat, FP64 sums). */
 int fepll_aggregate_cover_f32(const float* Zhat, const double* dc, const int32_t* ptr,

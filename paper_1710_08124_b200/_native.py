@@ -72,6 +72,12 @@ _SIGS = {
     "fepll_cover_scratch_ints": (i64, [i64]),
     "fepll_cover_build": (i32, [vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32,
                                 vp, vp, i64, vp, vp]),
+    "fepll_tiles_seg_cap": (i32, [i32, i32, i32]),
+    "fepll_tiles_width": (i32, []),
+    "fepll_tiles_smem_bytes": (i64, [i32, i32, i32, i32, i32]),
+    "fepll_tiles_build": (i32, [vp, vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
+    "fepll_aggregate_tiles": (i32, [vp, vp, vp, i32, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32,
+                                    vp, vp, f64, i32, vp, vp, vp, vp]),
     "fepll_aggregate_cover": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, vp, vp, f64,
                                     i32, vp, vp, vp, vp]),
     "fepll_op_create": (i32, [i32, i32, i32, i32, vp, i32, i32, vp, C.POINTER(vp)]),

@@ -276,7 +276,8 @@ int fepll_plan_set_option(fepll_plan_t plan, const char* name, int64_t value) {
   int* slot = plan_option(p, name);
   FEPLL_REQUIRE(slot != nullptr, std::string("plan_set_option: unknown option ") + (name ? name : "(null)"));
   const std::string n(name);
-  const bool ok = (n == "select_variant" || n == "l2_prefetch") ? (value >= 0 && value <= 2)
+  const bool ok = (n == "select_variant" || n == "l2_prefetch" || n == "aggregate_variant")
+                      ? (value >= 0 && value <= 2)
                   : (n == "wiener_rw")    ? (value == 8 || value == 16)
                                           : (value == 0 || value == 1);
   FEPLL_REQUIRE(ok, "plan_set_option: value out of range for " + n);

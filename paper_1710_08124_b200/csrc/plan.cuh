@@ -76,7 +76,7 @@ struct PlanOptions {
                            // smem once per CTA) — measured slower (select 11.3 -> 13.1 ms/step at 64 x 1024^2:
                            // one 208 KB CTA per SM leaves 8 warps for latency-bound chains), off
 
-  int aggregate_variant = 0; // batch reprojection kernel (read by the host for fepll_aggregate_cover_ex)
+  int aggregate_variant = 2; // batch reprojection kernel (host: 0/1 fepll_aggregate_cover_ex, 2 fepll_aggregate_tiles)
   int l2_prefetch = 0;     // ws2 loaders prefetch rows into L2 three tiles ahead of their cp.async: 1 per 128-B line, 2 one bulk prefetch per row (both measured slower: level 0.295 -> 0.324 / 0.486 ms)
 };
 

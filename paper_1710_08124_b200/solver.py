@@ -276,6 +276,9 @@ class Restorer:
             pm = np.asarray(A.pixel_map, dtype=np.float64)
             d = (pm != 0).astype(np.float64) if kind == "mask" else pm * pm
             self.diag = torch.from_numpy(d).to(dev).expand(B, H, W).contiguous()
+        # batches with aggregate_variant 2: the cover lists re-addressed into
+        # per-tile shared-memory stages (csrc/aggregate_tiles.cu)
+        self._tiles = [self._tile_tables(t) for t in range(config.iterations)]
         self.aty = torch.empty((B, H, W), dtype=f64, device=dev)
         self.pixel_kind = A.solve_strategy == "pixel_diagonal"
         # rhs of the FFT / CG image update and the solver infos
@@ -340,6 +343,41 @@ class Restorer:
                self.W, row0, H_glob, a_first, n_loc_rows, r0, r1, N.ptr(ptr), N.ptr(entries), cap,
                N.ptr(scratch), st)
         return ptr, entries, r0, r1
+
+    def _tile_tables(self, t: int):
+        """(seg_off, seg_cnt, cover16, seg_cap, max_seg) of iteration t's
+        cover lists for fepll_aggregate_tiles, or None (single images, the
+        candidate-search path, other variants, or a plan whose tiles do not
+        fit the tables — those keep fepll_aggregate_cover_ex)."""
+        if not (self._use_cover and self.batch > 1 and self._agg_variant == 2):
+            return None
+        torch = self.torch
+        ptr, entries, r0, r1 = self._covers[t]
+        _, _, _, half = self._grids[t]
+        rows = r1 - r0
+        tw = int(N.lib().fepll_tiles_width())
+        n_tiles = rows * ((self.W + tw - 1) // tw)
+        cap = int(N.lib().fepll_tiles_seg_cap(self.side, self.config.spacing, half))
+        if cap * self.side > 65536 or n_tiles == 0:
+            return None
+        dev = self.device
+        seg_off = torch.empty(n_tiles * cap, dtype=torch.int32, device=dev)
+        seg_cnt = torch.empty(n_tiles, dtype=torch.int32, device=dev)
+        cover16 = torch.empty(max(int(entries.numel()), 1), dtype=torch.int16, device=dev)
+        max_cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        N.call("fepll_tiles_build", N.ptr(ptr), N.ptr(entries), self.P, self.side, self.W, rows, cap,
+               N.ptr(seg_off), N.ptr(seg_cnt), N.ptr(cover16), N.ptr(max_cnt), N.ptr(status), st)
+        if int(status.item()) != 0:
+            return None
+        max_seg = int(max_cnt.item())
+        # the trace form stages dc too (the largest need), mask/gain a diagonal
+        need = int(N.lib().fepll_tiles_smem_bytes(max_seg, self.side, 4 if self.precision == "fp32-state" else 8,
+                                                  1, int(self.diag is not None)))
+        if need > 200 * 1024:
+            return None
+        return seg_off, seg_cnt, cover16, cap, max_seg
 
     # ---------------------------------------------------------------- loop
     def run(self, y_dev, trace: bool = False, timer: dict | None = None, exchange=None):
@@ -493,11 +531,18 @@ class Restorer:
             N.call("fepll_aggregate_strip" + sfx, N.ptr(self.Zhat), N.ptr(self._agg_dc), N.ptr(anchors), nr, nc,
                    self.config.spacing, half, side, B, H, W, row0, H_glob, a_first, n_loc, r0, r1,
                    N.ptr(aty), N.ptr(diag), bs2, kind, N.ptr(out), N.ptr(xt), N.ptr(self.status), st)
+        elif self._tiles[t] is not None:
+            z64, z32 = (None, self.Zhat) if sfx else (self.Zhat, None)
+            seg_off, seg_cnt, cover16, cap, max_seg = self._tiles[t]
+            N.call("fepll_aggregate_tiles", N.ptr(z64), N.ptr(z32), N.ptr(self._agg_dc), n, N.ptr(ptr),
+                   N.ptr(cover16),
+                   N.ptr(seg_off), N.ptr(seg_cnt), cap, max_seg, P, self.zhat_rows, B, H, W, r0, r1,
+                   N.ptr(aty), N.ptr(diag), bs2, kind, N.ptr(out), N.ptr(xt), N.ptr(self.status), st)
         else:
             z64, z32 = (None, self.Zhat) if sfx else (self.Zhat, None)
             N.call("fepll_aggregate_cover_ex", N.ptr(z64), N.ptr(z32), N.ptr(self._agg_dc), N.ptr(ptr),
                    N.ptr(entries), P, n, self.zhat_rows, B, H, W, r0, r1, N.ptr(aty), N.ptr(diag), bs2, kind,
-                   N.ptr(out), N.ptr(xt), N.ptr(self.status), self._agg_variant, st)
+                   N.ptr(out), N.ptr(xt), N.ptr(self.status), self._agg_variant % 2, st)
         self._mark(timer, "aggregate")
         if not self.pixel_kind:
             cg = self.config.cg

@@ -473,7 +473,7 @@ def test_operator_adjoint_identity_and_normal(name):
     ("wiener_add_dc", (1, 0)),       # est + dc from the Wiener kernel vs dc added by the gather
     ("l2_prefetch", (0, 1)),         # ws2 loaders: L2 prefetch three tiles ahead vs none
     ("rescore_by_node", (0, 1)),     # FP64 re-scoring per decision vs grouped by node (smem group)
-    ("aggregate_variant", (0, 1)),   # batch reprojection: thread per pixel vs per (pixel, image)
+    ("aggregate_variant", (2, 0, 1)),  # batch reprojection: staged tiles / thread per pixel / per (pixel, image)
 ])
 def test_kernel_variants_bitwise_equal(knob, values, models):
     """Every performance variant kept behind a plan option computes the same
@@ -501,6 +501,75 @@ def test_kernel_variants_bitwise_equal(knob, values, models):
         assert np.array_equal(x0, x1)
         for a, b in zip(l0, l1):
             np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("H,W,P,s,B", [(40, 300, 64, 4, 3), (64, 64, 64, 2, 5), (37, 530, 100, 4, 2),
+                                       (24, 256, 64, 8, 2), (33, 47, 64, 1, 2)])
+def test_aggregate_tiles_bitwise(H, W, P, s, B):
+    """fepll_aggregate_tiles (segments staged in shared memory) equals the
+    cover-list gather bit for bit — FP64 and FP32 Zhat, with and without dc,
+    pixel-diagonal update with and without a diagonal, the FFT/CG rhs form
+    with x~ out — on partial tiles (W not a multiple of 256), spacing 1, 2,
+    4 and 8, P = 64 and 100; constant inputs come back verbatim."""
+    import torch
+    from paper_1710_08124_b200 import _native as N, jitter_rng, jittered_grid
+    from paper_1710_08124_b200.patches import axis_anchors
+
+    side = int(round(P ** 0.5))
+    half = (side - s) // 2
+    pos = jittered_grid(H, W, P, s, jitter_rng(5, 1)).positions.astype(np.int32)
+    n = pos.shape[0]
+    nr, nc = axis_anchors(H, side, s).size, axis_anchors(W, side, s).size
+    st = torch.cuda.current_stream().cuda_stream
+    pd = _dev(pos)
+    ptr = torch.empty(H * W + 1, dtype=torch.int32, device="cuda")
+    ent = torch.empty(n * P, dtype=torch.int32, device="cuda")
+    scr = torch.empty(int(N.lib().fepll_cover_scratch_ints(H * W)), dtype=torch.int32, device="cuda")
+    N.call("fepll_cover_build", N.ptr(pd), nr, nc, s, half, side, W, 0, H, 0, nr, 0, H,
+           N.ptr(ptr), N.ptr(ent), n * P, N.ptr(scr), st)
+    tw = int(N.lib().fepll_tiles_width())
+    n_tiles = H * ((W + tw - 1) // tw)
+    cap = int(N.lib().fepll_tiles_seg_cap(side, s, half))
+    seg_off = torch.empty(n_tiles * cap, dtype=torch.int32, device="cuda")
+    seg_cnt = torch.empty(n_tiles, dtype=torch.int32, device="cuda")
+    c16 = torch.empty(n * P, dtype=torch.int16, device="cuda")
+    mx = torch.zeros(1, dtype=torch.int32, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    N.call("fepll_tiles_build", N.ptr(ptr), N.ptr(ent), P, side, W, H, cap, N.ptr(seg_off), N.ptr(seg_cnt),
+           N.ptr(c16), N.ptr(mx), N.ptr(status), st)
+    assert int(status.item()) == 0 and 0 < int(mx.item()) <= cap
+    max_seg = int(mx.item())
+    rng = np.random.default_rng(H * W + P)
+    zrows = n + 3  # padded rows per image
+    aty = _dev(rng.standard_normal((B, H, W)))
+    diag = _dev(rng.uniform(0.0, 2.0, (B, H, W)))
+    dc = _dev(rng.standard_normal(B * n))
+    for dtype in (np.float64, np.float32):
+        if dtype == np.float32 and (side * 4) % 16:
+            continue
+        z = torch.from_numpy(rng.standard_normal((B * zrows, P)).astype(dtype)).cuda()
+        zc = torch.from_numpy(np.full((B * zrows, P), 0.1 + 0.2).astype(dtype)).cuda()
+        f64 = dtype == np.float64
+        cover = "fepll_aggregate_cover" if f64 else "fepll_aggregate_cover_f32"
+        for zz, dcp, dg, kind in ((z, None, None, 0), (z, dc, diag, 0), (z, None, None, 1), (zc, None, diag, 1)):
+            outs = []
+            for tiles in (False, True):
+                x = torch.full((B, H, W), 7.0, dtype=torch.float64, device="cuda")
+                xt = torch.full((B, H, W), 7.0, dtype=torch.float64, device="cuda")
+                if tiles:
+                    N.call("fepll_aggregate_tiles", N.ptr(zz) if f64 else None, None if f64 else N.ptr(zz),
+                           N.ptr(dcp), n, N.ptr(ptr), N.ptr(c16), N.ptr(seg_off), N.ptr(seg_cnt), cap, max_seg,
+                           P, zrows, B, H, W, 0, H, N.ptr(aty), N.ptr(dg), 0.37, kind, N.ptr(x), N.ptr(xt),
+                           N.ptr(status), st)
+                else:
+                    N.call(cover, N.ptr(zz), N.ptr(dcp), N.ptr(ptr), N.ptr(ent), P, n, zrows, B, H, W, 0, H,
+                           N.ptr(aty), N.ptr(dg), 0.37, kind, N.ptr(x), N.ptr(xt), N.ptr(status), st)
+                outs.append((x.cpu().numpy(), xt.cpu().numpy()))
+            np.testing.assert_array_equal(outs[0][0], outs[1][0])
+            np.testing.assert_array_equal(outs[0][1], outs[1][1])
+            if zz is zc:
+                assert np.all(outs[1][1] == dtype(0.1 + 0.2).astype(np.float64))
+    assert int(status.item()) == 0
 
 
 def test_cover_gather_lo_eq_hi_verbatim_and_pipeline_errors(models):
