@@ -339,6 +339,11 @@ int fepll_cluster_swap(const double* D, int32_t n, int32_t L, int64_t* cid, doub
 /* debugging: record per-tile pipeline timestamps of one tree level of the
  * warp-specialized scorer into a device buffer (148 x 64 x 8 uint64). */
 int fepll_debug_ws_trace(void* device_buffer, int32_t level);
+/* debug: ws2 tree-level kernels write globaltimer stamps (CTA entry, after
+ * the prologue, end) to device_buffer[depth][148][4] (uint64), the
+ * re-scoring kernel its first entry / last exit to element 16*148*4 +
+ * 2*depth (+1) (atomic min / max: initialise to ~0 / 0); NULL: off */
+int fepll_debug_level_spans(void* device_buffer);
 
 #ifdef __cplusplus
 }

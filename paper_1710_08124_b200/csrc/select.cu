@@ -52,9 +52,21 @@ select_level_fp64_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __
 
 // exact FP64 re-scoring of decisions the tensor-core epilogue could not
 // certify: queue entries are (patch, node) pairs of level d.
+// debug (fepll_debug_level_spans): earliest CTA entry / latest CTA exit
+__device__ __forceinline__ void rs_span(uint64_t* sp, int slot) {
+  if (sp && threadIdx.x == 0) {
+    uint64_t g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    if (slot == 0) atomicMin((unsigned long long*)sp, (unsigned long long)g);
+    else atomicMax((unsigned long long*)sp + 1, (unsigned long long)g);
+  }
+}
+
 __global__ void __launch_bounds__(kSelWarps * 32, 4)
 rescore_fp64_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restrict__ sq,
-                    const int32_t* __restrict__ queue, const int32_t* __restrict__ queue_len) {
+                    const int32_t* __restrict__ queue, const int32_t* __restrict__ queue_len,
+                    uint64_t* sp) {
+  rs_span(sp, 0);
   // The level kernel already published the next level's segment offsets in
   // a.off (route.cuh level_tables, CTA 0), so no per-CTA table rebuild here.
   __shared__ double zbuf[kSelWarps][kMaxP];
@@ -80,6 +92,8 @@ rescore_fp64_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restr
     }
     __syncwarp();
   }
+  __syncthreads();
+  rs_span(sp, 1);
 }
 
 // Node-grouped form of rescore_fp64_kernel: CTA (k, j) takes the queued
@@ -409,6 +423,8 @@ int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double
 int select_level_ws(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                     cudaStream_t st);
 
+extern uint64_t* g_level_spans;
+
 static int side_of(int P) {
   int s = 1;
   while (s * s < P) ++s;
@@ -420,6 +436,7 @@ int rescore_queue_x(Plan* p, const LevelArgs& a, const double* x, const int32_t*
                     cudaStream_t st) {
   PatchSrc ps{x, anchors, dc, n_img, H, W, side_of(p->v.P), n_img, Z64};
   const int nd = a.lvl_end - a.lvl_begin;
+  uint64_t* sp = g_level_spans ? g_level_spans + (size_t)16 * kSMs * 4 + 2 * a.depth : nullptr;
   const size_t gbytes = sizeof(double) * (size_t)p->v.P * p->max_group_cols_at_depth[a.depth];
   if (p->opt.rescore_by_node && gbytes <= kRescoreSmem && !p->level_wide[a.depth]) {
     // node-grouped: the level's internal nodes x shares, ~two CTAs per SM
@@ -430,7 +447,7 @@ int rescore_queue_x(Plan* p, const LevelArgs& a, const double* x, const int32_t*
         p->v, a, ps, sq, p->rs.queue, p->rs.queue_len);
   } else {
     rescore_fp64_kernel<<<4 * kSMs, kSelWarps * 32, 0, st>>>(p->v, a, ps, sq, p->rs.queue,
-                                                             p->rs.queue_len);
+                                                             p->rs.queue_len, sp);
   }
   FEPLL_LAUNCH();
   return kOk;

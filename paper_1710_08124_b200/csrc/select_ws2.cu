@@ -136,6 +136,7 @@ struct Args {
   int katoms;
   int prefetch;          // tiles ahead whose rows the loaders prefetch into L2 (0: off)
   uint64_t* trace;       // debug timeline: [CTA][64 tiles][16] clock64 stamps (or NULL)
+  uint64_t* spans;       // debug: [CTA][4] globaltimer at entry, after the prologue, at the end (or NULL)
 };
 
 __device__ __forceinline__ void stamp(const Args& a, int i, int slot) {
@@ -143,6 +144,14 @@ __device__ __forceinline__ void stamp(const Args& a, int i, int slot) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));  // SM cycles (per-CTA relative timing)
     a.trace[((size_t)blockIdx.x * 64 + i) * 16 + slot] = t;
+  }
+}
+
+__device__ __forceinline__ void span_stamp(const Args& a, int slot) {
+  if (a.spans && threadIdx.x == 0) {
+    uint64_t g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    a.spans[(size_t)blockIdx.x * 4 + slot] = g;
   }
 }
 
@@ -198,6 +207,7 @@ select_level_ws2_kernel(PlanView pv, Args args) {
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
+  span_stamp(args, 0);
 
   if (warp == kMmaWarp) tc::tmem_alloc(&s.tmem_base, kTmemCols);
   if (tid == 0) {
@@ -235,6 +245,7 @@ select_level_ws2_kernel(PlanView pv, Args args) {
   tc::fence_after_sync();
   const uint32_t tmem = s.tmem_base;
   const int t_begin = s.t_begin, t_end = s.t_end;
+  span_stamp(args, 1);
   if (args.trace && tid == 0) {  // CTA span on the global clock (load-balance check)
     uint64_t g;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
@@ -636,6 +647,7 @@ select_level_ws2_kernel(PlanView pv, Args args) {
   }
   tc::fence_before_sync();
   __syncthreads();
+  span_stamp(args, 2);
   if (args.trace && tid == 0) {
     uint64_t g;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
@@ -649,6 +661,7 @@ select_level_ws2_kernel(PlanView pv, Args args) {
 
 extern uint64_t* g_ws_trace;
 extern int g_ws_trace_level;
+uint64_t* g_level_spans = nullptr;  // fepll_debug_level_spans: [depth][CTA][4]
 
 int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                      cudaStream_t st) {
@@ -664,6 +677,7 @@ int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double
   args.katoms = (p->v.P + 31) / 32;
   args.prefetch = p->opt.l2_prefetch;
   args.trace = (a.depth == g_ws_trace_level) ? g_ws_trace : nullptr;
+  args.spans = g_level_spans ? g_level_spans + (size_t)a.depth * kSMs * 4 : nullptr;
   auto launch = [&](auto kernel, size_t tables, int threads) -> int {
     const size_t smem = 1024 + ws2::kStages * ws2::kStageBytes + ws2::kBBytes + tables;
     FEPLL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -679,3 +693,8 @@ int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double
 }
 
 }  // namespace fepll
+
+extern "C" int fepll_debug_level_spans(void* device_buffer) {
+  fepll::g_level_spans = static_cast<uint64_t*>(device_buffer);
+  return 0;
+}

@@ -24,8 +24,10 @@ namespace wn {
 
 // debug timeline (fepll_debug_wiener_trace): [CTA][64 tiles][8] clock64
 __device__ uint64_t* g_trace = nullptr;
+// (callers test a trace flag read once per CTA: a global load of g_trace per
+// stamp stalled every tile behind its barrier)
 __device__ __forceinline__ void wstamp(int i, int slot) {
-  if (g_trace && i < 64 && threadIdx.x == 0 && blockIdx.x < 148) {
+  if (i < 64 && threadIdx.x == 0 && blockIdx.x < 148) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
     g_trace[((size_t)blockIdx.x * 64 + i) * 8 + slot] = t;
@@ -79,6 +81,19 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
                    static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
                "l"(src)
+               : "memory");
+}
+// src_bytes 0: the destination is zero-filled, nothing is read
+__device__ __forceinline__ void cp_async16z(void* dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8z(void* dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src), "r"(src_bytes)
                : "memory");
 }
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
@@ -260,6 +275,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
   int2* anc = reinterpret_cast<int2*>(dcs + NS * kRows);  // XW: [4][MT] anchors of the rows
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int P = geo.P;
+  const bool trace_on = g_trace != nullptr;
   // K padding columns of the row buffers stay zero (cp.async fills [0, P))
   for (int e = tid; e < NS * kRows * (geo.Pn - P); e += kThreads) {
     const int w = geo.Pn - P, i = e / w;  // row i of the adjacent buffers
@@ -374,11 +390,11 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
     const int li = cli;
     const int comp = h.leaf_cr[li] & 0xFFFF;
     const int r = h.leaf_cr[li] >> 16;
-    wstamp(i, 0);
+    if (trace_on) wstamp(i, 0);
     bulk_wait_read();  // the previous tile's row stores have left its buffer
     cp_async_wait_group<NS - 2>();
     __syncthreads();  // this tile's rows landed; the buffer refilled next is free
-    wstamp(i, 1);
+    if (trace_on) wstamp(i, 1);
     fetch_rows(tile + kLead);  // committed with the row copies below (one group per tile)
     fetch_anc(tile + 2);       // XW: its indices landed with the last group
     if (comp != cur_leaf) {
@@ -393,7 +409,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       cur_leaf = comp;
       __syncthreads();
     }
-    wstamp(i, 2);
+    if (trace_on) wstamp(i, 2);
     const ZT* Zs = Zs0 + (i % NS) * kRows * zld;
     const int g4 = lane >> 2, t4 = lane & 3;
     const int m0 = warp * RW;
@@ -426,12 +442,21 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
     } else {
       fetch_z_slices(jn, 0, n_slices);
     }
+    // this lane's 16-byte chunk of every Z64 row (rows past the bucket: zero-filled)
+    const ZT* zsrc = Z64 + kEl * lane;
     auto zstep = [&](int st) {
       if (!inter) return;
 #pragma unroll
       for (int q = st * (kRowsPerThread / 8); q < (st + 1) * (kRowsPerThread / 8); ++q) {
         ZT* d = zn + (warp + kWarps * q) * zld;
         if (kEl * lane >= 64) continue;  // FP32 rows: 16 lanes cover the 256-byte row
+        if constexpr (!XW) {
+          const int g = gsl[q];
+          const bool ok = g >= 0;
+          cp_async16z(d, ok ? zsrc + (int64_t)g * zin_pitch : zsrc, ok ? 16u : 0u);
+          if (lane == 0) cp_async8z(dcn + warp + kWarps * q, ok ? dc + g : dc, ok ? 8u : 0u);
+          continue;
+        }
         if (gsl[q] >= 0) {
           if constexpr (XW) {
             const int2 a = asl[XW ? q : 0];
@@ -468,9 +493,9 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       default: wiener_rows<NT2, 8, RW>(za, zb, da, db, Us, geo.uld, sh, t4, g4, zstep, acc); break;
     }
     cp_async_commit();
-    wstamp(i, 3);
+    if (trace_on) wstamp(i, 3);
     {
-      wstamp(i, 4);
+      if (trace_on) wstamp(i, 4);
       const double gt = h.leaf_gt[li];
       // Zhat + dc = (acc + gamma_tail z) + dc, written over this warp's own
       // rows of Zs (each element read and written by the same lane)...
@@ -507,7 +532,7 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
         }
         bulk_commit();
       }
-      wstamp(i, 5);
+      if (trace_on) wstamp(i, 5);
     }
   }
   bulk_wait_all();  // the last rows' stores are complete before the kernel ends
