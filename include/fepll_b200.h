@@ -87,6 +87,10 @@ int fepll_plan_destroy(fepll_plan_t plan);
  *   seg_sq 0 | 1              ws2 levels pass ||z||^2 in segment order (default 1);
  *   wiener_pair 0 | 1         two 64-row Wiener CTAs per SM when they fit (1);
  *   wiener_rw 8 | 16          rows per warp in that configuration (8);
+ *   wiener_split 0 | 1        Wiener warp pairs share 16 rows and issue m16n8k8
+ *                             DMMAs, C crossing through shared memory (1), or
+ *                             8-row warps with m8n8k4 (0, default: measured
+ *                             2 % faster) — bitwise the same;
  *   wiener_xw 0 | 1           Wiener reads 8x8 windows of x instead of Z64 (0);
  *   wiener_add_dc 0 | 1       fepll_wiener writes est + dc (1) or the bare
  *                             estimates (0: the trace's `estimates`; pass dc
@@ -100,6 +104,9 @@ int fepll_plan_destroy(fepll_plan_t plan);
  *                             over the images, 1: one per (pixel, image)) or
  *                             fepll_aggregate_tiles (2: staged in shared memory,
  *                             default; batches only);
+ *   pdl 0 | 1                 tree-level and re-scoring kernels launched with
+ *                             programmatic dependent launch: each one's prologue
+ *                             overlaps its predecessor's tail (default 1);
  *   rescore_by_node 0 | 1     FP64 re-scoring grouped by tree node, the node's
  *                             group matrix staged in shared memory (measured
  *                             slower, default 0).

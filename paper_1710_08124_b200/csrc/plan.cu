@@ -267,6 +267,8 @@ static int* plan_option(Plan* p, const char* name) {
   if (n == "l2_prefetch") return &p->opt.l2_prefetch;
   if (n == "rescore_by_node") return &p->opt.rescore_by_node;
   if (n == "aggregate_variant") return &p->opt.aggregate_variant;
+  if (n == "pdl") return &p->opt.pdl;
+  if (n == "wiener_split") return &p->opt.wiener_split;
   return nullptr;
 }
 

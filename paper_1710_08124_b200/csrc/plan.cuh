@@ -76,6 +76,8 @@ struct PlanOptions {
                            // smem once per CTA) — measured slower (select 11.3 -> 13.1 ms/step at 64 x 1024^2:
                            // one 208 KB CTA per SM leaves 8 warps for latency-bound chains), off
 
+  int wiener_split = 0;      // Wiener warp pairs on 16 rows with m16n8k8 DMMAs (0: 8-row warps, m8n8k4)
+  int pdl = 1;               // tree levels and re-scoring launched with programmatic dependent launch
   int aggregate_variant = 2; // batch reprojection kernel (host: 0/1 fepll_aggregate_cover_ex, 2 fepll_aggregate_tiles)
   int l2_prefetch = 0;     // ws2 loaders prefetch rows into L2 three tiles ahead of their cp.async: 1 per 128-B line, 2 one bulk prefetch per row (both measured slower: level 0.295 -> 0.324 / 0.486 ms)
 };

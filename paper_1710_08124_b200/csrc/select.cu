@@ -66,6 +66,8 @@ __global__ void __launch_bounds__(kSelWarps * 32, 4)
 rescore_fp64_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restrict__ sq,
                     const int32_t* __restrict__ queue, const int32_t* __restrict__ queue_len,
                     uint64_t* sp) {
+  pdl_wait();     // PDL behind the level kernel: its queue and counts
+  pdl_trigger();  // the next level's prologue may overlap this grid
   rs_span(sp, 0);
   // The level kernel already published the next level's segment offsets in
   // a.off (route.cuh level_tables, CTA 0), so no per-CTA table rebuild here.
@@ -446,8 +448,12 @@ int rescore_queue_x(Plan* p, const LevelArgs& a, const double* x, const int32_t*
     rescore_node_kernel<<<dim3(nd, shares), kRescoreWarps * 32, kRescoreWarpSmem + gbytes, st>>>(
         p->v, a, ps, sq, p->rs.queue, p->rs.queue_len);
   } else {
-    rescore_fp64_kernel<<<4 * kSMs, kSelWarps * 32, 0, st>>>(p->v, a, ps, sq, p->rs.queue,
-                                                             p->rs.queue_len, sp);
+    if (p->opt.pdl)
+      FEPLL_CUDA(launch_pdl(rescore_fp64_kernel, dim3(4 * kSMs), dim3(kSelWarps * 32), 0, st, p->v, a, ps, sq,
+                            (const int32_t*)p->rs.queue, (const int32_t*)p->rs.queue_len, sp));
+    else
+      rescore_fp64_kernel<<<4 * kSMs, kSelWarps * 32, 0, st>>>(p->v, a, ps, sq, p->rs.queue,
+                                                               p->rs.queue_len, sp);
   }
   FEPLL_LAUNCH();
   return kOk;

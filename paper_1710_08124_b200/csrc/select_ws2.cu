@@ -228,6 +228,10 @@ select_level_ws2_kernel(PlanView pv, Args args) {
     tc::fence_mbar_init();
   }
   if (tid < kGroups) s.epi[tid].node = -1;
+  // launched with PDL behind the previous level's re-scoring: everything
+  // above (TMEM, barriers) overlapped its tail; the counts are its output
+  pdl_wait();
+  pdl_trigger();  // the re-scoring grid may queue behind this one's CTAs
   level_tables(pv, a, s.lv, kRows);  // contains __syncthreads
   for (int k = tid; k < a.lvl_end - a.lvl_begin; k += blockDim.x) {
     const int u = a.lvl_begin + k;
@@ -681,7 +685,10 @@ int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double
   auto launch = [&](auto kernel, size_t tables, int threads) -> int {
     const size_t smem = 1024 + ws2::kStages * ws2::kStageBytes + ws2::kBBytes + tables;
     FEPLL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kernel<<<kSMs, threads, smem, st>>>(p->v, args);
+    if (p->opt.pdl)
+      FEPLL_CUDA(launch_pdl(kernel, dim3(kSMs), dim3(threads), smem, st, p->v, args));
+    else
+      kernel<<<kSMs, threads, smem, st>>>(p->v, args);
     return kOk;
   };
   if (p->level_tc_npad[a.depth] <= 96)

@@ -16,6 +16,8 @@
 // (37.2 TFLOP/s FP64 peak measured on B200 for every f64 shape,
 // tools/dmma_bench.cu; the k8 shape halves the B-fragment loads per FLOP of
 // m8n8k4): warp w owns rows 16w..16w+15 of the tile.
+#include <type_traits>
+
 #include "route.cuh"
 
 namespace fepll {
@@ -64,7 +66,7 @@ __device__ __forceinline__ void dmma8(double& d0, double& d1, double a, double b
 }
 
 __device__ __forceinline__ void dmma16(double (&d)[4], const double (&a)[4], const double (&b)[2]) {
-  asm volatile(
+  asm(
       "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%0,%1,%2,%3};"
       : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
@@ -133,6 +135,7 @@ struct Geo {
   int uld;       // Us [Pn][uld]  (phase-1 B: k = p, n = j; phase-2 B: k = j, n = p)
   int add_dc;    // 1: write est + dc (default), 0: the bare estimates (plan option wiener_add_dc)
   int zld32;     // row stride (floats) of the FP32-row variant: 4 mod 32, conflict-free fragment loads
+  int R8e;       // R8 rounded up to 16: basis / shrink columns staged (zero past the rank)
 };
 
 // NT2: phase-2 n-tiles (P/8 rounded up): 8 for P=64, 13 for P=100.
@@ -170,17 +173,23 @@ __device__ __forceinline__ void wiener_rows(const ZT* za, const ZT* zb, double d
       b0[n] = u0[n * 8];
       b1[n] = u1[n * 8];
     }
-    // the m16n8k8 product as four m8n8k4 steps, consecutive DMMAs on
-    // different accumulators (k 0-3 for every n, then k 4-7)
+    if constexpr (RW == 16) {
+      // one m16n8k8 per n-tile: bitwise the two m8n8k4 steps per row half
+      // below (DMMA accumulates k in order, tools/dmma_order_probe.cu) at a
+      // quarter of the instructions
+      const double af[4] = {a0, a1, a2, a3};
 #pragma unroll
-    for (int n = 0; n < NT1; ++n) {
-      dmma8(acc[n][0], acc[n][1], a0, b0[n]);
-      if (RW == 16) dmma8(acc[n][2], acc[n][3], a1, b0[n]);
-    }
+      for (int n = 0; n < NT1; ++n) {
+        const double bf[2] = {b0[n], b1[n]};
+        dmma16(acc[n], af, bf);
+      }
+    } else {
+      // m8n8k4 steps, consecutive DMMAs on different accumulators (k 0-3
+      // for every n, then k 4-7)
 #pragma unroll
-    for (int n = 0; n < NT1; ++n) {
-      dmma8(acc[n][0], acc[n][1], a2, b1[n]);
-      if (RW == 16) dmma8(acc[n][2], acc[n][3], a3, b1[n]);
+      for (int n = 0; n < NT1; ++n) dmma8(acc[n][0], acc[n][1], a0, b0[n]);
+#pragma unroll
+      for (int n = 0; n < NT1; ++n) dmma8(acc[n][0], acc[n][1], a2, b1[n]);
     }
   }
   // C = acc * shrink: lane (g, t) holds C[g][8n + 2t + e] (acc[n][e]) and
@@ -227,15 +236,70 @@ __device__ __forceinline__ void wiener_rows(const ZT* za, const ZT* zb, double d
       b0[n] = u0[n * 8 * uld];
       b1[n] = u0[n * 8 * uld + 4];
     }
+    if constexpr (RW == 16) {
 #pragma unroll
-    for (int n = 0; n < NT2; ++n) {
-      dmma8(acc2[n][0], acc2[n][1], a[0], b0[n]);
-      if (RW == 16) dmma8(acc2[n][2], acc2[n][3], a[1], b0[n]);
+      for (int n = 0; n < NT2; ++n) {
+        const double bf[2] = {b0[n], b1[n]};
+        dmma16(acc2[n], a, bf);
+      }
+    } else {
+#pragma unroll
+      for (int n = 0; n < NT2; ++n) dmma8(acc2[n][0], acc2[n][1], a[0], b0[n]);
+#pragma unroll
+      for (int n = 0; n < NT2; ++n) dmma8(acc2[n][0], acc2[n][1], a[2], b1[n]);
     }
+  }
+}
+
+// PAIR (split) form: warps 2q, 2q + 1 share rows 16q .. 16q + 15 and issue
+// m16n8k8 DMMAs (16 rows x 8 columns x 8 k each, bitwise the m8n8k4 pairs:
+// tools/dmma_order_probe.cu) — a quarter of the DMMA instructions and half
+// the basis fragment loads per flop of the 8-row warps, at the same 16
+// warps per SM: warp half hf takes rank tiles [hf NH, (hf+1) NH) in phase 1
+// and column tiles [hf NT2/2, (hf+1) NT2/2) in phase 2, C crossing between
+// the two warps through shared memory (Cs, 16 x uld per pair).
+template <int NT2, int NH, class ZT, class Step>
+__device__ __forceinline__ void wiener_rows_pair(const ZT* za, const ZT* zb, const double* Us, int uld,
+                                                 const double* sh, int t4, int g4, int hf, double* Cs,
+                                                 int bar_id, Step&& step, double (&acc2)[NT2 / 2][4]) {
+  double acc[NH][4];
 #pragma unroll
-    for (int n = 0; n < NT2; ++n) {
-      dmma8(acc2[n][0], acc2[n][1], a[2], b1[n]);
-      if (RW == 16) dmma8(acc2[n][2], acc2[n][3], a[3], b1[n]);
+  for (int n = 0; n < NH; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0;
+  const int c0 = hf * NH * 8;  // this warp's first rank column
+#pragma unroll
+  for (int k0 = 0; k0 < NT2 * 8; k0 += 8) {  // NT2 * 8 == Pn
+    step(k0 / 8);
+    const double af[4] = {(double)za[k0], (double)zb[k0], (double)za[k0 + 4], (double)zb[k0 + 4]};
+    const double* u0 = Us + (k0 + t4) * uld + g4 + c0;
+    const double* u1 = u0 + 4 * uld;
+#pragma unroll
+    for (int n = 0; n < NH; ++n) {
+      const double bf[2] = {u0[n * 8], u1[n * 8]};
+      dmma16(acc[n], af, bf);
+    }
+  }
+  // C = acc * shrink (rows g, g + 8; columns c0 + 8n + 2t, + 1)
+#pragma unroll
+  for (int n = 0; n < NH; ++n) {
+    const int col = c0 + n * 8 + 2 * t4;
+    Cs[g4 * uld + col] = acc[n][0] * sh[col];
+    Cs[g4 * uld + col + 1] = acc[n][1] * sh[col + 1];
+    Cs[(g4 + 8) * uld + col] = acc[n][2] * sh[col];
+    Cs[(g4 + 8) * uld + col + 1] = acc[n][3] * sh[col + 1];
+  }
+  asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+#pragma unroll
+  for (int n = 0; n < NT2 / 2; ++n) acc2[n][0] = acc2[n][1] = acc2[n][2] = acc2[n][3] = 0.0;
+  const int n0 = hf * (NT2 / 2);
+#pragma unroll
+  for (int kb = 0; kb < 2 * NH; ++kb) {
+    const double af[4] = {Cs[g4 * uld + 8 * kb + t4], Cs[(g4 + 8) * uld + 8 * kb + t4],
+                          Cs[g4 * uld + 8 * kb + 4 + t4], Cs[(g4 + 8) * uld + 8 * kb + 4 + t4]};
+    const double* u0 = Us + g4 * uld + 8 * kb + t4;  // U[8n + g][k + t] = U^T[k][n]
+#pragma unroll
+    for (int n = 0; n < NT2 / 2; ++n) {
+      const double bf[2] = {u0[(n0 + n) * 8 * uld], u0[(n0 + n) * 8 * uld + 4]};
+      dmma16(acc2[n], af, bf);
     }
   }
 }
@@ -247,8 +311,8 @@ __device__ __forceinline__ void wiener_rows(const ZT* za, const ZT* zb, double d
 // ZT: element type of the patch rows in and the estimate rows out (double;
 // float for the FP32-state mode — rows converted exactly to FP64 at the
 // fragment loads, the FP64 result rounded once to FP32 at the store)
-template <int NT2, int MT, int NS, int RW, bool XW, class ZT = double>
-__global__ void __launch_bounds__(MT / RW * 32, RW == 8 ? 2 : 1)
+template <int NT2, int MT, int NS, int RW, bool XW, class ZT = double, bool PAIR = false>
+__global__ void __launch_bounds__(PAIR ? MT / 16 * 64 : MT / RW * 32, (RW == 8 || PAIR) ? 2 : 1)
 wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, int n_leaf_nodes,
                    const int32_t* __restrict__ cnt, const int64_t* __restrict__ off,
                    const int32_t* __restrict__ leafseg, const ZT* __restrict__ Z64, int zin_pitch,
@@ -257,7 +321,8 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
                    Geo geo) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int kRows = MT;
-  constexpr int kThreads = MT / RW * 32;  // one warp per RW rows
+  constexpr int kThreads = PAIR ? MT / 16 * 64 : MT / RW * 32;  // one warp (pair) per RW (16) rows
+  static_assert(!PAIR || (RW == 16 && !XW && NT2 % 2 == 0), "PAIR: 16-row warp pairs, even column tiles");
   Head& h = *reinterpret_cast<Head*>(smem);
   constexpr int kRing = 2 * NS;      // index ring slots
   // tiles of indices fetched ahead of their rows' issue (XW: one more, for
@@ -270,9 +335,10 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
   ZT* Zs0 = reinterpret_cast<ZT*>(smem + ((sizeof(Head) + 127) & ~size_t(127)));
   double* Us = reinterpret_cast<double*>(
       reinterpret_cast<uint8_t*>(Zs0) + ((NS * kRows * zld * sizeof(ZT) + 15) & ~size_t(15)));  // [Pn][uld] (p, j)
-  double* sh = Us + geo.Pn * geo.uld;          // [R8]
-  double* dcs = sh + geo.R8;                   // [NS][MT] dc of the buffered rows
+  double* sh = Us + geo.Pn * geo.uld;          // [R8e]
+  double* dcs = sh + geo.R8e;                  // [NS][MT] dc of the buffered rows
   int2* anc = reinterpret_cast<int2*>(dcs + NS * kRows);  // XW: [4][MT] anchors of the rows
+  double* Cs = reinterpret_cast<double*>(anc + 4 * kRows);  // PAIR: [MT][uld] C of the tile
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int P = geo.P;
   const bool trace_on = g_trace != nullptr;
@@ -399,20 +465,20 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
     fetch_anc(tile + 2);       // XW: its indices landed with the last group
     if (comp != cur_leaf) {
       const double* U = pv.model_basis + pv.model_off64[comp];
-      for (int e = tid; e < geo.Pn * geo.R8; e += kThreads) {
-        const int p = e / geo.R8, j = e - p * geo.R8;
+      for (int e = tid; e < geo.Pn * geo.R8e; e += kThreads) {
+        const int p = e / geo.R8e, j = e - p * geo.R8e;
         const double u = (p < P && j < r) ? U[(int64_t)p * r + j] : 0.0;
         Us[p * geo.uld + j] = u;
       }
       const double* shrink = pv.model_shrink + (int64_t)t * pv.model_cols_total + pv.model_col_off[comp];
-      for (int j = tid; j < geo.R8; j += kThreads) sh[j] = j < r ? shrink[j] : 0.0;
+      for (int j = tid; j < geo.R8e; j += kThreads) sh[j] = j < r ? shrink[j] : 0.0;
       cur_leaf = comp;
       __syncthreads();
     }
     if (trace_on) wstamp(i, 2);
     const ZT* Zs = Zs0 + (i % NS) * kRows * zld;
     const int g4 = lane >> 2, t4 = lane & 3;
-    const int m0 = warp * RW;
+    const int m0 = PAIR ? (warp >> 1) * 16 : warp * RW;
     const ZT* za = Zs + (m0 + g4) * zld + t4;       // rows g (, g+8) of the warp
     const ZT* zb = za + 8 * zld;
     // ---- phase 1: C[m0..m0+15][0..R8) = (Z . U) * shrink, with the
@@ -478,10 +544,27 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
         }
       }
     };
-    double acc[NT2][4];
+    constexpr int kNA = PAIR ? NT2 / 2 : NT2;  // column tiles of this warp
+    double acc[kNA][4];
     const double* dcc = dcs + (i % NS) * kRows;  // dc of this tile's rows
     const double da = XW ? dcc[m0 + g4] : 0.0;
     const double db = XW && RW == 16 ? dcc[m0 + g4 + 8] : 0.0;
+    const int hf = warp & 1;
+    const int bar_id = 1 + (warp >> 1);
+    double* Cp = Cs + m0 * geo.uld;
+    if constexpr (PAIR) {
+      // rank tiles per half: ceil(r / 16) (zero basis columns up to R8e)
+      switch ((r + 15) / 16) {
+        case 1: wiener_rows_pair<NT2, 1>(za, zb, Us, geo.uld, sh, t4, g4, hf, Cp, bar_id, zstep,
+                                         acc); break;
+        case 2: wiener_rows_pair<NT2, 2>(za, zb, Us, geo.uld, sh, t4, g4, hf, Cp, bar_id, zstep,
+                                         acc); break;
+        case 3: wiener_rows_pair<NT2, 3>(za, zb, Us, geo.uld, sh, t4, g4, hf, Cp, bar_id, zstep,
+                                         acc); break;
+        default: wiener_rows_pair<NT2, 4>(za, zb, Us, geo.uld, sh, t4, g4, hf, Cp, bar_id, zstep,
+                                          acc); break;
+      }
+    } else
     switch ((r + 7) / 8) {
       case 1: wiener_rows<NT2, 1, RW>(za, zb, da, db, Us, geo.uld, sh, t4, g4, zstep, acc); break;
       case 2: wiener_rows<NT2, 2, RW>(za, zb, da, db, Us, geo.uld, sh, t4, g4, zstep, acc); break;
@@ -507,8 +590,8 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
         const double d = dct[m0 + g4 + 8 * half];
         const double dz = XW ? d : 0.0;  // XW rows hold the window: z = w - dc
 #pragma unroll
-        for (int n = 0; n < NT2; ++n) {
-          const int col = n * 8 + 2 * t4;
+        for (int n = 0; n < kNA; ++n) {
+          const int col = ((PAIR ? hf * kNA : 0) + n) * 8 + 2 * t4;
           if (col < P) {
             const double e0 = acc[n][2 * half] + gt * ((double)zr[col] - dz);
             const double e1 = acc[n][2 * half + 1] + gt * ((double)zr[col + 1] - dz);
@@ -523,7 +606,8 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
       // coalesced 16-byte stores from the same rows measured slower)
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane < RW) {
+      if (PAIR) asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");  // both column halves written
+      if (lane < RW && (!PAIR || hf == 0)) {
         const int gidx = h.rows[slot][m0 + lane];
         if (gidx >= 0) {
           const int64_t orow =  // padded image pitch (no division when dense)
@@ -550,6 +634,7 @@ static wn::Geo wiener_geo(const Plan* p) {
   geo.zld32 = geo.Pn;
   while (geo.zld32 % 32 != 4) ++geo.zld32;
   geo.R8 = (p->max_model_rank + 7) / 8 * 8;
+  geo.R8e = (geo.R8 + 15) / 16 * 16;
   geo.uld = ld(geo.R8, 4);
   geo.add_dc = p->opt.wiener_add_dc;
   return geo;
@@ -557,11 +642,11 @@ static wn::Geo wiener_geo(const Plan* p) {
 
 // dynamic shared memory of an (mt rows, ns stages) configuration: head,
 // row stages, basis, shrink, dc ring, XW anchors ring
-static size_t wiener_smem(const wn::Geo& geo, int mt, int ns, size_t zt_bytes = 8) {
+static size_t wiener_smem(const wn::Geo& geo, int mt, int ns, size_t zt_bytes = 8, bool pair = false) {
   const size_t rows = zt_bytes == 8 ? ns * (size_t)mt * geo.zld * 8 : ns * (size_t)mt * geo.zld32 * zt_bytes;
   return ((sizeof(wn::Head) + 127) & ~size_t(127)) + ((rows + 15) & ~size_t(15)) +
-         sizeof(double) * ((size_t)geo.Pn * geo.uld + geo.R8 + (size_t)ns * mt) +
-         sizeof(int2) * 4 * (size_t)mt;
+         sizeof(double) * ((size_t)geo.Pn * geo.uld + geo.R8e + (size_t)ns * mt) +
+         sizeof(int2) * 4 * (size_t)mt + (pair ? sizeof(double) * (size_t)mt * geo.uld : 0);
 }
 
 static bool wiener_pair_fits(const wn::Geo& geo) {
@@ -614,8 +699,14 @@ static int wiener_dmma_t(Plan* p, int t, const ZT* Z64, int zin_pitch, const dou
   const size_t smem = smem_for(mt, ns);
   const int nt2 = geo.Pn / 8;
   const int rw = pair && p->opt.wiener_rw == 8 ? 8 : 16;
-  const int threads = mt / rw * 32;
+  // split warp pairs (m16n8k8, plan option wiener_split): the pair
+  // configuration with an even column-tile count and room for the C tiles
+  const bool split = pair && !xw && p->opt.wiener_split && nt2 % 2 == 0 && nt2 <= 8 &&
+                     2 * (wiener_smem(geo, 64, 2, sizeof(ZT), true) + 1024) <= (size_t)per_sm_cap;
+  const size_t smem_launch = split ? wiener_smem(geo, 64, 2, sizeof(ZT), true) : smem;
+  const int threads = split ? 256 : mt / rw * 32;
   auto launch = [&](auto kernel) -> int {
+    const size_t smem = smem_launch;
     FEPLL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
@@ -625,8 +716,14 @@ static int wiener_dmma_t(Plan* p, int t, const ZT* Z64, int zin_pitch, const dou
     FEPLL_LAUNCH();
     return kOk;
   };
+  auto launch_split = [&](auto nt) -> int {
+    constexpr int N = decltype(nt)::value;
+    if constexpr (N % 2 == 0 && N <= 8) return launch(wn::wiener_dmma_kernel<N, 64, 2, 16, false, ZT, true>);
+    return kDataError;
+  };
 #define FEPLL_WN_CASE(N)                                                   \
   case N:                                                                  \
+    if (split) return launch_split(std::integral_constant<int, N>{});      \
     return big ? launch(wn::wiener_dmma_kernel<N, 128, 2, 16, false, ZT>)      \
                : ns == 4 ? launch(wn::wiener_dmma_kernel<N, 64, 4, 16, false, ZT>) \
                : rw == 8 ? launch(wn::wiener_dmma_kernel<N, 64, 2, 8, false, ZT>)  \
