@@ -239,10 +239,39 @@ select_level_ws2_kernel(PlanView pv, Args args) {
     s.nd_npad[k] = (int16_t)pv.tc_npad[u];
     s.nd_nk[k] = (int16_t)pv.child_count[u];
   }
+  __syncthreads();  // node tables
   if (tid == 0) {
+    // contiguous tile ranges of equal estimated cost: a tile costs 16 +
+    // npad / 8 (loads, epilogue and MMAs of its node's width) — on the leaf
+    // level of the cfg5 tree the 4-child nodes' tiles (128 columns) take
+    // ~15 % longer than the 3-child ones (96), and equal tile counts left
+    // the CTAs holding them 40 us behind
+    const int nd = a.lvl_end - a.lvl_begin;
     const int T = s.lv.total_tiles;
-    s.t_begin = (int)(((int64_t)T * blockIdx.x) / gridDim.x);
-    s.t_end = (int)(((int64_t)T * (blockIdx.x + 1)) / gridDim.x);
+    int64_t W = 0;
+    bool mixed = false;
+    for (int k = 0; k < nd; ++k) {
+      W += (int64_t)(s.lv.tpre[k + 1] - s.lv.tpre[k]) * (16 + s.nd_npad[k] / 8);
+      mixed |= s.nd_npad[k] != s.nd_npad[0];
+    }
+    if (!mixed) {
+      s.t_begin = (int)(((int64_t)T * blockIdx.x) / gridDim.x);
+      s.t_end = (int)(((int64_t)T * (blockIdx.x + 1)) / gridDim.x);
+    } else {
+      const int64_t x0 = W * blockIdx.x / gridDim.x, x1 = W * (blockIdx.x + 1) / gridDim.x;
+      int64_t acc = 0;
+      int tb = T, te = T;
+      for (int k = 0; k < nd; ++k) {
+        const int wk = 16 + s.nd_npad[k] / 8;
+        const int nt = s.lv.tpre[k + 1] - s.lv.tpre[k];
+        const int64_t nxt = acc + (int64_t)nt * wk;
+        if (tb == T && x0 < nxt) tb = s.lv.tpre[k] + (int)((x0 - acc + wk - 1) / wk);
+        if (te == T && x1 < nxt) te = s.lv.tpre[k] + (int)((x1 - acc + wk - 1) / wk);
+        acc = nxt;
+      }
+      s.t_begin = min(tb, T);
+      s.t_end = blockIdx.x + 1 == gridDim.x ? T : min(te, T);
+    }
   }
   tc::fence_before_sync();
   __syncthreads();
