@@ -107,6 +107,11 @@ int fepll_plan_destroy(fepll_plan_t plan);
  *   pdl 0 | 1                 tree-level and re-scoring kernels launched with
  *                             programmatic dependent launch: each one's prologue
  *                             overlaps its predecessor's tail (default 1);
+ *   defer 0 | 1               (ws2 trees) uncertified decisions are routed by the
+ *                             tensor-core argmin and verified in FP64 after the
+ *                             last level, mis-routed patches re-descended (1,
+ *                             default), or re-scored after every level (0) —
+ *                             the same labels, buckets and counts;
  *   rescore_by_node 0 | 1     FP64 re-scoring grouped by tree node, the node's
  *                             group matrix staged in shared memory (measured
  *                             slower, default 0).

@@ -18,6 +18,7 @@ constexpr int kMaxGroupCols = 512;  // sum of child ranks of one node (TMEM widt
 constexpr int kMaxChildren = 32;
 constexpr int kMaxDepth = 64;
 constexpr int kSMs = 148;
+constexpr int kLeafSlack = 32;  // extra leaf-bucket slots per leaf (deferred verification re-routes)
 
 void set_error(const std::string& msg);
 void count_launch();

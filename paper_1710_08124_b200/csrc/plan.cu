@@ -169,6 +169,12 @@ static int create(const fepll_plan_desc* d, Plan** out) {
   FEPLL_CUDA(cudaMalloc(&m, sizeof(int32_t) * kMaxDepth));
   p->owned.push_back(m);
   p->rs.queue_len = static_cast<int32_t*>(m);
+  FEPLL_CUDA(cudaMalloc(&m, sizeof(int32_t) * 2));
+  p->owned.push_back(m);
+  p->rs.vq_len = static_cast<int32_t*>(m);
+  FEPLL_CUDA(cudaMalloc(&m, sizeof(int32_t) * std::max(1, p->v.K)));
+  p->owned.push_back(m);
+  p->rs.holes = static_cast<int32_t*>(m);
   *out = p;
   return kOk;
 }
@@ -182,8 +188,15 @@ static void free_scratch(Plan* p) {
   r.segsq[0] = r.segsq[1] = nullptr;
   cudaFree(r.leafseg);
   cudaFree(r.queue);
+  cudaFree(r.vq);
+  cudaFree(r.dq);
+  cudaFree(r.first_bad);
+  cudaFree(r.pos_leaf);
   r.seg[0] = r.seg[1] = r.leafseg = r.queue = nullptr;
-  r.cap = r.seg_cap = r.queue_cap = 0;
+  r.vq = nullptr;
+  r.dq = nullptr;
+  r.first_bad = r.pos_leaf = nullptr;
+  r.cap = r.seg_cap = r.queue_cap = r.vq_cap = 0;
 }
 
 static int reserve(Plan* p, int64_t max_patches) {
@@ -198,9 +211,18 @@ static int reserve(Plan* p, int64_t max_patches) {
   FEPLL_CUDA(cudaMalloc(&r.seg[1], sizeof(int32_t) * seg));
   FEPLL_CUDA(cudaMalloc(&r.segsq[0], sizeof(double) * std::max(seg, np)));
   FEPLL_CUDA(cudaMalloc(&r.segsq[1], sizeof(double) * seg));
-  FEPLL_CUDA(cudaMalloc(&r.leafseg, sizeof(int32_t) * lseg));
+  // leaf buckets: capacity = the parent's count + kLeafSlack per leaf
+  // (route.cuh), room for patches re-routed by the deferred verification
+  FEPLL_CUDA(cudaMalloc(&r.leafseg, sizeof(int32_t) * (lseg + (int64_t)kLeafSlack * std::max(1, p->v.K))));
   r.queue_cap = std::max<int64_t>(1024, max_patches);
   FEPLL_CUDA(cudaMalloc(&r.queue, sizeof(int32_t) * 2 * r.queue_cap));
+  // every patch can be logged once per level
+  r.vq_cap = std::max<int64_t>(1024, np * std::max(1, p->n_levels));
+  FEPLL_CUDA(cudaMalloc(&r.vq, sizeof(int4) * r.vq_cap));
+  FEPLL_CUDA(cudaMalloc(&r.dq, sizeof(int2) * r.vq_cap));
+  FEPLL_CUDA(cudaMalloc(&r.first_bad, sizeof(int32_t) * np));
+  FEPLL_CUDA(cudaMemset(r.first_bad, 0x7f, sizeof(int32_t) * np));
+  FEPLL_CUDA(cudaMalloc(&r.pos_leaf, sizeof(int32_t) * np));
   r.cap = max_patches;
   r.seg_cap = seg;
   return kOk;
@@ -268,6 +290,7 @@ static int* plan_option(Plan* p, const char* name) {
   if (n == "rescore_by_node") return &p->opt.rescore_by_node;
   if (n == "aggregate_variant") return &p->opt.aggregate_variant;
   if (n == "pdl") return &p->opt.pdl;
+  if (n == "defer") return &p->opt.defer;
   if (n == "wiener_split") return &p->opt.wiener_split;
   return nullptr;
 }

@@ -60,6 +60,16 @@ struct RouteScratch {
   int32_t* queue_len = nullptr;
   int64_t queue_cap = 0;
   int32_t* node_tmp = nullptr;
+  // deferred verification (plan option defer): ws2 levels route every row
+  // by its tensor-core argmin and log the uncertified ones; after the last
+  // level they are re-scored in FP64 and the mis-routed patches re-descended
+  int4* vq = nullptr;            // (patch, node, depth, provisional child) [vq_cap]
+  int64_t vq_cap = 0;
+  int32_t* vq_len = nullptr;     // [2]: verify entries, repair entries
+  int2* dq = nullptr;            // (patch, depth << 24 | exact child) [vq_cap]
+  int32_t* first_bad = nullptr;  // [cap] earliest disagreeing depth per patch (INT_MAX-ish when none)
+  int32_t* pos_leaf = nullptr;   // [cap] leafseg slot of each patch (leaf level)
+  int32_t* holes = nullptr;      // [K] leaf-bucket holes per component (leaf counts subtract them)
 };
 
 // Per-plan kernel choices (fepll_plan_set_option): A/B switches between
@@ -77,7 +87,8 @@ struct PlanOptions {
                            // one 208 KB CTA per SM leaves 8 warps for latency-bound chains), off
 
   int wiener_split = 0;      // Wiener warp pairs on 16 rows with m16n8k8 DMMAs (0: 8-row warps, m8n8k4)
-  int pdl = 1;               // tree levels and re-scoring launched with programmatic dependent launch
+  int pdl = 1;
+  int defer = 1;             // deferred FP64 verification of uncertified ws2 decisions (0: re-score after every level)               // tree levels and re-scoring launched with programmatic dependent launch
   int aggregate_variant = 2; // batch reprojection kernel (host: 0/1 fepll_aggregate_cover_ex, 2 fepll_aggregate_tiles)
   int l2_prefetch = 0;     // ws2 loaders prefetch rows into L2 three tiles ahead of their cp.async: 1 per 128-B line, 2 one bulk prefetch per row (both measured slower: level 0.295 -> 0.324 / 0.486 ms)
 };

@@ -118,7 +118,7 @@ __device__ inline void level_tables(const PlanView& pv, const LevelArgs& a, LT& 
   for (int k = threadIdx.x; k < nn; k += blockDim.x) {
     const int v = a.nxt_begin + k;
     const uint64_t c = (uint64_t)(uint32_t)a.cnt[pv.parent[v]];
-    cap[k] = pv.child_count[v] > 0 ? c : (c << 32);
+    cap[k] = pv.child_count[v] > 0 ? c : ((c + kLeafSlack) << 32);
   }
   __syncthreads();
   const int32_t items = block_exscan(s.cpre, nd, s.scan_tmp);

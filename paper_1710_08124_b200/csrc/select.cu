@@ -207,6 +207,75 @@ rescore_node_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restr
   }
 }
 
+// ---- deferred verification (plan option defer; ws2 trees).  The level
+// kernels route an uncertified row by its tensor-core argmin like a
+// certified one and log (patch, node, depth, provisional child); nothing
+// waits between levels.  After the last level, verify_kernel re-scores every
+// logged decision in FP64 (score_children_fp64: the arithmetic of the
+// per-level re-scoring) and records the disagreements; the earliest one of a
+// patch (first_bad) is where its path first left the FP64 argmin path — all
+// its decisions before were certified or verified — so repair_kernel
+// re-descends it from the FP64 child in FP64, leaves a hole (-1) in the
+// provisional leaf bucket and appends it to the right one (kLeafSlack spare
+// slots per leaf; an error flag past them).  Labels, leaf buckets and
+// counts are those of re-scoring after every level.
+__global__ void __launch_bounds__(kSelWarps * 32, 4)
+verify_kernel(PlanView pv, int t, PatchSrc ps, const double* __restrict__ sq, const int4* __restrict__ vq,
+              int32_t* vq_len, int64_t cap, int2* __restrict__ dq, int32_t* first_bad) {
+  __shared__ double zbuf[kSelWarps][kMaxP];
+  __shared__ double tbuf[kSelWarps][kMaxGroupCols];
+  const int lane = lane_id();
+  double* zs = zbuf[warp_id()];
+  double* tv = tbuf[warp_id()];
+  const int64_t total = min((int64_t)vq_len[0], cap);
+  for (int64_t item = (int64_t)blockIdx.x * kSelWarps + warp_id(); item < total;
+       item += (int64_t)gridDim.x * kSelWarps) {
+    const int4 e = vq[item];
+    load_patch(ps, e.x, pv.P, zs);
+    const int v = score_children_fp64(pv, t, e.y, zs, sq[e.x], tv);
+    if (lane == 0 && v != e.w) {
+      atomicMin(&first_bad[e.x], e.z);
+      const int slot = atomicAdd(&vq_len[1], 1);
+      dq[slot] = make_int2(e.x, (e.z << 24) | v);
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(kSelWarps * 32, 4)
+repair_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restrict__ sq, const int2* __restrict__ dq,
+              const int32_t* __restrict__ vq_len, int32_t* first_bad, const int32_t* __restrict__ pos_leaf,
+              int32_t* holes, int32_t* flags) {
+  __shared__ double zbuf[kSelWarps][kMaxP];
+  __shared__ double tbuf[kSelWarps][kMaxGroupCols];
+  const int lane = lane_id();
+  double* zs = zbuf[warp_id()];
+  double* tv = tbuf[warp_id()];
+  const int total = vq_len[1];
+  for (int item = blockIdx.x * kSelWarps + warp_id(); item < total; item += gridDim.x * kSelWarps) {
+    const int2 e = dq[item];
+    const int g = e.x, d = e.y >> 24;
+    if (first_bad[g] != d) continue;  // a later entry of a patch already off the FP64 path
+    int v = e.y & 0xFFFFFF;
+    load_patch(ps, g, pv.P, zs);
+    const double sqv = sq[g];
+    while (pv.child_count[v] > 0) v = score_children_fp64(pv, a.t, v, zs, sqv, tv);
+    if (lane == 0) {
+      a.leafseg[pos_leaf[g]] = -1;  // hole in the provisional bucket
+      atomicAdd(&holes[a.labels[g]], 1);
+      const int slot = atomicAdd(&a.cnt[v], 1);
+      if (slot < a.cnt[pv.parent[v]] + kLeafSlack) {  // the bucket's capacity (route.cuh)
+        a.leafseg[a.off[v] + slot] = g;
+        a.labels[g] = pv.leaf_index[v];
+      } else {
+        atomicOr(flags, 2);
+      }
+      first_bad[g] = 0x7f7f7f7f;
+    }
+    __syncwarp();
+  }
+}
+
 // Wiener estimate per patch (fallback for large P / rank), iterating the leaf
 // buckets (gmm.py:352-359: U((gamma-gamma_tail) c) + gamma_tail z).  Every
 // Wiener kernel writes est + dc, the values patches.py:198-222 reprojects.
@@ -404,9 +473,13 @@ wiener_tile_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
 }
 
 __global__ void leaf_counts_kernel(const int32_t* leaf_nodes, int n_leaf_nodes,
-                                   const int32_t* leaf_index, const int32_t* cnt, int64_t* out) {
+                                   const int32_t* leaf_index, const int32_t* cnt, const int32_t* holes,
+                                   int64_t* out) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < n_leaf_nodes) out[leaf_index[leaf_nodes[k]]] = cnt[leaf_nodes[k]];
+  if (k < n_leaf_nodes) {
+    const int c = leaf_index[leaf_nodes[k]];
+    out[c] = cnt[leaf_nodes[k]] - (holes ? holes[c] : 0);
+  }
 }
 
 // tensor-core level kernels (select_tc.cu: K atoms streamed per tile, any
@@ -467,6 +540,15 @@ int wiener_dmma_f32(Plan* p, int t, const float* Z32, int z32_pitch, const doubl
 bool wiener_xw_supported(const Plan* p);
 bool wiener_dmma_supported(const Plan* p);
 
+// every level runs the ws2 kernel (select_variant 1, no wide level): the
+// deferred verification covers the whole tree
+bool deferred_verify(const Plan* p) {
+  if (!p->opt.defer || p->opt.select_variant != 1 || p->v.tc_x == nullptr || p->v.P > 64) return false;
+  for (int d = 0; d < p->n_levels; ++d)
+    if (p->level_wide[d] || p->level_tc_npad[d] > 256 || !select_ws_supported(p, d)) return false;
+  return true;
+}
+
 LevelArgs make_level(Plan* p, int d, int t, int32_t* labels) {
   LevelArgs a;
   a.depth = d;
@@ -510,6 +592,11 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
   p->last_n_total = (int)n_total;
   FEPLL_CUDA(cudaMemsetAsync(p->rs.cnt, 0, sizeof(int32_t) * p->v.n_nodes, st));
   FEPLL_CUDA(cudaMemsetAsync(p->rs.queue_len, 0, sizeof(int32_t) * kMaxDepth, st));
+  const bool defer = mode == 1 && deferred_verify(p);
+  if (defer) {
+    FEPLL_CUDA(cudaMemsetAsync(p->rs.vq_len, 0, sizeof(int32_t) * 2, st));
+    FEPLL_CUDA(cudaMemsetAsync(p->rs.holes, 0, sizeof(int32_t) * p->v.K, st));
+  }
   if (n_total == 0) {
     if (leaf_counts) FEPLL_CUDA(cudaMemsetAsync(leaf_counts, 0, sizeof(int64_t) * p->v.K, st));
     return kOk;
@@ -550,7 +637,7 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
                         : select_level_ws(p, a, Z32, sq, guard, st))
                  : select_level_tc(p, a, Z32, sq, guard, st);
         if (prof) FEPLL_CUDA(cudaEventRecord(p->prof_ev[2 * p->prof_used++ + 1], st));
-        if (!rc) rc = rescore_queue_x(p, a, x, anchors, n_img, H, W, dc, sq, Z64, st);
+        if (!rc && !defer) rc = rescore_queue_x(p, a, x, anchors, n_img, H, W, dc, sq, Z64, st);
       } else {  // exact mode, or P > 128 (beyond the tcgen05 kernels' K atoms):
                 // FP64 scoring (wide nodes: block-wise scan) — the same labels
         select_level_fp64_kernel<<<grid_for(n_total, kSelWarps, 148 * 8), kSelWarps * 32, 0, st>>>(
@@ -560,10 +647,20 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
       }
       if (rc) return rc;
     }
+    if (defer) {
+      LevelArgs a = make_level(p, 0, t, labels);
+      verify_kernel<<<4 * kSMs, kSelWarps * 32, 0, st>>>(p->v, t, ps, sq, p->rs.vq, p->rs.vq_len, p->rs.vq_cap,
+                                                         p->rs.dq, p->rs.first_bad);
+      FEPLL_LAUNCH();
+      repair_kernel<<<kSMs, kSelWarps * 32, 0, st>>>(p->v, a, ps, sq, p->rs.dq, p->rs.vq_len, p->rs.first_bad,
+                                                     p->rs.pos_leaf, p->rs.holes, &p->rs.queue_len[kMaxDepth - 1]);
+      FEPLL_LAUNCH();
+    }
   }
   if (leaf_counts) {
     leaf_counts_kernel<<<(p->n_leaf_nodes + 127) / 128, 128, 0, st>>>(
-        p->d_leaf_nodes, p->n_leaf_nodes, p->v.leaf_index, p->rs.cnt, leaf_counts);
+        p->d_leaf_nodes, p->n_leaf_nodes, p->v.leaf_index, p->rs.cnt, defer ? p->rs.holes : nullptr,
+        leaf_counts);
     FEPLL_LAUNCH();
   }
   return kOk;

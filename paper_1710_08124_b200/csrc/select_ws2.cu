@@ -133,6 +133,12 @@ struct Args {
   double guard;
   int32_t* queue;
   int32_t* queue_len;
+  // deferred verification (vq != NULL): uncertified rows are routed by
+  // their tensor-core argmin like the certified ones and logged to vq
+  int4* vq;
+  int32_t* vq_len;
+  int64_t vq_cap;
+  int32_t* pos_leaf;
   int katoms;
   int prefetch;          // tiles ahead whose rows the loaders prefetch into L2 (0: off)
   uint64_t* trace;       // debug timeline: [CTA][64 tiles][16] clock64 stamps (or NULL)
@@ -584,8 +590,9 @@ select_level_ws2_kernel(PlanView pv, Args args) {
     const int bar_id = 1 + grp;
     const double guard = args.guard;
     // pending (previous tile's) route of this thread's row
-    bool p_valid = false;
-    int p_kind = 0, p_key = 0, p_lrank = 0, p_g = 0, p_u = 0, p_leaf = 0;
+    bool p_valid = false, p_fl = false;
+    int p_kind = 0, p_key = 0, p_lrank = 0, p_g = 0, p_u = 0, p_leaf = 0, p_lrank2 = 0, p_v = 0;
+    const bool defer = args.vq != nullptr;
     double p_sq = 0.0;
     int64_t p_b0 = 0;
     int res = 0, res_key = -1;  // this thread's in-flight global atomic (count reservation)
@@ -604,6 +611,12 @@ select_level_ws2_kernel(PlanView pv, Args args) {
       } else {
         a.leafseg[p_b0 + slot] = p_g;
         a.labels[p_g] = p_leaf;
+        if (defer) args.pos_leaf[p_g] = (int32_t)(p_b0 + slot);
+      }
+      if (p_fl) {  // deferred: the provisional decision, verified after the last level
+        const int64_t s2 = (int64_t)E.bbase[buf][kMaxChildren] + p_lrank2;
+        if (s2 < args.vq_cap) args.vq[s2] = make_int4(p_g, p_u, a.depth, p_v);
+        else atomicOr(&args.queue_len[kMaxDepth - 1], 1);  // overflow (host raises)
       }
     };
     TileCursor tcur;
@@ -635,13 +648,25 @@ select_level_ws2_kernel(PlanView pv, Args args) {
       if (res_key >= 0) E.bbase[pb][res_key] = res;
       if (etid <= kMaxChildren) E.bcnt[nb][etid] = 0;
       // warp-aggregated local ranks of this tile's rows per key
-      const int key = valid ? (flagged ? kMaxChildren : bi) : -1;
+      const int key = valid ? ((flagged && !defer) ? kMaxChildren : bi) : -1;
       const unsigned peers = __match_any_sync(0xffffffffu, key);
       const int leader = __ffs(peers) - 1;
       int wbase = 0;
       if (key >= 0 && lane == leader) wbase = atomicAdd(&E.bcnt[cb][key], __popc(peers));
       wbase = __shfl_sync(0xffffffffu, wbase, leader);
       const int lrank = wbase + __popc(peers & ((1u << lane) - 1u));
+      // deferred: the uncertified rows also take a verify-log slot
+      int lrank2 = 0;
+      if (defer) {
+        const unsigned fl = __ballot_sync(0xffffffffu, valid && flagged);
+        if (fl) {
+          const int fl_lead = __ffs(fl) - 1;
+          int b2 = 0;
+          if (lane == fl_lead) b2 = atomicAdd(&E.bcnt[cb][kMaxChildren], __popc(fl));
+          b2 = __shfl_sync(0xffffffffu, b2, fl_lead);
+          lrank2 = b2 + __popc(fl & ((1u << lane) - 1u));
+        }
+      }
       named_bar(bar_id, 128);  // counts of this tile complete, bases of the previous visible
       // reserve this tile's segment ranges (results used next iteration)
       res_key = -1;
@@ -649,16 +674,23 @@ select_level_ws2_kernel(PlanView pv, Args args) {
         res = atomicAdd(&a.cnt[E.ch.bfs[etid]], E.bcnt[cb][etid]);
         res_key = etid;
       } else if (etid == 127 && E.bcnt[cb][kMaxChildren] > 0) {
-        res = atomicAdd(&args.queue_len[a.depth], E.bcnt[cb][kMaxChildren]);
+        if (defer) {
+          res = atomicAdd(args.vq_len, E.bcnt[cb][kMaxChildren]);
+          atomicAdd(&args.queue_len[a.depth], E.bcnt[cb][kMaxChildren]);  // per-level statistics
+        } else {
+          res = atomicAdd(&args.queue_len[a.depth], E.bcnt[cb][kMaxChildren]);
+        }
         res_key = kMaxChildren;
       }
       // write the previous tile's rows
       flush(pb);
       // this tile's row becomes pending
       p_valid = valid;
+      p_fl = defer && valid && flagged;
       if (valid) {
         p_key = key;
         p_lrank = lrank;
+        p_lrank2 = lrank2;
         p_g = g;
         p_sq = sqv;
         p_u = u;
@@ -666,6 +698,7 @@ select_level_ws2_kernel(PlanView pv, Args args) {
           p_kind = 0;
         } else {
           const int v = E.ch.bfs[key];
+          p_v = v;
           p_b0 = s.lv.child_off[v - a.nxt_begin];
           p_kind = pv.child_count[v] > 0 ? 1 : 2;
           p_leaf = pv.leaf_index[v];
@@ -694,6 +727,7 @@ select_level_ws2_kernel(PlanView pv, Args args) {
 
 extern uint64_t* g_ws_trace;
 extern int g_ws_trace_level;
+bool deferred_verify(const Plan* p);
 uint64_t* g_level_spans = nullptr;  // fepll_debug_level_spans: [depth][CTA][4]
 
 int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
@@ -707,6 +741,10 @@ int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double
   args.guard = 2.0 * (guard > 0 ? guard : kDefaultGuard);
   args.queue = p->rs.queue;
   args.queue_len = p->rs.queue_len;
+  args.vq = deferred_verify(p) ? p->rs.vq : nullptr;
+  args.vq_len = p->rs.vq_len;
+  args.vq_cap = p->rs.vq_cap;
+  args.pos_leaf = p->rs.pos_leaf;
   args.katoms = (p->v.P + 31) / 32;
   args.prefetch = p->opt.l2_prefetch;
   args.trace = (a.depth == g_ws_trace_level) ? g_ws_trace : nullptr;

@@ -26,7 +26,7 @@ from typing import Sequence
 import numpy as np
 
 from . import _native as N
-from .errors import DataError, NumericalError
+from .errors import DataError, DeviceError, NumericalError
 from .gmm import score_flat_cost, wiener_flat_cost
 from .operators import CgConfig
 from .patches import SampleGrid, axis_anchors, jitter_rng, jittered_grid, philox_key, regular_grid
@@ -645,6 +645,8 @@ class Restorer:
             raise DataError("reprojection target has uncovered pixels")
         if s & 2:
             raise NumericalError("non-finite image estimate")
+        if int(self.rescored[:, 63].max()) != 0:  # csrc/select.cu deferred verification
+            raise DeviceError("deferred verification ran out of log or leaf-bucket slots")
         if not self.pixel_kind and self.A.kind == "decimate":
             finite = self.solve_info[:, :, 3].cpu().numpy()
             if np.any(finite == 0):
