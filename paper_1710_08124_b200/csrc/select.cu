@@ -242,6 +242,87 @@ verify_kernel(PlanView pv, int t, PatchSrc ps, const double* __restrict__ sq, co
   }
 }
 
+// Repair with a CTA per mis-routed patch: the FP64 descent is a chain of
+// one scoring per level, so each level's projection is split over the four
+// warps (warp w: group columns w*32 + lane, + 128) — two 32-row chunks of
+// G per level instead of eight 8-row ones — with the column chains, terms
+// and first-minimum of score_children_fp64 / block_argmin (bitwise the same
+// child).  Groups up to 256 columns and 32 children (every ws2 tree).
+constexpr int kRpWarps = 4;
+
+__global__ void __launch_bounds__(kRpWarps * 32)
+repair_cta_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restrict__ sq,
+                  const int2* __restrict__ dq, const int32_t* __restrict__ vq_len, int32_t* first_bad,
+                  const int32_t* __restrict__ pos_leaf, int32_t* holes, int32_t* flags) {
+  __shared__ double zs[kMaxP];
+  __shared__ double tv[256];
+  __shared__ int s_v;
+  const int lane = lane_id(), warp = warp_id();
+  const int total = vq_len[1];
+  const int P = pv.P;
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    const int2 e = dq[item];
+    const int g = e.x, d = e.y >> 24;
+    if (first_bad[g] != d) continue;  // CTA-uniform
+    int v = e.y & 0xFFFFFF;
+    if (warp == 0) load_patch(ps, g, P, zs);
+    const double sqv = sq[g];
+    __syncthreads();
+    while (pv.child_count[v] > 0) {
+      const int u = v;
+      const int width = pv.grp_width[u];
+      const int nk = pv.child_count[u];
+      const double* G = pv.grp_basis + pv.grp_off64[u];
+      const double* w = pv.grp_sqw + (int64_t)a.t * pv.grp_cols_total + pv.grp_col_off[u];
+      double acc[2] = {0.0, 0.0};
+      for (int p0 = 0; p0 < P; p0 += 32) {
+        double gr[32][2];
+#pragma unroll
+        for (int r = 0; r < 32; ++r)
+#pragma unroll
+          for (int cb = 0; cb < 2; ++cb) {
+            const int col = cb * 128 + warp * 32 + lane;
+            gr[r][cb] = (p0 + r < P && col < width) ? __ldg(G + (int64_t)(p0 + r) * width + col) : 0.0;
+          }
+#pragma unroll
+        for (int r = 0; r < 32; ++r)
+          if (p0 + r < P) {
+            const double zp = zs[p0 + r];
+            acc[0] = fma(zp, gr[r][0], acc[0]);
+            acc[1] = fma(zp, gr[r][1], acc[1]);
+          }
+      }
+#pragma unroll
+      for (int cb = 0; cb < 2; ++cb) {
+        const int col = cb * 128 + warp * 32 + lane;
+        if (col < width) tv[col] = acc[cb] * acc[cb] * w[col];
+      }
+      __syncthreads();
+      if (warp == 0) {
+        double b;
+        int bk;
+        block_argmin(pv, a.t, u, 0, nk, 0, tv, sqv, b, bk);
+        if (lane == 0) s_v = pv.child_list[pv.child_start[u] + bk];
+      }
+      __syncthreads();
+      v = s_v;
+    }
+    if (threadIdx.x == 0) {
+      a.leafseg[pos_leaf[g]] = -1;  // hole in the provisional bucket
+      atomicAdd(&holes[a.labels[g]], 1);
+      const int slot = atomicAdd(&a.cnt[v], 1);
+      if (slot < a.cnt[pv.parent[v]] + kLeafSlack) {  // the bucket's capacity (route.cuh)
+        a.leafseg[a.off[v] + slot] = g;
+        a.labels[g] = pv.leaf_index[v];
+      } else {
+        atomicOr(flags, 2);
+      }
+      first_bad[g] = 0x7f7f7f7f;
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(kSelWarps * 32, 4)
 repair_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restrict__ sq, const int2* __restrict__ dq,
               const int32_t* __restrict__ vq_len, int32_t* first_bad, const int32_t* __restrict__ pos_leaf,
@@ -652,8 +733,13 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
       verify_kernel<<<4 * kSMs, kSelWarps * 32, 0, st>>>(p->v, t, ps, sq, p->rs.vq, p->rs.vq_len, p->rs.vq_cap,
                                                          p->rs.dq, p->rs.first_bad);
       FEPLL_LAUNCH();
-      repair_kernel<<<kSMs, kSelWarps * 32, 0, st>>>(p->v, a, ps, sq, p->rs.dq, p->rs.vq_len, p->rs.first_bad,
-                                                     p->rs.pos_leaf, p->rs.holes, &p->rs.queue_len[kMaxDepth - 1]);
+      if (p->max_group_cols <= 256 && p->max_inner_children <= 32 && p->max_leaf_children <= 32)
+        repair_cta_kernel<<<2 * kSMs, kRpWarps * 32, 0, st>>>(p->v, a, ps, sq, p->rs.dq, p->rs.vq_len,
+                                                             p->rs.first_bad, p->rs.pos_leaf, p->rs.holes,
+                                                             &p->rs.queue_len[kMaxDepth - 1]);
+      else
+        repair_kernel<<<kSMs, kSelWarps * 32, 0, st>>>(p->v, a, ps, sq, p->rs.dq, p->rs.vq_len, p->rs.first_bad,
+                                                       p->rs.pos_leaf, p->rs.holes, &p->rs.queue_len[kMaxDepth - 1]);
       FEPLL_LAUNCH();
     }
   }
