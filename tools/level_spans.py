@@ -56,3 +56,10 @@ for d in levels:
         prev_end = r1
 print(f"levels {len(levels)}: sum of kernel spans {tot/1e3:.1f} us, first entry -> last end "
       f"{(prev_end)/1e3:.1f} us")
+# per-CTA work of the last level (CTAs own contiguous tile ranges in node order)
+d = levels[-1]
+e, p, x = (t[d, :, k] for k in range(3))
+wk = (x - p) / 1e3
+order = np.argsort(-wk)
+print("slowest CTAs of level", d, [(int(i), round(float(wk[i]), 1)) for i in order[:12]])
+print("work by CTA block of 16:", [round(float(np.mean(wk[i:i + 16])), 1) for i in range(0, 148, 16)])
