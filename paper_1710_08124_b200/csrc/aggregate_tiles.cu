@@ -18,6 +18,7 @@
 // i*P + dr*side inside an image's Zhat rows) and per cover entry the
 // segment-local offset slot*side + dcol (uint16), i.e. the same entries
 // re-addressed into the stage.  Every image of a batch shares the plan.
+#include <algorithm>
 #include <climits>
 
 #include "common.cuh"
@@ -149,17 +150,19 @@ aggregate_tiles_kernel(const ZT* __restrict__ Zhat, const double* __restrict__ d
                        int64_t zimg, int n_chunks, int batch, int H, int W, int r_begin,
                        const double* __restrict__ aty, const double* __restrict__ diag, double bs2,
                        int kind, double* __restrict__ x_out, double* __restrict__ xt_out,
-                       int32_t* status, int ipb) {
+                       int32_t* status, int ipb, int ns_alloc) {
   constexpr int kNS = kTileStages;
   constexpr int kVec = 16 / (int)sizeof(ZT);  // elements per 16-byte chunk
   extern __shared__ __align__(16) unsigned char ta_smem[];
   const int stage_bytes = stage_elems * (int)sizeof(ZT);
   const int dc_elems = kDc ? stage_dc : 0;  // doubles per stage (16-byte multiple)
-  double* dcs = reinterpret_cast<double*>(ta_smem + (size_t)kNS * stage_bytes);
+  // ns_alloc = min(images per CTA, kNS) stages are allocated (the slots a
+  // CTA's images cycle through)
+  double* dcs = reinterpret_cast<double*>(ta_smem + (size_t)ns_alloc * stage_bytes);
   // per stage: this tile's A^T y (and diagonal) values, one per thread
-  double* pxs = dcs + (size_t)kNS * dc_elems;
+  double* pxs = dcs + (size_t)ns_alloc * dc_elems;
   const int px_elems = diag ? 2 * kTileThreads : kTileThreads;
-  uint32_t* coff = reinterpret_cast<uint32_t*>(pxs + (size_t)kNS * px_elems);  // [n_chunk] byte offsets
+  uint32_t* coff = reinterpret_cast<uint32_t*>(pxs + (size_t)ns_alloc * px_elems);  // [n_chunk] byte offsets
   const int tile = blockIdx.x;
   const int rr = tile / n_chunks, j = tile - rr * n_chunks;
   const int c = j * kTileThreads + threadIdx.x;
@@ -273,11 +276,11 @@ aggregate_tiles_kernel(const ZT* __restrict__ Zhat, const double* __restrict__ d
 
 // dynamic shared memory of aggregate_tiles_kernel: NS stages of segments (+
 // dc) and of the pixels' A^T y (+ diagonal), and the chunk offsets
-static size_t tiles_smem_bytes(int max_seg, int side, int esize, bool with_dc, bool with_diag) {
+static size_t tiles_smem_bytes(int max_seg, int side, int esize, bool with_dc, bool with_diag,
+                               int ns = kTileStages) {
   const size_t seg_bytes = ((size_t)max_seg * side * esize + 15) / 16 * 16;
-  return (size_t)kTileStages * seg_bytes + (with_dc ? (size_t)kTileStages * ((max_seg + 1) & ~1) * 8 : 0) +
-         (size_t)kTileStages * (with_diag ? 2 : 1) * kTileThreads * 8 +
-         (size_t)max_seg * (side * esize / 16) * 4 + 16;
+  return (size_t)ns * seg_bytes + (with_dc ? (size_t)ns * ((max_seg + 1) & ~1) * 8 : 0) +
+         (size_t)ns * (with_diag ? 2 : 1) * kTileThreads * 8 + (size_t)max_seg * (side * esize / 16) * 4 + 16;
 }
 
 template <typename ZT>
@@ -301,12 +304,14 @@ static int aggregate_tiles_impl(const ZT* Zhat, const double* dc, int32_t n_loca
   FEPLL_REQUIRE(n_tiles < (int64_t(1) << 31), "aggregate_tiles: too many tiles");
   const int stage_elems = ((max_seg * side * (int)sizeof(ZT) + 15) / 16) * 16 / (int)sizeof(ZT);
   const int stage_dc = (max_seg + 1) & ~1;
-  const size_t smem = tiles_smem_bytes(max_seg, side, (int)sizeof(ZT), dc != nullptr, diag != nullptr);
-  FEPLL_REQUIRE(smem <= 227 * 1024, "aggregate_tiles: tile segments exceed shared memory");
   // image groups: enough CTAs to fill the GPU, at least 8 images per group
+  // (a single image: one CTA per tile, the latency hidden by resident CTAs)
   int groups = 1;
   while (n_tiles * groups < 4 * kSMs * 4 && batch / (groups * 2) >= 8) groups *= 2;
   const int ipb = (batch + groups - 1) / groups;
+  const int ns_alloc = std::min(ipb, kTileStages);
+  const size_t smem = tiles_smem_bytes(max_seg, side, (int)sizeof(ZT), dc != nullptr, diag != nullptr, ns_alloc);
+  FEPLL_REQUIRE(smem <= 227 * 1024, "aggregate_tiles: tile segments exceed shared memory");
   auto k = dc ? aggregate_tiles_kernel<ZT, true> : aggregate_tiles_kernel<ZT, false>;
   static bool attr_set[2] = {false, false};  // per instantiation; set before any graph capture
   if (!attr_set[dc ? 1 : 0]) {
@@ -316,7 +321,7 @@ static int aggregate_tiles_impl(const ZT* Zhat, const double* dc, int32_t n_loca
   dim3 grid((unsigned)n_tiles, (unsigned)((batch + ipb - 1) / ipb));
   k<<<grid, kTileThreads, smem, (cudaStream_t)stream>>>(
       Zhat, dc, n_local, P, ptr, cover16, seg_off, seg_cnt, seg_cap, stage_elems, stage_dc, side, (int64_t)zhat_rows * P, n_chunks,
-      batch, H, W, r_begin, aty, diag, bs2, kind, x_out, xtilde_out, status, ipb);
+      batch, H, W, r_begin, aty, diag, bs2, kind, x_out, xtilde_out, status, ipb, ns_alloc);
   FEPLL_LAUNCH();
   return kOk;
 }

@@ -346,9 +346,12 @@ class Restorer:
 
     def _tile_tables(self, t: int):
         """(seg_off, seg_cnt, cover16, seg_cap, max_seg) of iteration t's
-        cover lists for fepll_aggregate_tiles, or None (single images, the
-        candidate-search path, other variants, or a plan whose tiles do not
-        fit the tables — those keep fepll_aggregate_cover_ex)."""
+        cover lists for fepll_aggregate_tiles (batches: several images in
+        flight per CTA), or None (single images — one tile per CTA measured
+        1.8x slower than the per-pixel gather at 8192^2, its copies not
+        pipelined — the candidate-search path, other variants, or a plan
+        whose tiles do not fit the tables: those keep the cover-list
+        gather)."""
         if not (self._use_cover and self.batch > 1 and self._agg_variant == 2):
             return None
         torch = self.torch
