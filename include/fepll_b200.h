@@ -112,6 +112,9 @@ int fepll_plan_destroy(fepll_plan_t plan);
  *                             last level, mis-routed patches re-descended (1,
  *                             default), or re-scored after every level (0) —
  *                             the same labels, buckets and counts;
+ *   defer_test 0 | 1          test hook: the uncertified rows are routed
+ *                             provisionally to a wrong child, so the
+ *                             verification has to repair each of them (0);
  *   rescore_by_node 0 | 1     FP64 re-scoring grouped by tree node, the node's
  *                             group matrix staged in shared memory (measured
  *                             slower, default 0).
@@ -169,7 +172,9 @@ int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32
                  int32_t* labels, int64_t* leaf_counts, void* stream);
 
 /* diagnostics: per-level count of decisions the last tensor-mode select sent
- * to exact FP64 re-scoring; dst: device int32[64]. */
+ * to exact FP64 re-scoring (dst[0..61]), the patches the deferred
+ * verification re-descended (dst[62]) and its overflow flags (dst[63]);
+ * dst: device int32[64]. */
 int fepll_select_rescored(fepll_plan_t plan, int32_t* dst, void* stream);
 
 /* gmm.py:352-359 / solver.py:233-241: FP64 Wiener estimates of the patches

@@ -211,9 +211,9 @@ static int reserve(Plan* p, int64_t max_patches) {
   FEPLL_CUDA(cudaMalloc(&r.seg[1], sizeof(int32_t) * seg));
   FEPLL_CUDA(cudaMalloc(&r.segsq[0], sizeof(double) * std::max(seg, np)));
   FEPLL_CUDA(cudaMalloc(&r.segsq[1], sizeof(double) * seg));
-  // leaf buckets: capacity = the parent's count + kLeafSlack per leaf
-  // (route.cuh), room for patches re-routed by the deferred verification
-  FEPLL_CUDA(cudaMalloc(&r.leafseg, sizeof(int32_t) * (lseg + (int64_t)kLeafSlack * std::max(1, p->v.K))));
+  // leaf buckets: capacity = leaf_capacity(the parent's count) (route.cuh),
+  // room for patches re-routed by the deferred verification
+  FEPLL_CUDA(cudaMalloc(&r.leafseg, sizeof(int32_t) * (lseg + lseg / 4 + (int64_t)kLeafSlack * std::max(1, p->v.K))));
   r.queue_cap = std::max<int64_t>(1024, max_patches);
   FEPLL_CUDA(cudaMalloc(&r.queue, sizeof(int32_t) * 2 * r.queue_cap));
   // every patch can be logged once per level
@@ -291,6 +291,7 @@ static int* plan_option(Plan* p, const char* name) {
   if (n == "aggregate_variant") return &p->opt.aggregate_variant;
   if (n == "pdl") return &p->opt.pdl;
   if (n == "defer") return &p->opt.defer;
+  if (n == "defer_test") return &p->opt.defer_test;
   if (n == "wiener_split") return &p->opt.wiener_split;
   return nullptr;
 }

@@ -88,6 +88,7 @@ struct PlanOptions {
 
   int wiener_split = 0;      // Wiener warp pairs on 16 rows with m16n8k8 DMMAs (0: 8-row warps, m8n8k4)
   int pdl = 1;
+  int defer_test = 0;        // test hook: uncertified rows routed provisionally to a wrong child
   int defer = 1;             // deferred FP64 verification of uncertified ws2 decisions (0: re-score after every level)               // tree levels and re-scoring launched with programmatic dependent launch
   int aggregate_variant = 2; // batch reprojection kernel (host: 0/1 fepll_aggregate_cover_ex, 2 fepll_aggregate_tiles)
   int l2_prefetch = 0;     // ws2 loaders prefetch rows into L2 three tiles ahead of their cp.async: 1 per 128-B line, 2 one bulk prefetch per row (both measured slower: level 0.295 -> 0.324 / 0.486 ms)

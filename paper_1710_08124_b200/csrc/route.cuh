@@ -102,6 +102,10 @@ __device__ __forceinline__ T block_exscan(T* data, int n, uint64_t* tmp) {
 }
 
 // Every CTA: count/tile prefixes of level d and the offsets of level d+1.
+// capacity of a leaf bucket whose parent holds c patches: c plus spare
+// slots for patches the deferred verification re-routes into it
+__host__ __device__ __forceinline__ int leaf_capacity(int c) { return c + c / 4 + kLeafSlack; }
+
 template <class LT>
 __device__ inline void level_tables(const PlanView& pv, const LevelArgs& a, LT& s,
                                     int rows_per_tile) {
@@ -118,7 +122,7 @@ __device__ inline void level_tables(const PlanView& pv, const LevelArgs& a, LT& 
   for (int k = threadIdx.x; k < nn; k += blockDim.x) {
     const int v = a.nxt_begin + k;
     const uint64_t c = (uint64_t)(uint32_t)a.cnt[pv.parent[v]];
-    cap[k] = pv.child_count[v] > 0 ? c : ((c + kLeafSlack) << 32);
+    cap[k] = pv.child_count[v] > 0 ? c : ((uint64_t)leaf_capacity((int)c) << 32);
   }
   __syncthreads();
   const int32_t items = block_exscan(s.cpre, nd, s.scan_tmp);

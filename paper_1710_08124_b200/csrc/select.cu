@@ -216,8 +216,9 @@ rescore_node_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restr
 // patch (first_bad) is where its path first left the FP64 argmin path — all
 // its decisions before were certified or verified — so repair_kernel
 // re-descends it from the FP64 child in FP64, leaves a hole (-1) in the
-// provisional leaf bucket and appends it to the right one (kLeafSlack spare
-// slots per leaf; an error flag past them).  Labels, leaf buckets and
+// provisional leaf bucket and appends it to the right one (leaf buckets hold
+// a quarter of the parent's count + 32 spare slots, route.cuh
+// leaf_capacity; an error flag past them).  Labels, leaf buckets and
 // counts are those of re-scoring after every level.
 __global__ void __launch_bounds__(kSelWarps * 32, 4)
 verify_kernel(PlanView pv, int t, PatchSrc ps, const double* __restrict__ sq, const int4* __restrict__ vq,
@@ -311,7 +312,7 @@ repair_cta_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restric
       a.leafseg[pos_leaf[g]] = -1;  // hole in the provisional bucket
       atomicAdd(&holes[a.labels[g]], 1);
       const int slot = atomicAdd(&a.cnt[v], 1);
-      if (slot < a.cnt[pv.parent[v]] + kLeafSlack) {  // the bucket's capacity (route.cuh)
+      if (slot < leaf_capacity(a.cnt[pv.parent[v]])) {  // the bucket's capacity (route.cuh)
         a.leafseg[a.off[v] + slot] = g;
         a.labels[g] = pv.leaf_index[v];
       } else {
@@ -345,7 +346,7 @@ repair_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restrict__ 
       a.leafseg[pos_leaf[g]] = -1;  // hole in the provisional bucket
       atomicAdd(&holes[a.labels[g]], 1);
       const int slot = atomicAdd(&a.cnt[v], 1);
-      if (slot < a.cnt[pv.parent[v]] + kLeafSlack) {  // the bucket's capacity (route.cuh)
+      if (slot < leaf_capacity(a.cnt[pv.parent[v]])) {  // the bucket's capacity (route.cuh)
         a.leafseg[a.off[v] + slot] = g;
         a.labels[g] = pv.leaf_index[v];
       } else {
@@ -674,8 +675,8 @@ extern "C" int fepll_select(fepll_plan_t plan, int32_t t, const double* x, int32
   FEPLL_CUDA(cudaMemsetAsync(p->rs.cnt, 0, sizeof(int32_t) * p->v.n_nodes, st));
   FEPLL_CUDA(cudaMemsetAsync(p->rs.queue_len, 0, sizeof(int32_t) * kMaxDepth, st));
   const bool defer = mode == 1 && deferred_verify(p);
+  FEPLL_CUDA(cudaMemsetAsync(p->rs.vq_len, 0, sizeof(int32_t) * 2, st));
   if (defer) {
-    FEPLL_CUDA(cudaMemsetAsync(p->rs.vq_len, 0, sizeof(int32_t) * 2, st));
     FEPLL_CUDA(cudaMemsetAsync(p->rs.holes, 0, sizeof(int32_t) * p->v.K, st));
   }
   if (n_total == 0) {
@@ -759,7 +760,12 @@ extern "C" int fepll_wiener_reads_image(fepll_plan_t plan) {
 extern "C" int fepll_select_rescored(fepll_plan_t plan, int32_t* dst, void* stream) {
   Plan* p = reinterpret_cast<Plan*>(plan);
   FEPLL_REQUIRE(p != nullptr && dst != nullptr, "select_rescored: bad arguments");
-  FEPLL_CUDA(cudaMemcpyAsync(dst, p->rs.queue_len, sizeof(int32_t) * kMaxDepth,
+  FEPLL_CUDA(cudaMemcpyAsync(dst, p->rs.queue_len, sizeof(int32_t) * (kMaxDepth - 2),
+                             cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  // [62]: patches the deferred verification re-descended; [63]: its flags
+  FEPLL_CUDA(cudaMemcpyAsync(dst + kMaxDepth - 2, p->rs.vq_len + 1, sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                             (cudaStream_t)stream));
+  FEPLL_CUDA(cudaMemcpyAsync(dst + kMaxDepth - 1, p->rs.queue_len + kMaxDepth - 1, sizeof(int32_t),
                              cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
   return kOk;
 }

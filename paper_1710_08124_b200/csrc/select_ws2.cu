@@ -139,6 +139,7 @@ struct Args {
   int32_t* vq_len;
   int64_t vq_cap;
   int32_t* pos_leaf;
+  int perturb;           // test hook (plan option defer_test): uncertified rows take the next child
   int katoms;
   int prefetch;          // tiles ahead whose rows the loaders prefetch into L2 (0: off)
   uint64_t* trace;       // debug timeline: [CTA][64 tiles][16] clock64 stamps (or NULL)
@@ -639,7 +640,10 @@ select_level_ws2_kernel(PlanView pv, Args args) {
       tc::fence_after_sync();
       if (etid == 0) stamp(args, i, 4);
       bool flagged;
-      const int bi = epi_score_row(E.ch, nk, d_acc, sqv, guard, &flagged);
+      int bi = epi_score_row(E.ch, nk, d_acc, sqv, guard, &flagged);
+      // test hook: route the uncertified rows provisionally to a wrong child,
+      // so the verification must repair every one of them
+      if (defer && args.perturb && flagged && nk > 1) bi = bi + 1 < nk ? bi + 1 : 0;
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s.acc_empty[grp]);
@@ -745,6 +749,7 @@ int select_level_ws2(Plan* p, const LevelArgs& a, const float* Z32, const double
   args.vq_len = p->rs.vq_len;
   args.vq_cap = p->rs.vq_cap;
   args.pos_leaf = p->rs.pos_leaf;
+  args.perturb = p->opt.defer_test;
   args.katoms = (p->v.P + 31) / 32;
   args.prefetch = p->opt.l2_prefetch;
   args.trace = (a.depth == g_ws_trace_level) ? g_ws_trace : nullptr;

@@ -98,6 +98,7 @@ class SolverStats:
     lam: float = 0.0
     trace: list = field(default_factory=list)
     rescored: list = field(default_factory=list)   # FP64 re-scored decisions / iteration
+    repaired: list = field(default_factory=list)   # patches re-descended by the deferred verification
 
     @property
     def total_patches(self) -> int:
@@ -872,6 +873,7 @@ def restore_batch(ys, A, model, tree=None, config=None, *, mode: str = "tensor",
                             times=times[t] if t < len(times) else {})
         stats.iterations.append(it)
     stats.trace = recs
-    stats.rescored = [int(v) for v in r.rescored.sum(dim=1).cpu()]
+    stats.rescored = [int(v) for v in r.rescored[:, :62].sum(dim=1).cpu()]
+    stats.repaired = [int(v) for v in r.rescored[:, 62].cpu()]
     stats.total_seconds = time.perf_counter() - t0
     return x, stats

@@ -174,7 +174,7 @@ def _leaf_groups(tree):
     return out
 
 
-def _run_all(y, A, model, tree, s, use_tree=True, runs=None):
+def _run_all(y, A, model, tree, s, use_tree=True, runs=None, stats=None):
     from paper_1710_08124_b200 import RestorationConfig, restore
 
     cfg = RestorationConfig(sigma=20.0, spacing=s, seed=4, trace=True, use_tree=use_tree)
@@ -186,6 +186,8 @@ def _run_all(y, A, model, tree, s, use_tree=True, runs=None):
             np.testing.assert_array_equal(a["selected"], b["selected"],
                                           err_msg=f"{mode} {opts} iteration {t}")
         assert rmse255(x, xo) <= RMSE_TOL
+        if stats is not None:
+            stats.append((mode, opts, st))
     return so
 
 
@@ -198,7 +200,8 @@ def _image(H, seed):
 
 
 TENSOR_P64 = [("exact", {}), ("tensor", {"select_variant": 1}), ("tensor", {"select_variant": 0}),
-              ("tensor", {"select_variant": 2}), ("tensor", {"rescore_by_node": 1})]
+              ("tensor", {"select_variant": 2}), ("tensor", {"rescore_by_node": 1, "defer": 0}),
+              ("tensor", {"defer": 0})]
 
 
 def test_ties_duplicated_leaves_p64(models):
@@ -210,7 +213,13 @@ def test_ties_duplicated_leaves_p64(models):
     dm = _dup_model(model, parts[0])
     dt = tree_from_partitions(dm, parts)
     y, A = _image(128, 3)
-    so = _run_all(y, A, dm, dt, 4, runs=TENSOR_P64)
+    runs = []
+    so = _run_all(y, A, dm, dt, 4, runs=TENSOR_P64 + [("tensor", {"defer_test": 1})], stats=runs)
+    # with the test hook every uncertified decision is routed provisionally
+    # to a wrong child: the deferred verification re-descended those patches
+    # and they still landed on the FP64 labels (asserted in _run_all)
+    hooked = [st for mode, opts, st in runs if opts == {"defer_test": 1}][0]
+    assert sum(hooked.repaired) > 0
     # ties were hit: patches chose the first member of an exact-tie pair
     exact_pairs = [g for i, g in enumerate(parts[0]) if len(g) > 1 and OFFSETS[i % 4] == 0.0]
     firsts = {g[0] for g in exact_pairs}
