@@ -507,7 +507,7 @@ def test_kernel_variants_bitwise_equal(knob, values, models):
 
 
 @pytest.mark.parametrize("H,W,P,s,B", [(40, 300, 64, 4, 3), (64, 64, 64, 2, 5), (37, 530, 100, 4, 2),
-                                       (24, 256, 64, 8, 2), (33, 47, 64, 1, 2)])
+                                       (24, 256, 64, 8, 2), (33, 47, 64, 1, 2), (40, 300, 64, 4, 1)])
 def test_aggregate_tiles_bitwise(H, W, P, s, B):
     """fepll_aggregate_tiles (segments staged in shared memory) equals the
     cover-list gather bit for bit — FP64 and FP32 Zhat, with and without dc,
