@@ -107,7 +107,8 @@ int fepll_plan_destroy(fepll_plan_t plan);
  *   pdl 0 | 1                 tree-level and re-scoring kernels launched with
  *                             programmatic dependent launch: each one's prologue
  *                             overlaps its predecessor's tail (default 1);
- *   defer 0 | 1               (ws2 trees) uncertified decisions are routed by the
+ *   defer 0 | 1               (ws2 / select_tc trees, select_variant 1)
+ *                             uncertified decisions are routed by the
  *                             tensor-core argmin and verified in FP64 after the
  *                             last level, mis-routed patches re-descended (1,
  *                             default), or re-scored after every level (0) —

@@ -625,9 +625,13 @@ bool wiener_dmma_supported(const Plan* p);
 // every level runs the ws2 kernel (select_variant 1, no wide level): the
 // deferred verification covers the whole tree
 bool deferred_verify(const Plan* p) {
-  if (!p->opt.defer || p->opt.select_variant != 1 || p->v.tc_x == nullptr || p->v.P > 64) return false;
-  for (int d = 0; d < p->n_levels; ++d)
-    if (p->level_wide[d] || p->level_tc_npad[d] > 256 || !select_ws_supported(p, d)) return false;
+  // every level runs ws2 (select_variant 1, P <= 64) or select_tc (P <= 128,
+  // the levels ws does not support) — both log their uncertified rows
+  if (!p->opt.defer || p->opt.select_variant != 1 || p->v.P > 128) return false;
+  for (int d = 0; d < p->n_levels; ++d) {
+    if (p->level_wide[d] || p->level_tc_npad[d] > 256) return false;
+    if (select_ws_supported(p, d) && p->v.tc_x == nullptr) return false;  // would run the 3xTF32 ws kernel
+  }
   return true;
 }
 

@@ -39,6 +39,7 @@ struct TcSmemTables {
   int32_t rows[kTcRows];
   int32_t key[kTcRows];
   int32_t lrank[kTcRows];
+  int32_t lrank2[kTcRows];  // deferred verification: the row's log slot
   int32_t bcnt[kMaxChildren + 1];
   int32_t bbase[kMaxChildren + 1];
   uint64_t mma_bar[2];
@@ -54,6 +55,13 @@ struct TcArgs {
   double guard;
   int32_t* queue;
   int32_t* queue_len;  // [depth]
+  // deferred verification (vq != NULL, select.cu): uncertified rows are
+  // routed by the tensor-core argmin and logged
+  int4* vq;
+  int32_t* vq_len;
+  int64_t vq_cap;
+  int32_t* pos_leaf;
+  int perturb;         // test hook (plan option defer_test): uncertified rows take the next child
   int katoms;
   int bmax_rows;       // padded N of the stage buffers
 };
@@ -170,20 +178,29 @@ select_level_tc_kernel(PlanView pv, TcArgs args) {
     const double sqv = valid ? args.sq[my_patch] : 0.0;
     const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
     bool flagged;
-    const int bi = epi_score_row(s.ch, nk, lane_base, sqv, guard, &flagged);
+    int bi = epi_score_row(s.ch, nk, lane_base, sqv, guard, &flagged);
+    if (args.vq && args.perturb && flagged && nk > 1) bi = bi + 1 < nk ? bi + 1 : 0;  // test hook
     // ---- routing (aggregated per tile: one global atomic per child)
     tc::fence_before_sync();
     if (tid <= kMaxChildren) s.bcnt[tid] = 0;
     __syncthreads();
+    const bool defer = args.vq != nullptr;
     if (valid) {
-      const int key = flagged ? kMaxChildren : bi;
+      const int key = (flagged && !defer) ? kMaxChildren : bi;
       s.key[tid] = key;
       s.lrank[tid] = atomicAdd(&s.bcnt[key], 1);
+      if (defer && flagged) s.lrank2[tid] = atomicAdd(&s.bcnt[kMaxChildren], 1);
     }
     __syncthreads();
     if (tid < nk && s.bcnt[tid] > 0) s.bbase[tid] = atomicAdd(&a.cnt[s.ch.bfs[tid]], s.bcnt[tid]);
-    if (tid == kTcThreads - 1 && s.bcnt[kMaxChildren] > 0)
-      s.bbase[kMaxChildren] = atomicAdd(&args.queue_len[a.depth], s.bcnt[kMaxChildren]);
+    if (tid == kTcThreads - 1 && s.bcnt[kMaxChildren] > 0) {
+      if (defer) {
+        s.bbase[kMaxChildren] = atomicAdd(args.vq_len, s.bcnt[kMaxChildren]);
+        atomicAdd(&args.queue_len[a.depth], s.bcnt[kMaxChildren]);  // per-level statistics
+      } else {
+        s.bbase[kMaxChildren] = atomicAdd(&args.queue_len[a.depth], s.bcnt[kMaxChildren]);
+      }
+    }
     __syncthreads();
     if (valid) {
       const int key = s.key[tid];
@@ -199,6 +216,12 @@ select_level_tc_kernel(PlanView pv, TcArgs args) {
         } else {
           a.leafseg[b0 + slot] = my_patch;
           a.labels[my_patch] = pv.leaf_index[v];
+          if (defer) args.pos_leaf[my_patch] = (int32_t)(b0 + slot);
+        }
+        if (defer && flagged) {  // the provisional decision, verified after the last level
+          const int64_t s2 = (int64_t)s.bbase[kMaxChildren] + s.lrank2[tid];
+          if (s2 < args.vq_cap) args.vq[s2] = make_int4(my_patch, u, a.depth, v);
+          else atomicOr(&args.queue_len[kMaxDepth - 1], 1);
         }
       }
     }
@@ -213,6 +236,8 @@ static size_t tc_smem_bytes(int bmax_rows) {
   const size_t stage = 2 * (size_t)kAtomBytesA + 2 * (size_t)bmax_rows * 128;
   return 1024 + 2 * stage + sizeof(TcSmemTables);
 }
+
+bool deferred_verify(const Plan* p);
 
 int select_level_tc(Plan* p, const LevelArgs& a, const float* Z32, const double* sq, double guard,
                     cudaStream_t st) {
@@ -229,6 +254,11 @@ int select_level_tc(Plan* p, const LevelArgs& a, const float* Z32, const double*
   args.guard = guard > 0 ? guard : kDefaultGuard;
   args.queue = p->rs.queue;
   args.queue_len = p->rs.queue_len;
+  args.vq = deferred_verify(p) ? p->rs.vq : nullptr;
+  args.vq_len = p->rs.vq_len;
+  args.vq_cap = p->rs.vq_cap;
+  args.pos_leaf = p->rs.pos_leaf;
+  args.perturb = p->opt.defer_test;
   args.katoms = ppad / 32;
   args.bmax_rows = bmax;
   const size_t smem = tc_smem_bytes(bmax);

@@ -241,7 +241,8 @@ def test_ties_duplicated_root_subtree_p64(models):
 
 
 def test_ties_duplicated_leaves_p100(models):
-    """P = 100: the streaming-K tcgen05 kernel (select_tc.cu) + re-scoring."""
+    """P = 100: the streaming-K tcgen05 kernel (select_tc.cu) + deferred
+    verification (and per-level re-scoring, and the wrong-child test hook)."""
     from paper_1710_08124_b200.tree import tree_from_partitions, tree_partitions
 
     model, tree = models[100]
@@ -249,7 +250,10 @@ def test_ties_duplicated_leaves_p100(models):
     dm = _dup_model(model, parts[0])
     dt = tree_from_partitions(dm, parts)
     y, A = _image(120, 7)
-    _run_all(y, A, dm, dt, 6, runs=[("exact", {}), ("tensor", {})])
+    runs = []
+    _run_all(y, A, dm, dt, 6, runs=[("exact", {}), ("tensor", {}), ("tensor", {"defer": 0}),
+                                    ("tensor", {"defer_test": 1})], stats=runs)
+    assert sum(runs[-1][2].repaired) > 0  # deferred verification repaired the hooked decisions
 
 
 def test_ties_duplicated_components_no_tree(models):
