@@ -257,14 +257,19 @@ repair_cta_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restric
                   const int32_t* __restrict__ pos_leaf, int32_t* holes, int32_t* flags) {
   __shared__ double zs[kMaxP];
   __shared__ double tv[256];
-  __shared__ int s_v;
+  __shared__ int s_v, s_go;
   const int lane = lane_id(), warp = warp_id();
   const int total = vq_len[1];
   const int P = pv.P;
   for (int item = blockIdx.x; item < total; item += gridDim.x) {
     const int2 e = dq[item];
     const int g = e.x, d = e.y >> 24;
-    if (first_bad[g] != d) continue;  // CTA-uniform
+    // thread 0's read decides for the CTA (another CTA may reset first_bad[g])
+    if (threadIdx.x == 0) s_go = first_bad[g] == d;
+    __syncthreads();
+    const bool go = s_go;
+    __syncthreads();
+    if (!go) continue;
     int v = e.y & 0xFFFFFF;
     if (warp == 0) load_patch(ps, g, P, zs);
     const double sqv = sq[g];
@@ -337,7 +342,9 @@ repair_kernel(PlanView pv, LevelArgs a, PatchSrc ps, const double* __restrict__ 
   for (int item = blockIdx.x * kSelWarps + warp_id(); item < total; item += gridDim.x * kSelWarps) {
     const int2 e = dq[item];
     const int g = e.x, d = e.y >> 24;
-    if (first_bad[g] != d) continue;  // a later entry of a patch already off the FP64 path
+    // a later entry of a patch already off the FP64 path; lane 0's read
+    // decides for the warp (another warp may reset first_bad[g] meanwhile)
+    if (__shfl_sync(0xffffffffu, first_bad[g], 0) != d) continue;
     int v = e.y & 0xFFFFFF;
     load_patch(ps, g, pv.P, zs);
     const double sqv = sq[g];
