@@ -91,6 +91,10 @@ int fepll_plan_destroy(fepll_plan_t plan);
  *                             DMMAs, C crossing through shared memory (1), or
  *                             8-row warps with m8n8k4 (0, default: measured
  *                             2 % faster) — bitwise the same;
+ *   wiener_tc 0 | 1           fepll_wiener_f32 runs on tcgen05 with 3xTF32 products
+ *                             (wiener_tc.cu; P % 16 == 0, P <= 64, ranks <= 64)
+ *                             instead of the FP64 DMMA kernel — NOT bitwise the
+ *                             same: ~1e-6 relative on the estimates;
  *   wiener_xw 0 | 1           Wiener reads 8x8 windows of x instead of Z64 (0);
  *   wiener_add_dc 0 | 1       fepll_wiener writes est + dc (1) or the bare
  *                             estimates (0: the trace's `estimates`; pass dc
@@ -199,7 +203,9 @@ int fepll_wiener(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32
 /* FP32-state mode (opt-in, Restorer(precision="fp32-state")): the Wiener
  * kernel reads the FP32 patch rows of fepll_extract (z32_pitch floats per
  * row, 16-byte aligned) and writes est + dc rounded once to FP32; the
- * arithmetic in between is the FP64 DMMA of fepll_wiener. */
+ * arithmetic in between is the FP64 DMMA of fepll_wiener, or — plan option
+ * wiener_tc — three kind::tf32 tcgen05 passes per product with FP32
+ * accumulation (HBM-bound instead of FP64-pipe-bound). */
 int fepll_wiener_f32(fepll_plan_t plan, int32_t t, const double* x, int32_t H, int32_t W,
                      const int32_t* anchors, int32_t n_img, const double* dc, const float* Z32,
                      int32_t z32_pitch, int64_t n_total, float* Zhat, int32_t zhat_rows, void* stream);

@@ -33,6 +33,8 @@ static int upload(Plan* p, const T* src, int64_t count, const T** dst) {
     if (_rc) return _rc;                                     \
   } while (0)
 
+int wiener_tc_prepare(Plan* p);  // wiener_tc.cu
+
 static int create(const fepll_plan_desc* d, Plan** out) {
   FEPLL_REQUIRE(d != nullptr && out != nullptr, "null plan descriptor");
   FEPLL_REQUIRE(d->patch_dim > 0 && d->patch_dim <= kMaxP, "patch_dim out of range (1..256)");
@@ -175,6 +177,10 @@ static int create(const fepll_plan_desc* d, Plan** out) {
   FEPLL_CUDA(cudaMalloc(&m, sizeof(int32_t) * std::max(1, p->v.K)));
   p->owned.push_back(m);
   p->rs.holes = static_cast<int32_t*>(m);
+  {
+    const int rc = wiener_tc_prepare(p);
+    if (rc) return rc;
+  }
   *out = p;
   return kOk;
 }
@@ -293,6 +299,7 @@ static int* plan_option(Plan* p, const char* name) {
   if (n == "defer") return &p->opt.defer;
   if (n == "defer_test") return &p->opt.defer_test;
   if (n == "wiener_split") return &p->opt.wiener_split;
+  if (n == "wiener_tc") return &p->opt.wiener_tc;
   return nullptr;
 }
 

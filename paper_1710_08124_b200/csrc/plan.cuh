@@ -86,6 +86,7 @@ struct PlanOptions {
                            // smem once per CTA) — measured slower (select 11.3 -> 13.1 ms/step at 64 x 1024^2:
                            // one 208 KB CTA per SM leaves 8 warps for latency-bound chains), off
 
+  int wiener_tc = 0;         // fepll_wiener_f32 on tcgen05 (3xTF32, wiener_tc.cu) when the shape allows; 0: FP64 DMMA
   int wiener_split = 0;      // Wiener warp pairs on 16 rows with m16n8k8 DMMAs (0: 8-row warps, m8n8k4)
   int pdl = 1;
   int defer_test = 0;        // test hook: uncertified rows routed provisionally to a wrong child
@@ -116,6 +117,7 @@ struct Plan {
   int32_t* d_leaf_nodes = nullptr;   // BFS ids of the leaves, ascending
   int n_leaf_nodes = 0;
   RouteScratch rs;
+  uint8_t* wtc_img = nullptr;        // tcgen05 Wiener basis images (wiener_tc.cu), owned
   int last_n_total = 0;
   // optional timing of the level kernels (fepll_plan_profile): event pairs
   std::vector<cudaEvent_t> prof_ev;

@@ -627,6 +627,9 @@ int wiener_dmma_f32(Plan* p, int t, const float* Z32, int z32_pitch, const doubl
                     int n_img, int zrows, const double* x, const int32_t* anchors, int H, int W,
                     cudaStream_t st);
 bool wiener_xw_supported(const Plan* p);
+bool wiener_tc_supported(const Plan* p);
+int wiener_tc_f32(Plan* p, int t, const float* Z32, int z32_pitch, const double* dc, float* Zhat, int n_img,
+                  int zrows, cudaStream_t st);
 bool wiener_dmma_supported(const Plan* p);
 
 // every level runs the ws2 kernel (select_variant 1, no wide level): the
@@ -851,5 +854,7 @@ extern "C" int fepll_wiener_f32(fepll_plan_t plan, int32_t t, const double* x, i
         n_total, p->rs.leafseg, p->rs.cnt, p->rs.off, p->rs.leaf_base, (int32_t*)nullptr, -1);
     FEPLL_LAUNCH();
   }
+  if (p->opt.wiener_tc && wiener_tc_supported(p) && z32_pitch == (p->v.P + 31) / 32 * 32)
+    return wiener_tc_f32(p, t, Z32, z32_pitch, dc, Zhat, n_img, zhat_rows, st);
   return wiener_dmma_f32(p, t, Z32, z32_pitch, dc, Zhat, n_img, zhat_rows, x, anchors, H, W, st);
 }

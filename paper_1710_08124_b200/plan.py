@@ -325,7 +325,8 @@ class DevicePlan:
         self.reserved = 0
 
     OPTIONS = ("select_variant", "seg_sq", "wiener_pair", "wiener_rw", "wiener_xw", "wiener_add_dc",
-               "l2_prefetch", "rescore_by_node", "aggregate_variant")
+               "l2_prefetch", "rescore_by_node", "aggregate_variant", "wiener_split", "wiener_tc", "pdl",
+               "defer", "defer_test")
 
     def set_option(self, name: str, value: int) -> None:
         """Per-plan kernel choice (include/fepll_b200.h fepll_plan_set_option)."""

@@ -24,27 +24,33 @@ def psnr(x, ref):
     return 10 * np.log10(1.0 / float(np.mean((np.clip(x, 0, 1) - ref) ** 2)))
 
 
+# the FP32-state Wiener step: FP64 DMMA arithmetic (0) or 3xTF32 on tcgen05 (1)
+WIENER = pytest.mark.parametrize("wtc", [0, 1], ids=["dmma", "tcgen05"])
+
+
+@WIENER
 @pytest.mark.parametrize("name", ["cfg1", "regular48", "gain64", "inpaint96", "deblur96", "sr96", "notree64"])
-def test_fp32_state_golden(name, models):
+def test_fp32_state_golden(name, wtc, models):
     from paper_1710_08124_b200 import RestorationConfig, restore
 
     g, A, y, s8, s, P = golden_inputs(name)
     model, tree = models[P]
     cfg = RestorationConfig(sigma=s8, spacing=s, seed=0, trace=True, sampling=g["meta"]["sampling"],
                             use_tree=bool(g["meta"]["use_tree"]))
-    x, st = restore(y, A, model, tree, cfg, precision="fp32-state")
+    x, st = restore(y, A, model, tree, cfg, precision="fp32-state", options={"wiener_tc": wtc})
     agree = [float(np.mean(rec["selected"] == g["labels"][t])) for t, rec in enumerate(st.trace)]
     assert min(agree) >= LABELS, agree
     assert rmse255(x, g["x"]) <= 1e-3
 
 
-def test_fp32_state_cfg2_full_size(models):
+@WIENER
+def test_fp32_state_cfg2_full_size(wtc, models):
     from paper_1710_08124_b200 import RestorationConfig, restore, synthetic
 
     c = synthetic.baseline_case("cfg2")
     model, tree = models[64]
     cfg = RestorationConfig(sigma=c.sigma8, spacing=c.spacing, seed=0, trace=True)
-    x, st = restore(c.y, c.A, model, tree, cfg, precision="fp32-state")
+    x, st = restore(c.y, c.A, model, tree, cfg, precision="fp32-state", options={"wiener_tc": wtc})
     xo, so = O.restore(c.y, c.A, model, tree, sigma=c.sigma8, spacing=c.spacing, seed=0, trace=True)
     agree = [float(np.mean(a["selected"] == b["selected"])) for a, b in zip(st.trace, so.trace)]
     assert min(agree) >= LABELS, agree
@@ -52,7 +58,8 @@ def test_fp32_state_cfg2_full_size(models):
     assert abs(psnr(x, c.clean) - psnr(xo, c.clean)) <= 0.01
 
 
-def test_fp32_state_cfg5_batch(models):
+@WIENER
+def test_fp32_state_cfg5_batch(wtc, models):
     """4 of the 64 cfg5 images, inside the 64-image fp32-state batch; the
     HostPipeline (bench e2e path) gives the same images."""
     import torch
@@ -65,7 +72,8 @@ def test_fp32_state_cfg5_batch(models):
     A = cases[0].A
     model, tree = models[64]
     cfg = RestorationConfig(sigma=spec["sigma"], spacing=spec["spacing"], seed=0)
-    r = Restorer(A, model, tree, cfg, batch=B, precision="fp32-state")
+    opts = {"wiener_tc": wtc}
+    r = Restorer(A, model, tree, cfg, batch=B, precision="fp32-state", options=opts)
     pick = [0, 21, 42, 63]
     labels = []
     r.start(torch.from_numpy(ys).cuda())
@@ -74,7 +82,7 @@ def test_fp32_state_cfg5_batch(models):
         labels.append(r.labels.view(B, r.n)[pick].cpu().numpy())
     x = r.x.cpu().numpy()
     r.check_status()
-    hp = HostPipeline(A, model, tree, cfg, batch=B, lam=r.lam, precision="fp32-state")
+    hp = HostPipeline(A, model, tree, cfg, batch=B, lam=r.lam, precision="fp32-state", options=opts)
     pin_in = torch.from_numpy(ys.astype(np.float32)).pin_memory()
     pin_out = torch.empty(ys.shape, dtype=torch.float32).pin_memory()
     hp.run(pin_in, pin_out)
@@ -87,3 +95,38 @@ def test_fp32_state_cfg5_batch(models):
         assert min(agree) >= LABELS, (i, agree)
         assert rmse255(x[i], xo) <= 1e-3
         assert abs(psnr(x[i], cases[i].clean) - psnr(xo, cases[i].clean)) <= 0.01
+
+
+@pytest.mark.parametrize("P,K,rho,size,B,use_tree", [(64, 200, 0.95, 144, 3, True), (16, 12, 0.9, 64, 2, False),
+                                                     (16, 6, 1.0, 48, 1, False), (64, 9, 0.999, 96, 2, False)])
+def test_wiener_tc_matches_dmma(P, K, rho, size, B, use_tree, models):
+    """Kernel level: the tcgen05 3xTF32 Wiener step against the FP64 DMMA one
+    on the same patches and leaf buckets (iteration 0 of an fp32-state
+    restore) — ranks 30 (R = 32), 7 and 16 at P = 16, and 50+ (R = 64, two
+    K atoms in the second product).  Estimates agree to 2e-6 of the patch
+    scale (3xTF32: ~2^-20 per product), far inside the 1e-3 / 255 image bar."""
+    import torch
+    from paper_1710_08124_b200 import RestorationConfig, Restorer, synthetic
+
+    if use_tree:
+        model, tree = models[P]
+    else:
+        model, tree = synthetic.synthetic_gmm(K, P, 3, rho), None
+    cases = [synthetic.baseline_case("cfg1", size, image_seed=i, noise_seed=40 + i) for i in range(B)]
+    y = torch.from_numpy(np.stack([c.y for c in cases])).cuda()
+    cfg = RestorationConfig(sigma=20.0, spacing=2 if P == 16 else 4, seed=4, use_tree=use_tree)
+    out = []
+    for wtc in (0, 1):
+        r = Restorer(cases[0].A, model, tree, cfg, batch=B, precision="fp32-state", options={"wiener_tc": wtc})
+        r.start(y)
+        r.iterate(0)
+        torch.cuda.synchronize()
+        r.check_status()
+        rows = r.Zhat.view(B, r.zhat_rows, P)[:, :r.n].cpu().numpy().astype(np.float64)
+        out.append((rows, r.labels.cpu().numpy().copy(), r.x.cpu().numpy().copy()))
+        del r
+    np.testing.assert_array_equal(out[0][1], out[1][1])
+    scale = float(np.abs(out[0][0]).max())
+    err = float(np.abs(out[0][0] - out[1][0]).max())
+    assert err <= 2e-6 * max(scale, 1.0), (err, scale)
+    assert rmse255(out[0][2], out[1][2]) <= 1e-4

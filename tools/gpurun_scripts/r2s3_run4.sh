@@ -1,0 +1,4 @@
+timeout 600 python -m pytest tests/test_gpu_fp32_state.py -m gpu -x -q -k "wiener_tc_matches" > gpurun_out/s3_t4.log 2>&1
+timeout 600 python tools/wtc_prof.py 64 > gpurun_out/s3_wtc_prof.log 2>&1
+timeout 300 python bench.py --precision fp32-state --no-cpu-baseline --option wiener_tc=1 > gpurun_out/s3_fp32_tc.json 2> gpurun_out/s3_fp32_tc.err
+timeout 900 python -m pytest tests/test_gpu_fp32_state.py -m gpu -q > gpurun_out/s3_t4b.log 2>&1
