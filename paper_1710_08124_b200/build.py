@@ -57,7 +57,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if (not force and obj.exists() and obj.stat().st_mtime > src.stat().st_mtime
                 and obj.stat().st_mtime > newest_header):
             return obj  # object is current
-        cmd = [cc, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+        # FEPLL_WTC_PROF=1: the tcgen05 Wiener kernel's wait-time counters (tools/wtc_prof.py)
+        extra = ["-DFEPLL_WTC_PROF"] if os.environ.get("FEPLL_WTC_PROF") else []
+        cmd = [cc, *ARCH, *FLAGS, *extra, "-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stderr}")

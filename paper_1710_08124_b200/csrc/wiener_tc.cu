@@ -20,21 +20,23 @@
 // FP32 row in, P x sizeof(OT) out per patch.
 //
 // One CTA per SM walks a contiguous range of 128-patch tiles in leaf order.
-// Warp roles (21 warps):
+// Warp roles (22 warps):
 //   0-3   loaders: the tile's FP32 rows by cp.async into one of NS 32 KB
 //         stages, K-major 128B-swizzled (the layout tcgen05 reads); row
 //         indices arrive a few tiles earlier in a ring;
 //   4-7   converters: z_lo = z - trunc_tf32(z) into tensor memory (the
 //         tensor core truncates FP32 operands to TF32, tools/
 //         tf32_trunc_test.cu, so the raw row is z_hi as is);
-//   8     MMA issuer; also rebuilds the leaf's basis images (U_k as the B
-//         operand of both products, hi = rna_tf32, lo = u - hi) when the
-//         leaf changes (2-3 times per CTA per launch);
+//   8     first product issuer (the leaf's basis image arrives by one TMA
+//         bulk copy when the leaf changes, 2-3 times per CTA per launch);
+//   21    second product issuer (its own warp: a tile's second product
+//         goes out as soon as its W is ready);
 //   9-12  first epilogue: C (TMEM) * shrink -> W, W_lo = W - trunc(W), both
 //         back into tensor memory as the second product's A operand;
 //   13-20 second epilogue, two groups (one per TMEM set): Zhat = acc +
 //         gamma_tail z (z from the raw stage) + dc, staged per warp in
-//         shared memory and written as whole 256-byte row pieces.
+//         shared memory and written as whole 256-byte row pieces (one TMA
+//         bulk store per piece measured the same: 2.69 vs 2.64 ms/step).
 // Tensor memory, two sets of 256 columns: [0,64) z_lo then W_lo, [64,128) C
 // ([Z b_hi | Z b_lo] halves at rank <= 32) then W (in place), [128,256) the
 // Zhat accumulator halves [W b_hi | W b_lo].
@@ -50,17 +52,23 @@ namespace fepll {
 namespace wtc {
 
 constexpr int kRows = 128;
-constexpr int kLoaderWarps = 4;
+constexpr int kLoaderWarps = 4;                  // 32 rows each (two measured slower: the loaders became the limit)
+constexpr int kLoaderRows = kRows / kLoaderWarps;
+constexpr int kLoaderQ = kLoaderRows / 4;        // rows per lane (4 rows per instruction)
 constexpr int kLoaderThreads = 32 * kLoaderWarps;
 constexpr int kConvWarp0 = kLoaderWarps;
 constexpr int kMmaWarp = kConvWarp0 + 4;
 constexpr int kEp1Warp0 = kMmaWarp + 1;
 constexpr int kEp2Warp0 = kEp1Warp0 + 4;
-constexpr int kThreads = (kEp2Warp0 + 8) * 32;  // 672
+constexpr int kMma2Warp = kEp2Warp0 + 8;        // second product issuer
+constexpr int kThreads = (kMma2Warp + 1) * 32;  // 704 (79 registers, no spills)
 constexpr int kAtomA = kRows * 128;              // bytes of one K atom of a row stage
 constexpr int kStageBytes = 2 * kAtomA;          // P <= 64: two K atoms
 constexpr int kMaxR = 64;
-constexpr int kOutPitch = 256 + 16;              // staged output piece per row (+16: conflict-free 16-byte stores)
+template <class OT>
+constexpr int unit_cols() { return 256 / (int)sizeof(OT); }  // columns per staged 256-byte output piece
+template <class OT>
+constexpr int out_pitch() { return 256 + 16; }  // +16: conflict-free 16-byte stores
 constexpr int kIdxAhead = 4;
 constexpr int kSwitchCost = 3;                   // tiles' worth of time a leaf switch costs (CTA split)
 constexpr int kMaxStages = 4;
@@ -80,7 +88,7 @@ struct Smem {
   float shrink[kMaxR];               // first epilogue: the current leaf's gamma - gamma_tail
   uint64_t raw_full[kMaxStages], stage_free[kMaxStages];
   uint64_t lo_full[2], c_full[2], w_full[2], out_full[2], out_empty[2];
-  uint64_t drain, b_full;
+  uint64_t drain, b_full, drain2, b2_full;
   uint32_t tmem_base;
   int32_t t_begin, t_end;
 };
@@ -115,6 +123,7 @@ __device__ __forceinline__ float trunc_tf32(float x) {
 // debug profile (fepll_debug_wtc_prof): [CTA][32] cycles spent in each role's
 // waits, accumulated by the role's first lane
 __device__ uint64_t* g_prof = nullptr;
+#ifdef FEPLL_WTC_PROF
 struct Prof {
   uint64_t* out;
   bool on;
@@ -136,6 +145,19 @@ struct Prof {
       for (int k = 0; k < n; ++k) out[(size_t)blockIdx.x * 32 + slot0 + k] = acc[k];
   }
 };
+#else
+// compiled out by default (build with -DFEPLL_WTC_PROF, tools/wtc_prof.py): the
+// counters cost the epilogue roles registers
+struct Prof {
+  static constexpr bool on = false;
+  uint64_t* out = nullptr;
+  uint64_t acc[4] = {0, 0, 0, 0};
+  __device__ __forceinline__ Prof(bool) {}
+  __device__ __forceinline__ uint64_t now() const { return 0; }
+  __device__ __forceinline__ void add(int, uint64_t) {}
+  __device__ __forceinline__ void flush(int, int) {}
+};
+#endif
 
 // tile -> leaf (index into the leaf tables); tiles ascend
 struct LeafCursor {
@@ -155,6 +177,8 @@ __global__ void __launch_bounds__(kThreads, 1) wiener_tc_kernel(PlanView pv, Arg
   uint8_t* stageA = base;
   uint8_t* bbuf = base + NS * kStageBytes;           // B1 (a.bq1 bytes), B2 (a.bq2 bytes)
   uint8_t* outbuf = bbuf + a.bq1 + a.bq2;            // [8 warps][32 rows][kOutPitch]
+  constexpr int kOutPitch = out_pitch<OT>();
+  constexpr int kUnitCols = unit_cols<OT>();
   Smem& s = *reinterpret_cast<Smem*>(outbuf + 8 * 32 * kOutPitch);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nl = a.n_leaf_nodes;
@@ -175,6 +199,8 @@ __global__ void __launch_bounds__(kThreads, 1) wiener_tc_kernel(PlanView pv, Arg
     }
     tc::mbar_init(&s.drain, 1);
     tc::mbar_init(&s.b_full, 1);
+    tc::mbar_init(&s.drain2, 1);
+    tc::mbar_init(&s.b2_full, 1);
     tc::fence_mbar_init();
   }
   for (int k = tid; k < nl; k += kThreads) {
@@ -222,16 +248,19 @@ __global__ void __launch_bounds__(kThreads, 1) wiener_tc_kernel(PlanView pv, Arg
 
   if (warp < kLoaderWarps) {
     // ------------------------------------------------------------ loaders
-    const int r0 = 32 * warp;
+    const int r0 = kLoaderRows * warp;
     LeafCursor cur;
     auto issue_idx = [&](int j) {
       if (j < ntile) {
         const int li = cur.at(s, nl, t_begin + j);
         const int first = (t_begin + j - s.tpre[li]) * kRows;
         int32_t* ring = s.idx_ring[j % kIdxRing];
-        const int row = r0 + lane;
-        if (row < s.leaf_cnt[li] - first) tc::cp_async4(ring + row, a.leafseg + s.leaf_off[li] + first + row);
-        else ring[row] = -1;
+#pragma unroll
+        for (int h = 0; h < kLoaderRows / 32; ++h) {
+          const int row = r0 + 32 * h + lane;
+          if (row < s.leaf_cnt[li] - first) tc::cp_async4(ring + row, a.leafseg + s.leaf_off[li] + first + row);
+          else ring[row] = -1;
+        }
       }
     };
     const int c16 = lane & 7;
@@ -249,16 +278,16 @@ __global__ void __launch_bounds__(kThreads, 1) wiener_tc_kernel(PlanView pv, Arg
       tc::cp_async_wait<kIdxAhead - 1>();  // idx(i) landed (one group per tile)
       __syncwarp();
       const int32_t* rg = s.idx_ring[i % kIdxRing] + r0;
-      int g[8];
+      int g[kLoaderQ];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) g[q] = rg[4 * q + (lane >> 3)];
+      for (int q = 0; q < kLoaderQ; ++q) g[q] = rg[4 * q + (lane >> 3)];
       uint8_t* stg = stageA + st * kStageBytes + (r0 >> 3) * 1024;
 #pragma unroll
       for (int ka = 0; ka < 2; ++ka) {
         if (ka < a.katoms) {
           const float* zb = a.Z32 + ka * 32 + 4 * c16;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
+          for (int q = 0; q < kLoaderQ; ++q) {
             const int r = 4 * q + (lane >> 3);
             uint8_t* dst = stg + ka * kAtomA + (r >> 3) * 1024 + (r & 7) * 128 + ((c16 ^ (r & 7)) << 4);
             // holes and rows past the bucket's end land as zeros (no bytes read)
@@ -317,57 +346,23 @@ __global__ void __launch_bounds__(kThreads, 1) wiener_tc_kernel(PlanView pv, Arg
     pf.add(2, tl0);
     pf.flush(2, 3);  // [2] raw_full wait, [3] out_full wait, [4] converter loop total
   } else if (warp == kMmaWarp) {
-    // ------------------------------------------------------------ MMA issuer
+    // ------------------------------------------------------------ first product issuer
     // The whole warp runs this loop (uniform values); one elected lane
-    // issues each tcgen05 instruction (tc.cuh *_warp).  The pass loops are
-    // unrolled at compile time so the issue sequence is branch-free.
+    // issues each tcgen05 instruction (tc.cuh *_warp).
     const uint64_t a_base = tc::desc_sw128(tc::smem_u32(stageA));
     const uint64_t d_b1 = tc::desc_sw128(tc::smem_u32(bbuf));
-    const uint64_t d_b2 = d_b1 + (uint64_t)(a.bq1 >> 4);
     LeafCursor cur;
     int cur_leaf = -1, R = 16;
     uint32_t drains = 0, b_loads = 0;
     Prof pf(lane == 0);
     Prof pf2(lane == 0);
     const uint64_t tl0 = pf.now();
-    const uint32_t idesc2w = tc::idesc_tf32(kRows, 2 * P), idesc2 = tc::idesc_tf32(kRows, P);
-    // second product of tile j (K = R): Out[0,2P) = W [B2_hi; B2_lo], Out[0,P) += W_lo B2_hi
-    auto gemm2 = [&](int j) {
-      const int set = j & 1;
-      uint64_t tw = pf.now();
-      tc::mbar_wait(&s.w_full[set], (j >> 1) & 1);
-      pf.add(2, tw);
-      tw = pf.now();
-      if (j >= 2) tc::mbar_wait(&s.out_empty[set], ((j - 2) >> 1) & 1);
-      pf.add(3, tw);
-      tc::fence_after_sync();
-      const uint64_t tg = pf2.now();
-      const uint32_t d = tmem + set * kSetCols + kColOut;
-      const uint32_t w_hi = tmem + set * kSetCols + kColC, w_lo = tmem + set * kSetCols + kColLo;
-      const int kpairs = R >> 4;  // R is a multiple of 16: two K steps per trip
-#pragma unroll
-      for (int pass = 0; pass < 2; ++pass) {
-        const uint32_t aw = pass == 1 ? w_lo : w_hi;
-        const uint32_t id = pass == 1 ? idesc2 : idesc2w;
-        for (int kp = 0; kp < kpairs; ++kp) {
-          // K steps 2 kp, 2 kp + 1: atom kp / 2 (32 columns, 2P rows), 32-byte steps inside
-          const uint64_t bo = (uint64_t)(((kp >> 1) * 2 * P * 128 + (kp & 1) * 64) >> 4);
-          tc::mma_tf32_tmemA_warp(d, aw + 16 * kp, d_b2 + bo, id, (pass > 0 || kp > 0) ? 1u : 0u);
-          tc::mma_tf32_tmemA_warp(d, aw + 16 * kp + 8, d_b2 + bo + 2, id, 1u);
-        }
-      }
-      tc::mma_commit_warp(&s.out_full[set]);
-      pf2.add(3, tg);
-    };
-    int g2_next = 0;  // next tile whose second product is to be issued
     for (int i = 0; i < ntile; ++i) {
       const int st = i % NS, set = i & 1;
       const int li = cur.at(s, nl, t_begin + i);
       if (li != cur_leaf) {
         const uint64_t tb = pf2.now();
-        // the previous tiles' second products still read the old images
-        while (g2_next < i) gemm2(g2_next++);
-        if (i > 0) {
+        if (i > 0) {  // the previous tiles' first products still read the old image
           tc::mma_commit_warp(&s.drain);
           tc::mbar_wait(&s.drain, drains & 1);
           ++drains;
@@ -375,9 +370,8 @@ __global__ void __launch_bounds__(kThreads, 1) wiener_tc_kernel(PlanView pv, Arg
         const int comp = s.leaf_cr[li] & 0xFFFF, r = s.leaf_cr[li] >> 16;
         R = max(16, (r + 15) & ~15);
         if (lane == 0) {
-          const uint32_t nb = (uint32_t)(a.bq1 + a.bq2);
-          tc::mbar_arrive_expect_tx(&s.b_full, nb);
-          tc::bulk_g2s(bbuf, a.img + (size_t)comp * nb, nb, &s.b_full);
+          tc::mbar_arrive_expect_tx(&s.b_full, (uint32_t)a.bq1);
+          tc::bulk_g2s(bbuf, a.img + (size_t)comp * (a.bq1 + a.bq2), (uint32_t)a.bq1, &s.b_full);
         }
         __syncwarp();
         tc::mbar_wait(&s.b_full, b_loads & 1);
@@ -385,13 +379,14 @@ __global__ void __launch_bounds__(kThreads, 1) wiener_tc_kernel(PlanView pv, Arg
         cur_leaf = li;
         pf2.add(0, tb);
       }
-      // first product of tile i: C = Z B1_hi + Z_lo B1_hi + Z B1_lo  (K = 32 katoms)
+      // first product of tile i (K = 32 katoms): C = Z [B1_hi; B1_lo], C[0,R) += Z_lo B1_hi.
+      // The passes that read Z from the raw stage start as soon as the rows
+      // land and the set's C columns are free (tile i - 2's second product has
+      // read W there); the Z_lo pass follows once the converters are done.
       uint64_t tw = pf.now();
       tc::mbar_wait(&s.raw_full[st], (i / NS) & 1);
+      if (i >= 2) tc::mbar_wait(&s.out_full[set], ((i - 2) >> 1) & 1);
       pf.add(0, tw);
-      tw = pf.now();
-      tc::mbar_wait(&s.lo_full[set], (i >> 1) & 1);
-      pf.add(1, tw);
       tc::fence_after_sync();
       tc::fence_proxy_async_smem();
       {
@@ -426,6 +421,10 @@ __global__ void __launch_bounds__(kThreads, 1) wiener_tc_kernel(PlanView pv, Arg
           }
         }
         // Z_lo (TMEM) . B1_hi
+        tw = pf.now();
+        tc::mbar_wait(&s.lo_full[set], (i >> 1) & 1);
+        pf.add(1, tw);
+        tc::fence_after_sync();
         for (int kq = 0; kq < a.katoms; ++kq) {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
@@ -434,16 +433,73 @@ __global__ void __launch_bounds__(kThreads, 1) wiener_tc_kernel(PlanView pv, Arg
         tc::mma_commit_warp(&s.c_full[set]);
         pf2.add(2, tg);
       }
-      // the previous tile's second product (its first epilogue ran meanwhile)
-      while (g2_next < i) gemm2(g2_next++);
     }
-    while (g2_next < ntile) gemm2(g2_next++);
     pf2.add(1, tl0);
-    pf.flush(5, 4);   // [5] raw_full, [6] lo_full, [7] w_full, [8] out_empty waits
-    pf2.flush(9, 2);  // [9] leaf switches (flush + drain + image load), [10] issuer loop total
-    if (pf2.on) {
-      pf2.out[(size_t)blockIdx.x * 32 + 21] = pf2.acc[2];  // first product issue
-      pf2.out[(size_t)blockIdx.x * 32 + 22] = pf2.acc[3];  // second product issue
+    pf.flush(5, 2);   // [5] raw_full, [6] lo_full waits
+    pf2.flush(9, 2);  // [9] leaf switches (drain + image load), [10] issuer loop total
+    if (pf2.on) pf2.out[(size_t)blockIdx.x * 32 + 21] = pf2.acc[2];  // first product issue
+  } else if (warp == kMma2Warp) {
+    // ------------------------------------------------------------ second product issuer
+    // its own warp: tile i's second product goes out as soon as the first
+    // epilogue hands W over, not behind tile i + 1's first product
+    const uint64_t d_b2 = tc::desc_sw128(tc::smem_u32(bbuf + a.bq1));
+    const uint32_t idesc2w = tc::idesc_tf32(kRows, 2 * P), idesc2 = tc::idesc_tf32(kRows, P);
+    LeafCursor cur;
+    int cur_leaf = -1, R = 16;
+    uint32_t drains = 0, b_loads = 0;
+    Prof pf(lane == 0);
+    const uint64_t tl0 = pf.now();
+    for (int j = 0; j < ntile; ++j) {
+      const int set = j & 1;
+      const int li = cur.at(s, nl, t_begin + j);
+      if (li != cur_leaf) {
+        if (j > 0) {
+          tc::mma_commit_warp(&s.drain2);
+          tc::mbar_wait(&s.drain2, drains & 1);
+          ++drains;
+        }
+        const int comp = s.leaf_cr[li] & 0xFFFF, r = s.leaf_cr[li] >> 16;
+        R = max(16, (r + 15) & ~15);
+        if (lane == 0) {
+          tc::mbar_arrive_expect_tx(&s.b2_full, (uint32_t)a.bq2);
+          tc::bulk_g2s(bbuf + a.bq1, a.img + (size_t)comp * (a.bq1 + a.bq2) + a.bq1, (uint32_t)a.bq2, &s.b2_full);
+        }
+        __syncwarp();
+        tc::mbar_wait(&s.b2_full, b_loads & 1);
+        ++b_loads;
+        cur_leaf = li;
+      }
+      // second product of tile j (K = R): Out[0,2P) = W [B2_hi; B2_lo], Out[0,P) += W_lo B2_hi
+      uint64_t tw = pf.now();
+      tc::mbar_wait(&s.w_full[set], (j >> 1) & 1);
+      pf.add(0, tw);
+      tw = pf.now();
+      if (j >= 2) tc::mbar_wait(&s.out_empty[set], ((j - 2) >> 1) & 1);
+      pf.add(1, tw);
+      tc::fence_after_sync();
+      const uint64_t tg = pf.now();
+      const uint32_t d = tmem + set * kSetCols + kColOut;
+      const uint32_t w_hi = tmem + set * kSetCols + kColC, w_lo = tmem + set * kSetCols + kColLo;
+      const int kpairs = R >> 4;  // R is a multiple of 16: two K steps per trip
+#pragma unroll
+      for (int pass = 0; pass < 2; ++pass) {
+        const uint32_t aw = pass == 1 ? w_lo : w_hi;
+        const uint32_t id = pass == 1 ? idesc2 : idesc2w;
+        for (int kp = 0; kp < kpairs; ++kp) {
+          // K steps 2 kp, 2 kp + 1: atom kp / 2 (32 columns, 2P rows), 32-byte steps inside
+          const uint64_t bo = (uint64_t)(((kp >> 1) * 2 * P * 128 + (kp & 1) * 64) >> 4);
+          tc::mma_tf32_tmemA_warp(d, aw + 16 * kp, d_b2 + bo, id, (pass > 0 || kp > 0) ? 1u : 0u);
+          tc::mma_tf32_tmemA_warp(d, aw + 16 * kp + 8, d_b2 + bo + 2, id, 1u);
+        }
+      }
+      tc::mma_commit_warp(&s.out_full[set]);
+      pf.add(2, tg);
+    }
+    pf.add(3, tl0);
+    pf.flush(7, 2);  // [7] w_full, [8] out_empty waits
+    if (pf.on) {
+      pf.out[(size_t)blockIdx.x * 32 + 22] = pf.acc[2];  // second product issue
+      pf.out[(size_t)blockIdx.x * 32 + 23] = pf.acc[3];  // its loop total
     }
   } else if (warp < kEp2Warp0) {
     // ------------------------------------------------------------ first epilogue
@@ -472,14 +528,15 @@ __global__ void __launch_bounds__(kThreads, 1) wiener_tc_kernel(PlanView pv, Arg
       tc::fence_after_sync();
       const uint32_t cb = tmem + lane_off + set * kSetCols + kColC;
       const uint32_t lb = tmem + lane_off + set * kSetCols + kColLo;
+      const bool wide = R <= 32;
       for (int c = 0; c < R; c += 16) {
         uint32_t w[16], wl[16];
         tmem_ld16(cb + c, w);
-        if (R <= 32) tmem_ld16(cb + R + c, wl);  // the Z B1_lo half
+        if (wide) tmem_ld16(cb + R + c, wl);  // the Z B1_lo half
         tc::tmem_ld_wait();
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-          const float cv = R <= 32 ? __uint_as_float(w[k]) + __uint_as_float(wl[k]) : __uint_as_float(w[k]);
+          const float cv = wide ? __uint_as_float(w[k]) + __uint_as_float(wl[k]) : __uint_as_float(w[k]);
           const float v = cv * s.shrink[c + k];
           w[k] = __float_as_uint(v);  // read as trunc_tf32(v) by the tensor core
           wl[k] = __float_as_uint(v - trunc_tf32(v));
@@ -504,7 +561,6 @@ __global__ void __launch_bounds__(kThreads, 1) wiener_tc_kernel(PlanView pv, Arg
     const uint32_t d_acc = tmem + ((uint32_t)(32 * quarter) << 16) + grp * kSetCols + kColOut;
     uint8_t* ob = outbuf + ew * 32 * kOutPitch;  // this warp's 32 staged row pieces
     uint8_t* orow_s = ob + lane * kOutPitch;
-    constexpr int kUnitCols = 256 / (int)sizeof(OT);  // columns per staged piece
     OT* Zhat = static_cast<OT*>(a.Zhat);
     LeafCursor cur;
     Prof pf((ew & 3) == 0 && lane == 0);
@@ -570,12 +626,13 @@ __global__ void __launch_bounds__(kThreads, 1) wiener_tc_kernel(PlanView pv, Arg
           mbar_arrive(&s.out_empty[grp]);
           mbar_arrive(&s.stage_free[st]);
         }
-        // write the warp's 32 row pieces: half a warp per row, 16 bytes per lane
         const int ubytes = ucols * (int)sizeof(OT);
-        const int hl = lane & 15;
+        // write the warp's 32 row pieces: kLpr lanes cover a piece (16 bytes each), 32 / kLpr rows per instruction
+        constexpr int kLpr = kUnitCols * (int)sizeof(OT) / 16;
+        const int hl = lane % kLpr;
 #pragma unroll 4
-        for (int rr = 0; rr < 32; rr += 2) {
-          const int lr = rr + (lane >> 4);
+        for (int rr = 0; rr < 32; rr += 32 / kLpr) {
+          const int lr = rr + lane / kLpr;
           const int gg = ring[32 * quarter + lr];
           if (gg >= 0 && hl * 16 < ubytes) {
             const int64_t orow =
@@ -691,7 +748,7 @@ static int wiener_tc_t(Plan* p, int t, const float* Z32, int z32_pitch, const do
   FEPLL_CUDA(cudaGetDevice(&dev));
   FEPLL_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   auto smem_for = [&](int ns) {
-    return 1024 + (size_t)ns * wtc::kStageBytes + (size_t)(a.bq1 + a.bq2) + 8 * 32 * wtc::kOutPitch + sizeof(wtc::Smem);
+    return 1024 + (size_t)ns * wtc::kStageBytes + (size_t)(a.bq1 + a.bq2) + 8 * 32 * wtc::out_pitch<OT>() + sizeof(wtc::Smem);
   };
   a.ns = smem_for(4) <= (size_t)optin ? 4 : smem_for(3) <= (size_t)optin ? 3 : 2;
   const size_t smem = smem_for(a.ns);

@@ -1,5 +1,7 @@
 """Where the tcgen05 Wiener kernel waits: per-role wait cycles summed over a
-launch (fepll_debug_wtc_prof), averaged over the CTAs, in microseconds."""
+launch (fepll_debug_wtc_prof), averaged over the CTAs, in microseconds.
+Needs the library built with the counters: FEPLL_WTC_PROF=1 python -m
+paper_1710_08124_b200.build --force (they are compiled out by default)."""
 import ctypes
 import os
 import sys
@@ -20,8 +22,8 @@ r.run(y)
 buf = torch.zeros(148 * 32, dtype=torch.int64, device="cuda")
 fn = N.lib().fepll_debug_wtc_prof
 fn.argtypes = [ctypes.c_void_p]
-fn(buf.data_ptr())
 r.start(y)
+fn(buf.data_ptr())
 r.iterate(0)
 torch.cuda.synchronize()
 fn(None)
@@ -31,6 +33,6 @@ names = ["loader: stage_free wait", "loader: loop total", "conv: raw_full wait",
          "mma: out_empty wait", "mma: leaf switches", "mma: loop total", "ep1: c_full wait", "ep1: loop total",
          "ep2a: raw_full wait", "ep2a: out_full wait", "ep2a: compute", "ep2a: loop total",
          "ep2b: raw_full wait", "ep2b: out_full wait", "ep2b: compute", "ep2b: loop total",
-         "mma: first product issue", "mma: second product issue"]
+         "mma: first product issue", "mma: second product issue", "mma2: loop total"]
 for k, nm in enumerate(names):
     print(f"{nm:28s} mean {p[:, k].mean():9.1f} us   min {p[:, k].min():9.1f}   max {p[:, k].max():9.1f}")
