@@ -265,6 +265,8 @@ class Restorer:
                                        device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.rescored = torch.zeros((config.iterations, 64), dtype=torch.int32, device=dev)
+        self._ts = None        # torch stream of the current run (event marks)
+        self._wcost = None     # per-component Wiener cost (counters)
         self.x = torch.empty((B, H, W), dtype=f64, device=dev)
         self._y_in = None  # identity restores: the observation, read in place
         self._force_z64 = False
@@ -400,7 +402,8 @@ class Restorer:
     def start(self, y_dev, timer: dict | None = None) -> None:
         """x0 (solver.py:195-198) for a device-resident observation batch."""
         torch = self.torch
-        st = torch.cuda.current_stream(self.device).cuda_stream
+        self._ts = torch.cuda.current_stream(self.device)
+        st = self._ts.cuda_stream
         A = self.A
         self.status.zero_()
         self._mark(timer, "start")
@@ -430,7 +433,9 @@ class Restorer:
         (`pkg/src/fepll/solver.py:258-266`): beta, grid (a SampleGrid),
         patches, dc, selected, estimates (the bare Wiener estimates, without
         dc), x_tilde — each with a leading batch axis — plus x."""
-        st = self.torch.cuda.current_stream(self.device).cuda_stream
+        ts = self.torch.cuda.current_stream(self.device) if timer is None or self._ts is None else self._ts
+        self._ts = ts
+        st = ts.cuda_stream
         self._want_xt = trace
         if not trace:
             self._iteration(t, st, timer)
@@ -485,7 +490,13 @@ class Restorer:
         if timer is None:
             return
         ev = self.torch.cuda.Event(enable_timing=True)
-        ev.record()
+        # the stream object is looked up once per run (start()): torch's
+        # current_stream() costs ~15 us a call, 27 marks per restore
+        ts = self._ts
+        if ts is None:
+            ev.record()
+        else:
+            ev.record(ts)
         timer.setdefault("_marks", []).append((name, ev))
 
     def _iteration(self, t: int, st, timer=None) -> None:
@@ -580,10 +591,20 @@ class Restorer:
         counts as "gap", so the phases add up to the run's span."""
         out: dict = {}
         marks = timer.get("_marks", [])
-        for (n0, e0), (n1, e1) in zip(marks, marks[1:]):
+        for ((n0, e0), (n1, e1)), ms in zip(zip(marks, marks[1:]), Restorer._mark_ms(timer)):
             key = "gap" if n1 == "start" else n1
-            out[key] = out.get(key, 0.0) + e0.elapsed_time(e1)
+            out[key] = out.get(key, 0.0) + ms
         return out
+
+    @staticmethod
+    def _mark_ms(timer: dict) -> list:
+        """Milliseconds between consecutive marks (read once per timer)."""
+        marks = timer.get("_marks", [])
+        ms = timer.get("_ms")
+        if ms is None or len(ms) != max(0, len(marks) - 1):
+            ms = [e0.elapsed_time(e1) for (_, e0), (_, e1) in zip(marks, marks[1:])]
+            timer["_ms"] = ms
+        return ms
 
     @classmethod
     def iteration_times(cls, timer: dict) -> list:
@@ -596,7 +617,7 @@ class Restorer:
         out = []
         marks = timer.get("_marks", [])
         cur = None
-        for (n0, e0), (n1, e1) in zip(marks, marks[1:]):
+        for ((n0, e0), (n1, e1)), ms in zip(zip(marks, marks[1:]), cls._mark_ms(timer)):
             if n1 == "start":
                 continue
             if n1 == "extract":
@@ -604,7 +625,7 @@ class Restorer:
                 out.append(cur)
             if cur is None or n1 not in cls.PHASE_NAMES:
                 continue
-            cur[cls.PHASE_NAMES[n1]] = e0.elapsed_time(e1) / 1e3
+            cur[cls.PHASE_NAMES[n1]] = ms / 1e3
         return out
 
     # ---------------------------------------------------------------- graphs
@@ -635,7 +656,9 @@ class Restorer:
         from the label histograms (every leaf has one root path)."""
         hist = self.leaf_counts.cpu().numpy()
         P = self.P
-        wcost = np.array([wiener_flat_cost(c.kept_basis.shape[1], P) for c in self.model.components])
+        if self._wcost is None:
+            self._wcost = np.array([wiener_flat_cost(c.kept_basis.shape[1], P) for c in self.model.components])
+        wcost = self._wcost
         out = []
         for t in range(hist.shape[0]):
             h = hist[t]
@@ -643,13 +666,14 @@ class Restorer:
                         int(h @ wcost)))
         return out
 
-    def check_status(self, t_last: int | None = None):
+    def check_status(self, t_last: int | None = None, rescored_host=None):
         s = int(self.status.item())
         if s & 1:
             raise DataError("reprojection target has uncovered pixels")
         if s & 2:
             raise NumericalError("non-finite image estimate")
-        if int(self.rescored[:, 63].max()) != 0:  # csrc/select.cu deferred verification
+        rs = self.rescored.cpu().numpy() if rescored_host is None else rescored_host
+        if int(rs[:, 63].max()) != 0:  # csrc/select.cu deferred verification
             raise DeviceError("deferred verification ran out of log or leaf-bucket slots")
         if not self.pixel_kind and self.A.kind == "decimate":
             finite = self.solve_info[:, :, 3].cpu().numpy()
@@ -859,7 +883,8 @@ def restore_batch(ys, A, model, tree=None, config=None, *, mode: str = "tensor",
     timer: dict = {}
     x_dev, recs = r.run(y_dev, trace=config.trace, timer=timer)
     x = x_dev.cpu().numpy()
-    r.check_status()
+    rescored = r.rescored.cpu().numpy()
+    r.check_status(rescored_host=rescored)
     stats = SolverStats(lam=r.lam)
     phases = Restorer.phase_times(timer)
     stats.init_seconds = (t1 - t0) + phases.get("init", 0.0) / 1e3
@@ -873,7 +898,7 @@ def restore_batch(ys, A, model, tree=None, config=None, *, mode: str = "tensor",
                             times=times[t] if t < len(times) else {})
         stats.iterations.append(it)
     stats.trace = recs
-    stats.rescored = [int(v) for v in r.rescored[:, :62].sum(dim=1).cpu()]
-    stats.repaired = [int(v) for v in r.rescored[:, 62].cpu()]
+    stats.rescored = [int(v) for v in rescored[:, :62].sum(axis=1)]
+    stats.repaired = [int(v) for v in rescored[:, 62]]
     stats.total_seconds = time.perf_counter() - t0
     return x, stats
