@@ -369,6 +369,12 @@ int fepll_debug_ws_trace(void* device_buffer, int32_t level);
  * 2*depth (+1) (atomic min / max: initialise to ~0 / 0); NULL: off */
 int fepll_debug_level_spans(void* device_buffer);
 
+/* Stream-ordered device timestamp: *dst = %globaltimer (nanoseconds) when the
+ * stream reaches this point.  A one-thread kernel, so it can be captured in
+ * a CUDA graph: restore() replays a captured restore and still fills
+ * IterationStats.times (pkg/src/fepll/solver.py:206-254) per call. */
+int fepll_stamp(uint64_t* dst, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -75,6 +75,7 @@ _SIGS = {
     "fepll_tiles_seg_cap": (i32, [i32, i32, i32]),
     "fepll_tiles_width": (i32, []),
     "fepll_debug_level_spans": (i32, [vp]),
+    "fepll_stamp": (i32, [vp, vp]),
     "fepll_tiles_smem_bytes": (i64, [i32, i32, i32, i32, i32]),
     "fepll_tiles_build": (i32, [vp, vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
     "fepll_aggregate_tiles": (i32, [vp, vp, vp, i32, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32,

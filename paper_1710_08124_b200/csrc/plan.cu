@@ -327,6 +327,21 @@ int fepll_plan_get_option(fepll_plan_t plan, const char* name, int64_t* value) {
   return fepll::kOk;
 }
 
+namespace {
+__global__ void stamp_kernel(uint64_t* dst) {
+  uint64_t g;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+  *dst = g;
+}
+}  // namespace
+
+int fepll_stamp(uint64_t* dst, void* stream) {
+  FEPLL_REQUIRE(dst != nullptr, "stamp: bad arguments");
+  stamp_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(dst);
+  FEPLL_LAUNCH();
+  return fepll::kOk;
+}
+
 int fepll_plan_destroy(fepll_plan_t plan) {
   Plan* p = reinterpret_cast<Plan*>(plan);
   if (!p) return fepll::kOk;

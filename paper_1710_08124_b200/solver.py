@@ -266,6 +266,8 @@ class Restorer:
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.rescored = torch.zeros((config.iterations, 64), dtype=torch.int32, device=dev)
         self._ts = None        # torch stream of the current run (event marks)
+        self._tg_graph = None  # timed CUDA graph of restore() (capture_timed)
+        self.use_graph = True  # restore() replays a captured graph when the plan is cached
         self._wcost = None     # per-component Wiener cost (counters)
         self.x = torch.empty((B, H, W), dtype=f64, device=dev)
         self._y_in = None  # identity restores: the observation, read in place
@@ -489,6 +491,15 @@ class Restorer:
     def _mark(self, timer, name):
         if timer is None:
             return
+        stamps = timer.get("_stamps")
+        if stamps is not None:
+            # graph capture (capture_timed): a device timestamp kernel per mark
+            names = timer.setdefault("_names", [])
+            if len(names) >= stamps.numel():
+                raise DeviceError("timestamp buffer too small for this restore")
+            N.call("fepll_stamp", stamps.data_ptr() + 8 * len(names), self._ts.cuda_stream)
+            names.append(name)
+            return
         ev = self.torch.cuda.Event(enable_timing=True)
         # the stream object is looked up once per run (start()): torch's
         # current_stream() costs ~15 us a call, 27 marks per restore
@@ -650,6 +661,39 @@ class Restorer:
     def replay(self):
         self.graph.replay()
         return self.x
+
+    def capture_timed(self):
+        """As :meth:`capture` on an observation buffer owned by the restorer,
+        with a device timestamp (``fepll_stamp``) at every phase mark, so a
+        replay still yields the per-phase times of that call."""
+        torch = self.torch
+        self._tg_y = torch.zeros((self.batch,) + tuple(self.A.output_dims), dtype=torch.float64,
+                                 device=self.device)
+        self._tg_stamps = torch.zeros(16 + 8 * len(self.betas), dtype=torch.int64, device=self.device)
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):  # warm-up off the capture (lazy allocations)
+            self.run(self._tg_y)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        timer = {"_stamps": self._tg_stamps}
+        self._tg_graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self._tg_graph):
+            self.run(self._tg_y, timer=timer)
+        self._tg_names = list(timer["_names"])
+
+    def run_timed_graph(self, ys_host):
+        """Upload ``ys_host`` (B, Ho, Wo float64 numpy), replay the timed
+        graph and return (x on the device, timer) — the timer carries the
+        phase names and the milliseconds between consecutive marks, the form
+        :meth:`phase_times` / :meth:`iteration_times` read."""
+        torch = self.torch
+        if getattr(self, "_tg_graph", None) is None:
+            self.capture_timed()
+        self._tg_y.copy_(torch.from_numpy(ys_host))
+        self._tg_graph.replay()
+        st = self._tg_stamps[:len(self._tg_names)].cpu().numpy()
+        ms = [float(b - a) / 1e6 for a, b in zip(st[:-1], st[1:])]
+        return self.x, {"_marks": [(n, None) for n in self._tg_names], "_ms": ms}
 
     def counters(self):
         """(patches, evals, selection mults, estimation mults) per iteration
@@ -878,10 +922,17 @@ def restore_batch(ys, A, model, tree=None, config=None, *, mode: str = "tensor",
     if r.batch != ys.shape[0]:
         raise DataError(f"restorer batch {r.batch} != {ys.shape[0]} observations")
     torch = r.torch
-    y_dev = torch.from_numpy(np.ascontiguousarray(ys)).to(r.device)
-    t1 = time.perf_counter()
-    timer: dict = {}
-    x_dev, recs = r.run(y_dev, trace=config.trace, timer=timer)
+    if restorer is None and not config.trace and r.strip is None and r.use_graph:
+        # cached plan, no trace: one CUDA-graph replay of the whole restore
+        # (device timestamps keep IterationStats.times per call)
+        t1 = time.perf_counter()
+        x_dev, timer = r.run_timed_graph(np.ascontiguousarray(ys))
+        recs = []
+    else:
+        y_dev = torch.from_numpy(np.ascontiguousarray(ys)).to(r.device)
+        t1 = time.perf_counter()
+        timer = {}
+        x_dev, recs = r.run(y_dev, trace=config.trace, timer=timer)
     x = x_dev.cpu().numpy()
     rescored = r.rescored.cpu().numpy()
     r.check_status(rescored_host=rescored)
