@@ -171,8 +171,8 @@ extract_pow2_kernel(const double* __restrict__ x, int batch, int H, int W,
 // store each — hence the alignment rule of paired_stores_ok().  No
 // shared memory, no barriers: a few dozen instructions per patch (a staged
 // shared-memory tile kernel measured several hundred, round 1).
-template <int SIDE, int U>
-__global__ void __launch_bounds__(256)
+template <int SIDE, int U, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB)
 extract_cols_kernel(const double* __restrict__ x, int batch, int H, int W,
                     const int32_t* __restrict__ anchors, int n, double* __restrict__ Z64,
                     float* __restrict__ Z32, int z32_pitch, double* __restrict__ dc_out,
@@ -284,7 +284,12 @@ extern "C" int fepll_extract(const double* x, int32_t batch, int32_t H, int32_t 
     // it measured 2-4 % faster than two or four (fewer registers)
     const int u = side == 4 ? 2 : 1;
     const int grid = grid_for((warps + u - 1) / u, 8, 148 * 8);
-    if (side == 8)
+    // FP32 rows only (fp32-state): six CTAs per SM at 40 registers hide more of
+    // the window-load latency (2.48 -> 2.37 ms/step at 64 x 1024^2); with the
+    // FP64 rows as well the same cap measured slower (3.24 -> 3.64)
+    if (side == 8 && Z64 == nullptr)
+      extract_cols_kernel<8, 1, 6><<<grid_for(warps, 8, 148 * 12), 256, 0, st>>>(x, batch, H, W, anchors, n, Z64, Z32, z32_pitch, dc, sq);
+    else if (side == 8)
       extract_cols_kernel<8, 1><<<grid, 256, 0, st>>>(x, batch, H, W, anchors, n, Z64, Z32, z32_pitch, dc, sq);
     else if (side == 4)
       extract_cols_kernel<4, 2><<<grid, 256, 0, st>>>(x, batch, H, W, anchors, n, Z64, Z32, z32_pitch, dc, sq);

@@ -619,3 +619,40 @@ def test_cover_gather_lo_eq_hi_verbatim_and_pipeline_errors(models):
     hp.submit(pin_in, pin_out)
     with pytest.raises(NumericalError):
         hp.wait()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "deblur96", "sr96"])
+def test_restore_graph_replay_equals_eager_and_fills_times(name, models):
+    """restore() with a cached plan replays one timed CUDA graph of the whole
+    restore (device timestamps at the phase marks); the image, counters and
+    CG flags are bitwise those of the eager path, also when the observation
+    changes between calls, and IterationStats.times carries the reference's
+    keys (pkg/src/fepll/solver.py:206-254) with that call's device times."""
+    from paper_1710_08124_b200 import RestorationConfig, restore
+    from paper_1710_08124_b200.solver import cached_restorer, clear_plan_cache
+
+    clear_plan_cache()
+    g, A, y, s8, s, P = golden_inputs(name)
+    model, tree = models[P]
+    cfg = RestorationConfig(sigma=s8, spacing=s, seed=0, sampling=g["meta"]["sampling"])
+    y2 = np.ascontiguousarray(y[::-1, ::-1])
+    r = cached_restorer(A, model, tree, cfg, batch=1)
+    r.use_graph = False
+    x_e, st_e = restore(y, A, model, tree, cfg)
+    x2_e, _ = restore(y2, A, model, tree, cfg)
+    r.use_graph = True
+    x_g, st_g = restore(y, A, model, tree, cfg)    # captures
+    x2_g, _ = restore(y2, A, model, tree, cfg)     # replays on another observation
+    x_g2, st_g2 = restore(y, A, model, tree, cfg)  # replays
+    assert r._tg_graph is not None
+    assert np.array_equal(x_e, x_g) and np.array_equal(x_g, x_g2) and np.array_equal(x2_e, x2_g)
+    keys = {"grid", "extract", "select", "estimate", "reproject"}
+    if A.kind in ("convolution", "decimate"):
+        keys.add("image_solve")
+    for a, b in zip(st_e.iterations, st_g2.iterations):
+        assert (a.patches, a.score_evaluations, a.selection_multiplies, a.estimation_multiplies) == \
+               (b.patches, b.score_evaluations, b.selection_multiplies, b.estimation_multiplies)
+        assert a.image_solve_converged == b.image_solve_converged
+        assert set(b.times) >= keys
+        assert all(0.0 <= b.times[k] < 0.05 for k in keys) and b.times["select"] > 0.0
+    clear_plan_cache()
