@@ -398,13 +398,21 @@ __global__ void __launch_bounds__(kThreads, 1) wiener_tc_kernel(PlanView pv, Arg
         const uint64_t rstep = (uint64_t)((2 * R * 128) >> 4);  // B1 atom stride ([hi; lo] rows)
         const uint64_t lo_rows = (uint64_t)((R * 128) >> 4);    // the lo rows inside an atom
         if (R <= 32) {
-          // Z (smem, read as trunc_tf32) . [B1_hi; B1_lo]: both halves in one pass
+          // Z (smem, read as trunc_tf32) . [B1_hi; B1_lo] (both halves in one pass) alternating with
+          // Z_lo (TMEM) . B1_hi: a run of TMEM-operand MMAs alone issues at ~131 cycles each, one
+          // between two shared-memory-operand MMAs at ~50 (tools/mma_bench.cu, Wiener tile patterns)
           const uint32_t idescw = tc::idesc_tf32(kRows, 2 * R);
+          tw = pf.now();
+          tc::mbar_wait(&s.lo_full[set], (i >> 1) & 1);
+          pf.add(1, tw);
+          tc::fence_after_sync();
           for (int kq = 0; kq < a.katoms; ++kq) {
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
+            for (int kk = 0; kk < 4; ++kk) {
               tc::mma_tf32_warp(d, A0 + (uint64_t)(kq * (kAtomA >> 4) + 2 * kk), d_b1 + kq * rstep + 2 * kk,
                                 idescw, (kq > 0 || kk > 0) ? 1u : 0u);
+              tc::mma_tf32_tmemA_warp(d, z_lo + 32 * kq + 8 * kk, d_b1 + kq * rstep + 2 * kk, idesc, 1u);
+            }
           }
         } else {
           for (int kq = 0; kq < a.katoms; ++kq) {
@@ -413,22 +421,19 @@ __global__ void __launch_bounds__(kThreads, 1) wiener_tc_kernel(PlanView pv, Arg
               tc::mma_tf32_warp(d, A0 + (uint64_t)(kq * (kAtomA >> 4) + 2 * kk), d_b1 + kq * rstep + 2 * kk, idesc,
                                 (kq > 0 || kk > 0) ? 1u : 0u);
           }
+          tw = pf.now();
+          tc::mbar_wait(&s.lo_full[set], (i >> 1) & 1);
+          pf.add(1, tw);
+          tc::fence_after_sync();
+          // Z . B1_lo alternating with Z_lo (TMEM) . B1_hi
           for (int kq = 0; kq < a.katoms; ++kq) {
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
+            for (int kk = 0; kk < 4; ++kk) {
               tc::mma_tf32_warp(d, A0 + (uint64_t)(kq * (kAtomA >> 4) + 2 * kk),
                                 d_b1 + lo_rows + kq * rstep + 2 * kk, idesc, 1u);
+              tc::mma_tf32_tmemA_warp(d, z_lo + 32 * kq + 8 * kk, d_b1 + kq * rstep + 2 * kk, idesc, 1u);
+            }
           }
-        }
-        // Z_lo (TMEM) . B1_hi
-        tw = pf.now();
-        tc::mbar_wait(&s.lo_full[set], (i >> 1) & 1);
-        pf.add(1, tw);
-        tc::fence_after_sync();
-        for (int kq = 0; kq < a.katoms; ++kq) {
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            tc::mma_tf32_tmemA_warp(d, z_lo + 32 * kq + 8 * kk, d_b1 + kq * rstep + 2 * kk, idesc, 1u);
         }
         tc::mma_commit_warp(&s.c_full[set]);
         pf2.add(2, tg);
