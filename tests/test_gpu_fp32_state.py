@@ -107,12 +107,15 @@ def test_fp32_state_cfg5_batch(wtc, models):
 
 
 @pytest.mark.parametrize("P,K,rho,size,B,use_tree", [(64, 200, 0.95, 144, 3, True), (16, 12, 0.9, 64, 2, False),
-                                                     (16, 6, 1.0, 48, 1, False), (64, 9, 0.999, 96, 2, False)])
+                                                     (16, 6, 1.0, 48, 1, False), (64, 9, 0.999, 96, 2, False),
+                                                     (64, 1, 0.95, 56, 2, False), (64, 300, 0.8, 200, 1, False)])
 def test_wiener_tc_matches_dmma(P, K, rho, size, B, use_tree, models):
     """Kernel level: the tcgen05 3xTF32 Wiener step against the FP64 DMMA one
     on the same patches and leaf buckets (iteration 0 of an fp32-state
-    restore) — ranks 30 (R = 32), 7 and 16 at P = 16, and 50+ (R = 64, two
-    K atoms in the second product).  Estimates agree to 2e-6 of the patch
+    restore) — ranks 30 (R = 32), 7 and 16 at P = 16, 50+ (R = 64, two
+    K atoms in the second product), a single component (the root is the only
+    leaf) and 300 components of rank ~10 (many near-empty buckets, a leaf
+    change every tile or two).  Estimates agree to 2e-6 of the patch
     scale (3xTF32: ~2^-20 per product), far inside the 1e-3 / 255 image bar."""
     import torch
     from paper_1710_08124_b200 import RestorationConfig, Restorer, synthetic
