@@ -95,6 +95,11 @@ int fepll_plan_destroy(fepll_plan_t plan);
  *                             (wiener_tc.cu; P % 16 == 0, P <= 64, ranks <= 64)
  *                             instead of the FP64 DMMA kernel — NOT bitwise the
  *                             same: ~1e-6 relative on the estimates;
+ *   wiener_ws 0 | 1 | 2       FP64 Wiener (P = 64): warp-specialised kernel — 12 compute
+ *                             warps + 2 loader warps, one CTA per SM, no CTA barrier
+ *                             between tiles — bitwise the two-CTA kernel; 2 (default):
+ *                             from 2^20 patches per call (measured +3 % there, -8 %
+ *                             at 8 x 1024^2);
  *   wiener_xw 0 | 1           Wiener reads 8x8 windows of x instead of Z64 (0);
  *   wiener_add_dc 0 | 1       fepll_wiener writes est + dc (1) or the bare
  *                             estimates (0: the trace's `estimates`; pass dc

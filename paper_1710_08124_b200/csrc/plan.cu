@@ -300,6 +300,7 @@ static int* plan_option(Plan* p, const char* name) {
   if (n == "defer_test") return &p->opt.defer_test;
   if (n == "wiener_split") return &p->opt.wiener_split;
   if (n == "wiener_tc") return &p->opt.wiener_tc;
+  if (n == "wiener_ws") return &p->opt.wiener_ws;
   return nullptr;
 }
 
@@ -309,7 +310,7 @@ int fepll_plan_set_option(fepll_plan_t plan, const char* name, int64_t value) {
   int* slot = plan_option(p, name);
   FEPLL_REQUIRE(slot != nullptr, std::string("plan_set_option: unknown option ") + (name ? name : "(null)"));
   const std::string n(name);
-  const bool ok = (n == "select_variant" || n == "l2_prefetch" || n == "aggregate_variant")
+  const bool ok = (n == "select_variant" || n == "l2_prefetch" || n == "aggregate_variant" || n == "wiener_ws")
                       ? (value >= 0 && value <= 2)
                   : (n == "wiener_rw")    ? (value == 8 || value == 16)
                                           : (value == 0 || value == 1);

@@ -86,6 +86,8 @@ struct PlanOptions {
                            // smem once per CTA) — measured slower (select 11.3 -> 13.1 ms/step at 64 x 1024^2:
                            // one 208 KB CTA per SM leaves 8 warps for latency-bound chains), off
 
+  int wiener_ws = 2;         // FP64 Wiener: warp-specialised kernel (12 compute + 2 loader warps, one CTA per SM; P = 64):
+                             // 0 off, 1 on, 2 on from 2^20 patches (64 x 1024^2: 7.26 -> 7.06 ms/step; 8 images: 1.06 -> 1.14)
   int wiener_tc = 0;         // fepll_wiener_f32 on tcgen05 (3xTF32, wiener_tc.cu) when the shape allows; 0: FP64 DMMA
   int wiener_split = 0;      // Wiener warp pairs on 16 rows with m16n8k8 DMMAs (0: 8-row warps, m8n8k4)
   int pdl = 1;

@@ -622,6 +622,231 @@ wiener_dmma_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, i
   bulk_wait_all();  // the last rows' stores are complete before the kernel ends
 }
 
+
+// ---------------------------------------------------------------------------
+// Warp-specialised form (plan option wiener_ws; P = 64, FP64 rows): one CTA
+// per SM, 12 compute warps (8 rows each of a 96-row tile: the same DMMA
+// sequence per element as wiener_dmma_kernel<8, 64, 2, 8>, bitwise the same
+// estimates) and 2 loader warps that run two tiles ahead (patch indices one
+// tile further) through a three-stage ring of row buffers guarded by
+// mbarriers.  A compute warp never meets a CTA barrier between tiles: it
+// waits for its tile's rows, runs both products and the epilogue on its own
+// 8 rows, hands them to the TMA as bulk stores and moves on; the stage goes
+// back to the loaders once every warp's stores have read it.  The FP64 pipe
+// keeps the other warps' DMMAs while one warp is in its epilogue (the
+// two-CTA kernel holds ~64 % of the pipe: all 8 warps of a CTA reach their
+// barrier, epilogue and stores together).
+namespace ws {
+constexpr int kCW = 12;               // compute warps
+constexpr int kLW = 2;                // loader warps
+constexpr int kThreads = 32 * (kCW + kLW);
+constexpr int kMT = 8 * kCW;          // rows per tile
+constexpr int kNS = 3;                // row stages
+constexpr int kRing = kNS + 3;        // index ring slots
+
+struct Head {
+  int32_t tpre[kMaxLevelNodes + 1];
+  uint64_t scan_tmp[256];
+  int32_t leaf_cr[kMaxLevelNodes];
+  int32_t leaf_cnt[kMaxLevelNodes];
+  double leaf_gt[kMaxLevelNodes];
+  int64_t leaf_off[kMaxLevelNodes];
+  int32_t rows[kRing][kMT];
+  uint64_t full[kNS], empty[kNS];
+  int32_t t_begin, t_end;
+};
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+               "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+wiener_ws_kernel(PlanView pv, int t, const int32_t* __restrict__ leaf_nodes, int n_leaf_nodes,
+                 const int32_t* __restrict__ cnt, const int64_t* __restrict__ off,
+                 const int32_t* __restrict__ leafseg, const double* __restrict__ Z64,
+                 const double* __restrict__ dc, double* __restrict__ Zhat, int n_img, int zrows, Geo geo) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  Head& h = *reinterpret_cast<Head*>(smem);
+  constexpr int P = 64;
+  const int zld = geo.zld;
+  double* Zs0 = reinterpret_cast<double*>(smem + ((sizeof(Head) + 127) & ~size_t(127)));  // [kNS][kMT][zld]
+  double* Us = Zs0 + (size_t)kNS * kMT * zld;  // [64][uld]
+  double* sh = Us + 64 * geo.uld;              // [R8e]
+  double* dcs = sh + geo.R8e;                  // [kNS][kMT]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < kNS; ++i) {
+      mbar_init(&h.full[i], 32 * kLW);
+      mbar_init(&h.empty[i], kCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int k = tid; k < n_leaf_nodes; k += kThreads) {
+    const int v = leaf_nodes[k];
+    const int comp = pv.leaf_index[v];
+    h.leaf_cr[k] = comp | (pv.model_rank[comp] << 16);
+    h.leaf_gt[k] = pv.model_gamma_tail[(int64_t)t * pv.K + comp];
+    h.leaf_cnt[k] = cnt[v];
+    h.leaf_off[k] = off[v];
+    h.tpre[k] = (cnt[v] + kMT - 1) / kMT;
+  }
+  __syncthreads();
+  const int tiles = block_exscan(h.tpre, n_leaf_nodes, h.scan_tmp);
+  if (tid == 0) {
+    h.tpre[n_leaf_nodes] = tiles;
+    h.t_begin = (int)(((int64_t)tiles * blockIdx.x) / gridDim.x);
+    h.t_end = (int)(((int64_t)tiles * (blockIdx.x + 1)) / gridDim.x);
+  }
+  __syncthreads();
+  const int t_begin = h.t_begin, t_end = h.t_end;
+  const int ntile = t_end - t_begin;
+
+  if (warp >= kCW) {
+    // ------------------------------------------------------------ loaders
+    const int lt = tid - 32 * kCW;  // 0 .. 63
+    int fli = prefix_find(h.tpre, n_leaf_nodes, t_begin);
+    auto issue_idx = [&](int j) {  // tile t_begin + j: its patch indices into ring slot j % kRing
+      if (j < ntile) {
+        const int tile = t_begin + j;
+        while (fli + 1 < n_leaf_nodes && h.tpre[fli + 1] <= tile) ++fli;
+        const int first = (tile - h.tpre[fli]) * kMT;
+        for (int r = lt; r < kMT; r += 32 * kLW) {
+          int32_t* dst = &h.rows[j % kRing][r];
+          if (r < h.leaf_cnt[fli] - first) cp_async4(dst, leafseg + h.leaf_off[fli] + first + r);
+          else *dst = -1;
+        }
+      }
+    };
+    issue_idx(0);
+    cp_async_commit();
+    issue_idx(1);
+    cp_async_commit();
+    issue_idx(2);
+    cp_async_commit();
+    for (int j = 0; j < ntile; ++j) {
+      const int st = j % kNS;
+      if (j >= kNS) mbar_wait(&h.empty[st], ((j / kNS) - 1) & 1);
+      cp_async_wait_group<2>();  // idx(j) landed (this thread's copies; the barrier below covers the others)
+      asm volatile("bar.sync 2, %0;" ::"n"(32 * kLW) : "memory");
+      const int32_t* rows = h.rows[j % kRing];
+      double* Zs = Zs0 + (size_t)st * kMT * zld;
+      // 32 chunks of 16 bytes per row: a warp instruction copies one whole row
+      for (int e = lt; e < kMT * 32; e += 32 * kLW) {
+        const int i = e >> 5, c = e & 31;
+        const int g = rows[i];
+        const bool ok = g >= 0;
+        cp_async16z(Zs + i * zld + 2 * c, ok ? Z64 + (int64_t)g * P + 2 * c : Z64, ok ? 16u : 0u);
+        if (c == 0) cp_async8z(dcs + st * kMT + i, ok ? dc + g : dc, ok ? 8u : 0u);
+      }
+      issue_idx(j + 3);
+      cp_async_commit();
+      cp_async_mbar_arrive(&h.full[st]);
+    }
+    cp_async_wait_all();
+    return;
+  }
+
+  // -------------------------------------------------------------- compute
+  const int g4 = lane >> 2, t4 = lane & 3;
+  const int m0 = warp * 8;
+  int cli = prefix_find(h.tpre, n_leaf_nodes, t_begin);
+  int cur_leaf = -1;
+  for (int j = 0; j < ntile; ++j) {
+    const int tile = t_begin + j;
+    const int st = j % kNS;
+    while (cli + 1 < n_leaf_nodes && h.tpre[cli + 1] <= tile) ++cli;
+    const int li = cli;
+    const int comp = h.leaf_cr[li] & 0xFFFF;
+    const int r = h.leaf_cr[li] >> 16;
+    if (comp != cur_leaf) {
+      // every compute warp is done with the previous leaf's basis
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kCW) : "memory");
+      const double* U = pv.model_basis + pv.model_off64[comp];
+      for (int e = tid; e < 64 * geo.R8e; e += 32 * kCW) {
+        const int p = e / geo.R8e, q = e - p * geo.R8e;
+        Us[p * geo.uld + q] = q < r ? U[(int64_t)p * r + q] : 0.0;
+      }
+      const double* shrink = pv.model_shrink + (int64_t)t * pv.model_cols_total + pv.model_col_off[comp];
+      for (int q = tid; q < geo.R8e; q += 32 * kCW) sh[q] = q < r ? shrink[q] : 0.0;
+      cur_leaf = comp;
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kCW) : "memory");
+    }
+    mbar_wait(&h.full[st], (j / kNS) & 1);
+    double* Zs = Zs0 + (size_t)st * kMT * zld;
+    const double* za = Zs + (m0 + g4) * zld + t4;
+    double acc[8][4];
+    auto nostep = [](int) {};
+    switch ((r + 7) / 8) {
+      case 1: wiener_rows<8, 1, 8>(za, za, 0.0, 0.0, Us, geo.uld, sh, t4, g4, nostep, acc); break;
+      case 2: wiener_rows<8, 2, 8>(za, za, 0.0, 0.0, Us, geo.uld, sh, t4, g4, nostep, acc); break;
+      case 3: wiener_rows<8, 3, 8>(za, za, 0.0, 0.0, Us, geo.uld, sh, t4, g4, nostep, acc); break;
+      case 4: wiener_rows<8, 4, 8>(za, za, 0.0, 0.0, Us, geo.uld, sh, t4, g4, nostep, acc); break;
+      case 5: wiener_rows<8, 5, 8>(za, za, 0.0, 0.0, Us, geo.uld, sh, t4, g4, nostep, acc); break;
+      case 6: wiener_rows<8, 6, 8>(za, za, 0.0, 0.0, Us, geo.uld, sh, t4, g4, nostep, acc); break;
+      case 7: wiener_rows<8, 7, 8>(za, za, 0.0, 0.0, Us, geo.uld, sh, t4, g4, nostep, acc); break;
+      default: wiener_rows<8, 8, 8>(za, za, 0.0, 0.0, Us, geo.uld, sh, t4, g4, nostep, acc); break;
+    }
+    {
+      // Zhat + dc = (acc + gamma_tail z) + dc over this warp's own rows of the stage
+      const double gt = h.leaf_gt[li];
+      double* zr = Zs + (m0 + g4) * zld;
+      const double d = dcs[st * kMT + m0 + g4];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        const int col = n * 8 + 2 * t4;
+        const double e0 = acc[n][0] + gt * zr[col];
+        const double e1 = acc[n][1] + gt * zr[col + 1];
+        zr[col] = geo.add_dc ? __dadd_rn(e0, d) : e0;
+        zr[col + 1] = geo.add_dc ? __dadd_rn(e1, d) : e1;
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane < 8) {
+        const int gidx = h.rows[j % kRing][m0 + lane];
+        if (gidx >= 0) {
+          const int64_t orow = zrows == n_img ? (int64_t)gidx : (int64_t)(gidx / n_img) * zrows + gidx % n_img;
+          bulk_s2g(Zhat + orow * P, Zs + (m0 + lane) * zld, P * 8u);
+        }
+        bulk_commit();
+      }
+      // the previous tile's stores have read their stage: hand it back
+      if (j > 0) {
+        bulk_wait_read1();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&h.empty[(j - 1) % kNS]);
+      }
+    }
+  }
+  bulk_wait_all();
+}
+
+}  // namespace ws
+
 }  // namespace wn
 
 static wn::Geo wiener_geo(const Plan* p) {
@@ -677,6 +902,27 @@ static int wiener_dmma_t(Plan* p, int t, const ZT* Z64, int zin_pitch, const dou
   const wn::Geo geo = wiener_geo(p);
   auto smem_for = [&](int mt, int ns) { return wiener_smem(geo, mt, ns, sizeof(ZT)); };
   const bool xw = Z64 == nullptr;
+  if constexpr (sizeof(ZT) == 8) {
+    // warp-specialised kernel (plan option wiener_ws): P = 64, dense FP64 rows
+    const bool ws_on = p->opt.wiener_ws == 1 || (p->opt.wiener_ws == 2 && p->last_n_total >= (1 << 20));
+    if (ws_on && !xw && p->v.P == 64 && zin_pitch == 64 && p->max_model_rank <= wn::kMaxR) {
+      const size_t smem_ws = ((sizeof(wn::ws::Head) + 127) & ~size_t(127)) +
+                             sizeof(double) * ((size_t)wn::ws::kNS * wn::ws::kMT * geo.zld + 64 * (size_t)geo.uld +
+                                               geo.R8e + (size_t)wn::ws::kNS * wn::ws::kMT);
+      int dev_ws = 0, optin_ws = 0;
+      FEPLL_CUDA(cudaGetDevice(&dev_ws));
+      FEPLL_CUDA(cudaDeviceGetAttribute(&optin_ws, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev_ws));
+      if (smem_ws <= (size_t)optin_ws) {
+        FEPLL_CUDA(cudaFuncSetAttribute(wn::ws::wiener_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem_ws));
+        wn::ws::wiener_ws_kernel<<<kSMs, wn::ws::kThreads, smem_ws, st>>>(
+            p->v, t, p->d_leaf_nodes, p->n_leaf_nodes, p->rs.cnt, p->rs.off, p->rs.leafseg, Z64, dc, Zhat, n_img,
+            zrows, geo);
+        FEPLL_LAUNCH();
+        return kOk;
+      }
+    }
+  }
   FEPLL_REQUIRE(!xw || wiener_xw_supported(p),
                 "wiener: the window-source kernel needs P = 64 and two CTAs per SM");
   // 128-row tiles (16 warps) once the average leaf bucket is large enough

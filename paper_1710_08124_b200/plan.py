@@ -325,7 +325,7 @@ class DevicePlan:
         self.reserved = 0
 
     OPTIONS = ("select_variant", "seg_sq", "wiener_pair", "wiener_rw", "wiener_xw", "wiener_add_dc",
-               "l2_prefetch", "rescore_by_node", "aggregate_variant", "wiener_split", "wiener_tc", "pdl",
+               "l2_prefetch", "rescore_by_node", "aggregate_variant", "wiener_split", "wiener_tc", "wiener_ws", "pdl",
                "defer", "defer_test")
 
     def set_option(self, name: str, value: int) -> None:

@@ -474,6 +474,7 @@ def test_operator_adjoint_identity_and_normal(name):
     ("l2_prefetch", (0, 1)),         # ws2 loaders: L2 prefetch three tiles ahead vs none
     ("rescore_by_node", (0, 1)),     # FP64 re-scoring per decision vs grouped by node (smem group)
     ("wiener_split", (0, 1)),          # Wiener: 8-row m8n8k4 warps vs m16n8k8 warp pairs
+    ("wiener_ws", (2, 0, 1)),          # Wiener: two 64-row CTAs per SM (2 = by size: here too) vs the warp-specialised single CTA
     ("defer", (1, 0)),                 # deferred FP64 verification vs re-scoring after every level
     ("pdl", (1, 0)),                   # programmatic dependent launch of the level / re-scoring kernels
     ("aggregate_variant", (2, 0, 1)),  # batch reprojection: staged tiles / thread per pixel / per (pixel, image)
