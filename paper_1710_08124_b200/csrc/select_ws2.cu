@@ -247,37 +247,68 @@ select_level_ws2_kernel(PlanView pv, Args args) {
     s.nd_nk[k] = (int16_t)pv.child_count[u];
   }
   __syncthreads();  // node tables
-  if (tid == 0) {
+  if (warp == 0) {
     // contiguous tile ranges of equal estimated cost: a tile costs 16 +
     // npad / 8 (loads, epilogue and MMAs of its node's width) — on the leaf
     // level of the cfg5 tree the 4-child nodes' tiles (128 columns) take
     // ~15 % longer than the 3-child ones (96), and equal tile counts left
-    // the CTAs holding them 40 us behind
+    // the CTAs holding them 40 us behind.  Warp 0 does it with four nodes
+    // per lane and a shuffle scan: one thread walking the nodes twice cost
+    // ~5 us of every CTA's prologue at 8 nodes and ~10 us at 64.
+    static_assert(kMaxNodes <= 128, "four nodes per lane");
     const int nd = a.lvl_end - a.lvl_begin;
     const int T = s.lv.total_tiles;
-    int64_t W = 0;
-    bool mixed = false;
-    for (int k = 0; k < nd; ++k) {
-      W += (int64_t)(s.lv.tpre[k + 1] - s.lv.tpre[k]) * (16 + s.nd_npad[k] / 8);
-      mixed |= s.nd_npad[k] != s.nd_npad[0];
+    int64_t c[4];
+    int wk[4];
+    int64_t sum = 0;
+    bool mix = false;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = 4 * lane + q;
+      c[q] = 0;
+      wk[q] = 1;
+      if (k < nd) {
+        wk[q] = 16 + s.nd_npad[k] / 8;
+        c[q] = (int64_t)(s.lv.tpre[k + 1] - s.lv.tpre[k]) * wk[q];
+        mix |= s.nd_npad[k] != s.nd_npad[0];
+      }
+      sum += c[q];
     }
+    int64_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int64_t W = __shfl_sync(0xffffffffu, incl, 31);
+    const bool mixed = __any_sync(0xffffffffu, mix);
     if (!mixed) {
-      s.t_begin = (int)(((int64_t)T * blockIdx.x) / gridDim.x);
-      s.t_end = (int)(((int64_t)T * (blockIdx.x + 1)) / gridDim.x);
+      if (lane == 0) {
+        s.t_begin = (int)(((int64_t)T * blockIdx.x) / gridDim.x);
+        s.t_end = (int)(((int64_t)T * (blockIdx.x + 1)) / gridDim.x);
+      }
     } else {
       const int64_t x0 = W * blockIdx.x / gridDim.x, x1 = W * (blockIdx.x + 1) / gridDim.x;
-      int64_t acc = 0;
+      int64_t acc = incl - sum;
       int tb = T, te = T;
-      for (int k = 0; k < nd; ++k) {
-        const int wk = 16 + s.nd_npad[k] / 8;
-        const int nt = s.lv.tpre[k + 1] - s.lv.tpre[k];
-        const int64_t nxt = acc + (int64_t)nt * wk;
-        if (tb == T && x0 < nxt) tb = s.lv.tpre[k] + (int)((x0 - acc + wk - 1) / wk);
-        if (te == T && x1 < nxt) te = s.lv.tpre[k] + (int)((x1 - acc + wk - 1) / wk);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = 4 * lane + q;
+        const int64_t nxt = acc + c[q];
+        // the first node whose cost range holds x: acc <= x < nxt (empty nodes have nxt == acc)
+        if (acc <= x0 && x0 < nxt) tb = s.lv.tpre[k] + (int)((x0 - acc + wk[q] - 1) / wk[q]);
+        if (acc <= x1 && x1 < nxt) te = s.lv.tpre[k] + (int)((x1 - acc + wk[q] - 1) / wk[q]);
         acc = nxt;
       }
-      s.t_begin = min(tb, T);
-      s.t_end = blockIdx.x + 1 == gridDim.x ? T : min(te, T);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        tb = min(tb, __shfl_xor_sync(0xffffffffu, tb, o));
+        te = min(te, __shfl_xor_sync(0xffffffffu, te, o));
+      }
+      if (lane == 0) {
+        s.t_begin = min(tb, T);
+        s.t_end = blockIdx.x + 1 == gridDim.x ? T : min(te, T);
+      }
     }
   }
   tc::fence_before_sync();
