@@ -271,3 +271,26 @@ def test_reference_objects_pack_like_native_ones():
         restore(y, A, rmodel, rtree, RConfig(sigma=20.0, spacing=9))
     with pytest.raises(DataError):
         restore(y, A, rmodel, rtree, RConfig(sigma=20.0, iterations=2))
+
+
+def test_phase_and_iteration_times_from_timestamp_marks():
+    """restore()'s timed CUDA-graph replay hands the phase bookkeeping a list
+    of mark names and the milliseconds between consecutive marks
+    (Restorer.run_timed_graph): every interval is attributed to the mark that
+    closes it, the stretch into an iteration's "start" mark counts as gap,
+    and IterationStats.times gets the reference's keys
+    (pkg/src/fepll/solver.py:206-254) in seconds."""
+    from paper_1710_08124_b200.solver import Restorer
+
+    names = ["start", "init", "start", "extract", "select", "wiener", "aggregate",
+             "start", "extract", "select", "wiener", "aggregate", "image_solve"]
+    ms = [0.5, 0.01, 1.0, 2.0, 3.0, 4.0, 0.02, 1.5, 2.5, 3.5, 4.5, 5.5]
+    timer = {"_marks": [(n, None) for n in names], "_ms": ms}
+    ph = Restorer.phase_times(timer)
+    assert ph == {"init": 0.5, "gap": 0.01 + 0.02, "extract": 2.5, "select": 4.5, "wiener": 6.5,
+                  "aggregate": 8.5, "image_solve": 5.5}
+    assert abs(sum(ph.values()) - sum(ms)) < 1e-12
+    it = Restorer.iteration_times(timer)
+    assert it == [{"grid": 0.0, "extract": 1e-3, "select": 2e-3, "estimate": 3e-3, "reproject": 4e-3},
+                  {"grid": 0.0, "extract": 1.5e-3, "select": 2.5e-3, "estimate": 3.5e-3, "reproject": 4.5e-3,
+                   "image_solve": 5.5e-3}]
