@@ -147,6 +147,97 @@ __device__ inline void level_tables(const PlanView& pv, const LevelArgs& a, LT& 
     for (int k = threadIdx.x; k < nn; k += blockDim.x) a.off[a.nxt_begin + k] = s.child_off[k];
 }
 
+// level_tables for levels of at most 256 nodes on both sides (every level the
+// ws2 kernel takes): warp 0 computes the three prefix sums with eight entries
+// per lane and shuffle scans, so the CTA meets one barrier instead of a
+// dozen — the same tables bit for bit.  On small images the tree walk is
+// launch- and prologue-bound (a 256^2 image has 33 tiles per level), and the
+// prologue was mostly these barriers.  Every thread calls it; ends with a
+// __syncthreads.
+template <class LT>
+__device__ inline void level_tables_warp(const PlanView& pv, const LevelArgs& a, LT& s,
+                                         int rows_per_tile) {
+  const int nd = a.lvl_end - a.lvl_begin;
+  const int nn = a.nxt_end - a.nxt_begin;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    // counts and tiles of the depth-d internal nodes
+    int c[8], tl[8];
+    int sc = 0, st = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int k = 8 * lane + q;
+      c[q] = 0;
+      if (k < nd) {
+        const int u = a.lvl_begin + k;
+        c[q] = pv.child_count[u] > 0 ? a.cnt[u] : 0;
+      }
+      tl[q] = (c[q] + rows_per_tile - 1) / rows_per_tile;
+      sc += c[q];
+      st += tl[q];
+    }
+    // capacities of the depth-(d+1) nodes: (leaf << 32 | internal)
+    uint64_t cap[8];
+    uint64_t scap = 0;
+    bool leaf[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int k = 8 * lane + q;
+      cap[q] = 0;
+      leaf[q] = false;
+      if (k < nn) {
+        const int v = a.nxt_begin + k;
+        const uint64_t pc = (uint64_t)(uint32_t)a.cnt[pv.parent[v]];
+        leaf[q] = pv.child_count[v] == 0;
+        cap[q] = leaf[q] ? ((uint64_t)leaf_capacity((int)pc) << 32) : pc;
+      }
+      scap += cap[q];
+    }
+    const int64_t lb = a.leaf_base[a.depth];
+    int ic = sc, it = st;
+    uint64_t icap = scap;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int yc = __shfl_up_sync(0xffffffffu, ic, o);
+      const int yt = __shfl_up_sync(0xffffffffu, it, o);
+      const uint64_t yp = __shfl_up_sync(0xffffffffu, icap, o);
+      if (lane >= o) {
+        ic += yc;
+        it += yt;
+        icap += yp;
+      }
+    }
+    const int items = __shfl_sync(0xffffffffu, ic, 31), tiles = __shfl_sync(0xffffffffu, it, 31);
+    const uint64_t tot = __shfl_sync(0xffffffffu, icap, 31);
+    int rc = ic - sc, rt = it - st;
+    uint64_t rp = icap - scap;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int k = 8 * lane + q;
+      if (k < nd) {
+        s.cpre[k] = rc;
+        s.tpre[k] = rt;
+      }
+      rc += c[q];
+      rt += tl[q];
+      if (k < nn) {
+        const int64_t o = leaf[q] ? lb + (int64_t)(rp >> 32) : (int64_t)(rp & 0xffffffffull);
+        s.child_off[k] = o;
+        if (blockIdx.x == 0) a.off[a.nxt_begin + k] = o;
+      }
+      rp += cap[q];
+    }
+    if (lane == 0) {
+      s.cpre[nd] = items;
+      s.tpre[nd] = tiles;
+      s.total_items = items;
+      s.total_tiles = tiles;
+      if (blockIdx.x == 0) a.leaf_base[a.depth + 1] = lb + (int64_t)(tot >> 32);
+    }
+  }
+  __syncthreads();
+}
+
 // smallest k with pre[k+1] > x  (pre[0] = 0, pre[n] = total)
 __device__ __forceinline__ int prefix_find(const int32_t* pre, int n, int x) {
   int lo = 0, hi = n;

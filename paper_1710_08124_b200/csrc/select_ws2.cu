@@ -239,7 +239,7 @@ select_level_ws2_kernel(PlanView pv, Args args) {
   // above (TMEM, barriers) overlapped its tail; the counts are its output
   pdl_wait();
   pdl_trigger();  // the re-scoring grid may queue behind this one's CTAs
-  level_tables(pv, a, s.lv, kRows);  // contains __syncthreads
+  level_tables_warp(pv, a, s.lv, kRows);  // ends with a __syncthreads (nodes <= 256 on both sides)
   for (int k = tid; k < a.lvl_end - a.lvl_begin; k += blockDim.x) {
     const int u = a.lvl_begin + k;
     s.nd_off[k] = a.off[u];
