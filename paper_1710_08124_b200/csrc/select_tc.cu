@@ -90,7 +90,9 @@ select_level_tc_kernel(PlanView pv, TcArgs args) {
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = s.tmem_base;
-  level_tables(pv, a, s.lv, kTcRows);
+  // levels of <= 256 nodes on both sides: the one-warp tables (one barrier), else the block scans
+  if (a.lvl_end - a.lvl_begin <= 256 && a.nxt_end - a.nxt_begin <= 256) level_tables_warp(pv, a, s.lv, kTcRows);
+  else level_tables(pv, a, s.lv, kTcRows);
 
   const int nd = a.lvl_end - a.lvl_begin;
   const int t = a.t;
