@@ -240,24 +240,32 @@ select_level_ws2_kernel(PlanView pv, Args args) {
   pdl_wait();
   pdl_trigger();  // the re-scoring grid may queue behind this one's CTAs
   level_tables_warp(pv, a, s.lv, kRows);  // ends with a __syncthreads (nodes <= 256 on both sides)
-  for (int k = tid; k < a.lvl_end - a.lvl_begin; k += blockDim.x) {
-    const int u = a.lvl_begin + k;
-    s.nd_off[k] = a.off[u];
-    s.nd_npad[k] = (int16_t)pv.tc_npad[u];
-    s.nd_nk[k] = (int16_t)pv.child_count[u];
-  }
-  __syncthreads();  // node tables
   if (warp == 0) {
-    // contiguous tile ranges of equal estimated cost: a tile costs 16 +
-    // npad / 8 (loads, epilogue and MMAs of its node's width) — on the leaf
-    // level of the cfg5 tree the 4-child nodes' tiles (128 columns) take
-    // ~15 % longer than the 3-child ones (96), and equal tile counts left
-    // the CTAs holding them 40 us behind.  Warp 0 does it with four nodes
-    // per lane and a shuffle scan: one thread walking the nodes twice cost
-    // ~5 us of every CTA's prologue at 8 nodes and ~10 us at 64.
+    // node tables (four nodes per lane) and, from them, contiguous tile
+    // ranges of equal estimated cost: a tile costs 16 + npad / 8 (loads,
+    // epilogue and MMAs of its node's width) — on the leaf level of the cfg5
+    // tree the 4-child nodes' tiles (128 columns) take ~15 % longer than the
+    // 3-child ones (96), and equal tile counts left the CTAs holding them
+    // 40 us behind.  One warp with a shuffle scan: one thread walking the
+    // nodes twice cost ~5 us of every CTA's prologue at 8 nodes and ~10 us
+    // at 64, and filling the tables from every thread one more CTA barrier.
     static_assert(kMaxNodes <= 128, "four nodes per lane");
     const int nd = a.lvl_end - a.lvl_begin;
     const int T = s.lv.total_tiles;
+    int npad_r[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = 4 * lane + q;
+      npad_r[q] = 0;
+      if (k < nd) {
+        const int u = a.lvl_begin + k;
+        npad_r[q] = pv.tc_npad[u];
+        s.nd_off[k] = a.off[u];
+        s.nd_npad[k] = (int16_t)npad_r[q];
+        s.nd_nk[k] = (int16_t)pv.child_count[u];
+      }
+    }
+    const int npad0 = __shfl_sync(0xffffffffu, npad_r[0], 0);
     int64_t c[4];
     int wk[4];
     int64_t sum = 0;
@@ -268,9 +276,9 @@ select_level_ws2_kernel(PlanView pv, Args args) {
       c[q] = 0;
       wk[q] = 1;
       if (k < nd) {
-        wk[q] = 16 + s.nd_npad[k] / 8;
+        wk[q] = 16 + npad_r[q] / 8;
         c[q] = (int64_t)(s.lv.tpre[k + 1] - s.lv.tpre[k]) * wk[q];
-        mix |= s.nd_npad[k] != s.nd_npad[0];
+        mix |= npad_r[q] != npad0;
       }
       sum += c[q];
     }
